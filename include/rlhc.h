@@ -1,0 +1,177 @@
+/*
+ * rlhc.h -- C ABI of the B200 (sm_100a) hot path of randomized LU-Householder
+ * CholeskyQR (rLHC), arXiv 2412.06551: SLHC3 (PAPER.md Algorithm alg:SLHC3,
+ * P:301-311) and SSLHC3 (alg:SSLHC3) for tall-skinny fp64 X (m >> n).
+ *
+ * Conventions for every entry point
+ *   - Matrices are IEEE fp64, ROW-major, with a leading dimension (ld >= number of
+ *     columns).  Pointers named X, A, Q, R, U, L, G, S, T, out, ws are DEVICE pointers
+ *     owned by the caller; nothing is allocated inside a call.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default).
+ *   - The int return value is host-side only: RLHC_OK, RLHC_EINVAL for an invalid
+ *     argument (sizes, null pointers, leading dimensions, aliasing), RLHC_EWORKSPACE
+ *     for a too-small workspace, RLHC_ECUDA for a launch failure (rlhc_last_error()
+ *     gives the CUDA message).  Nothing is launched when the return value is not OK.
+ *   - Numerical failures are written by the device into `info` (device pointer,
+ *     first failure in pipeline order wins) and read by the caller after the stream
+ *     is synchronised; outputs are unspecified when info->code != RLHC_OK.  Errors are
+ *     values, never silent NaNs.
+ *   - Inputs are never modified.  Results are bitwise reproducible for fixed inputs,
+ *     seed, configuration and device (fixed-order reductions, no floating atomics).
+ *   - Global row ids: `row0` is the global id of the first local row, so every
+ *     random draw (Omega column, CountSketch hash) is indexed by the global row
+ *     and row-sharded calls compose (R#2).
+ */
+#ifndef RLHC_H_
+#define RLHC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* rlhc_stream_t; /* == cudaStream_t */
+
+/* Device-written status.  code: enum rlhc_code; stage: enum rlhc_stage; index:
+ * the offending pivot / column / linear element index. */
+typedef struct {
+  int32_t code;
+  int32_t stage;
+  int64_t index;
+} rlhc_info_t;
+
+enum rlhc_code {
+  RLHC_OK = 0,
+  RLHC_EINVAL = 1,      /* host: invalid argument */
+  RLHC_ENONFINITE = 2,  /* device: NaN/Inf in X (index = i*n + j) */
+  RLHC_ERANKDEF = 3,    /* device: zero root pivot in PX = LU (index = k) or zero HQR column */
+  RLHC_ESINGULAR = 4,   /* device: zero / non-finite diagonal of a triangular factor */
+  RLHC_EBREAKDOWN = 5,  /* device: Cholesky pivot <= 0 or non-finite (index = k) */
+  RLHC_ECUDA = 6,       /* host: CUDA launch error */
+  RLHC_EWORKSPACE = 7   /* host: workspace too small */
+};
+
+enum rlhc_stage {
+  RLHC_STAGE_INPUT = 0,   /* finiteness of X */
+  RLHC_STAGE_LU = 1,      /* PX = LU */
+  RLHC_STAGE_SKETCH = 2,  /* L_s = Omega L / L_ss = Omega_2 Omega_1 L */
+  RLHC_STAGE_HQR = 3,     /* [H, S] = HouseholderQR(L_s) */
+  RLHC_STAGE_SOLVE_Y = 4, /* W = X Y^{-1}, Y = S U */
+  RLHC_STAGE_CHOL1 = 5,   /* D = chol(W^T W) (P:27-28 inside CholeskyQR2) */
+  RLHC_STAGE_SOLVE_D = 6, /* V = W D^{-1} */
+  RLHC_STAGE_CHOL2 = 7,   /* J = chol(V^T V) */
+  RLHC_STAGE_SOLVE_J = 8  /* Q = V J^{-1} */
+};
+
+enum rlhc_algo { RLHC_SLHC3 = 0, RLHC_SSLHC3 = 1 };
+enum rlhc_trsm_mode { RLHC_SUBST = 0, RLHC_INV_GEMM = 1 };
+
+/* Pivot-rule contract of PX = LU (R#3-R#5; the paper only says "P is a
+ * permutation"): tournament pivoting over column panels of width `panel`
+ * (panel = n is plain TSLU; a single leaf is GEPP).  Leaves are global row blocks
+ * [l*leaf_rows, (l+1)*leaf_rows); each tree node runs GEPP on the stacked winners of
+ * `arity` consecutive children (ties -> smallest global row id).  The result depends
+ * only on (X, leaf_rows, arity, panel), never on the GPU count.  Supported on the
+ * device: panel in {16, 32, 64} with leaf_rows == rows_per_select(panel) and
+ * arity * panel <= rows_per_select(panel) (see rlhc_default_tslu_cfg). */
+typedef struct {
+  int64_t leaf_rows;
+  int32_t arity;
+  int32_t panel;
+} rlhc_tslu_cfg;
+
+/* Fills cfg with the device's default contract for an m x n problem (panel =
+ * min(n rounded up to 16/32/64, 64), leaf_rows = candidate rows one select CTA
+ * holds in registers, the largest arity that fits).  Never fails. */
+void rlhc_default_tslu_cfg(int64_t m, int64_t n, rlhc_tslu_cfg* cfg);
+
+/* Bytes of device workspace rlhc_slhc3 (algo = RLHC_SLHC3, s_or_s1 = s, s2 ignored) or
+ * rlhc_sslhc3 (algo = RLHC_SSLHC3, s_or_s1 = s1, s2) needs; 0 on invalid sizes. */
+size_t rlhc_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg* cfg);
+
+/* SLHC3 (alg:SLHC3):  PX = LU; L_s = Omega L (Omega s x m Gaussian,
+ * entries N(0, 1/s) from Philox stream 0, R#1/R#19); [H,S] =
+ * HouseholderQR(L_s); Y = S U with sign(S_kk) = sign(U_kk) (R#7); W = X Y^{-1} by
+ * substitution; [Q, Z] = CholeskyQR2(W); R = Z Y evaluated as J (D Y).
+ *   X  : m x n, ldx >= n, rank n, m >= n, n <= s <= m.  Not modified.
+ *   Q  : m x n output, ldq >= n; must not overlap X.  Used in place for L, W and V.
+ *   R  : n x n output (row-major, strict lower part exactly 0, diag(R) > 0).
+ *   piv: n int64 output, global row ids of the pivot rows in pivot order.
+ *   ws : >= rlhc_workspace_size(RLHC_SLHC3, m, n, s, 0, cfg) bytes, 256-byte aligned.
+ *   cfg: NULL = rlhc_default_tslu_cfg.  info: device pointer. */
+int rlhc_slhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s, uint64_t seed,
+               const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq, double* R, int64_t* piv, void* ws,
+               size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+
+/* SSLHC3 (alg:SSLHC3): as rlhc_slhc3 with L_ss = Omega_2 (Omega_1 L)
+ * (P:294): Omega_1 s1 x m CountSketch (bucket/sign from Philox stream 2),
+ * Omega_2 s2 x s1 Gaussian N(0, 1/s2) (stream 1).  n <= s2 <= s1 <= m. */
+int rlhc_sslhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed,
+                const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq, double* R, int64_t* piv, void* ws,
+                size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+
+/* ---------------------------------------------------------------- per-stage */
+/* Row-pivoted tall-skinny LU "PX = LU" under the tslu contract.
+ *   X: rows x n (rows = m, global ids row0..row0+rows-1; row0 must be 0 here).
+ *   piv: n int64 out; U, L11: n x n out (U upper, L11 unit lower: multipliers of the
+ *   pivot rows); L: nullable, rows x n out (ldl >= n), original row order.
+ *   ws >= rlhc_getrf_ts_workspace_size(rows, n, cfg). */
+size_t rlhc_getrf_ts_workspace_size(int64_t rows, int64_t n, const rlhc_tslu_cfg* cfg);
+int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg* cfg,
+                  int64_t* piv, double* U, double* L11, double* L, int64_t ldl, void* ws, size_t ws_bytes,
+                  rlhc_info_t* info, rlhc_stream_t stream);
+
+/* Gaussian sketch out (s x n, overwritten) = Omega A, where A is rows x n (lda) and
+ * Omega's columns are the global rows row0..row0+rows-1: Omega[i, j] =
+ * z_{i mod 2}(Philox(seed; j, i>>1, stream_id)) / sqrt(s) (R#19).
+ * stream_id 0 = SLHC3's Omega, 1 = SSLHC3's Omega_2.  ws >= rlhc_sketch_gauss_workspace_size. */
+size_t rlhc_sketch_gauss_workspace_size(int64_t rows, int64_t n, int64_t s);
+int rlhc_sketch_gauss(const double* A, int64_t rows, int64_t n, int64_t lda, int64_t row0, int64_t s, uint64_t seed,
+                      uint32_t stream_id, double* out, void* ws, size_t ws_bytes, rlhc_stream_t stream);
+
+/* CountSketch out (s1 x n, overwritten) = Omega_1 A: global row j goes to
+ * bucket(j) = (w0 * s1) >> 32 with sign (w1 >> 31 ? -1 : +1), (w0, w1) = Philox(seed;
+ * j, 0, 2).  Each bucket is summed in ascending row order (deterministic).
+ * bucket (int32[rows]) and sign (int8[rows]) are optional outputs (nullable). */
+size_t rlhc_sketch_count_workspace_size(int64_t rows, int64_t n, int64_t s1);
+int rlhc_sketch_count(const double* A, int64_t rows, int64_t n, int64_t lda, int64_t row0, int64_t s1, uint64_t seed,
+                      double* out, int32_t* bucket, int8_t* sign, void* ws, size_t ws_bytes, rlhc_stream_t stream);
+
+/* Gram G = A^T A, n x n full symmetric output (upper computed, mirrored:
+ * exactly symmetric), split over rows with a fixed-order reduction. */
+size_t rlhc_gram_workspace_size(int64_t rows, int64_t n);
+int rlhc_gram(const double* A, int64_t rows, int64_t n, int64_t lda, double* G, void* ws, size_t ws_bytes,
+              rlhc_stream_t stream);
+
+/* out = A T^{-1} for n x n upper-triangular T ("Q = X R^{-1}").
+ * mode RLHC_SUBST: row-wise substitution (backward stable for any kappa(T); used for
+ * U and Y).  mode RLHC_INV_GEMM: T^{-1} formed once (n x n) then a streaming product
+ * (used in the CholeskyQR2 tail where kappa(T) <= ~7).  out may equal A
+ * (same pointer and ld: in place) but must not partially overlap it.  G_out: nullable
+ * n x n, the Gram of out fused into the same pass.  A zero diagonal of T ->
+ * ESINGULAR(SOLVE_Y, k) in info. */
+size_t rlhc_trsm_apply_workspace_size(int64_t rows, int64_t n);
+int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int mode, double* out,
+                    int64_t ldo, double* G_out, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+
+/* Householder R of an s x n matrix (LAPACK dgeqr2 order, H never formed):
+ * S (n x n, upper) with the sign of row k flipped so sign(S_kk) = sign(sgn_ref_kk)
+ * when sgn_ref (n x n, nullable) is given (R#7). A zero column -> ERANKDEF(HQR, k). */
+size_t rlhc_hqr_workspace_size(int64_t s, int64_t n);
+int rlhc_hqr_r(const double* A, int64_t s, int64_t n, int64_t lda, const double* sgn_ref, double* S, void* ws,
+               size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+
+/* Upper Cholesky factor of an n x n SPD matrix: pivot <= 0 or non-finite ->
+ * EBREAKDOWN(stage, k) with the given stage tag. */
+int rlhc_cholesky(const double* G, int64_t n, double* Rout, int stage, rlhc_info_t* info, rlhc_stream_t stream);
+
+/* Library identification and the last host-side error message (thread-local). */
+const char* rlhc_version(void);
+const char* rlhc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLHC_H_ */

@@ -1,0 +1,106 @@
+"""ctypes binding of include/rlhc.h (argument marshalling only).
+
+The library is built in-tree (paper_2412_06551_b200/librlhc.so).  There is no CPU
+fallback: loading fails loudly when the library or a CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librlhc.so")
+
+# enum rlhc_code / rlhc_stage / rlhc_algo / rlhc_trsm_mode (include/rlhc.h)
+RLHC_OK, RLHC_EINVAL, RLHC_ENONFINITE, RLHC_ERANKDEF, RLHC_ESINGULAR, RLHC_EBREAKDOWN, RLHC_ECUDA, RLHC_EWORKSPACE = range(8)
+(STAGE_INPUT, STAGE_LU, STAGE_SKETCH, STAGE_HQR, STAGE_SOLVE_Y, STAGE_CHOL1, STAGE_SOLVE_D, STAGE_CHOL2,
+ STAGE_SOLVE_J) = range(9)
+RLHC_SLHC3, RLHC_SSLHC3 = 0, 1
+RLHC_SUBST, RLHC_INV_GEMM = 0, 1
+
+CODE_NAMES = {0: "OK", 1: "EINVAL", 2: "ENONFINITE", 3: "ERANKDEF", 4: "ESINGULAR", 5: "EBREAKDOWN", 6: "ECUDA",
+              7: "EWORKSPACE"}
+STAGE_NAMES = {0: "INPUT", 1: "LU", 2: "SKETCH", 3: "HQR", 4: "SOLVE_Y", 5: "CHOL1", 6: "SOLVE_D", 7: "CHOL2",
+               8: "SOLVE_J"}
+
+
+class TsluCfg(ctypes.Structure):
+    _fields_ = [("leaf_rows", ctypes.c_int64), ("arity", ctypes.c_int32), ("panel", ctypes.c_int32)]
+
+    def as_tuple(self):
+        return int(self.leaf_rows), int(self.arity), int(self.panel)
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("stage", ctypes.c_int32), ("index", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load librlhc.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from . import build as _build
+    try:
+        _build.build()
+    except Exception as e:  # pragma: no cover - no nvcc on the target is fatal only when stale
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"librlhc.so is missing and could not be built: {e}") from e
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, U64, U32, SZ, I = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
+                               ctypes.c_int)
+    PC = ctypes.POINTER(TsluCfg)
+    L.rlhc_default_tslu_cfg.argtypes = [I64, I64, PC]
+    L.rlhc_default_tslu_cfg.restype = None
+    L.rlhc_workspace_size.argtypes = [I, I64, I64, I64, I64, PC]
+    L.rlhc_workspace_size.restype = SZ
+    L.rlhc_slhc3.argtypes = [P, I64, I64, I64, I64, U64, PC, P, I64, P, P, P, SZ, P, P]
+    L.rlhc_sslhc3.argtypes = [P, I64, I64, I64, I64, I64, U64, PC, P, I64, P, P, P, SZ, P, P]
+    L.rlhc_getrf_ts_workspace_size.argtypes = [I64, I64, PC]
+    L.rlhc_getrf_ts_workspace_size.restype = SZ
+    L.rlhc_getrf_ts.argtypes = [P, I64, I64, I64, I64, PC, P, P, P, P, I64, P, SZ, P, P]
+    L.rlhc_sketch_gauss_workspace_size.argtypes = [I64, I64, I64]
+    L.rlhc_sketch_gauss_workspace_size.restype = SZ
+    L.rlhc_sketch_gauss.argtypes = [P, I64, I64, I64, I64, I64, U64, U32, P, P, SZ, P]
+    L.rlhc_sketch_count_workspace_size.argtypes = [I64, I64, I64]
+    L.rlhc_sketch_count_workspace_size.restype = SZ
+    L.rlhc_sketch_count.argtypes = [P, I64, I64, I64, I64, I64, U64, P, P, P, P, SZ, P]
+    L.rlhc_gram_workspace_size.argtypes = [I64, I64]
+    L.rlhc_gram_workspace_size.restype = SZ
+    L.rlhc_gram.argtypes = [P, I64, I64, I64, P, P, SZ, P]
+    L.rlhc_trsm_apply_workspace_size.argtypes = [I64, I64]
+    L.rlhc_trsm_apply_workspace_size.restype = SZ
+    L.rlhc_trsm_apply.argtypes = [P, I64, I64, I64, P, I, P, I64, P, P, SZ, P, P]
+    L.rlhc_hqr_workspace_size.argtypes = [I64, I64]
+    L.rlhc_hqr_workspace_size.restype = SZ
+    L.rlhc_hqr_r.argtypes = [P, I64, I64, I64, P, P, P, SZ, P, P]
+    L.rlhc_cholesky.argtypes = [P, I64, P, I, P, P]
+    L.rlhc_version.restype = ctypes.c_char_p
+    L.rlhc_last_error.restype = ctypes.c_char_p
+    for name in ("rlhc_slhc3", "rlhc_sslhc3", "rlhc_getrf_ts", "rlhc_sketch_gauss", "rlhc_sketch_count", "rlhc_gram",
+                 "rlhc_trsm_apply", "rlhc_hqr_r", "rlhc_cholesky"):
+        getattr(L, name).restype = I
+    _lib = L
+    return L
+
+
+# Every symbol include/rlhc.h declares (checked by tests/test_abi.py).
+EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_sslhc3",
+            "rlhc_getrf_ts_workspace_size", "rlhc_getrf_ts", "rlhc_sketch_gauss_workspace_size",
+            "rlhc_sketch_gauss", "rlhc_sketch_count_workspace_size", "rlhc_sketch_count",
+            "rlhc_gram_workspace_size", "rlhc_gram", "rlhc_trsm_apply_workspace_size", "rlhc_trsm_apply",
+            "rlhc_hqr_workspace_size", "rlhc_hqr_r", "rlhc_cholesky", "rlhc_version", "rlhc_last_error"]
+
+
+class RlhcError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"rlhc {CODE_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def check(rc: int):
+    if rc != RLHC_OK:
+        raise RlhcError(rc, lib().rlhc_last_error().decode())

@@ -1,0 +1,60 @@
+// kernels.cuh -- launch wrappers of the rLHC sm_100a kernels (internal; not the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rlhc {
+
+int select_rows(int W);
+
+// tslu.cu
+cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st);
+cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
+                             int w, int* ids, int* cnt, double* vals, cudaStream_t st);
+cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
+                                     const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
+                                     uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st);
+cudaError_t launch_l11_fixup(double* L11, int n, cudaStream_t st);
+cudaError_t launch_gather_rows(const double* src, int64_t lds, const int64_t* ids, int64_t row0, int cnt, int ncols,
+                               double* dst, int64_t ldd, cudaStream_t st);
+cudaError_t launch_pivpos(const int64_t* piv, int n, int64_t row0, int64_t rows, int* pivpos, cudaStream_t st);
+
+// rows.cu
+cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,
+                                cudaStream_t st);
+cudaError_t launch_rdiag(const double* T, int n, int64_t ldt, double* rdiag, int stage, unsigned long long* status,
+                         cudaStream_t st);
+// out = A T^{-1} (substitution, fma chain in increasing k) on the first nsub columns,
+// remaining columns [nsub, ncols) receive only the updates.  pivpos/L11: pivot-row override.
+cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int ncols, int nsub, const double* T,
+                             int64_t ldt, const double* rdiag, double* out, int64_t ldo, const int* pivpos,
+                             const double* L11, int64_t ldl11, cudaStream_t st);
+// out = A Tinv (Tinv upper, full n x n storage with zero lower part); out may equal A.
+cudaError_t launch_rows_upper(const double* A, int64_t lda, int64_t rows, int n, const double* Tinv, double* out,
+                              int64_t ldo, cudaStream_t st);
+size_t gram_partials_bytes(int64_t rows, int n);
+cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st);
+
+// sketch.cu
+size_t gauss_partials_bytes(int64_t rows, int n, int s);
+cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s, uint64_t seed,
+                                uint32_t stream_id, double* part, double* out, cudaStream_t st);
+size_t cs_plan_bytes(int64_t rows, int s1);
+cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s1,
+                                uint64_t seed, void* plan_ws, double* out, int32_t* bucket_out, int8_t* sign_out,
+                                cudaStream_t st);
+
+// small.cu
+size_t hqr_ws_bytes(int s, int n);
+cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double* sgn_ref, double* S, double* work,
+                       unsigned long long* status, cudaStream_t st);
+cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
+                        cudaStream_t st);
+cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
+cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);
+cudaError_t launch_status_init(unsigned long long* status, cudaStream_t st);
+cudaError_t launch_status_finish(const unsigned long long* status, void* info, cudaStream_t st);
+cudaError_t launch_fill_i32(int* p, int64_t count, int value, cudaStream_t st);
+
+}  // namespace rlhc

@@ -1,0 +1,433 @@
+// rlhc.cu -- the C ABI (include/rlhc.h): argument checks, workspace carving and the
+// stream-ordered pipelines of SLHC3 and SSLHC3.  No host
+// synchronisation and no allocation inside a call; every stage is a kernel of this
+// library (tslu.cu, rows.cu, sketch.cu, small.cu).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace rlhc;
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                         \
+  do {                                                                      \
+    cudaError_t e_ = (x);                                                   \
+    if (e_ != cudaSuccess) {                                                \
+      g_last_error = std::string(#x) + ": " + cudaGetErrorString(e_);       \
+      return RLHC_ECUDA;                                                    \
+    }                                                                       \
+  } while (0)
+
+namespace {
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int kernel_width(int panel) { return panel <= 16 ? 16 : (panel <= 32 ? 32 : 64); }
+
+bool cfg_ok(const rlhc_tslu_cfg& c, int64_t n) {
+  if (c.panel < 1 || c.panel > 64 || c.panel > n) return false;
+  int W = kernel_width(c.panel);
+  if (c.leaf_rows != select_rows(W)) return false;
+  if (c.arity < 2 || (int64_t)c.arity * c.panel > select_rows(W)) return false;
+  return true;
+}
+
+struct Carver {
+  char* p;
+  size_t used = 0;
+  explicit Carver(void* base) : p((char*)base) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* r = (T*)(p ? p + used : nullptr);
+    used += al(count * sizeof(T));
+    return r;
+  }
+};
+
+struct TsluWs {
+  unsigned long long* status;
+  uint8_t* chosen;
+  int* ids[2];
+  int* cnt[2];
+  double* vals[2];
+  double* rd;
+  double* Xp;
+};
+
+void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, TsluWs& t) {
+  int W = kernel_width(cfg.panel);
+  int64_t nleaves = ceil_div<int64_t>(rows, cfg.leaf_rows);
+  for (int b = 0; b < 2; b++) {
+    t.ids[b] = c.take<int>((size_t)nleaves * W);
+    t.cnt[b] = c.take<int>((size_t)nleaves);
+    t.vals[b] = c.take<double>((size_t)nleaves * W * W);
+  }
+  t.chosen = c.take<uint8_t>((size_t)rows);
+  t.rd = c.take<double>((size_t)n);
+  t.Xp = c.take<double>((size_t)n * n);
+}
+
+// PX = LU on rows x n (global ids row0..): piv, U, L11; the trailing matrix of later
+// panels lives in `tw` (rows x n, ldt).  Returns RLHC_OK or RLHC_ECUDA.
+int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg& cfg,
+             TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st) {
+  const int W = kernel_width(cfg.panel);
+  const int nleaves = (int)ceil_div<int64_t>(rows, cfg.leaf_rows);
+  const bool panels = cfg.panel < n;
+  if (panels) CUDA_TRY(cudaMemsetAsync(t.chosen, 0, (size_t)rows, st));
+  CUDA_TRY(cudaMemsetAsync(U, 0, (size_t)n * n * sizeof(double), st));  // strict lower part of U is 0
+  for (int64_t p0 = 0; p0 < n; p0 += cfg.panel) {
+    const int w = (int)std::min<int64_t>(cfg.panel, n - p0);
+    const double* src = (p0 == 0) ? X : tw;
+    const int64_t lds = (p0 == 0) ? ldx : ldtw;
+    CUDA_TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
+                              t.cnt[0], t.vals[0], st));
+    int cur = 0, nslots = nleaves;
+    while (nslots > 1) {
+      CUDA_TRY(launch_tslu_node(W, t.ids[cur], t.cnt[cur], t.vals[cur], nslots, cfg.arity, w, t.ids[cur ^ 1],
+                                t.cnt[cur ^ 1], t.vals[cur ^ 1], st));
+      nslots = (int)ceil_div<int64_t>(nslots, cfg.arity);
+      cur ^= 1;
+    }
+    CUDA_TRY(launch_tslu_panel_factor(src, lds, rows, row0, (int)p0, w, (int)n, t.ids[cur], t.cnt[cur], U, piv,
+                                      panels ? t.chosen : nullptr, nullptr, t.status, st));
+    CUDA_TRY(launch_rdiag(U + p0 * n + p0, w, n + 0, t.rd + p0, RLHC_STAGE_LU, t.status, st));
+    if (p0 + w < n) {
+      // eliminate every row with this panel's pivots: multipliers (substitution over
+      // the panel) and the fma-chain update of the trailing columns
+      CUDA_TRY(launch_trsm_rows(src + p0, lds, rows, (int)(n - p0), w, U + p0 * n + p0, n, t.rd + p0, tw + p0, ldtw,
+                                nullptr, nullptr, 0, st));
+    }
+  }
+  // L11: the pivot rows' X rows run through the same substitution, unit diagonal
+  CUDA_TRY(launch_gather_rows(X, ldx, piv, row0, (int)n, (int)n, t.Xp, n, st));
+  CUDA_TRY(launch_trsm_rows(t.Xp, n, n, (int)n, (int)n, U, n, t.rd, L11, n, nullptr, nullptr, 0, st));
+  CUDA_TRY(launch_l11_fixup(L11, (int)n, st));
+  return RLHC_OK;
+}
+
+struct AlgoWs {
+  TsluWs t;
+  int* pivpos;
+  double *U, *L11, *S, *Y, *G, *D, *Di, *J, *Ji, *N, *rdY;
+  double *Lt, *Ls, *part, *work;
+  void* plan;
+};
+
+void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg& cfg,
+                AlgoWs& a) {
+  a.t.status = c.take<unsigned long long>(4);
+  carve_tslu(c, m, n, cfg, a.t);
+  a.pivpos = c.take<int>((size_t)m);
+  double** sq[] = {&a.U, &a.L11, &a.S, &a.Y, &a.G, &a.D, &a.Di, &a.J, &a.Ji, &a.N};
+  for (double** q : sq) *q = c.take<double>((size_t)n * n);
+  a.rdY = c.take<double>((size_t)n);
+  const int64_t srows = algo == RLHC_SLHC3 ? s_or_s1 : s2;
+  a.Ls = c.take<double>((size_t)srows * n);
+  a.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
+  size_t part = gram_partials_bytes(m, (int)n);
+  part = std::max(part, algo == RLHC_SLHC3 ? gauss_partials_bytes(m, (int)n, (int)s_or_s1)
+                                           : gauss_partials_bytes(s_or_s1, (int)n, (int)s2));
+  a.part = c.take<double>(part / sizeof(double) + 1);
+  size_t work = std::max(hqr_ws_bytes((int)srows, (int)n), (size_t)n * n * sizeof(double));
+  a.work = c.take<double>(work / sizeof(double) + 1);
+  a.plan = algo == RLHC_SSLHC3 ? (void*)c.take<char>(cs_plan_bytes(m, (int)s_or_s1)) : nullptr;
+}
+
+int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s_or_s1, int64_t s2, uint64_t seed,
+             const rlhc_tslu_cfg& cfg, double* Q, int64_t ldq, double* R, int64_t* piv, AlgoWs& a, rlhc_info_t* info,
+             cudaStream_t st) {
+  const int ni = (int)n;
+  unsigned long long* status = a.t.status;
+  CUDA_TRY(launch_status_init(status, st));
+  CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
+  // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
+  int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st);
+  if (rc) return rc;
+  CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
+  CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+  // L in original row order (R#2), into the Q buffer
+  CUDA_TRY(launch_trsm_rows(X, ldx, m, ni, ni, a.U, n, a.t.rd, Q, ldq, a.pivpos, a.L11, n, st));
+  int64_t srows;
+  if (algo == RLHC_SLHC3) {  // L_s = Omega L
+    srows = s_or_s1;
+    CUDA_TRY(launch_sketch_gauss(Q, ldq, m, ni, 0, (int)srows, seed, 0u, a.part, a.Ls, st));
+  } else {                   // L_t = Omega_1 L, L_ss = Omega_2 L_t
+    srows = s2;
+    CUDA_TRY(launch_sketch_count(Q, ldq, m, ni, 0, (int)s_or_s1, seed, a.plan, a.Lt, nullptr, nullptr, st));
+    CUDA_TRY(launch_sketch_gauss(a.Lt, n, s_or_s1, ni, 0, (int)s2, seed, 1u, a.part, a.Ls, st));
+  }
+  // [H, S] = HouseholderQR(L_s), sign(S_kk) = sign(U_kk) (R#7); Y = S U
+  CUDA_TRY(launch_hqr(a.Ls, (int)srows, ni, n, a.U, a.S, a.work, status, st));
+  CUDA_TRY(launch_trmm_uu(a.S, a.U, ni, a.Y, st));
+  // W = X Y^{-1} by substitution
+  CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
+  CUDA_TRY(launch_trsm_rows(X, ldx, m, ni, ni, a.Y, n, a.rdY, Q, ldq, nullptr, nullptr, 0, st));
+  // CholeskyQR2(W): D = chol(W^T W), V = W D^{-1}, J = chol(V^T V), Q = V J^{-1}
+  CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
+  CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st));
+  CUDA_TRY(launch_tri_inv(a.D, ni, a.Di, st));
+  CUDA_TRY(launch_rows_upper(Q, ldq, m, ni, a.Di, Q, ldq, st));
+  CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
+  CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st));
+  CUDA_TRY(launch_tri_inv(a.J, ni, a.Ji, st));
+  CUDA_TRY(launch_rows_upper(Q, ldq, m, ni, a.Ji, Q, ldq, st));
+  // R = Z Y = J (D Y)
+  CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, a.N, st));
+  CUDA_TRY(launch_trmm_uu(a.J, a.N, ni, R, st));
+  CUDA_TRY(launch_status_finish(status, info, st));
+  return RLHC_OK;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + nb && pb < pa + na;
+}
+
+int check_common(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R, int64_t* piv,
+                 void* ws, rlhc_info_t* info) {
+  if (!X || !Q || !R || !piv || !ws || !info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (n < 1 || m < n) return fail(RLHC_EINVAL, "need m >= n >= 1");
+  if (m > 0x7fffffffLL) return fail(RLHC_EINVAL, "m must be < 2^31 (int32 row ids)");
+  if (ldx < n || ldq < n) return fail(RLHC_EINVAL, "leading dimension < n");
+  if (((uintptr_t)ws) & 255) return fail(RLHC_EINVAL, "workspace must be 256-byte aligned");
+  if (overlaps(X, (size_t)((m - 1) * ldx + n) * 8, Q, (size_t)((m - 1) * ldq + n) * 8))
+    return fail(RLHC_EINVAL, "Q overlaps X");
+  return RLHC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void rlhc_default_tslu_cfg(int64_t m, int64_t n, rlhc_tslu_cfg* cfg) {
+  (void)m;
+  if (!cfg) return;
+  int panel = (int)std::min<int64_t>(std::max<int64_t>(n, 1), 64);
+  int W = kernel_width(panel);
+  cfg->panel = panel;
+  cfg->leaf_rows = select_rows(W);
+  cfg->arity = std::max(2, select_rows(W) / panel);
+}
+
+size_t rlhc_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg* cfgp) {
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
+  if (n < 1 || m < n || !cfg_ok(cfg, n)) return 0;
+  if (algo == RLHC_SLHC3 && (s_or_s1 < n || s_or_s1 > m)) return 0;
+  if (algo == RLHC_SSLHC3 && (s2 < n || s_or_s1 < s2 || s_or_s1 > m)) return 0;
+  if (algo != RLHC_SLHC3 && algo != RLHC_SSLHC3) return 0;
+  Carver c(nullptr);
+  AlgoWs a;
+  carve_algo(c, algo, m, n, s_or_s1, s2, cfg, a);
+  return c.used;
+}
+
+static int algo_entry(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s_or_s1, int64_t s2,
+                      uint64_t seed, const rlhc_tslu_cfg* cfgp, double* Q, int64_t ldq, double* R, int64_t* piv,
+                      void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  int rc = check_common(X, m, n, ldx, Q, ldq, R, piv, ws, info);
+  if (rc) return rc;
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
+  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
+  if (algo == RLHC_SLHC3 && (s_or_s1 < n || s_or_s1 > m)) return fail(RLHC_EINVAL, "need n <= s <= m");
+  if (algo == RLHC_SSLHC3 && (s2 < n || s_or_s1 < s2 || s_or_s1 > m))
+    return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
+  size_t need = rlhc_workspace_size(algo, m, n, s_or_s1, s2, &cfg);
+  if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
+  Carver c(ws);
+  AlgoWs a;
+  carve_algo(c, algo, m, n, s_or_s1, s2, cfg, a);
+  return run_algo(algo, X, m, n, ldx, s_or_s1, s2, seed, cfg, Q, ldq, R, piv, a, info, (cudaStream_t)stream);
+}
+
+int rlhc_slhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s, uint64_t seed, const rlhc_tslu_cfg* cfg,
+               double* Q, int64_t ldq, double* R, int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info,
+               rlhc_stream_t stream) {
+  return algo_entry(RLHC_SLHC3, X, m, n, ldx, s, 0, seed, cfg, Q, ldq, R, piv, ws, ws_bytes, info, stream);
+}
+
+int rlhc_sslhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed,
+                const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq, double* R, int64_t* piv, void* ws, size_t ws_bytes,
+                rlhc_info_t* info, rlhc_stream_t stream) {
+  return algo_entry(RLHC_SSLHC3, X, m, n, ldx, s1, s2, seed, cfg, Q, ldq, R, piv, ws, ws_bytes, info, stream);
+}
+
+// ---------------------------------------------------------------- per-stage
+static size_t getrf_carve(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, TsluWs& t, double** tw,
+                          int** pivpos) {
+  t.status = c.take<unsigned long long>(4);
+  carve_tslu(c, rows, n, cfg, t);
+  *tw = cfg.panel < n ? c.take<double>((size_t)rows * n) : nullptr;
+  *pivpos = c.take<int>((size_t)rows);
+  return c.used;
+}
+
+size_t rlhc_getrf_ts_workspace_size(int64_t rows, int64_t n, const rlhc_tslu_cfg* cfgp) {
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(rows, n, &cfg);
+  if (n < 1 || rows < n || !cfg_ok(cfg, n)) return 0;
+  Carver c(nullptr);
+  TsluWs t;
+  double* tw;
+  int* pp;
+  return getrf_carve(c, rows, n, cfg, t, &tw, &pp);
+}
+
+int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg* cfgp,
+                  int64_t* piv, double* U, double* L11, double* L, int64_t ldl, void* ws, size_t ws_bytes,
+                  rlhc_info_t* info, rlhc_stream_t stream) {
+  if (!X || !piv || !U || !L11 || !ws || !info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (n < 1 || rows < n || ldx < n || (L && ldl < n)) return fail(RLHC_EINVAL, "bad sizes");
+  if (row0 != 0) return fail(RLHC_EINVAL, "row0 must be 0 for the single-device entry point");
+  if (rows > 0x7fffffffLL) return fail(RLHC_EINVAL, "rows must be < 2^31");
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(rows, n, &cfg);
+  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration");
+  size_t need = rlhc_getrf_ts_workspace_size(rows, n, &cfg);
+  if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
+  Carver c(ws);
+  TsluWs t;
+  double* tw;
+  int* pivpos;
+  getrf_carve(c, rows, n, cfg, t, &tw, &pivpos);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(launch_status_init(t.status, st));
+  CUDA_TRY(launch_check_finite(X, rows, (int)n, ldx, t.status, st));
+  int rc = run_tslu(X, rows, n, ldx, row0, cfg, t, tw, n, piv, U, L11, st);
+  if (rc) return rc;
+  if (L) {
+    CUDA_TRY(launch_fill_i32(pivpos, rows, -1, st));
+    CUDA_TRY(launch_pivpos(piv, (int)n, row0, rows, pivpos, st));
+    CUDA_TRY(launch_trsm_rows(X, ldx, rows, (int)n, (int)n, U, n, t.rd, L, ldl, pivpos, L11, n, st));
+  }
+  CUDA_TRY(launch_status_finish(t.status, info, st));
+  return RLHC_OK;
+}
+
+size_t rlhc_sketch_gauss_workspace_size(int64_t rows, int64_t n, int64_t s) {
+  if (rows < 1 || n < 1 || s < 1) return 0;
+  return al(gauss_partials_bytes(rows, (int)n, (int)s));
+}
+
+int rlhc_sketch_gauss(const double* A, int64_t rows, int64_t n, int64_t lda, int64_t row0, int64_t s, uint64_t seed,
+                      uint32_t stream_id, double* out, void* ws, size_t ws_bytes, rlhc_stream_t stream) {
+  if (!A || !out || !ws) return fail(RLHC_EINVAL, "null pointer argument");
+  if (rows < 1 || n < 1 || s < 1 || lda < n || row0 < 0) return fail(RLHC_EINVAL, "bad sizes");
+  if (ws_bytes < rlhc_sketch_gauss_workspace_size(rows, n, s)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  CUDA_TRY(launch_sketch_gauss(A, lda, rows, (int)n, row0, (int)s, seed, stream_id, (double*)ws, out,
+                               (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+size_t rlhc_sketch_count_workspace_size(int64_t rows, int64_t n, int64_t s1) {
+  if (rows < 1 || n < 1 || s1 < 1) return 0;
+  return al(cs_plan_bytes(rows, (int)s1));
+}
+
+int rlhc_sketch_count(const double* A, int64_t rows, int64_t n, int64_t lda, int64_t row0, int64_t s1, uint64_t seed,
+                      double* out, int32_t* bucket, int8_t* sign, void* ws, size_t ws_bytes, rlhc_stream_t stream) {
+  if (!A || !out || !ws) return fail(RLHC_EINVAL, "null pointer argument");
+  if (rows < 1 || n < 1 || s1 < 1 || lda < n || row0 < 0 || rows > 0x7fffffffLL || s1 > 65536)
+    return fail(RLHC_EINVAL, "bad sizes");
+  if (ws_bytes < rlhc_sketch_count_workspace_size(rows, n, s1)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  CUDA_TRY(launch_sketch_count(A, lda, rows, (int)n, row0, (int)s1, seed, ws, out, bucket, sign, (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+size_t rlhc_gram_workspace_size(int64_t rows, int64_t n) {
+  if (rows < 1 || n < 1) return 0;
+  return al(gram_partials_bytes(rows, (int)n));
+}
+
+int rlhc_gram(const double* A, int64_t rows, int64_t n, int64_t lda, double* G, void* ws, size_t ws_bytes,
+              rlhc_stream_t stream) {
+  if (!A || !G || !ws) return fail(RLHC_EINVAL, "null pointer argument");
+  if (rows < 1 || n < 1 || lda < n) return fail(RLHC_EINVAL, "bad sizes");
+  if (ws_bytes < rlhc_gram_workspace_size(rows, n)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  CUDA_TRY(launch_gram(A, lda, rows, (int)n, (double*)ws, G, (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+size_t rlhc_trsm_apply_workspace_size(int64_t rows, int64_t n) {
+  if (rows < 1 || n < 1) return 0;
+  return al(256) + al((size_t)n * 8) + al((size_t)n * n * 8) + al(gram_partials_bytes(rows, (int)n));
+}
+
+int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int mode, double* out,
+                    int64_t ldo, double* G_out, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  if (!A || !T || !out || !ws || !info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (rows < 1 || n < 1 || lda < n || ldo < n) return fail(RLHC_EINVAL, "bad sizes");
+  if (mode != RLHC_SUBST && mode != RLHC_INV_GEMM) return fail(RLHC_EINVAL, "bad mode");
+  if (out != A && overlaps(A, (size_t)((rows - 1) * lda + n) * 8, out, (size_t)((rows - 1) * ldo + n) * 8))
+    return fail(RLHC_EINVAL, "out partially overlaps A");
+  if (out == A && lda != ldo) return fail(RLHC_EINVAL, "in place needs lda == ldo");
+  if (ws_bytes < rlhc_trsm_apply_workspace_size(rows, n)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  Carver c(ws);
+  unsigned long long* status = c.take<unsigned long long>(4);
+  double* rd = c.take<double>((size_t)n);
+  double* Ti = c.take<double>((size_t)n * n);
+  double* part = c.take<double>(gram_partials_bytes(rows, (int)n) / 8 + 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(launch_status_init(status, st));
+  CUDA_TRY(launch_rdiag(T, (int)n, n, rd, RLHC_STAGE_SOLVE_Y, status, st));
+  if (mode == RLHC_SUBST) {
+    CUDA_TRY(launch_trsm_rows(A, lda, rows, (int)n, (int)n, T, n, rd, out, ldo, nullptr, nullptr, 0, st));
+  } else {
+    CUDA_TRY(launch_tri_inv(T, (int)n, Ti, st));
+    CUDA_TRY(launch_rows_upper(A, lda, rows, (int)n, Ti, out, ldo, st));
+  }
+  if (G_out) CUDA_TRY(launch_gram(out, ldo, rows, (int)n, part, G_out, st));
+  CUDA_TRY(launch_status_finish(status, info, st));
+  return RLHC_OK;
+}
+
+size_t rlhc_hqr_workspace_size(int64_t s, int64_t n) {
+  if (s < n || n < 1) return 0;
+  return al(256) + al(hqr_ws_bytes((int)s, (int)n));
+}
+
+int rlhc_hqr_r(const double* A, int64_t s, int64_t n, int64_t lda, const double* sgn_ref, double* S, void* ws,
+               size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  if (!A || !S || !ws || !info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (n < 1 || s < n || lda < n) return fail(RLHC_EINVAL, "bad sizes");
+  if (ws_bytes < rlhc_hqr_workspace_size(s, n)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  Carver c(ws);
+  unsigned long long* status = c.take<unsigned long long>(4);
+  double* work = c.take<double>(hqr_ws_bytes((int)s, (int)n) / 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(launch_status_init(status, st));
+  CUDA_TRY(launch_hqr(A, (int)s, (int)n, lda, sgn_ref, S, work, status, st));
+  CUDA_TRY(launch_status_finish(status, info, st));
+  return RLHC_OK;
+}
+
+int rlhc_cholesky(const double* G, int64_t n, double* Rout, int stage, rlhc_info_t* info, rlhc_stream_t stream) {
+  if (!G || !Rout || !info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (n < 1 || n > 4096) return fail(RLHC_EINVAL, "bad size");
+  // status and working copy live in the caller's info / output buffers: the status
+  // word is kept in info->index's storage until the final decode
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* status = (unsigned long long*)&info->index;
+  CUDA_TRY(launch_status_init(status, st));
+  size_t need = (size_t)n * n * sizeof(double);
+  if (need > 200 * 1024) return fail(RLHC_EINVAL, "rlhc_cholesky entry point supports n <= 160");
+  CUDA_TRY(launch_chol(G, (int)n, Rout, nullptr, stage, status, st));
+  CUDA_TRY(launch_status_finish(status, info, st));
+  return RLHC_OK;
+}
+
+const char* rlhc_version(void) { return "rlhc-b200 0.1 (sm_100a, fp64 DMMA)"; }
+const char* rlhc_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

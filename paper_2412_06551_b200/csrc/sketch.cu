@@ -1,0 +1,300 @@
+// sketch.cu -- the sketches of the L factor ("L_s = Omega L",
+// P:294 "L_ss = Omega_2 Omega_1 L"):
+//   * Gaussian: out = Omega A with Omega generated in-kernel from Philox (never
+//     stored), contracted on the FP64 tensor cores (DMMA), split over rows with a
+//     fixed-order reduction of the partial tiles;
+//   * CountSketch: deterministic bucket gather -- rows are stably sorted by bucket
+//     (counting sort on the Philox hash) and each bucket is summed in ascending row
+//     order, so the result is bitwise reproducible without floating atomics.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rlhc {
+
+// ------------------------------------------------------------------ Gaussian
+constexpr int ST = 64;   // output tile (sketch rows) x (columns)
+constexpr int SK = 32;   // rows of A per chunk
+
+struct GaussGeom {
+  int ti, tj, nsplit;
+  int64_t rows_per_split;
+};
+static GaussGeom gauss_geom(int64_t rows, int n, int s) {
+  GaussGeom g;
+  g.ti = ceil_div(s, ST);
+  g.tj = ceil_div(n, ST);
+  int tiles = g.ti * g.tj;
+  int64_t want = std::max<int64_t>(1, (2 * kSMs + tiles - 1) / tiles);
+  int64_t maxs = std::max<int64_t>(1, rows / 128);
+  g.nsplit = (int)std::min<int64_t>(want, maxs);
+  g.rows_per_split = ceil_div<int64_t>(ceil_div<int64_t>(rows, g.nsplit), SK) * SK;
+  g.nsplit = (int)std::max<int64_t>(1, ceil_div<int64_t>(rows, g.rows_per_split));
+  return g;
+}
+size_t gauss_partials_bytes(int64_t rows, int n, int s) {
+  GaussGeom g = gauss_geom(rows, n, s);
+  return (size_t)g.nsplit * g.ti * g.tj * ST * ST * sizeof(double);
+}
+
+__global__ void __launch_bounds__(128)
+gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
+                    uint64_t seed, uint32_t stream_id, int64_t rows_per_split, double* __restrict__ part) {
+  __shared__ double Om[ST][SK + 1];
+  __shared__ double At[SK][ST + 4];
+  const int tile_i = blockIdx.x / ((n + ST - 1) / ST), tile_j = blockIdx.x % ((n + ST - 1) / ST);
+  const int i0 = tile_i * ST, j0 = tile_j * ST;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = std::min<int64_t>(rows, r0 + rows_per_split);
+  const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)s));
+  const int lane = lane_id(), w = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int wi = (w >> 1) * 32, wj = (w & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = r0; k0 < r1; k0 += SK) {
+    // Omega tile: rows i0..i0+63 (pairs i, i+1 share one Philox block), columns k0..k0+31
+    for (int idx = threadIdx.x; idx < (ST / 2) * SK; idx += blockDim.x) {
+      int ip = idx / SK, kk = idx - ip * SK;
+      int i = i0 + 2 * ip;
+      int64_t gr = k0 + kk;
+      double z0 = 0.0, z1 = 0.0;
+      if (gr < r1 && i < s) {
+        gauss_pair(seed, (uint64_t)(row0 + gr), (uint32_t)(i >> 1), stream_id, &z0, &z1);
+        z0 = __dmul_rn(z0, scale);
+        z1 = (i + 1 < s) ? __dmul_rn(z1, scale) : 0.0;
+      }
+      Om[2 * ip][kk] = z0;
+      Om[2 * ip + 1][kk] = z1;
+    }
+    for (int idx = threadIdx.x; idx < SK * ST; idx += blockDim.x) {
+      int kk = idx / ST, c = idx - kk * ST;
+      int64_t gr = k0 + kk;
+      At[kk][c] = (gr < r1 && j0 + c < n) ? A[gr * lda + j0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) af[a] = Om[wi + a * 8 + g][kk + t];
+#pragma unroll
+      for (int b = 0; b < 4; b++) bf[b] = At[kk + t][wj + b * 8 + g];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+  double* P = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * ST * ST;
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      int r = wi + a * 8 + g, c = wj + b * 8 + 2 * t;
+      P[r * ST + c] = acc[a][b][0];
+      P[r * ST + c + 1] = acc[a][b][1];
+    }
+}
+
+__global__ void gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int tjn, int n, int s,
+                                    double* __restrict__ out) {
+  const int64_t total = (int64_t)s * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    int tile = (i / ST) * tjn + j / ST;
+    int r = i % ST, c = j % ST;
+    double acc = 0.0;
+    for (int p = 0; p < nsplit; p++) acc += part[((size_t)p * ntiles + tile) * ST * ST + r * ST + c];
+    out[e] = acc;
+  }
+}
+
+cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s, uint64_t seed,
+                                uint32_t stream_id, double* part, double* out, cudaStream_t st) {
+  GaussGeom gg = gauss_geom(rows, n, s);
+  dim3 grid(gg.ti * gg.tj, gg.nsplit);
+  gauss_sketch_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  int64_t total = (int64_t)s * n;
+  gauss_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 2048), 256, 0, st>>>(
+      part, gg.nsplit, gg.ti * gg.tj, gg.tj, n, s, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ CountSketch
+// plan: bucket[r], sign[r] (Philox stream 2), per-chunk histograms, bucket offsets,
+// stable scatter of row ids into perm (ascending row id inside each bucket).
+constexpr int CS_CHUNK = 8192;
+
+struct CsPlan {
+  int32_t* bucket;  // rows
+  int8_t* sign;     // rows
+  int32_t* perm;    // rows
+  int32_t* hist;    // nchunks * s1 (becomes per-(chunk,bucket) base offsets)
+  int32_t* start;   // s1 + 1
+};
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+static CsPlan carve_plan(void* ws, int64_t rows, int s1) {
+  char* p = (char*)ws;
+  CsPlan pl;
+  int64_t nch = ceil_div<int64_t>(rows, CS_CHUNK);
+  pl.bucket = (int32_t*)p; p += align256(rows * 4);
+  pl.sign = (int8_t*)p; p += align256(rows);
+  pl.perm = (int32_t*)p; p += align256(rows * 4);
+  pl.hist = (int32_t*)p; p += align256((size_t)nch * s1 * 4);
+  pl.start = (int32_t*)p; p += align256((size_t)(s1 + 1) * 4);
+  return pl;
+}
+size_t cs_plan_bytes(int64_t rows, int s1) {
+  int64_t nch = ceil_div<int64_t>(rows, CS_CHUNK);
+  return align256(rows * 4) + align256(rows) + align256(rows * 4) + align256((size_t)nch * s1 * 4) +
+         align256((size_t)(s1 + 1) * 4);
+}
+
+__global__ void cs_hash_hist_kernel(int64_t rows, int64_t row0, int s1, uint64_t seed, int32_t* __restrict__ bucket,
+                                    int8_t* __restrict__ sign, int32_t* __restrict__ hist) {
+  extern __shared__ int h[];
+  for (int b = threadIdx.x; b < s1; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t c0 = (int64_t)blockIdx.x * CS_CHUNK;
+  for (int64_t r = c0 + threadIdx.x; r < std::min<int64_t>(rows, c0 + CS_CHUNK); r += blockDim.x) {
+    int b, sg;
+    cs_hash(seed, (uint64_t)(row0 + r), (uint32_t)s1, &b, &sg);
+    bucket[r] = b;
+    sign[r] = (int8_t)sg;
+    atomicAdd(&h[b], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < s1; b += blockDim.x) hist[(int64_t)blockIdx.x * s1 + b] = h[b];
+}
+
+// per bucket: running sum over chunks -> per-(chunk, bucket) offset relative to the bucket start
+__global__ void cs_bucket_totals_kernel(int nch, int s1, int32_t* __restrict__ hist, int32_t* __restrict__ start) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= s1) return;
+  int run = 0;
+  for (int c = 0; c < nch; c++) {
+    int v = hist[(int64_t)c * s1 + b];
+    hist[(int64_t)c * s1 + b] = run;
+    run += v;
+  }
+  start[b + 1] = run;  // totals; scanned below
+}
+
+__global__ void cs_scan_kernel(int s1, int32_t* __restrict__ start) {
+  // single CTA exclusive scan of totals in start[1..s1] -> start[0..s1]
+  __shared__ int part[1024];
+  const int per = ceil_div(s1, (int)blockDim.x);
+  int b0 = threadIdx.x * per, b1 = min(s1, b0 + per);
+  int sum = 0;
+  for (int b = b0; b < b1; b++) sum += start[b + 1];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int q = 0; q < (int)blockDim.x; q++) { int v = part[q]; part[q] = run; run += v; }
+  }
+  __syncthreads();
+  int run = part[threadIdx.x];
+  // totals are overwritten in place with inclusive prefixes: start[b] = offset of bucket b
+  for (int b = b0; b < b1; b++) { run += start[b + 1]; start[b + 1] = run; }
+  __syncthreads();
+  if (threadIdx.x == 0) start[0] = 0;
+}
+
+// one warp per chunk, 32 rows at a time in ascending order: stable ranks via match_any
+__global__ void cs_scatter_kernel(int64_t rows, int s1, const int32_t* __restrict__ bucket,
+                                  const int32_t* __restrict__ hist, const int32_t* __restrict__ start,
+                                  int32_t* __restrict__ perm) {
+  extern __shared__ int cnt[];
+  const int lane = threadIdx.x;
+  for (int b = lane; b < s1; b += 32) cnt[b] = hist[(int64_t)blockIdx.x * s1 + b] + start[b];
+  __syncwarp();
+  const int64_t c0 = (int64_t)blockIdx.x * CS_CHUNK, c1 = std::min<int64_t>(rows, c0 + CS_CHUNK);
+  for (int64_t base = c0; base < c1; base += 32) {
+    int64_t r = base + lane;
+    bool ok = r < c1;
+    int b = ok ? bucket[r] : -1 - lane;
+    unsigned mask = __match_any_sync(0xffffffffu, b);
+    int rank = __popc(mask & ((1u << lane) - 1));
+    int pos = ok ? cnt[b] + rank : 0;
+    __syncwarp();
+    if (ok) {
+      perm[pos] = (int32_t)r;
+      if (rank == 0) cnt[b] += __popc(mask);
+    }
+    __syncwarp();
+  }
+}
+
+// out[b, :] = sum over the bucket's rows (ascending) of sign * A[row, :]: one warp per
+// bucket, lanes over columns, 4-row prefetch.
+__global__ void cs_apply_kernel(const double* __restrict__ A, int64_t lda, int n, int s1,
+                                const int32_t* __restrict__ perm, const int32_t* __restrict__ start,
+                                const int8_t* __restrict__ sign, double* __restrict__ out) {
+  const int wpb = blockDim.x >> 5;
+  const int b = blockIdx.x * wpb + warp_id();
+  if (b >= s1) return;
+  const int lane = lane_id();
+  const int p0 = start[b], p1 = start[b + 1];
+  for (int c0 = 0; c0 < n; c0 += 32 * 8) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) acc[q] = 0.0;
+    for (int p = p0; p < p1; p++) {
+      int r = perm[p];
+      const double* row = A + (int64_t)r * lda;
+      bool neg = sign[r] < 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        int c = c0 + q * 32 + lane;
+        if (c < n) {
+          double v = row[c];
+          acc[q] = neg ? __dadd_rn(acc[q], -v) : __dadd_rn(acc[q], v);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      int c = c0 + q * 32 + lane;
+      if (c < n) out[(int64_t)b * n + c] = acc[q];
+    }
+  }
+}
+
+__global__ void copy_i32_kernel(const int32_t* a, int32_t* b, int64_t cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+__global__ void copy_i8_kernel(const int8_t* a, int8_t* b, int64_t cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s1,
+                                uint64_t seed, void* plan_ws, double* out, int32_t* bucket_out, int8_t* sign_out,
+                                cudaStream_t st) {
+  CsPlan pl = carve_plan(plan_ws, rows, s1);
+  int nch = (int)ceil_div<int64_t>(rows, CS_CHUNK);
+  size_t hsm = (size_t)s1 * sizeof(int);
+  cudaError_t e;
+  if (hsm > 48 * 1024) {
+    e = cudaFuncSetAttribute(cs_hash_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    if (e) return e;
+    e = cudaFuncSetAttribute(cs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    if (e) return e;
+  }
+  cs_hash_hist_kernel<<<nch, 256, hsm, st>>>(rows, row0, s1, seed, pl.bucket, pl.sign, pl.hist);
+  cs_bucket_totals_kernel<<<ceil_div(s1, 256), 256, 0, st>>>(nch, s1, pl.hist, pl.start);
+  cs_scan_kernel<<<1, 1024, 0, st>>>(s1, pl.start);
+  cs_scatter_kernel<<<nch, 32, hsm, st>>>(rows, s1, pl.bucket, pl.hist, pl.start, pl.perm);
+  cs_apply_kernel<<<ceil_div(s1, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start, pl.sign, out);
+  if (bucket_out) copy_i32_kernel<<<256, 256, 0, st>>>(pl.bucket, bucket_out, rows);
+  if (sign_out) copy_i8_kernel<<<256, 256, 0, st>>>(pl.sign, sign_out, rows);
+  return cudaGetLastError();
+}
+
+}  // namespace rlhc

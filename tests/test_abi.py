@@ -1,0 +1,78 @@
+"""CPU-side checks of the C ABI: the library builds for sm_100a, loads, exports every
+symbol include/rlhc.h declares, and rejects invalid arguments on the host (no device
+calls -- this container has no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rlhc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rlhc_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2412_06551_b200 import _lib
+    return _lib.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    from paper_2412_06551_b200 import _lib
+    names = _declared()
+    assert "rlhc_slhc3" in names and "rlhc_sslhc3" in names and "rlhc_getrf_ts" in names
+    for nm in names:
+        assert hasattr(L, nm), nm
+    assert sorted(_lib.EXPORTED) == names
+
+
+def test_sm100a_cubin(L):
+    import subprocess
+    from paper_2412_06551_b200 import _lib
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "DMMA" in sass  # FP64 tensor-core path present
+
+
+def test_default_cfg_and_workspace(L):
+    from paper_2412_06551_b200 import _lib
+    c = _lib.TsluCfg()
+    for (m, n, exp) in [(2048, 16, (512, 32, 16)), (65536, 64, (256, 4, 64)), (1 << 20, 128, (256, 4, 64)),
+                        (262144, 512, (256, 4, 64)), (1000, 40, (256, 6, 40))]:
+        L.rlhc_default_tslu_cfg(m, n, ctypes.byref(c))
+        assert c.as_tuple() == exp, (m, n, c.as_tuple())
+    assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, None) > 0
+    assert L.rlhc_workspace_size(1, 1 << 20, 128, 1024, 256, None) > 0
+    assert L.rlhc_workspace_size(0, 65536, 64, 32, 0, None) == 0        # s < n
+    assert L.rlhc_workspace_size(1, 65536, 64, 128, 256, None) == 0     # s2 > s1
+    bad = _lib.TsluCfg(100, 4, 64)
+    assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(bad)) == 0
+
+
+def test_host_argument_errors(L):
+    from paper_2412_06551_b200 import _lib
+    info = ctypes.c_void_p(0x1000)
+    fake = ctypes.c_void_p(0x10000)
+    # null X
+    rc = L.rlhc_slhc3(None, 100, 4, 4, 8, 0, None, fake, 4, fake, fake, fake, 1 << 20, info, None)
+    assert rc == _lib.RLHC_EINVAL
+    # m < n
+    rc = L.rlhc_slhc3(fake, 3, 4, 4, 8, 0, None, ctypes.c_void_p(0x900000), 4, fake, fake, fake, 1 << 20, info, None)
+    assert rc == _lib.RLHC_EINVAL
+    # Q overlapping X
+    rc = L.rlhc_slhc3(fake, 100, 4, 4, 8, 0, None, ctypes.c_void_p(0x10000 + 64), 4, fake, fake,
+                      ctypes.c_void_p(0x100000), 1 << 24, info, None)
+    assert rc == _lib.RLHC_EINVAL
+    assert b"overlap" in L.rlhc_last_error()
+    # workspace too small
+    rc = L.rlhc_slhc3(fake, 100, 4, 4, 8, 0, None, ctypes.c_void_p(0x900000), 4, fake, fake,
+                      ctypes.c_void_p(0x100000), 16, info, None)
+    assert rc == _lib.RLHC_EWORKSPACE
+    assert L.rlhc_version().startswith(b"rlhc-b200")

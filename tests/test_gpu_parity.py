@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bit-exact for integer/index work and for the quantities whose
+arithmetic the contract fixes (Omega, CountSketch hash and sums, pivots, U, L11, L);
+within the BASELINE.json tolerances for Q and R."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from conftest import orth_err, qr_signed, rel_fro, rel_residual
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def rl():
+    import paper_2412_06551_b200 as rl
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return rl
+
+
+def _x(m, n, kexp, seed, colscale=False):
+    return synth.baseline_matrix(m, n, kexp, seed, colscale, device=DEV)
+
+
+# ------------------------------------------------------------------ RNG pieces
+def test_omega_bitwise(rl, ora):
+    """Omega columns via A = I: out = Omega[:, row0:row0+k] exactly (one-hot rows)."""
+    for (s, k, row0, seed, stream) in [(32, 64, 0, 0, 0), (128, 96, 12345, 7, 0), (37, 50, 2 ** 33 + 5, 3, 1)]:
+        A = torch.eye(k, dtype=torch.float64, device=DEV)
+        out = rl.sketch_gauss(A, s, seed, stream, row0=row0).cpu().numpy()
+        ref = ora.omega_block(seed, stream, s, row0, k)
+        assert np.array_equal(out, ref), (s, k, row0, np.abs(out - ref).max())
+
+
+def test_countsketch_bitwise(rl, ora):
+    for (rows, n, s1, row0, seed) in [(5000, 16, 64, 0, 2), (70000, 40, 1024, 3, 9), (9000, 130, 4096, 1 << 20, 4)]:
+        A = torch.randn(rows, n, dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(rows))
+        out, b, sg = rl.sketch_count(A, s1, seed, row0=row0, want_hash=True)
+        rb, rs = ora.cs_hash(seed, row0, rows, s1)
+        assert np.array_equal(b.cpu().numpy(), rb) and np.array_equal(sg.cpu().numpy(), rs)
+        ref = ora.cs_apply(A.cpu().numpy(), rb, rs, s1)
+        assert np.array_equal(out.cpu().numpy(), ref)  # same ascending-row order per bucket
+
+
+def test_sketch_gauss_values(rl, ora):
+    for (rows, n, s, row0) in [(3000, 16, 32, 0), (10000, 64, 128, 100), (777, 130, 70, 5)]:
+        A = torch.randn(rows, n, dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
+        out = rl.sketch_gauss(A, s, 11, 0, row0=row0).cpu().numpy()
+        ref = ora.sketch_gauss(A.cpu().numpy(), s, 11, 0, row0=row0)
+        assert rel_fro(out, ref) < 1e-14
+
+
+# ------------------------------------------------------------------ PX = LU
+LU_CASES = [
+    (2048, 16, None), (5000, 16, None), (65536, 64, None), (10000, 40, None), (3000, 33, None),
+    (4100, 100, None), (20000, 128, None), (9000, 200, None), (6000, 64, (256, 2, 64)), (8192, 32, (512, 8, 32)),
+    (300, 64, None), (64, 64, None),
+]
+
+
+@pytest.mark.parametrize("m,n,cfg", LU_CASES)
+def test_getrf_ts_bitwise(rl, ora, m, n, cfg):
+    X = _x(m, n, 8, m + n)
+    from paper_2412_06551_b200._lib import TsluCfg
+    c = rl.default_cfg(m, n) if cfg is None else TsluCfg(*cfg)
+    piv, U, L11, L, info = rl.getrf_ts(X, cfg=c, want_L=True)
+    assert info[0] == 0
+    Xh = X.cpu().numpy()
+    b, a, p = c.as_tuple()
+    rp, rU, rL11, rL = ora.tslu(Xh, b, a, p, want_L=True)
+    assert np.array_equal(piv.cpu().numpy(), rp)
+    assert np.array_equal(U.cpu().numpy(), rU)
+    assert np.array_equal(L11.cpu().numpy(), rL11)
+    assert np.array_equal(L.cpu().numpy(), rL)
+
+
+def test_getrf_ts_rank_deficient(rl):
+    X = _x(3000, 24, 4, 1)
+    X[:, 5] = 0.0
+    *_, info = rl.getrf_ts(X)
+    assert info[:2] == (3, 1) and info[2] == 5  # ERANKDEF at stage LU, pivot 5
+
+
+# ------------------------------------------------------------------ dense stages
+def test_gram(rl):
+    for (rows, n) in [(100000, 64), (5000, 16), (3333, 130), (20000, 256)]:
+        A = torch.randn(rows, n, dtype=torch.float64, device=DEV)
+        G = rl.gram(A)
+        assert torch.equal(G, G.T)
+        ref = (A.cpu().double().numpy().T @ A.cpu().numpy())
+        assert rel_fro(G.cpu().numpy(), ref) < 1e-14
+
+
+def test_trsm_apply(rl, ora):
+    g = torch.Generator(DEV).manual_seed(3)
+    for (rows, n) in [(4000, 16), (7000, 64), (1500, 200)]:
+        A = torch.randn(rows, n, dtype=torch.float64, device=DEV, generator=g)
+        T = torch.triu(torch.randn(n, n, dtype=torch.float64, device=DEV, generator=g)) + 4 * torch.eye(n, device=DEV, dtype=torch.float64)
+        ref = ora.trsm_right_upper(A.cpu().numpy(), T.cpu().numpy())
+        for mode in (rl.RLHC_SUBST, rl.RLHC_INV_GEMM):
+            out, G, info = rl.trsm_apply(A, T, mode=mode, want_gram=True)
+            assert info[0] == 0
+            assert rel_fro(out.cpu().numpy(), ref) < 1e-13
+            assert rel_fro(G.cpu().numpy(), ref.T @ ref) < 1e-13
+    T[3, 3] = 0.0
+    _, _, info = rl.trsm_apply(A, T)
+    assert info == (4, 4, 3)  # ESINGULAR, SOLVE_Y, index 3
+
+
+def test_hqr_and_cholesky(rl, ora):
+    g = torch.Generator(DEV).manual_seed(5)
+    for (s, n) in [(32, 16), (128, 64), (256, 128), (96, 40)]:
+        A = torch.randn(s, n, dtype=torch.float64, device=DEV, generator=g)
+        S, info = rl.hqr_r(A)
+        assert info[0] == 0
+        ref = ora.hqr_r(A.cpu().numpy())
+        assert rel_fro(S.cpu().numpy(), ref) < 1e-13
+        G = A.T @ A
+        Rm, info = rl.cholesky(G)
+        assert info[0] == 0
+        assert rel_fro(Rm.cpu().numpy(), ora.chol(G.cpu().numpy())) < 1e-12
+    Rm, info = rl.cholesky(torch.diag(torch.tensor([1.0, 4.0, -1.0, 2.0], dtype=torch.float64, device=DEV)),
+                           stage=rl.STAGE_CHOL2)
+    assert info == (5, 7, 2)  # EBREAKDOWN, CHOL2, pivot 2
+
+
+# ------------------------------------------------------------------ end to end
+E2E = [
+    ("slhc3", 2048, 16, 8, False, dict(s=32)),                 # cfg1
+    ("slhc3", 20000, 64, 12, False, dict(s=128)),
+    ("sslhc3", 30000, 40, 15, True, dict(s1=320, s2=80)),
+    ("sslhc3", 65536, 128, 10, False, dict(s1=1024, s2=256)),
+    ("slhc3", 3000, 100, 8, False, dict(s=200)),
+]
+
+
+@pytest.mark.parametrize("algo,m,n,kexp,colscale,kw", E2E)
+def test_end_to_end_vs_oracle(rl, ora, algo, m, n, kexp, colscale, kw):
+    X = _x(m, n, kexp, 17, colscale)
+    c = rl.default_cfg(m, n)
+    fn = rl.slhc3 if algo == "slhc3" else rl.sslhc3
+    res = fn(X, seed=3, cfg=c, **kw)
+    assert res.info() == (0, 0, 0)
+    Xh = X.cpu().numpy()
+    b, a, p = c.as_tuple()
+    if algo == "slhc3":
+        ref = ora.slhc3(Xh, kw["s"], 3, b, a, p)
+    else:
+        ref = ora.sslhc3(Xh, kw["s1"], kw["s2"], 3, b, a, p)
+    Q, R = res.Q.cpu().numpy(), res.R.cpu().numpy()
+    assert np.array_equal(res.piv.cpu().numpy(), ref.piv)
+    assert np.all(np.diag(R) > 0) and np.array_equal(np.tril(R, -1), np.zeros_like(R))
+    assert orth_err(Q) <= 1e-13 * math.sqrt(n)
+    assert rel_residual(Q, R, Xh) <= 1e-14 * n
+    assert rel_fro(R, ref.R) <= (1e-9 if kexp <= 8 else 1e-12)
