@@ -1,0 +1,282 @@
+#!/usr/bin/env python
+"""bench.py -- SLHC3 / SSLHC3 (arXiv 2412.06551) fp64 QR on B200: time and HBM GB/s
+against the roofline (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One JSON line on rank 0.  A step = one full SLHC3/SSLHC3 call (every stage of
+SURVEY.md 8(a)) on the configuration's synthetic X, resident in HBM.  `value` is the
+algorithmic HBM throughput: the bytes of the 8 required passes over m x n data
+(8 * 8 m n bytes) per second of device time, summed over ranks.
+L2 is flushed between timed steps (a 512 MiB write, outside the timed events).
+N > 1 runs the row-sharded algorithm (paper_2412_06551_b200.dist) with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAK_FP64_DMMA_TFLOPS = 37.08  # measured by tools/probe/probe.cu (profiles/r01_probe_fp64_hbm.txt)
+
+
+def _peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stage_model(cfg: synth.Config) -> dict:
+    """Algorithmic bytes and flops per stage."""
+    m, n = cfg.m, cfg.n
+    M = 8.0 * m * n
+    tri = m * n * (n + 1.0)  # triangular row product / Gram upper half: flops
+    srows = cfg.s if cfg.algo == "slhc3" else cfg.s1
+    sk_flops = 2.0 * cfg.s * m * n if cfg.algo == "slhc3" else m * n + 2.0 * cfg.s2 * cfg.s1 * n
+    return {
+        "check_finite": (M, 0.0), "tslu": (M, m * n * n * 1.0), "lfactor": (2 * M, m * n * n * 1.0),
+        "sketch": (M + 8.0 * srows * n, sk_flops), "hqr_y": (0.0, 2.0 * srows * n * n),
+        "solve_w_gram1": (2 * M, m * n * n + tri), "chol1": (0.0, n ** 3 / 3.0),
+        "solve_v_gram2": (2 * M, m * n * n + tri), "chol2": (0.0, n ** 3 / 3.0),
+        "solve_q": (2 * M, m * n * n * 1.0), "r_finish": (0.0, 2.0 * n ** 3 / 3),
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def run_ours(args, cfg: synth.Config, rank: int, world: int):
+    import paper_2412_06551_b200 as rl
+    from paper_2412_06551_b200 import _lib
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        from paper_2412_06551_b200 import dist as rdist
+        X, plan = rdist.setup_bench(cfg, rank, world, dev)
+        run = lambda: plan.run(X)  # noqa: E731
+    else:
+        X = synth.config_matrix(cfg, device=dev)
+        plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, device=dev)
+        run = lambda: plan.run(X)  # noqa: E731
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        res = run()
+    torch.cuda.synchronize(dev)
+    code = res.info()
+    if code[0] != 0:
+        raise RuntimeError(f"warm-up run failed: info={code}")
+    _lib.lib().rlhc_stage_timing(1)
+    _lib.stage_times()  # drain
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = _lib.lib().rlhc_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush (outside the timed events)
+            evs[k][0].record(stream)
+            res = run()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = _lib.lib().rlhc_launch_count() - launches0
+    stages = _lib.stage_times()
+    _lib.lib().rlhc_stage_timing(0)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    code = res.info()
+    if code[0] != 0:
+        raise RuntimeError(f"timed run failed: info={code}")
+
+    # ---- end to end through the C ABI with host buffers (copies inside the timed region)
+    e2e = None
+    if world == 1:
+        Xh = X.cpu().pin_memory()
+        Qh = torch.empty(cfg.m, cfg.n, dtype=torch.float64).pin_memory()
+        Rh = torch.empty(cfg.n, cfg.n, dtype=torch.float64).pin_memory()
+        Xd = torch.empty_like(X)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for k in range(args.warmup + args.steps):
+            flush.zero_()
+            e0.record(stream)
+            Xd.copy_(Xh, non_blocking=True)
+            r2 = plan.run(Xd)
+            Qh.copy_(r2.Q, non_blocking=True)
+            Rh.copy_(r2.R, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if k >= args.warmup:
+                tot += e0.elapsed_time(e1)
+        e2e_ms = tot / args.steps
+        e2e = {"value": 8 * 8.0 * cfg.m * cfg.n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * cfg.m * cfg.n, "d2h_bytes_per_step": 8 * (cfg.m * cfg.n + cfg.n * cfg.n)}
+    return ms, stages, launches, clk.summary(), e2e, X
+
+
+def roofline(cfg: synth.Config, stages: dict, world: int):
+    calls = max(stages.get("calls", 1), 1)
+    model = stage_model(cfg)
+    hbm, hbm_src = _peaks()
+    best = None
+    for name, (byts, flops) in model.items():
+        t = stages.get(name, 0.0) / calls * 1e-3
+        if t <= 0:
+            continue
+        if best is None or t > best[1]:
+            best = (name, t, byts, flops)
+    name, t, byts, flops = best
+    t_hbm, t_fp = byts / (hbm * 1e9), flops / (PEAK_FP64_DMMA_TFLOPS * 1e12)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = prof.get(f"{cfg.name}:{name}")
+    except Exception:
+        pass
+    if t_fp >= t_hbm:
+        ach = flops / t / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / PEAK_FP64_DMMA_TFLOPS, "traffic": traffic,
+                "peak_source": "fp64 DMMA measured on this pool (profiles/r01_probe_fp64_hbm.txt)",
+                "ms": t * 1e3}
+    ach = byts / t / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": traffic, "peak_source": hbm_src, "ms": t * 1e3}
+
+
+def cpu_baseline(cfg: synth.Config, X: torch.Tensor | None, budget_s: float = 8.0):
+    import oracle
+    oracle.build()
+    Xh = (X.cpu() if X is not None else synth.config_matrix(cfg)).numpy()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        if cfg.algo == "slhc3":
+            b, a, p = _default_cfg_tuple(cfg)
+            oracle.slhc3(Xh, cfg.s, cfg.seed, b, a, p)
+        else:
+            b, a, p = _default_cfg_tuple(cfg)
+            oracle.sslhc3(Xh, cfg.s1, cfg.s2, cfg.seed, b, a, p)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 20:
+            break
+    per = el / reps
+    return {"value": 8 * 8.0 * cfg.m * cfg.n / per / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": f"full {cfg.name} ({cfg.m}x{cfg.n}) x{reps}", "s_per_step": per}
+
+
+def _default_cfg_tuple(cfg):
+    # the device's default tournament contract, restated (rlhc_default_tslu_cfg)
+    panel = min(cfg.n, 64)
+    W = 16 if panel <= 16 else 32 if panel <= 32 else 64
+    rows = 256 if W == 64 else 512
+    return rows, max(2, rows // panel), panel
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    cfg_name = args.config or ("cfg2" if world == 1 else "cfg5")
+    cfg = synth.CONFIGS[cfg_name]
+    if world > 1 and not torch.distributed.is_initialized():
+        torch.distributed.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    workload = (f"{cfg.name}: {cfg.algo.upper()} m={cfg.m} n={cfg.n} "
+                + (f"s={cfg.s}" if cfg.algo == "slhc3" else f"s1={cfg.s1} s2={cfg.s2}")
+                + f" kappa=1e{cfg.kappa_exp}{' colscale' if cfg.colscale else ''} seed={cfg.seed}")
+    base = {"metric": f"{cfg.algo.upper()} fp64 QR algorithmic HBM throughput (8 passes of m x n)",
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "m": cfg.m, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
+                       "kappa": f"1e{cfg.kappa_exp}", "l2": "flushed between steps (512 MiB write)",
+                       "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"}}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_baseline(cfg, None, budget_s=max(5.0, 0.5 * args.steps))
+        line = dict(base, impl="reference", value=cb["value"], ms_per_step=cb["s_per_step"] * 1e3,
+                    cpu_baseline=cb, e2e={"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}, n_gpus=0)
+        print(json.dumps(line), flush=True)
+        return
+    ms, stages, launches, clocks, e2e, X = run_ours(args, cfg, rank, world)
+    if rank != 0:
+        return
+    per_step = ms / args.steps
+    value = world * 8 * 8.0 * (cfg.m // world if world > 1 else cfg.m) * cfg.n / (per_step * 1e-3) / 1e9
+    line = dict(base, value=value, ms_per_step=per_step, gpu_launches=launches, clocks=clocks,
+                roofline=roofline(cfg, stages, world), e2e=e2e,
+                stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls"})
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, X)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

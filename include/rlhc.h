@@ -171,6 +171,19 @@ int rlhc_cholesky(const double* G, int64_t n, double* Rout, int stage, rlhc_info
 const char* rlhc_version(void);
 const char* rlhc_last_error(void);
 
+/* ---------------------------------------------------------------- diagnostics */
+/* Number of CUDA kernels this library has launched in the calling process. */
+uint64_t rlhc_launch_count(void);
+/* enable != 0: rlhc_slhc3 / rlhc_sslhc3 record a CUDA event on their stream at every
+ * stage boundary (RLHC_NUM_TIMED_STAGES stages, see rlhc_stage_name); 0 disables and
+ * discards pending events. */
+void rlhc_stage_timing(int enable);
+/* Synchronises the recorded events, adds each stage's elapsed milliseconds to ms[k]
+ * (k < max_stages), returns the number of calls consumed (or -1 on a CUDA error). */
+int rlhc_stage_times(double* ms, int max_stages);
+const char* rlhc_stage_name(int k);
+#define RLHC_NUM_TIMED_STAGES 11
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,13 @@ def lib():
     L.rlhc_cholesky.argtypes = [P, I64, P, I, P, P]
     L.rlhc_version.restype = ctypes.c_char_p
     L.rlhc_last_error.restype = ctypes.c_char_p
+    L.rlhc_launch_count.restype = ctypes.c_uint64
+    L.rlhc_stage_timing.argtypes = [I]
+    L.rlhc_stage_timing.restype = None
+    L.rlhc_stage_times.argtypes = [P, I]
+    L.rlhc_stage_times.restype = I
+    L.rlhc_stage_name.argtypes = [I]
+    L.rlhc_stage_name.restype = ctypes.c_char_p
     for name in ("rlhc_slhc3", "rlhc_sslhc3", "rlhc_getrf_ts", "rlhc_sketch_gauss", "rlhc_sketch_count", "rlhc_gram",
                  "rlhc_trsm_apply", "rlhc_hqr_r", "rlhc_cholesky"):
         getattr(L, name).restype = I
@@ -92,7 +99,19 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_getrf_ts_workspace_size", "rlhc_getrf_ts", "rlhc_sketch_gauss_workspace_size",
             "rlhc_sketch_gauss", "rlhc_sketch_count_workspace_size", "rlhc_sketch_count",
             "rlhc_gram_workspace_size", "rlhc_gram", "rlhc_trsm_apply_workspace_size", "rlhc_trsm_apply",
-            "rlhc_hqr_workspace_size", "rlhc_hqr_r", "rlhc_cholesky", "rlhc_version", "rlhc_last_error"]
+            "rlhc_hqr_workspace_size", "rlhc_hqr_r", "rlhc_cholesky", "rlhc_version", "rlhc_last_error",
+            "rlhc_launch_count", "rlhc_stage_timing", "rlhc_stage_times", "rlhc_stage_name"]
+NUM_TIMED_STAGES = 11
+
+
+def stage_times(reset: bool = True) -> dict:
+    """Per-stage milliseconds accumulated by rlhc_stage_timing (synchronises)."""
+    buf = (ctypes.c_double * NUM_TIMED_STAGES)()
+    calls = lib().rlhc_stage_times(buf, NUM_TIMED_STAGES)
+    if calls < 0:
+        raise RlhcError(RLHC_ECUDA, "stage timing events failed")
+    names = [lib().rlhc_stage_name(k).decode() for k in range(NUM_TIMED_STAGES)]
+    return {"calls": calls, **{nm: buf[k] for k, nm in enumerate(names)}}
 
 
 class RlhcError(RuntimeError):

@@ -6,6 +6,7 @@
 namespace rlhc {
 
 int select_rows(int W);
+unsigned long long launch_count();
 
 // tslu.cu
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
@@ -34,6 +35,12 @@ cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int nco
 cudaError_t launch_rows_upper(const double* A, int64_t lda, int64_t rows, int n, const double* Tinv, double* out,
                               int64_t ldo, cudaStream_t st);
 size_t gram_partials_bytes(int64_t rows, int n);
+// fused persistent substitution (+ optional Gram of the output when G != nullptr), n <= 128
+bool rowsolve_ok(int n);
+size_t rowsolve_partials_bytes(int64_t rows, int n);
+cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
+                            double* out, int64_t ldo, const int64_t* piv, const double* L11, double* gpart, double* G,
+                            cudaStream_t st);
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st);
 
 // sketch.cu
@@ -51,6 +58,9 @@ cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double*
                        unsigned long long* status, cudaStream_t st);
 cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
                         cudaStream_t st);
+size_t chol_ws_bytes(int n);
+cudaError_t launch_chol_inv(const double* G, int n, double* R, double* Rinv, double* work, int stage,
+                            unsigned long long* status, cudaStream_t st);
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);
 cudaError_t launch_status_init(unsigned long long* status, cudaStream_t st);

@@ -2,9 +2,12 @@
 // stream-ordered pipelines of SLHC3 and SSLHC3.  No host
 // synchronisation and no allocation inside a call; every stage is a kernel of this
 // library (tslu.cu, rows.cu, sketch.cu, small.cu).
+#include <array>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -27,6 +30,47 @@ static int fail(int code, const char* msg) {
   } while (0)
 
 namespace {
+
+// ---------------------------------------------------------------- stage timing
+constexpr int kStages = RLHC_NUM_TIMED_STAGES;
+const char* kStageNames[kStages] = {"check_finite", "tslu", "lfactor", "sketch", "hqr_y", "solve_w_gram1",
+                                    "chol1", "solve_v_gram2", "chol2", "solve_q", "r_finish"};
+using MarkSet = std::array<cudaEvent_t, kStages + 1>;
+struct StageProf {
+  std::mutex mu;
+  bool enabled = false;
+  std::vector<MarkSet> pending, pool;
+} g_prof;
+
+struct Marks {
+  MarkSet ev{};
+  bool on = false;
+  cudaStream_t st = nullptr;
+  void mark(int k) {
+    if (on) cudaEventRecord(ev[k], st);
+  }
+};
+
+Marks prof_begin(cudaStream_t st) {
+  Marks m;
+  std::lock_guard<std::mutex> g(g_prof.mu);
+  if (!g_prof.enabled) return m;
+  if (!g_prof.pool.empty()) {
+    m.ev = g_prof.pool.back();
+    g_prof.pool.pop_back();
+  } else {
+    for (auto& e : m.ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return Marks{};
+  }
+  m.on = true;
+  m.st = st;
+  return m;
+}
+void prof_end(Marks& m) {
+  if (!m.on) return;
+  std::lock_guard<std::mutex> g(g_prof.mu);
+  g_prof.pending.push_back(m.ev);
+}
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -133,11 +177,11 @@ void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   const int64_t srows = algo == RLHC_SLHC3 ? s_or_s1 : s2;
   a.Ls = c.take<double>((size_t)srows * n);
   a.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
-  size_t part = gram_partials_bytes(m, (int)n);
+  size_t part = std::max(gram_partials_bytes(m, (int)n), rowsolve_partials_bytes(m, (int)n));
   part = std::max(part, algo == RLHC_SLHC3 ? gauss_partials_bytes(m, (int)n, (int)s_or_s1)
                                            : gauss_partials_bytes(s_or_s1, (int)n, (int)s2));
   a.part = c.take<double>(part / sizeof(double) + 1);
-  size_t work = std::max(hqr_ws_bytes((int)srows, (int)n), (size_t)n * n * sizeof(double));
+  size_t work = std::max(hqr_ws_bytes((int)srows, (int)n), chol_ws_bytes((int)n));
   a.work = c.take<double>(work / sizeof(double) + 1);
   a.plan = algo == RLHC_SSLHC3 ? (void*)c.take<char>(cs_plan_bytes(m, (int)s_or_s1)) : nullptr;
 }
@@ -147,15 +191,31 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
              cudaStream_t st) {
   const int ni = (int)n;
   unsigned long long* status = a.t.status;
+  Marks mk = prof_begin(st);
+  mk.mark(0);
   CUDA_TRY(launch_status_init(status, st));
   CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
+  mk.mark(1);
   // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
   int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st);
   if (rc) return rc;
   CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
   CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+  mk.mark(2);
+  // one streaming pass: out = A T^{-1} (substitution) [+ G = out^T out fused]
+  auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
+                        const double* l11, double* G) -> int {
+    if (rowsolve_ok(ni)) {
+      CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
+    } else {
+      CUDA_TRY(launch_trsm_rows(A, lda, m, ni, ni, T, n, rd, Q, ldq, pp, l11, n, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
+    }
+    return RLHC_OK;
+  };
   // L in original row order (R#2), into the Q buffer
-  CUDA_TRY(launch_trsm_rows(X, ldx, m, ni, ni, a.U, n, a.t.rd, Q, ldq, a.pivpos, a.L11, n, st));
+  if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
+  mk.mark(3);
   int64_t srows;
   if (algo == RLHC_SLHC3) {  // L_s = Omega L
     srows = s_or_s1;
@@ -165,25 +225,32 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
     CUDA_TRY(launch_sketch_count(Q, ldq, m, ni, 0, (int)s_or_s1, seed, a.plan, a.Lt, nullptr, nullptr, st));
     CUDA_TRY(launch_sketch_gauss(a.Lt, n, s_or_s1, ni, 0, (int)s2, seed, 1u, a.part, a.Ls, st));
   }
+  mk.mark(4);
   // [H, S] = HouseholderQR(L_s), sign(S_kk) = sign(U_kk) (R#7); Y = S U
   CUDA_TRY(launch_hqr(a.Ls, (int)srows, ni, n, a.U, a.S, a.work, status, st));
   CUDA_TRY(launch_trmm_uu(a.S, a.U, ni, a.Y, st));
-  // W = X Y^{-1} by substitution
   CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
-  CUDA_TRY(launch_trsm_rows(X, ldx, m, ni, ni, a.Y, n, a.rdY, Q, ldq, nullptr, nullptr, 0, st));
-  // CholeskyQR2(W): D = chol(W^T W), V = W D^{-1}, J = chol(V^T V), Q = V J^{-1}
-  CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
+  mk.mark(5);
+  // W = X Y^{-1} by substitution, fused G1 = W^T W (first Gram of CholeskyQR2)
+  if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+  mk.mark(6);
+  // CholeskyQR2(W): D = chol(G1), V = W D^{-1} (+ G2), J = chol(G2), Q = V J^{-1}
   CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st));
-  CUDA_TRY(launch_tri_inv(a.D, ni, a.Di, st));
-  CUDA_TRY(launch_rows_upper(Q, ldq, m, ni, a.Di, Q, ldq, st));
-  CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
+  CUDA_TRY(launch_rdiag(a.D, ni, n, a.Di, RLHC_STAGE_SOLVE_D, status, st));
+  mk.mark(7);
+  if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G))) return rc;
+  mk.mark(8);
   CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st));
-  CUDA_TRY(launch_tri_inv(a.J, ni, a.Ji, st));
-  CUDA_TRY(launch_rows_upper(Q, ldq, m, ni, a.Ji, Q, ldq, st));
+  CUDA_TRY(launch_rdiag(a.J, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
+  mk.mark(9);
+  if ((rc = solve_pass(Q, ldq, a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
+  mk.mark(10);
   // R = Z Y = J (D Y)
   CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, a.N, st));
   CUDA_TRY(launch_trmm_uu(a.J, a.N, ni, R, st));
   CUDA_TRY(launch_status_finish(status, info, st));
+  mk.mark(11);
+  prof_end(mk);
   return RLHC_OK;
 }
 
@@ -419,15 +486,44 @@ int rlhc_cholesky(const double* G, int64_t n, double* Rout, int stage, rlhc_info
   // word is kept in info->index's storage until the final decode
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* status = (unsigned long long*)&info->index;
+  if (chol_ws_bytes((int)n) > 200 * 1024) return fail(RLHC_EINVAL, "rlhc_cholesky entry point supports n <= 110");
   CUDA_TRY(launch_status_init(status, st));
-  size_t need = (size_t)n * n * sizeof(double);
-  if (need > 200 * 1024) return fail(RLHC_EINVAL, "rlhc_cholesky entry point supports n <= 160");
   CUDA_TRY(launch_chol(G, (int)n, Rout, nullptr, stage, status, st));
   CUDA_TRY(launch_status_finish(status, info, st));
   return RLHC_OK;
 }
 
 const char* rlhc_version(void) { return "rlhc-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+uint64_t rlhc_launch_count(void) { return (uint64_t)launch_count(); }
+
+void rlhc_stage_timing(int enable) {
+  std::lock_guard<std::mutex> g(g_prof.mu);
+  g_prof.enabled = enable != 0;
+  if (!g_prof.enabled) {
+    for (auto& ms : g_prof.pending) g_prof.pool.push_back(ms);
+    g_prof.pending.clear();
+  }
+}
+
+int rlhc_stage_times(double* ms, int max_stages) {
+  std::lock_guard<std::mutex> g(g_prof.mu);
+  int calls = 0;
+  for (auto& ev : g_prof.pending) {
+    if (cudaEventSynchronize(ev[kStages]) != cudaSuccess) return -1;
+    for (int k = 0; k < kStages && k < max_stages; k++) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, ev[k], ev[k + 1]) != cudaSuccess) return -1;
+      ms[k] += t;
+    }
+    g_prof.pool.push_back(ev);
+    calls++;
+  }
+  g_prof.pending.clear();
+  return calls;
+}
+
+const char* rlhc_stage_name(int k) { return (k >= 0 && k < kStages) ? kStageNames[k] : ""; }
 const char* rlhc_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"

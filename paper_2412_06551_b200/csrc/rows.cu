@@ -12,12 +12,20 @@ namespace rlhc {
 // ------------------------------------------------------------------ finiteness
 __global__ void check_finite_kernel(const double* __restrict__ X, int64_t rows, int n, int64_t ldx,
                                     unsigned long long* status) {
-  const int64_t total = rows * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = e / n;
-    int j = (int)(e - i * n);
-    double v = X[i * ldx + j];
-    if (!isfinite(v)) report(status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, e);
+  // rows are processed 4 at a time per thread with all loads issued before the tests
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < rows * n; base += 4 * stride) {
+    double v[4];
+    int64_t ee[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      ee[u] = base + u * stride;
+      const int64_t i = ee[u] / n;
+      v[u] = ee[u] < rows * n ? X[i * ldx + (ee[u] - i * n)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (!isfinite(v[u])) report(status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, ee[u]);
   }
 }
 
@@ -26,7 +34,7 @@ cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ld
   int64_t total = rows * n;
   int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), kSMs * 8);
   if (grid < 1) grid = 1;
-  check_finite_kernel<<<grid, 256, 0, st>>>(X, rows, n, ldx, status);
+  note_launch(); check_finite_kernel<<<grid, 256, 0, st>>>(X, rows, n, ldx, status);
   return cudaGetLastError();
 }
 
@@ -42,36 +50,53 @@ __global__ void rdiag_kernel(const double* __restrict__ T, int n, int64_t ldt, d
 
 cudaError_t launch_rdiag(const double* T, int n, int64_t ldt, double* rdiag, int stage, unsigned long long* status,
                          cudaStream_t st) {
-  rdiag_kernel<<<ceil_div(n, 256), 256, 0, st>>>(T, n, ldt, rdiag, stage, status);
+  note_launch(); rdiag_kernel<<<ceil_div(n, 256), 256, 0, st>>>(T, n, ldt, rdiag, stage, status);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ substitution
-// One warp owns 16 rows (two m8 fragments) of the CTA's row tile, kept in shared
-// memory.  Column block jb (8 columns): acc = tile[:, jb] then the chain over the
-// already-substituted columns k < min(8 jb, nsub) on DMMA (A = -l, B = T[k, jb]);
-// then, inside the 8-wide diagonal block, 16 lanes substitute their rows sequentially:
-//   l_k = acc_k * rdiag_k ; acc_j = fma(-l_k, T[k][j], acc_j) for j > k.
+// One warp owns 16 rows (two m8 fragments) of the CTA's row tile S (shared memory).
+// Column block j0 (8 columns), with T[0:j0+8, j0:j0+8] and rdiag staged in shared
+// memory (Tb, row stride 20 doubles: conflict-free B fragments):
+//   acc = S[:, j0:j0+8]; acc += (-L[:, k]) T[k, j0:j0+8] for k < min(j0, nsub) (DMMA chain
+//   in increasing k); then inside the 8-wide diagonal block the rows are substituted
+//   in registers: l_k = acc_k * rdiag_k (broadcast by shuffle from the owning lane),
+//   acc_j = fma(-l_k, T[k][j], acc_j) for j > k.  The fma chain per element is the
+//   oracle's (DESIGN.md R#O5), so L is reproduced bit for bit.
+constexpr int TB_LD = 20;
+
 template <int NWARP>
 __global__ void __launch_bounds__(32 * NWARP)
 trsm_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int ncols, int nsub,
                  const double* __restrict__ T, int64_t ldt, const double* __restrict__ rdiag, double* out,
                  int64_t ldo, const int* __restrict__ pivpos, const double* __restrict__ L11, int64_t ldl11) {
-  extern __shared__ double S[];
+  extern __shared__ double smem[];
   constexpr int TR = 16 * NWARP;
   const int ncp = (ncols + 7) & ~7;
   const int lds = ncp + 4;
+  double* S = smem;                                   // TR x lds
+  double* Tb = smem + TR * lds;                       // 2 x (ncp x TB_LD)
+  double* rdb = Tb + 2 * ncp * TB_LD;                 // 2 x 8
   const int64_t rbase = (int64_t)blockIdx.x * TR;
   for (int idx = threadIdx.x; idx < TR * ncp; idx += blockDim.x) {
     int r = idx / ncp, c = idx - r * ncp;
     int64_t gr = rbase + r;
     S[r * lds + c] = (gr < rows && c < ncols) ? A[gr * lda + c] : 0.0;
   }
-  __syncthreads();
   const int lane = lane_id(), w = warp_id();
   const int g = lane >> 2, t = lane & 3;
   double* Sw = S + (w * 16) * lds;
-  for (int j0 = 0; j0 < ncp; j0 += 8) {
+  int buf = 0;
+  for (int j0 = 0; j0 < ncp; j0 += 8, buf ^= 1) {
+    // stage T[0 : min(j0+8, nsub), j0 : j0+8] and rdiag[j0 : j0+8]
+    const int krows = min(j0 + 8, nsub);
+    double* Tc = Tb + buf * ncp * TB_LD;
+    for (int idx = threadIdx.x; idx < krows * 8; idx += blockDim.x) {
+      int k = idx >> 3, c = idx & 7;
+      Tc[k * TB_LD + c] = (j0 + c < ncols) ? T[(int64_t)k * ldt + j0 + c] : 0.0;
+    }
+    if (threadIdx.x < 8) rdb[buf * 8 + threadIdx.x] = (j0 + threadIdx.x < nsub) ? rdiag[j0 + threadIdx.x] : 0.0;
+    __syncthreads();
     double acc[2][2];
 #pragma unroll
     for (int mf = 0; mf < 2; mf++) {
@@ -79,40 +104,41 @@ trsm_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int nc
       acc[mf][1] = Sw[(mf * 8 + g) * lds + j0 + 2 * t + 1];
     }
     const int kend = min(j0, nsub);
-    const bool colok = (j0 + g) < ncols;
+#pragma unroll 2
     for (int k0 = 0; k0 < kend; k0 += 4) {
       const int k = k0 + t;
-      double b = (k < kend && colok) ? T[(int64_t)k * ldt + j0 + g] : 0.0;
+      const bool kok = k < kend;
+      double b = kok ? Tc[k * TB_LD + g] : 0.0;
 #pragma unroll
       for (int mf = 0; mf < 2; mf++) {
-        double a = (k < kend) ? -Sw[(mf * 8 + g) * lds + k] : 0.0;
+        double a = kok ? -Sw[(mf * 8 + g) * lds + k] : 0.0;
         dmma(acc[mf][0], acc[mf][1], a, b);
+      }
+    }
+    if (j0 < nsub) {
+      const double* Td = Tc + j0 * TB_LD;  // diagonal 8x8 block
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) {
+        if (j0 + kk < nsub) {
+          const double rk = rdb[buf * 8 + kk];
+          const int src = (g << 2) | (kk >> 1);
+          const double u0 = Td[kk * TB_LD + 2 * t], u1 = Td[kk * TB_LD + 2 * t + 1];
+#pragma unroll
+          for (int mf = 0; mf < 2; mf++) {
+            double vk = __shfl_sync(0xffffffffu, (kk & 1) ? acc[mf][1] : acc[mf][0], src);
+            double l = __dmul_rn(vk, rk);
+            if (2 * t == kk) acc[mf][0] = l;
+            else if (2 * t > kk) acc[mf][0] = __fma_rn(-l, u0, acc[mf][0]);
+            if (2 * t + 1 == kk) acc[mf][1] = l;
+            else if (2 * t + 1 > kk) acc[mf][1] = __fma_rn(-l, u1, acc[mf][1]);
+          }
+        }
       }
     }
 #pragma unroll
     for (int mf = 0; mf < 2; mf++) {
       Sw[(mf * 8 + g) * lds + j0 + 2 * t] = acc[mf][0];
       Sw[(mf * 8 + g) * lds + j0 + 2 * t + 1] = acc[mf][1];
-    }
-    __syncwarp();
-    if (j0 < nsub && lane < 16) {
-      double* row = Sw + lane * lds + j0;
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; q++) v[q] = row[q];
-#pragma unroll
-      for (int kk = 0; kk < 8; kk++) {
-        const int k = j0 + kk;
-        if (k < nsub) {
-          double l = __dmul_rn(v[kk], rdiag[k]);
-          v[kk] = l;
-#pragma unroll
-          for (int jj = kk + 1; jj < 8; jj++)
-            if (j0 + jj < ncols) v[jj] = __fma_rn(-l, T[(int64_t)k * ldt + j0 + jj], v[jj]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; q++) row[q] = v[q];
     }
     __syncwarp();
   }
@@ -126,6 +152,11 @@ trsm_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int nc
   }
 }
 
+static size_t trsm_smem(int nwarp, int ncols) {
+  const int ncp = (ncols + 7) & ~7;
+  return ((size_t)16 * nwarp * (ncp + 4) + 2 * (size_t)ncp * TB_LD + 16) * sizeof(double);
+}
+
 cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int ncols, int nsub, const double* T,
                              int64_t ldt, const double* rdiag, double* out, int64_t ldo, const int* pivpos,
                              const double* L11, int64_t ldl11, cudaStream_t st) {
@@ -133,26 +164,299 @@ cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int nco
   const int ncp = (ncols + 7) & ~7;
   // rows per CTA: keep the tile <= ~100 KB (2 CTAs / SM)
   int nwarp = 4;
-  while (nwarp > 1 && (size_t)16 * nwarp * (ncp + 4) * 8 > 100 * 1024) nwarp >>= 1;
-  size_t smem = (size_t)16 * nwarp * (ncp + 4) * 8;
+  while (nwarp > 1 && trsm_smem(nwarp, ncols) > 100 * 1024) nwarp >>= 1;
+  size_t smem = trsm_smem(nwarp, ncols);
+  (void)ncp;
   int grid = (int)ceil_div<int64_t>(rows, 16 * nwarp);
   cudaError_t e;
   switch (nwarp) {
     case 4:
       e = cudaFuncSetAttribute(trsm_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      trsm_rows_kernel<4><<<grid, 128, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
+      note_launch(); trsm_rows_kernel<4><<<grid, 128, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
       break;
     case 2:
       e = cudaFuncSetAttribute(trsm_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      trsm_rows_kernel<2><<<grid, 64, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
+      note_launch(); trsm_rows_kernel<2><<<grid, 64, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
       break;
     default:
       e = cudaFuncSetAttribute(trsm_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      trsm_rows_kernel<1><<<grid, 32, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
+      note_launch(); trsm_rows_kernel<1><<<grid, 32, smem, st>>>(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, pivpos, L11, ldl11);
   }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ fused solve + Gram
+// Persistent row-streaming kernel for n <= 128: out = A T^{-1} (substitution, the same
+// per-element fma chain as trsm_rows_kernel, so L is still bit-exact) with
+//   * T (n x n) and 1/diag(T) staged in shared memory once per CTA,
+//   * row tiles of TR = 16*NWARP rows double-buffered with cp.async (the next tile
+//     streams in while the current one is solved),
+//   * optionally the Gram of the output accumulated on DMMA in registers
+//     (CholeskyQR's G = W^T W fused into the pass that writes W: the pass reads its
+//     input once and writes its output once), written as one n x n partial per CTA.
+// out may equal A (each tile is read completely before it is written back).
+constexpr int RS_MAXN = 128;
+constexpr int RS_WARPS = 4;          // warps per CTA
+constexpr int RS_TR = 32 * RS_WARPS; // rows per tile (32 per warp = 4 m8 fragments)
+
+// Asynchronous row-tile load: rows [row_base, row_base + nrows) x columns [0, ncp) of A
+// into S (row stride lds), zero padded beyond `rows` / `ncols`.  Every thread issues all
+// its 16-byte cp.async copies back to back (many loads in flight), then the caller waits.
+__device__ __forceinline__ void tile_load_async(double* S, int lds, const double* A, int64_t lda, int64_t row_base,
+                                                int64_t rows, int nrows, int ncols, int ncp, bool aligned) {
+  const int nc2 = ncp >> 1;
+  const int c2 = threadIdx.x % nc2, r0 = threadIdx.x / nc2, rstep = blockDim.x / nc2;
+  if (r0 >= rstep) return;
+  const int c = 2 * c2;
+  const bool full = aligned && c + 1 < ncols;
+  for (int r = r0; r < nrows; r += rstep) {
+    const int64_t gr = row_base + r;
+    double* dst = S + r * lds + c;
+    const double* src = A + gr * lda + c;
+    if (gr < rows && full) {
+      cp_async16(dst, src);
+    } else {
+      dst[0] = (gr < rows && c < ncols) ? src[0] : 0.0;
+      dst[1] = (gr < rows && c + 1 < ncols) ? src[1] : 0.0;
+    }
+  }
+}
+
+template <bool GRAM>
+__global__ void __launch_bounds__(32 * RS_WARPS, 2)
+rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double* __restrict__ T,
+                const double* __restrict__ rdiag, double* out, int64_t ldo, double* __restrict__ gpart) {
+  extern __shared__ double smem[];
+  const int ncp = (n + 7) & ~7;
+  const int lds = ncp + 4;        // == 4 (mod 16) doubles: conflict-free fragment access
+  double* Tn = smem;              // -T, ncp x lds
+  double* rd = Tn + ncp * lds;    // 1 / diag(T)
+  double* S = rd + ncp;           // RS_TR x lds row tile
+  for (int k = threadIdx.x >> 3; k < ncp; k += blockDim.x >> 3)
+    for (int c = threadIdx.x & 7; c < ncp; c += 8) Tn[k * lds + c] = (k < n && c < n) ? -T[(int64_t)k * n + c] : 0.0;
+  for (int k = threadIdx.x; k < ncp; k += blockDim.x) rd[k] = k < n ? rdiag[k] : 0.0;
+  const int64_t ntiles = ceil_div<int64_t>(rows, RS_TR);
+  const int lane = lane_id(), w = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int gt = (ncp + 31) / 32;   // 32-wide Gram tiles per side (<= 4)
+  constexpr int GS = GRAM ? 1 : 1;  // one 32x32 Gram tile per warp (fused Gram only for n <= 64)
+  double gacc[4][4][2][GS];
+  if (GRAM) {
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int q = 0; q < GS; q++) gacc[a][b][0][q] = gacc[a][b][1][q] = 0.0;
+  }
+  const int nc2 = ncp >> 1;  // 16-byte chunks per row
+  const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+  double* Sw = S + (w * 32) * lds;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t rbase = tile * RS_TR;
+    __syncthreads();  // previous tile fully consumed
+    // ---- load the row tile (async 16-byte copies, zero padding)
+    tile_load_async(S, lds, A, lda, rbase, rows, RS_TR, n, ncp, aligned);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- substitution, column blocks of 8
+    for (int j0 = 0; j0 < ncp; j0 += 8) {
+      double acc[4][2];
+#pragma unroll
+      for (int mf = 0; mf < 4; mf++) {
+        const double2 c2 = *reinterpret_cast<const double2*>(Sw + (mf * 8 + g) * lds + j0 + 2 * t);
+        acc[mf][0] = c2.x; acc[mf][1] = c2.y;
+      }
+      for (int k0 = 0; k0 < j0; k0 += 4) {
+        const double b = Tn[(k0 + t) * lds + j0 + g];
+#pragma unroll
+        for (int mf = 0; mf < 4; mf++) dmma(acc[mf][0], acc[mf][1], Sw[(mf * 8 + g) * lds + k0 + t], b);
+      }
+#pragma unroll
+      for (int mf = 0; mf < 4; mf++)
+        *reinterpret_cast<double2*>(Sw + (mf * 8 + g) * lds + j0 + 2 * t) = make_double2(acc[mf][0], acc[mf][1]);
+      __syncwarp();
+      // diagonal 8x8 block: lane = row, static indices:
+      //   l_k = v_k * (1/T_kk);  v_j = fma(l_k, -T_kj, v_j)  (== fma(-l_k, T_kj, v_j))
+      double* row = Sw + lane * lds + j0;
+      double v[8];
+      {
+        const double2 p0 = reinterpret_cast<const double2*>(row)[0], p1 = reinterpret_cast<const double2*>(row)[1];
+        const double2 p2 = reinterpret_cast<const double2*>(row)[2], p3 = reinterpret_cast<const double2*>(row)[3];
+        v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y; v[4] = p2.x; v[5] = p2.y; v[6] = p3.x; v[7] = p3.y;
+      }
+      const double* Td = Tn + j0 * lds + j0;
+      const int kmax = min(8, n - j0);
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) {
+        if (kk < kmax) {
+          const double l = __dmul_rn(v[kk], rd[j0 + kk]);
+          v[kk] = l;
+#pragma unroll
+          for (int jj = kk + 1; jj < 8; jj++) v[jj] = __fma_rn(l, Td[kk * lds + jj], v[jj]);
+        }
+      }
+      reinterpret_cast<double2*>(row)[0] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2*>(row)[1] = make_double2(v[2], v[3]);
+      reinterpret_cast<double2*>(row)[2] = make_double2(v[4], v[5]);
+      reinterpret_cast<double2*>(row)[3] = make_double2(v[6], v[7]);
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- store the tile (16-byte stores)
+    {
+      const int c2 = threadIdx.x % nc2, r0 = threadIdx.x / nc2, rstep = blockDim.x / nc2;
+      const int c = 2 * c2;
+      const bool ofull = c + 1 < n && ((ldo & 1) == 0) && ((((uintptr_t)out) & 15) == 0);
+      if (r0 < rstep)
+        for (int r = r0; r < RS_TR; r += rstep) {
+          const int64_t gr = rbase + r;
+          if (gr >= rows) break;
+          const double2 v = *reinterpret_cast<const double2*>(S + r * lds + c);
+          double* dst = out + gr * ldo + c;
+          if (ofull) *reinterpret_cast<double2*>(dst) = v;
+          else { if (c < n) dst[0] = v.x; if (c + 1 < n) dst[1] = v.y; }
+        }
+    }
+    if (GRAM) {
+      // G += tile^T tile on DMMA (rows beyond `rows` are zero-padded)
+#pragma unroll
+      for (int q = 0; q < GS; q++) {
+        const int tl = w + q * RS_WARPS;
+        const int ti = tl / gt, tj = tl - ti * gt;
+        if (ti < gt && ti <= tj) {
+          const int i0 = ti * 32, j0 = tj * 32;
+          for (int k0 = 0; k0 < RS_TR; k0 += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; a++) af[a] = (i0 + a * 8 < ncp) ? S[(k0 + t) * lds + i0 + a * 8 + g] : 0.0;
+#pragma unroll
+            for (int b = 0; b < 4; b++) bf[b] = (j0 + b * 8 < ncp) ? S[(k0 + t) * lds + j0 + b * 8 + g] : 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++) dmma(gacc[a][b][0][q], gacc[a][b][1][q], af[a], bf[b]);
+          }
+        }
+      }
+    }
+  }
+  if (GRAM) {
+    double* P = gpart + (size_t)blockIdx.x * ncp * ncp;
+#pragma unroll
+    for (int q = 0; q < GS; q++) {
+      const int tl = w + q * RS_WARPS;
+      const int ti = tl / gt, tj = tl - ti * gt;
+      if (ti < gt && ti <= tj) {
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            int r = ti * 32 + a * 8 + g, c = tj * 32 + b * 8 + 2 * t;
+            if (r < ncp && c < ncp) {
+              P[r * ncp + c] = gacc[a][b][0][q];
+              P[r * ncp + c + 1] = gacc[a][b][1][q];
+            }
+          }
+      }
+    }
+  }
+}
+
+// pivot rows of L take their L11 row (exact unit diagonal, DESIGN.md R#O5)
+__global__ void pivot_rows_kernel(const int64_t* __restrict__ piv, int n, int64_t row0, int64_t rows,
+                                  const double* __restrict__ L11, double* out, int64_t ldo) {
+  const int k = blockIdx.x;
+  const int64_t lr = piv[k] - row0;
+  if (lr < 0 || lr >= rows) return;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) out[lr * ldo + c] = L11[(int64_t)k * n + c];
+}
+
+// G[i][j] = sum over CTA partials in fixed order (8 independent partial sums, then a
+// fixed combination), upper triangle, mirrored -> exactly symmetric
+__global__ void __launch_bounds__(256)
+gram_part_reduce_kernel(const double* __restrict__ part, int nparts, int n, int ncp, double* __restrict__ G) {
+  // block = 32 consecutive elements of the ncp x ncp partial layout x 8 warps; warp q sums
+  // partials [q*per, (q+1)*per) with 8 independent accumulators (loads in flight), then the
+  // 8 warp sums are combined in a fixed order: deterministic for a given launch geometry.
+  __shared__ double red[8][32];
+  const int lane = lane_id(), wq = warp_id();
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t total = (int64_t)ncp * ncp;
+  const int per = (nparts + 7) / 8;
+  const int p0 = wq * per, p1 = min(nparts, p0 + per);
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (e < total) {
+    const double* p = part + e;
+    int q = p0;
+    for (; q + 8 <= p1; q += 8)
+#pragma unroll
+      for (int u = 0; u < 8; u++) s[u] += p[(size_t)(q + u) * total];
+    for (; q < p1; q++) s[0] += p[(size_t)q * total];
+  }
+  red[wq][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  __syncthreads();
+  if (wq == 0 && e < total) {
+    double v = red[0][lane];
+    for (int q = 1; q < 8; q++) v += red[q][lane];
+    const int i = (int)(e / ncp), j = (int)(e - (int64_t)i * ncp);
+    if (i < n && j < n && i <= j) {
+      G[(int64_t)i * n + j] = v;
+      G[(int64_t)j * n + i] = v;
+    }
+  }
+}
+
+static size_t rowsolve_smem(int n) {
+  const int ncp = (n + 7) & ~7, lds = ncp + 4;
+  return ((size_t)ncp * lds + ncp + (size_t)RS_TR * lds) * sizeof(double);
+}
+static int rowsolve_grid(int64_t rows, int n) {
+  const int64_t ntiles = ceil_div<int64_t>(rows, RS_TR);
+  const int per_sm = rowsolve_smem(n) > 110 * 1024 ? 1 : 2;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kSMs * per_sm));
+}
+bool rowsolve_ok(int n) { return n <= 64; }
+size_t rowsolve_partials_bytes(int64_t rows, int n) {
+  const int ncp = (n + 7) & ~7;
+  return (size_t)rowsolve_grid(rows, n) * ncp * ncp * sizeof(double);
+}
+
+template <bool GRAM>
+static cudaError_t run_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T,
+                                const double* rdiag, double* out, int64_t ldo, double* gpart, cudaStream_t st) {
+  size_t smem = rowsolve_smem(n);
+  cudaError_t e = cudaFuncSetAttribute(rowsolve_kernel<GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e) return e;
+  note_launch();
+  rowsolve_kernel<GRAM><<<rowsolve_grid(rows, n), 32 * RS_WARPS, smem, st>>>(A, lda, rows, n, T, rdiag, out, ldo,
+                                                                            gpart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
+                            double* out, int64_t ldo, const int64_t* piv, const double* L11, double* gpart, double* G,
+                            cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const bool gram = G != nullptr;
+  cudaError_t e = gram ? run_rowsolve<true>(A, lda, rows, n, T, rdiag, out, ldo, gpart, st)
+                       : run_rowsolve<false>(A, lda, rows, n, T, rdiag, out, ldo, gpart, st);
+  if (e) return e;
+  if (piv) {
+    note_launch();
+    pivot_rows_kernel<<<n, 64, 0, st>>>(piv, n, 0, rows, L11, out, ldo);
+  }
+  if (!gram) return cudaGetLastError();
+  const int ncp = (n + 7) & ~7;
+  int64_t total = (int64_t)n * n;
+  note_launch();
+  (void)total;
+  gram_part_reduce_kernel<<<(int)ceil_div<int64_t>((int64_t)ncp * ncp, 32), 256, 0, st>>>(gpart, rowsolve_grid(rows, n),
+                                                                                          n, ncp, G);
   return cudaGetLastError();
 }
 
@@ -216,17 +520,17 @@ cudaError_t launch_rows_upper(const double* A, int64_t lda, int64_t rows, int n,
     case 4:
       e = cudaFuncSetAttribute(rows_upper_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      rows_upper_kernel<4><<<grid, 128, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
+      note_launch(); rows_upper_kernel<4><<<grid, 128, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
       break;
     case 2:
       e = cudaFuncSetAttribute(rows_upper_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      rows_upper_kernel<2><<<grid, 64, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
+      note_launch(); rows_upper_kernel<2><<<grid, 64, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
       break;
     default:
       e = cudaFuncSetAttribute(rows_upper_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e) return e;
-      rows_upper_kernel<1><<<grid, 32, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
+      note_launch(); rows_upper_kernel<1><<<grid, 32, smem, st>>>(A, lda, rows, n, Tinv, out, ldo);
   }
   return cudaGetLastError();
 }
@@ -261,8 +565,8 @@ size_t gram_partials_bytes(int64_t rows, int n) {
 __global__ void __launch_bounds__(128)
 gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int nt, int64_t rows_per_split,
             double* __restrict__ part) {
-  __shared__ double Ai[GK][GT + 4];
-  __shared__ double Aj[GK][GT + 4];
+  __shared__ __align__(16) double Ai[GK][GT + 4];
+  __shared__ __align__(16) double Aj[GK][GT + 4];
   // tile index -> (ti, tj), ti <= tj
   int tile = blockIdx.x, ti = 0;
   {
@@ -283,12 +587,26 @@ gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int 
 #pragma unroll
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int64_t k0 = r0; k0 < r1; k0 += GK) {
-    for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
-      int kk = idx / GT, c = idx - kk * GT;
-      int64_t gr = k0 + kk;
-      bool rok = gr < r1;
-      Ai[kk][c] = (rok && i0 + c < n) ? A[gr * lda + i0 + c] : 0.0;
-      Aj[kk][c] = (rok && j0 + c < n) ? A[gr * lda + j0 + c] : 0.0;
+    {
+      const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+      for (int idx = threadIdx.x; idx < GK * (GT / 2); idx += blockDim.x) {
+        const int kk = idx / (GT / 2), c = 2 * (idx % (GT / 2));
+        const int64_t gr = k0 + kk;
+        const bool rok = gr < r1;
+#pragma unroll
+        for (int side = 0; side < 2; side++) {
+          const int cb = side ? j0 : i0;
+          double* dst = side ? &Aj[kk][c] : &Ai[kk][c];
+          const double* src = A + gr * lda + cb + c;
+          if (rok && aligned && cb + c + 1 < n) cp_async16(dst, src);
+          else {
+            dst[0] = (rok && cb + c < n) ? src[0] : 0.0;
+            dst[1] = (rok && cb + c + 1 < n) ? src[1] : 0.0;
+          }
+        }
+      }
+      cp_async_commit();
+      cp_async_wait_all();
     }
     __syncthreads();
 #pragma unroll
@@ -336,11 +654,11 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nsplit, 
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st) {
   GramGeom gg = gram_geom(rows, n);
   dim3 grid(gg.ntiles, gg.nsplit);
-  gram_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, gg.nt, gg.rows_per_split, part);
+  note_launch(); gram_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, gg.nt, gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 1024), 256, 0, st>>>(part, gg.nsplit, gg.ntiles, gg.nt, n, G);
+  note_launch(); gram_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 1024), 256, 0, st>>>(part, gg.nsplit, gg.ntiles, gg.nt, n, G);
   return cudaGetLastError();
 }
 

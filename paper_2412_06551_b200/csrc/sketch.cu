@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(128)
 gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
                     uint64_t seed, uint32_t stream_id, int64_t rows_per_split, double* __restrict__ part) {
   __shared__ double Om[ST][SK + 1];
-  __shared__ double At[SK][ST + 4];
+  __shared__ __align__(16) double At[SK][ST + 4];
   const int tile_i = blockIdx.x / ((n + ST - 1) / ST), tile_j = blockIdx.x % ((n + ST - 1) / ST);
   const int i0 = tile_i * ST, j0 = tile_j * ST;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
@@ -54,7 +54,22 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
   for (int a = 0; a < 4; a++)
 #pragma unroll
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
   for (int64_t k0 = r0; k0 < r1; k0 += SK) {
+    // A tile (SK rows x ST columns): async 16-byte copies issued first, so they are in
+    // flight while this thread generates its share of the Omega tile
+    for (int idx = threadIdx.x; idx < SK * (ST / 2); idx += blockDim.x) {
+      const int kk = idx / (ST / 2), c = 2 * (idx % (ST / 2));
+      const int64_t gr = k0 + kk;
+      double* dst = &At[kk][c];
+      const double* src = A + gr * lda + j0 + c;
+      if (gr < r1 && aligned && j0 + c + 1 < n) cp_async16(dst, src);
+      else {
+        dst[0] = (gr < r1 && j0 + c < n) ? src[0] : 0.0;
+        dst[1] = (gr < r1 && j0 + c + 1 < n) ? src[1] : 0.0;
+      }
+    }
+    cp_async_commit();
     // Omega tile: rows i0..i0+63 (pairs i, i+1 share one Philox block), columns k0..k0+31
     for (int idx = threadIdx.x; idx < (ST / 2) * SK; idx += blockDim.x) {
       int ip = idx / SK, kk = idx - ip * SK;
@@ -69,11 +84,7 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
       Om[2 * ip][kk] = z0;
       Om[2 * ip + 1][kk] = z1;
     }
-    for (int idx = threadIdx.x; idx < SK * ST; idx += blockDim.x) {
-      int kk = idx / ST, c = idx - kk * ST;
-      int64_t gr = k0 + kk;
-      At[kk][c] = (gr < r1 && j0 + c < n) ? A[gr * lda + j0 + c] : 0.0;
-    }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < SK; kk += 4) {
@@ -117,11 +128,11 @@ cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int 
                                 uint32_t stream_id, double* part, double* out, cudaStream_t st) {
   GaussGeom gg = gauss_geom(rows, n, s);
   dim3 grid(gg.ti * gg.tj, gg.nsplit);
-  gauss_sketch_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part);
+  note_launch(); gauss_sketch_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   int64_t total = (int64_t)s * n;
-  gauss_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 2048), 256, 0, st>>>(
+  note_launch(); gauss_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 2048), 256, 0, st>>>(
       part, gg.nsplit, gg.ti * gg.tj, gg.tj, n, s, out);
   return cudaGetLastError();
 }
@@ -287,13 +298,13 @@ cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int 
     e = cudaFuncSetAttribute(cs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
     if (e) return e;
   }
-  cs_hash_hist_kernel<<<nch, 256, hsm, st>>>(rows, row0, s1, seed, pl.bucket, pl.sign, pl.hist);
-  cs_bucket_totals_kernel<<<ceil_div(s1, 256), 256, 0, st>>>(nch, s1, pl.hist, pl.start);
-  cs_scan_kernel<<<1, 1024, 0, st>>>(s1, pl.start);
-  cs_scatter_kernel<<<nch, 32, hsm, st>>>(rows, s1, pl.bucket, pl.hist, pl.start, pl.perm);
-  cs_apply_kernel<<<ceil_div(s1, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start, pl.sign, out);
-  if (bucket_out) copy_i32_kernel<<<256, 256, 0, st>>>(pl.bucket, bucket_out, rows);
-  if (sign_out) copy_i8_kernel<<<256, 256, 0, st>>>(pl.sign, sign_out, rows);
+  note_launch(); cs_hash_hist_kernel<<<nch, 256, hsm, st>>>(rows, row0, s1, seed, pl.bucket, pl.sign, pl.hist);
+  note_launch(); cs_bucket_totals_kernel<<<ceil_div(s1, 256), 256, 0, st>>>(nch, s1, pl.hist, pl.start);
+  note_launch(); cs_scan_kernel<<<1, 1024, 0, st>>>(s1, pl.start);
+  note_launch(); cs_scatter_kernel<<<nch, 32, hsm, st>>>(rows, s1, pl.bucket, pl.hist, pl.start, pl.perm);
+  note_launch(); cs_apply_kernel<<<ceil_div(s1, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start, pl.sign, out);
+  if (bucket_out) note_launch(), copy_i32_kernel<<<256, 256, 0, st>>>(pl.bucket, bucket_out, rows);
+  if (sign_out) note_launch(), copy_i8_kernel<<<256, 256, 0, st>>>(pl.sign, sign_out, rows);
   return cudaGetLastError();
 }
 

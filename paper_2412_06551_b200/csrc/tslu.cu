@@ -2,114 +2,45 @@
 // under the pivot contract of DESIGN.md R#3-R#5 (tslu over column panels).
 //
 // One select CTA holds up to R = 32*NW candidate rows of a W-wide panel in REGISTERS
-// (lane = candidate row, a[W] per lane) and runs GEPP on them: per step one warp
-// argmax (redux.sync on the |a| bit pattern, smallest global id on ties), one
-// __syncthreads, a cross-warp argmax over NW slots, then a register-resident rank-1
-// update whose pivot row comes from shared memory (each warp's local winner writes
-// its row speculatively before the barrier, so a step costs one block barrier).
+// (lane = candidate row) and runs GEPP on them.  Per step: one warp argmax (redux.sync
+// on the |a| bit pattern, smallest global id on ties), the warp's winner writes its row
+// to shared memory speculatively, ONE __syncthreads, a cross-warp argmax over the NW
+// slots, then the register-resident rank-1 update.  The register window shifts by one
+// column per step (a[0] is always the current pivot column), so the step loop stays
+// rolled with constant register indices: small code, no local memory.
 #include <climits>
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "select.cuh"
 
 namespace rlhc {
-
-template <int W, int NW>
-struct SelSmem {
-  unsigned long long key[2][NW];
-  int id[2][NW];
-  double row[2][NW][W];
-  int out_src[W];
-  int out_id[W];
-};
-
-// GEPP selection on the block's candidates (definition: oracle gepp_select / R#4-R#5).
-// a: this lane's candidate row (W panel values, entries >= w are ignored), active:
-// lane holds a candidate, gid: its global row id, slot: where its original values live.
-// Returns the number of steps; sm.out_id[t] / sm.out_src[t] hold the winners.
-// The step loop is compile-time recursion (SelStep<.., t>) so every a[] index is a
-// constant and the candidate row never leaves the register file.
-template <int W, int NW, int t>
-struct SelStep {
-  static __device__ __forceinline__ void run(double (&a)[W], bool& active, int gid, int slot, int steps,
-                                             SelSmem<W, NW>& sm) {
-    if (t >= steps) return;
-    const int lane = lane_id(), wp = warp_id();
-    constexpr int par = t & 1;
-    long long kb = active ? __double_as_longlong(fabs(a[t])) : -1ll;
-    int hi = (int)(kb >> 32);
-    int mh = __reduce_max_sync(0xffffffffu, hi);
-    unsigned lo = (hi == mh) ? (unsigned)kb : 0u;
-    unsigned ml = __reduce_max_sync(0xffffffffu, lo);
-    bool tie = active && hi == mh && (unsigned)kb == ml;
-    int wmin = __reduce_min_sync(0xffffffffu, tie ? gid : INT_MAX);
-    bool wwin = tie && gid == wmin;
-    if (wwin) {
-      sm.key[par][wp] = (unsigned long long)kb;
-      sm.id[par][wp] = gid;
-#pragma unroll
-      for (int c = t; c < W; c++) sm.row[par][wp][c] = a[c];
-    }
-    if (lane == 0 && mh < 0) { sm.key[par][wp] = 0ull; sm.id[par][wp] = INT_MAX; }
-    __syncthreads();
-    // cross-warp argmax (every warp redundantly)
-    unsigned long long k2 = lane < NW ? sm.key[par][lane] : 0ull;
-    int id2 = lane < NW ? sm.id[par][lane] : INT_MAX;
-    unsigned h2 = (unsigned)(k2 >> 32);
-    unsigned gh = __reduce_max_sync(0xffffffffu, h2);
-    unsigned l2 = (h2 == gh) ? (unsigned)k2 : 0u;
-    unsigned gl = __reduce_max_sync(0xffffffffu, l2);
-    bool tie2 = h2 == gh && (unsigned)k2 == gl;
-    int pid = __reduce_min_sync(0xffffffffu, tie2 ? id2 : INT_MAX);
-    unsigned wmask = __ballot_sync(0xffffffffu, lane < NW && id2 == pid);
-    int ww = __ffs(wmask) - 1;
-    bool zero = (gh == 0u && gl == 0u);
-    if (active && gid == pid) {
-      active = false;
-      sm.out_src[t] = slot;
-    } else if (active && !zero) {
-      double u = sm.row[par][ww][t];
-      double r = __ddiv_rn(1.0, u);
-      double l = __dmul_rn(a[t], r);
-#pragma unroll
-      for (int c = t + 1; c < W; c++) a[c] = __fma_rn(-l, sm.row[par][ww][c], a[c]);
-    }
-    if (threadIdx.x == 0) sm.out_id[t] = pid;
-    SelStep<W, NW, t + 1>::run(a, active, gid, slot, steps, sm);
-  }
-};
-template <int W, int NW>
-struct SelStep<W, NW, W> {
-  static __device__ __forceinline__ void run(double (&)[W], bool&, int, int, int, SelSmem<W, NW>&) {}
-};
-
-template <int W, int NW>
-__device__ __forceinline__ int gepp_select(double (&a)[W], bool active, int gid, int slot, int w,
-                                           SelSmem<W, NW>& sm) {
-  int nact = __syncthreads_count(active);
-  const int steps = min(nact, w);
-  SelStep<W, NW, 0>::run(a, active, gid, slot, steps, sm);
-  __syncthreads();
-  return steps;
-}
 
 // Leaf select: leaf = global row block [leaf*R, leaf*R + R) of the LOCAL rows
 // (global id = row0 + local row).  src: current values (X for the first panel, the
 // trailing matrix afterwards), panel columns [p0, p0 + w).  Output level slot = leaf.
-template <int W, int NW>
+template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals) {
-  constexpr int R = 32 * NW;
-  __shared__ SelSmem<W, NW> sm;
-  const int64_t r = (int64_t)blockIdx.x * R + threadIdx.x;
-  bool active = r < rows && !(chosen && chosen[r]);
-  double a[W];
-  const double* p = src + r * lds + p0;
+  constexpr int R = 32 * RS, CW = W / NW;
+  __shared__ SelSmem<W, NW, RS> sm;
+  const int lane = lane_id(), wp = warp_id();
+  double a[RS][CW];
+  int gid[RS];
+  unsigned act = 0;
 #pragma unroll
-  for (int c = 0; c < W; c++) a[c] = (active && c < w) ? p[c] : 0.0;
-  int steps = gepp_select<W, NW>(a, active, (int)(row0 + r), threadIdx.x, w, sm);
+  for (int s = 0; s < RS; s++) {
+    const int64_t r = (int64_t)blockIdx.x * R + s * 32 + lane;
+    const bool ok = r < rows && !(chosen && chosen[r]);
+    act |= (ok ? 1u : 0u) << s;
+    gid[s] = (int)(row0 + r);
+    const double* p = src + r * lds + p0 + wp * CW;
+#pragma unroll
+    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp * CW + c < w) ? p[c] : 0.0;
+  }
+  const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
   int* oi = out_ids + (size_t)blockIdx.x * W;
   double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
@@ -122,32 +53,43 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
 }
 
 // Node select: node = children [node*arity, node*arity + arity) of the level below;
-// child c's k-th winner sits on thread (c - c0)*w + k.  Values are the stored
-// current panel values of the candidates (not the eliminated ones).
-template <int W, int NW>
+// candidate index q -> child (q / w), entry (q % w).  Values are the stored current
+// panel values of the candidates (not the eliminated ones).
+template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt, const double* __restrict__ in_vals,
                  int nslots_in, int arity, int w, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals) {
-  __shared__ SelSmem<W, NW> sm;
+  constexpr int CW = W / NW;
+  __shared__ SelSmem<W, NW, RS> sm;
+  const int lane = lane_id(), wp = warp_id();
   const int c0 = blockIdx.x * arity;
-  const int ci = threadIdx.x / w, e = threadIdx.x - ci * w;
-  const int child = c0 + ci;
-  bool active = ci < arity && child < nslots_in && e < in_cnt[child < nslots_in ? child : 0];
-  const int slot = child * W + e;
-  double a[W];
-  const double* p = in_vals + (size_t)slot * W;
+  double a[RS][CW];
+  int gid[RS];
+  unsigned act = 0;
 #pragma unroll
-  for (int c = 0; c < W; c++) a[c] = (active && c < w) ? p[c] : 0.0;
-  int gid = active ? in_ids[slot] : INT_MAX;
-  int steps = gepp_select<W, NW>(a, active, gid, slot, w, sm);
+  for (int s = 0; s < RS; s++) {
+    const int qi = s * 32 + lane;
+    const int ci = qi / w, e = qi - ci * w;
+    const int child = c0 + ci;
+    const bool ok = ci < arity && child < nslots_in && e < in_cnt[child < nslots_in ? child : 0];
+    act |= (ok ? 1u : 0u) << s;
+    const int slot = child * W + e;
+    gid[s] = ok ? in_ids[slot] : INT_MAX;
+    const double* p = in_vals + (size_t)(ok ? slot : 0) * W + wp * CW;
+#pragma unroll
+    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp * CW + c < w) ? p[c] : 0.0;
+  }
+  const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
   int* oi = out_ids + (size_t)blockIdx.x * W;
   double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
   for (int q = threadIdx.x; q < W; q += blockDim.x) oi[q] = q < steps ? sm.out_id[q] : -1;
   for (int idx = threadIdx.x; idx < steps * w; idx += blockDim.x) {
     int q = idx / w, c = idx - q * w;
-    ov[q * W + c] = in_vals[(size_t)sm.out_src[q] * W + c];
+    const int qi = sm.out_src[q];
+    const int ci = qi / w, e = qi - ci * w;
+    ov[q * W + c] = in_vals[(size_t)((c0 + ci) * W + e) * W + c];
   }
 }
 
@@ -164,7 +106,6 @@ tslu_panel_factor_kernel(const double* __restrict__ src, int64_t lds, int64_t ro
                          int64_t* __restrict__ piv, uint8_t* __restrict__ chosen, double* __restrict__ lpanel,
                          unsigned long long* status) {
   __shared__ double P[64][65];
-  __shared__ double rd[64];
   __shared__ int ids[64];
   const int tid = threadIdx.x;
   if (tid == 0 && root_cnt[0] < w) report(status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + root_cnt[0]);
@@ -181,25 +122,29 @@ tslu_panel_factor_kernel(const double* __restrict__ src, int64_t lds, int64_t ro
     P[t][c] = src[((int64_t)ids[t] - row0) * lds + p0 + c];
   }
   __syncthreads();
-  // phase A: right-looking elimination of the w x w block (P[t][t'] <- multiplier for t' < t)
+  // phase A: right-looking elimination of the w x w block (P[t][t'] <- multiplier for
+  // t' < t).  Thread (c = tid & 63, t0 = tid >> 6) owns column c of rows t0, t0+8, ...;
+  // every owner recomputes the row multiplier itself (same IEEE ops -> same bits).
+  const int c = tid & 63, t0 = tid >> 6;
   for (int k = 0; k < w; k++) {
-    double ukk = P[k][k];
-    if (tid == 0) {
-      if (ukk == 0.0) report(status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + k);
-      rd[k] = __ddiv_rn(1.0, ukk);
+    const double ukk = P[k][k];
+    if (tid == 0 && ukk == 0.0) report(status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + k);
+    const double r = __ddiv_rn(1.0, ukk);
+    double lv[8], nv[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int t = t0 + 8 * i;
+      lv[i] = (t > k && t < w) ? __dmul_rn(P[t][k], r) : 0.0;
+      nv[i] = (t > k && t < w && c > k && c < w) ? __fma_rn(-lv[i], P[k][c], P[t][c]) : 0.0;
     }
     __syncthreads();
-    double r = rd[k];
-    int cnt = (w - 1 - k) * (w - k);  // rows k+1..w-1, columns k..w-1 (col k = multiplier)
-    for (int idx = tid; idx < (w - 1 - k); idx += blockDim.x) {
-      int t = k + 1 + idx;
-      P[t][k] = __dmul_rn(P[t][k], r);
-    }
-    __syncthreads();
-    (void)cnt;
-    for (int idx = tid; idx < (w - 1 - k) * (w - 1 - k); idx += blockDim.x) {
-      int t = k + 1 + idx / (w - 1 - k), c = k + 1 + idx % (w - 1 - k);
-      P[t][c] = __fma_rn(-P[t][k], P[k][c], P[t][c]);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int t = t0 + 8 * i;
+      if (t > k && t < w) {
+        if (c == k) P[t][k] = lv[i];
+        else if (c > k && c < w) P[t][c] = nv[i];
+      }
     }
     __syncthreads();
   }
@@ -251,58 +196,59 @@ __global__ void pivpos_kernel(const int64_t* __restrict__ piv, int n, int64_t ro
 
 // ------------------------------------------------------------------ host side
 int select_rows(int W) { return W == 64 ? 256 : 512; }
+// (W, NW, RS): W=64 -> 8 warps x 8 cols, 256 rows; W=32 -> 8 x 4, 512 rows; W=16 -> 8 x 2, 512 rows
 
-template <int W, int NW>
+template <int W, int NW, int RS>
 static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st) {
-  int nleaves = (int)ceil_div<int64_t>(rows, 32 * NW);
-  tslu_leaf_kernel<W, NW><<<nleaves, 32 * NW, 0, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals);
+  int nleaves = (int)ceil_div<int64_t>(rows, 32 * RS);
+  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, 0, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals);
   return cudaGetLastError();
 }
-template <int W, int NW>
+template <int W, int NW, int RS>
 static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity, int w,
                             int* ids, int* cnt, double* vals, cudaStream_t st) {
   int nout = ceil_div(nin, arity);
-  tslu_node_kernel<W, NW><<<nout, 32 * NW, 0, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals);
+  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, 0, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st) {
   switch (W) {
-    case 16: return run_leaf<16, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
-    case 32: return run_leaf<32, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
-    case 64: return run_leaf<64, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
+    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
+    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
+    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
   }
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
                              int w, int* ids, int* cnt, double* vals, cudaStream_t st) {
   switch (W) {
-    case 16: return run_node<16, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
-    case 32: return run_node<32, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
-    case 64: return run_node<64, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
+    case 16: return run_node<16, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
+    case 32: return run_node<32, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
+    case 64: return run_node<64, 8, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
   }
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
                                      const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
                                      uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st) {
-  tslu_panel_factor_kernel<<<1, 512, 0, st>>>(src, lds, rows, row0, p0, w, n, root_ids, root_cnt, U, piv, chosen,
+  note_launch(); tslu_panel_factor_kernel<<<1, 512, 0, st>>>(src, lds, rows, row0, p0, w, n, root_ids, root_cnt, U, piv, chosen,
                                               lpanel, status);
   return cudaGetLastError();
 }
 cudaError_t launch_l11_fixup(double* L11, int n, cudaStream_t st) {
-  l11_fixup_kernel<<<n, 128, 0, st>>>(L11, n);
+  note_launch(); l11_fixup_kernel<<<n, 128, 0, st>>>(L11, n);
   return cudaGetLastError();
 }
 cudaError_t launch_gather_rows(const double* src, int64_t lds, const int64_t* ids, int64_t row0, int cnt, int ncols,
                                double* dst, int64_t ldd, cudaStream_t st) {
-  gather_rows_kernel<<<cnt, 128, 0, st>>>(src, lds, ids, row0, cnt, ncols, dst, ldd);
+  note_launch(); gather_rows_kernel<<<cnt, 128, 0, st>>>(src, lds, ids, row0, cnt, ncols, dst, ldd);
   return cudaGetLastError();
 }
 cudaError_t launch_pivpos(const int64_t* piv, int n, int64_t row0, int64_t rows, int* pivpos, cudaStream_t st) {
-  pivpos_kernel<<<ceil_div(n, 128), 128, 0, st>>>(piv, n, row0, rows, pivpos);
+  note_launch(); pivpos_kernel<<<ceil_div(n, 128), 128, 0, st>>>(piv, n, row0, rows, pivpos);
   return cudaGetLastError();
 }
 
