@@ -1,0 +1,443 @@
+// factor.cu -- the small n x n / s x n factorizations (replicated work, no m dependence):
+// HouseholderQR of the sketch (only R kept, H never formed) and Cholesky with
+// breakdown detection.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rlhc {
+
+// ------------------------------------------------------------------ Householder R
+// LAPACK dgeqr2 order (DESIGN.md R#O7): beta = -sign(alpha) ||x||, tau = (beta - alpha)/beta,
+// v = x(2:)/(alpha - beta); A(k:, k+1:) -= tau v (v^T A(k:, k+1:)).
+// One CTA, column j owned by warp (j mod NW).  Look-ahead: in step k every warp applies
+// reflector k to its columns; the owner of column k+1 does that column first and then
+// immediately forms reflector k+1 (norm, beta, tau, v scaled in place) and publishes
+// (beta, tau) -- so one barrier per step and the reflector never waits for the other
+// columns.  Working copy with row stride n+1 (conflict-free column access); explicit
+// shared memory when it fits (SMEM), else global `work`.
+template <bool SMEM>
+__global__ void __launch_bounds__(1024)
+hqr2_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const double* __restrict__ sgn_ref,
+            double* __restrict__ S, double* __restrict__ work, unsigned long long* status) {
+  extern __shared__ double dsm[];
+  __shared__ double tauS[2];
+  __shared__ int flag;
+  double* Wm = SMEM ? dsm : work;
+  const int ld = n + 1;
+  const int lane = lane_id(), wp = warp_id(), nw = blockDim.x >> 5;
+  for (int i = wp; i < s; i += nw) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) v[q] = (lane + 32 * q < n) ? A[(int64_t)i * lda + lane + 32 * q] : 0.0;
+    for (int j = lane + 128; j < n; j += 32) Wm[(int64_t)i * ld + j] = A[(int64_t)i * lda + j];
+#pragma unroll
+    for (int q = 0; q < 4; q++) if (lane + 32 * q < n) Wm[(int64_t)i * ld + lane + 32 * q] = v[q];
+  }
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  // reflector of column k (called by the owner warp of column k); returns nothing,
+  // publishes tau in tauS[k & 1], writes beta on the diagonal and v below it
+  // all row loops run a warp-uniform trip count with a predicated body, so the warp is
+  // converged at every shuffle (no WARPSYNC.COLLECTIVE slow path)
+  auto reflector = [&](int k) {
+    double part = 0.0;
+    for (int i0 = k + 1; i0 < s; i0 += 32) {
+      const int i = i0 + lane;
+      const double x = i < s ? Wm[(int64_t)i * ld + k] : 0.0;
+      part = __fma_rn(x, x, part);
+    }
+    __syncwarp();
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const double alpha = Wm[(int64_t)k * ld + k];
+    const double xnorm = __dsqrt_rn(part);
+    double beta = alpha, tau = 0.0;
+    if (xnorm != 0.0) {
+      beta = -(alpha >= 0.0 ? 1.0 : -1.0) * hypot(alpha, xnorm);
+      tau = __ddiv_rn(beta - alpha, beta);
+      const double sc = __ddiv_rn(1.0, alpha - beta);
+      for (int i0 = k + 1; i0 < s; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < s) Wm[(int64_t)i * ld + k] *= sc;
+      }
+    } else if (alpha == 0.0 && lane == 0) {
+      report(status, RLHC_ERANKDEF, RLHC_STAGE_HQR, k);
+      flag = 1;
+    }
+    __syncwarp();
+    if (lane == 0) { tauS[k & 1] = tau; Wm[(int64_t)k * ld + k] = beta; }
+  };
+  auto apply = [&](int k, int j, double tau) {
+    double acc = 0.0;
+    for (int i0 = k + 1; i0 < s; i0 += 32) {
+      const int i = i0 + lane;
+      if (i < s) acc = __fma_rn(Wm[(int64_t)i * ld + k], Wm[(int64_t)i * ld + j], acc);
+    }
+    __syncwarp();
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const double tw = tau * (Wm[(int64_t)k * ld + j] + acc);
+    __syncwarp();
+    if (lane == 0) Wm[(int64_t)k * ld + j] -= tw;
+    for (int i0 = k + 1; i0 < s; i0 += 32) {
+      const int i = i0 + lane;
+      if (i < s) Wm[(int64_t)i * ld + j] = __fma_rn(-Wm[(int64_t)i * ld + k], tw, Wm[(int64_t)i * ld + j]);
+    }
+    __syncwarp();
+  };
+  if (wp == 0) reflector(0);
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    if (flag) break;
+    const double tau = tauS[k & 1];
+    const int jn = k + 1;  // next pivot column
+    if (jn < n && (jn % nw) == wp) {
+      if (tau != 0.0) apply(k, jn, tau);
+      reflector(jn);
+    }
+    if (tau != 0.0)
+      for (int j = k + 1 + ((wp - (k + 1)) % nw + nw) % nw; j < n; j += nw)
+        if (j != jn) apply(k, j, tau);
+    __syncthreads();
+  }
+  for (int i = wp; i < n; i += nw) {
+    const double d = Wm[(int64_t)i * ld + i];
+    const bool flip = sgn_ref && ((d < 0.0) != (sgn_ref[(int64_t)i * n + i] < 0.0));
+    for (int j = lane; j < n; j += 32) {
+      double v = (j >= i) ? Wm[(int64_t)i * ld + j] : 0.0;
+      S[(int64_t)i * n + j] = flip ? -v : v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ register-resident HQR
+// For s <= 32*RR, n <= 16*QC: the s x n matrix lives in REGISTERS of 16 warps: warp w owns
+// columns {w + 16 q : q < QC}, lane l holds rows {l + 32 r : r < RR}; a[r][q].  Step k:
+// the owner of column k forms the reflector (norm by warp reduction), writes v (zeros
+// above row k, 1 at row k) to shared memory and publishes tau; one barrier; every warp
+// applies it to its columns j > k: dot = v . a[:, j] (RR FMAs + warp reduction), a[:, j]
+// -= (tau dot) v.  Look-ahead: the owner of column k+1 applies reflector k to that column
+// first and forms reflector k+1 before its other columns.  No shared-memory traffic on
+// the matrix itself (the smem-resident kernel above is bandwidth bound).
+constexpr int HQ_WARPS = 16;
+
+template <int RR, int QC, int Q>
+__device__ __forceinline__ void hq_get_col(const double (&a)[RR][QC], int q, double (&x)[RR]) {
+  if constexpr (Q < QC) {
+    if (q == Q) {
+#pragma unroll
+      for (int r = 0; r < RR; r++) x[r] = a[r][Q];
+    } else {
+      hq_get_col<RR, QC, Q + 1>(a, q, x);
+    }
+  }
+}
+template <int RR, int QC, int Q>
+__device__ __forceinline__ void hq_set_col(double (&a)[RR][QC], int q, const double (&x)[RR]) {
+  if constexpr (Q < QC) {
+    if (q == Q) {
+#pragma unroll
+      for (int r = 0; r < RR; r++) a[r][Q] = x[r];
+    } else {
+      hq_set_col<RR, QC, Q + 1>(a, q, x);
+    }
+  }
+}
+
+template <int RR, int QC>
+__global__ void __launch_bounds__(32 * HQ_WARPS)
+hqr_reg_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const double* __restrict__ sgn_ref,
+               double* __restrict__ S, unsigned long long* status) {
+  __shared__ double vbuf[2][32 * RR];
+  __shared__ double tauS[2], betaS[HQ_WARPS * QC];
+  __shared__ int flag;
+  const int lane = lane_id(), wp = warp_id();
+  double a[RR][QC];
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int q = 0; q < QC; q++) {
+      const int i = lane + 32 * r, j = wp + HQ_WARPS * q;
+      a[r][q] = (i < s && j < n) ? A[(int64_t)i * lda + j] : 0.0;
+    }
+  if (threadIdx.x == 0) flag = 0;
+  // reflector of column k, owned by this warp at slot q (x = the column's values)
+  auto reflector = [&](int k, int q) {
+    double x[RR];
+    hq_get_col<RR, QC, 0>(a, q, x);
+    double part = 0.0, alpha = 0.0;
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      const int i = lane + 32 * r;
+      if (i > k && i < s) part = __fma_rn(x[r], x[r], part);
+      if (i == k) alpha = x[r];
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    alpha = __shfl_sync(0xffffffffu, alpha, k & 31);
+    const double xnorm = __dsqrt_rn(part);
+    double beta = alpha, tau = 0.0, sc = 0.0;
+    if (xnorm != 0.0) {
+      beta = -(alpha >= 0.0 ? 1.0 : -1.0) * hypot(alpha, xnorm);
+      tau = __ddiv_rn(beta - alpha, beta);
+      sc = __ddiv_rn(1.0, alpha - beta);
+    } else if (alpha == 0.0 && lane == 0) {
+      report(status, RLHC_ERANKDEF, RLHC_STAGE_HQR, k);
+      flag = 1;
+    }
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      const int i = lane + 32 * r;
+      const double v = (i > k) ? x[r] * sc : (i == k ? 1.0 : 0.0);
+      vbuf[k & 1][i] = v;
+      x[r] = (i > k) ? x[r] : (i == k ? beta : x[r]);  // column k of R: beta on the diagonal
+    }
+    hq_set_col<RR, QC, 0>(a, q, x);
+    if (lane == 0) { tauS[k & 1] = tau; betaS[k] = beta; }
+  };
+  // apply reflector k (v in vbuf[k & 1], tau) to this warp's slot q
+  auto apply = [&](int k, int q, const double (&v)[RR], double tau) {
+    double x[RR];
+    hq_get_col<RR, QC, 0>(a, q, x);
+    double dot = 0.0;
+#pragma unroll
+    for (int r = 0; r < RR; r++) dot = __fma_rn(v[r], x[r], dot);
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const double tw = tau * dot;
+#pragma unroll
+    for (int r = 0; r < RR; r++) x[r] = __fma_rn(-v[r], tw, x[r]);
+    hq_set_col<RR, QC, 0>(a, q, x);
+  };
+  __syncthreads();
+  if (wp == 0) reflector(0, 0);
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    if (flag) break;
+    const double tau = tauS[k & 1];
+    double v[RR];
+#pragma unroll
+    for (int r = 0; r < RR; r++) v[r] = vbuf[k & 1][lane + 32 * r];
+    const int jn = k + 1;
+    const bool own_next = jn < n && (jn % HQ_WARPS) == wp;
+    if (own_next) {
+      if (tau != 0.0) apply(k, jn / HQ_WARPS, v, tau);
+      reflector(jn, jn / HQ_WARPS);
+    }
+    if (tau != 0.0) {
+#pragma unroll
+      for (int q = 0; q < QC; q++) {
+        const int j = wp + HQ_WARPS * q;
+        if (j > k && j < n && j != jn) apply(k, q, v, tau);
+      }
+    }
+    __syncthreads();
+  }
+  // R = upper n x n part (diag from the reflectors), sign-aligned with sgn_ref
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int q = 0; q < QC; q++) {
+      const int i = lane + 32 * r, j = wp + HQ_WARPS * q;
+      if (i < n && j < n) {
+        double val = (j >= i) ? a[r][q] : 0.0;
+        if (sgn_ref) {
+          const double d = betaS[i];
+          if ((d < 0.0) != (sgn_ref[(int64_t)i * n + i] < 0.0)) val = -val;
+        }
+        S[(int64_t)i * n + j] = val;
+      }
+    }
+}
+
+size_t hqr_ws_bytes(int s, int n) { return ((size_t)s * (n + 1)) * sizeof(double); }
+
+cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double* sgn_ref, double* S, double* work,
+                       unsigned long long* status, cudaStream_t st) {
+  const size_t need = hqr_ws_bytes(s, n);
+  const int threads = n >= 512 ? 1024 : 512;
+#define HQR_REG(RR, QC)                                                                            \
+  if (s <= 32 * RR && n <= HQ_WARPS * QC) {                                                        \
+    note_launch();                                                                                 \
+    hqr_reg_kernel<RR, QC><<<1, 32 * HQ_WARPS, 0, st>>>(A, s, n, lda, sgn_ref, S, status);         \
+    return cudaGetLastError();                                                                     \
+  }
+  HQR_REG(1, 1)
+  HQR_REG(2, 2)
+  HQR_REG(4, 4)
+  HQR_REG(8, 4)
+  HQR_REG(4, 8)
+#undef HQR_REG
+  if (need <= 200 * 1024) {
+    if (need > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(hqr2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+      if (e) return e;
+    }
+    note_launch();
+    hqr2_kernel<true><<<1, threads, need, st>>>(A, s, n, lda, sgn_ref, S, work, status);
+  } else {
+    note_launch();
+    hqr2_kernel<false><<<1, 1024, 0, st>>>(A, s, n, lda, sgn_ref, S, work, status);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ Cholesky
+// Upper R with R^T R = G, right-looking on a working copy (row stride n+1): per
+// step k one thread forms r_kk (a pivot <= 0 or non-finite -> EBREAKDOWN(stage, k), SPEC
+// S:55, and the factorization stops), row k is divided by r_kk, and warp (j mod NW)
+// updates column j of the trailing matrix.
+template <bool SMEM>
+__global__ void __launch_bounds__(256)
+chol2_kernel(const double* __restrict__ G, int n, double* __restrict__ R, double* __restrict__ work, int stage,
+             unsigned long long* status) {
+  extern __shared__ double dsm[];
+  __shared__ int flag;
+  __shared__ double rkk_s;
+  const int ld = n + 1;
+  double* C = SMEM ? dsm : work;
+  const int lane = lane_id(), wp = warp_id(), nw = blockDim.x >> 5;
+  for (int i = wp; i < n; i += nw) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) v[q] = (lane + 32 * q < n) ? G[(int64_t)i * n + lane + 32 * q] : 0.0;
+    for (int j = lane + 128; j < n; j += 32) C[(int64_t)i * ld + j] = G[(int64_t)i * n + j];
+#pragma unroll
+    for (int q = 0; q < 4; q++) if (lane + 32 * q < n) C[(int64_t)i * ld + lane + 32 * q] = v[q];
+  }
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    if (threadIdx.x == 0) {
+      const double d = C[(int64_t)k * ld + k];
+      if (!(d > 0.0) || !isfinite(d)) { report(status, RLHC_EBREAKDOWN, stage, k); flag = 1; }
+      else { rkk_s = __dsqrt_rn(d); C[(int64_t)k * ld + k] = rkk_s; }
+    }
+    __syncthreads();
+    if (flag) break;
+    const double rkk = rkk_s;
+    for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x)
+      C[(int64_t)k * ld + j] = __ddiv_rn(C[(int64_t)k * ld + j], rkk);
+    __syncthreads();
+    for (int j = k + 1 + wp; j < n; j += nw) {
+      const double ckj = C[(int64_t)k * ld + j];
+      for (int i = k + 1 + lane; i <= j; i += 32)
+        C[(int64_t)i * ld + j] = __fma_rn(-C[(int64_t)k * ld + i], ckj, C[(int64_t)i * ld + j]);
+    }
+    __syncthreads();
+  }
+  for (int i = wp; i < n; i += nw)
+    for (int j = lane; j < n; j += 32) R[(int64_t)i * n + j] = (j >= i) ? C[(int64_t)i * ld + j] : 0.0;
+}
+
+// Register-resident Cholesky for n <= 32*RR (rows) and n <= 8*QC (columns): warp w owns
+// columns {w + 8 q}, lane l holds rows {l + 32 r}.  Step k: the owner of (k, k) forms
+// r_kk (breakdown check) -> barrier -> the holders of row k divide it by r_kk and publish
+// it through shared memory -> barrier -> every lane updates its entries (i, j), k < i <= j:
+// C_ij -= C_ki C_kj.  Same operation order per element as the smem kernel.
+constexpr int CH_WARPS = 8;
+
+template <int RR, int QC>
+__global__ void __launch_bounds__(32 * CH_WARPS)
+chol_reg_kernel(const double* __restrict__ G, int n, double* __restrict__ R, int stage, unsigned long long* status) {
+  __shared__ double rowk[2][CH_WARPS * QC];
+  __shared__ double rkk[2], rinv[2];
+  __shared__ int flag;
+  const int lane = lane_id(), wp = warp_id();
+  double c[RR][QC];
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int q = 0; q < QC; q++) {
+      const int i = lane + 32 * r, j = wp + CH_WARPS * q;
+      c[r][q] = (i < n && j < n) ? G[(int64_t)i * n + j] : 0.0;
+    }
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    const int par = k & 1;
+    const int kr = k >> 5, kq = k / CH_WARPS;
+    if (wp == (k % CH_WARPS) && lane == (k & 31)) {
+      double d = 0.0;
+#pragma unroll
+      for (int r = 0; r < RR; r++)
+#pragma unroll
+        for (int q = 0; q < QC; q++) d = (r == kr && q == kq) ? c[r][q] : d;
+      if (!(d > 0.0) || !isfinite(d)) { report(status, RLHC_EBREAKDOWN, stage, k); flag = 1; }
+      const double sq = __dsqrt_rn(d);
+      rkk[par] = sq;
+      rinv[par] = __drcp_rn(sq);
+    }
+    __syncthreads();
+    if (flag) break;
+    const double rk = rkk[par], ri_k = rinv[par];
+    if (lane == (k & 31)) {  // holders of row k: scale by 1/r_kk (one IEEE reciprocal per step) and publish
+#pragma unroll
+      for (int r = 0; r < RR; r++)
+        if (r == kr) {
+#pragma unroll
+          for (int q = 0; q < QC; q++) {
+            const int j = wp + CH_WARPS * q;
+            const double v = __dmul_rn(c[r][q], ri_k);
+            if (j == k) c[r][q] = rk;
+            else if (j > k && j < n) c[r][q] = v;
+            if (j > k && j < n) rowk[par][j] = v;
+          }
+        }
+    }
+    __syncthreads();
+    double rj[QC], ri[RR];
+#pragma unroll
+    for (int q = 0; q < QC; q++) {
+      const int j = wp + CH_WARPS * q;
+      rj[q] = (j > k && j < n) ? rowk[par][j] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      const int i = lane + 32 * r;
+      ri[r] = (i > k && i < n) ? rowk[par][i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < RR; r++)
+#pragma unroll
+      for (int q = 0; q < QC; q++) {
+        const int i = lane + 32 * r, j = wp + CH_WARPS * q;
+        if (i > k && i <= j) c[r][q] = __fma_rn(-ri[r], rj[q], c[r][q]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int q = 0; q < QC; q++) {
+      const int i = lane + 32 * r, j = wp + CH_WARPS * q;
+      if (i < n && j < n) R[(int64_t)i * n + j] = (j >= i) ? c[r][q] : 0.0;
+    }
+}
+
+size_t chol_ws_bytes(int n) { return (size_t)n * (n + 1) * sizeof(double); }
+
+cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
+                        cudaStream_t st) {
+  const size_t need = chol_ws_bytes(n);
+#define CHOL_REG(RR, QC)                                                                  \
+  if (n <= 32 * RR && n <= CH_WARPS * QC) {                                               \
+    note_launch();                                                                        \
+    chol_reg_kernel<RR, QC><<<1, 32 * CH_WARPS, 0, st>>>(G, n, R, stage, status);         \
+    return cudaGetLastError();                                                            \
+  }
+  CHOL_REG(1, 4)
+  CHOL_REG(2, 8)
+  CHOL_REG(4, 16)
+#undef CHOL_REG
+  if (need <= 200 * 1024) {
+    if (need > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(chol2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+      if (e) return e;
+    }
+    note_launch();
+    chol2_kernel<true><<<1, 256, need, st>>>(G, n, R, work, stage, status);
+  } else {
+    if (!work) return cudaErrorInvalidValue;
+    note_launch();
+    chol2_kernel<false><<<1, 256, 0, st>>>(G, n, R, work, stage, status);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rlhc

@@ -59,8 +59,6 @@ cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double*
 cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
                         cudaStream_t st);
 size_t chol_ws_bytes(int n);
-cudaError_t launch_chol_inv(const double* G, int n, double* R, double* Rinv, double* work, int stage,
-                            unsigned long long* status, cudaStream_t st);
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);
 cudaError_t launch_status_init(unsigned long long* status, cudaStream_t st);

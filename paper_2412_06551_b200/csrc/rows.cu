@@ -235,9 +235,13 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
   double* Tn = smem;              // -T, ncp x lds
   double* rd = Tn + ncp * lds;    // 1 / diag(T)
   double* S = rd + ncp;           // RS_TR x lds row tile
-  for (int k = threadIdx.x >> 3; k < ncp; k += blockDim.x >> 3)
-    for (int c = threadIdx.x & 7; c < ncp; c += 8) Tn[k * lds + c] = (k < n && c < n) ? -T[(int64_t)k * n + c] : 0.0;
+  // stage T with async copies (all in flight), then negate in shared memory
+  tile_load_async(Tn, lds, T, n, 0, n, ncp, n, ncp, ((n & 1) == 0) && ((((uintptr_t)T) & 15) == 0));
+  cp_async_commit();
   for (int k = threadIdx.x; k < ncp; k += blockDim.x) rd[k] = k < n ? rdiag[k] : 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < ncp * lds; idx += blockDim.x) Tn[idx] = -Tn[idx];
   const int64_t ntiles = ceil_div<int64_t>(rows, RS_TR);
   const int lane = lane_id(), w = warp_id();
   const int g = lane >> 2, t = lane & 3;

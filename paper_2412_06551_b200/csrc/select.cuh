@@ -32,12 +32,27 @@ struct SelSmem {
   int out_id[W];
 };
 
+// v[c - C_LO] = a[pslot][c] for a warp-uniform runtime slot (compile-time recursion over
+// slots -> a chain of uniform branches, each copying statically indexed registers)
+template <int W, int NW, int RS, int C_LO, int C_HI, int S>
+__device__ __forceinline__ void sel_extract(const double (&a)[RS][W / NW], int pslot, double* v) {
+  if constexpr (S < RS) {
+    if (pslot == S) {
+#pragma unroll
+      for (int c = C_LO; c < C_HI; c++) v[c - C_LO] = a[S][c];
+    } else {
+      sel_extract<W, NW, RS, C_LO, C_HI, S + 1>(a, pslot, v);
+    }
+  }
+}
+
 // Apply the published step (par) to columns [c_lo, c_hi) of this warp (compile-time
 // bounds), for the rows still active after removing the pivot row.
 template <int W, int NW, int RS, int C_LO, int C_HI>
 __device__ __forceinline__ void sel_apply(double (&a)[RS][W / NW], unsigned act, int pslot, int plane, int par,
                                           const SelSmem<W, NW, RS>& sm) {
   if (C_LO >= C_HI) return;
+  __syncwarp();
   double u[C_HI > C_LO ? C_HI - C_LO : 1];
 #pragma unroll
   for (int c = C_LO; c < C_HI; c++) {
@@ -46,14 +61,15 @@ __device__ __forceinline__ void sel_apply(double (&a)[RS][W / NW], unsigned act,
     for (int s = 0; s < RS; s++) v = (s == pslot) ? a[s][c] : v;
     u[c - C_LO] = __shfl_sync(0xffffffffu, v, plane);
   }
+  // applied to every slot without a branch (keeps the warp converged for the collectives
+  // that follow): rows no longer in the candidate set are never read again
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    if ((act >> s) & 1u) {
-      const double l = sm.l[par][s * 32 + lane_id()];
+    const double l = sm.l[par][s * 32 + lane_id()];
 #pragma unroll
-      for (int c = C_LO; c < C_HI; c++) a[s][c] = __fma_rn(-l, u[c - C_LO], a[s][c]);
-    }
+    for (int c = C_LO; c < C_HI; c++) a[s][c] = __fma_rn(-l, u[c - C_LO], a[s][c]);
   }
+  (void)act;
 }
 
 // Argmax + publish for pivot column CC of the calling (owner) warp, step t.
@@ -62,6 +78,7 @@ __device__ __forceinline__ void sel_pivot(double (&a)[RS][W / NW], unsigned act,
                                           SelSmem<W, NW, RS>& sm) {
   const int lane = lane_id();
   const int par = t & 1;
+  __syncwarp();
   long long bk = -1ll;
   int bid = INT_MAX, bs = 0;
 #pragma unroll
@@ -84,7 +101,7 @@ __device__ __forceinline__ void sel_pivot(double (&a)[RS][W / NW], unsigned act,
   const double pv = __shfl_sync(0xffffffffu, mv, plane);
   const int pslot = __shfl_sync(0xffffffffu, bs, plane);
   const bool zero = (mh == 0 && ml == 0u);
-  const double r = zero ? 0.0 : __ddiv_rn(1.0, pv);
+  const double r = zero ? 0.0 : __drcp_rn(pv);  // correctly rounded 1/pv (== IEEE 1.0/pv)
 #pragma unroll
   for (int s = 0; s < RS; s++) sm.l[par][s * 32 + lane] = zero ? 0.0 : __dmul_rn(a[s][CC], r);
   if (lane == 0) {
