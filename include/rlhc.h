@@ -167,6 +167,50 @@ int rlhc_hqr_r(const double* A, int64_t s, int64_t n, int64_t lda, const double*
  * EBREAKDOWN(stage, k) with the given stage tag. */
 int rlhc_cholesky(const double* G, int64_t n, double* Rout, int stage, rlhc_info_t* info, rlhc_stream_t stream);
 
+/* ------------------------------------------------- row-sharded (multi-GPU) building blocks */
+/* SURVEY 8(e), DESIGN.md section 7.  Rank r holds global rows [row0, row0 + rows); the
+ * orchestration (all-gather of tournament candidates, all-reduce of sketches / Grams /
+ * pivot rows) is done by the caller (paper_2412_06551_b200/dist.py, torch.distributed);
+ * every arithmetic step is one of these calls or a stage entry point above.
+ * Tournament "slot" = (ids int32[W], cnt int32[1], vals double[W*W]) with W = 16/32/64 the
+ * kernel width of cfg->panel: the winners of one tree node (global row ids in pivot
+ * order, their current panel values row-major with stride W). */
+size_t rlhc_tslu_local_workspace_size(int64_t rows, int64_t nslots_in, const rlhc_tslu_cfg* cfg);
+/* leaves of this rank's rows + all local tree levels down to ONE slot (panel columns
+ * [p0, p0 + w) of `src`; `chosen` (int8[rows], nullable) marks rows already pivots). */
+int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
+                     const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals,
+                     void* ws, size_t ws_bytes, rlhc_stream_t stream);
+/* the tree levels above `nslots` consecutive slots (e.g. the all-gathered rank roots). */
+int rlhc_tslu_combine(const int* in_ids, const int* in_cnt, const double* in_vals, int64_t nslots, int64_t w,
+                      const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals, void* ws, size_t ws_bytes,
+                      rlhc_stream_t stream);
+/* out (w x ncols) = rows ids[t] (global, int32 or int64 list) of src, columns [c0, c0+ncols),
+ * for the rows this rank owns, 0 otherwise (an all-reduce SUM then yields the rows exactly). */
+int rlhc_owned_rows(const double* src, int64_t lds, int64_t rows, int64_t row0, const int* ids32, const int64_t* ids64,
+                    int64_t w, int64_t c0, int64_t ncols, double* out, rlhc_stream_t stream);
+/* U rows p0..p0+w-1 (columns p0..n-1) from the pivot rows `prow` (w x (n - p0), pivot order,
+ * current values), piv[p0..), chosen[] of local pivot rows; zero pivot -> ERANKDEF(LU, k). */
+size_t rlhc_tslu_panel_workspace_size(int64_t n);
+int rlhc_tslu_panel_factor_rows(const double* prow, const int* ids, int64_t p0, int64_t w, int64_t n, int64_t row0,
+                                int64_t rows, double* U, int64_t* piv, uint8_t* chosen, void* ws, size_t ws_bytes,
+                                rlhc_info_t* info, rlhc_stream_t stream);
+/* trailing update of this rank's rows with panel [p0, p0+w): dst[:, p0+w:] (dst may be src). */
+size_t rlhc_tslu_eliminate_workspace_size(int64_t n);
+int rlhc_tslu_eliminate(const double* src, int64_t lds, int64_t rows, int64_t p0, int64_t w, int64_t n,
+                        const double* U, double* dst, int64_t ldd, void* ws, size_t ws_bytes, rlhc_stream_t stream);
+/* L11 from the pivot rows of X (n x n, pivot order) and U; L of this rank's rows. */
+size_t rlhc_lfactor_workspace_size(int64_t rows, int64_t n);
+int rlhc_l11(const double* Xp, int64_t n, const double* U, double* L11, void* ws, size_t ws_bytes,
+             rlhc_stream_t stream);
+int rlhc_lfactor(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const double* U, const double* L11,
+                 const int64_t* piv, double* L, int64_t ldl, void* ws, size_t ws_bytes, rlhc_stream_t stream);
+/* C = A B for n x n upper-triangular A, B (zero lower parts); Cholesky with workspace (any n). */
+int rlhc_trmm_upper(const double* A, const double* B, int64_t n, double* C, rlhc_stream_t stream);
+size_t rlhc_cholesky_workspace_size(int64_t n);
+int rlhc_cholesky_ws(const double* G, int64_t n, double* Rout, int stage, void* ws, size_t ws_bytes, rlhc_info_t* info,
+                     rlhc_stream_t stream);
+
 /* Library identification and the last host-side error message (thread-local). */
 const char* rlhc_version(void);
 const char* rlhc_last_error(void);

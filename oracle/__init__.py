@@ -72,6 +72,10 @@ def lib():
         L.ora_orthogonality.argtypes = [P, I64, I64, I64]; L.ora_orthogonality.restype = D
         L.ora_residual.argtypes = [P, P, P, I64, I64, I64, I64]; L.ora_residual.restype = D
         L.ora_num_threads.restype = ctypes.c_int
+        L.ora_select.argtypes = [P, P, I64, I64, P]; L.ora_select.restype = I64
+        L.ora_panel_rows.argtypes = [P, I64, I64]
+        L.ora_eliminate_rows.argtypes = [P, I64, I64, I64, I64, P, P]
+        L.ora_lfactor_rows.argtypes = [P, I64, I64, I64, P, P, P, P]
     return _lib
 
 
@@ -258,6 +262,36 @@ def orthogonality(Q) -> float:
 def residual(Q, R, X) -> float:
     Q = _f64(Q); R = _f64(R); X = _f64(X); m, n = Q.shape
     return lib().ora_residual(_p(Q), _p(R), _p(X), m, n, n, n)
+
+
+# ---- pieces for the row-sharded orchestration check (tests/test_dist_cpu.py)
+def select(B, ids, w: int):
+    """GEPP selection on candidate rows B (cnt x w) with global ids: winners in pivot order."""
+    B = _f64(B).copy(); ids = np.ascontiguousarray(ids, np.int64)
+    out = np.zeros(max(w, 1), np.int64)
+    k = lib().ora_select(_p(B), _p(ids), len(ids), w, _p(out))
+    return out[:k]
+
+
+def panel_rows(prow):
+    prow = _f64(prow).copy(); w, ncols = prow.shape
+    lib().ora_panel_rows(_p(prow), w, ncols)
+    return prow
+
+
+def eliminate_rows(A, p0: int, w: int, U, chosen):
+    A = _f64(A); U = _f64(U); rows, n = A.shape
+    ch = np.ascontiguousarray(chosen, np.uint8)
+    lib().ora_eliminate_rows(_p(A), rows, n, p0, w, _p(U), _p(ch))
+    return A
+
+
+def lfactor_rows(X, row0: int, piv, U, L11):
+    X = _f64(X); rows, n = X.shape
+    piv = np.ascontiguousarray(piv, np.int64); U = _f64(U); L11 = _f64(L11)
+    L = np.zeros((rows, n))
+    lib().ora_lfactor_rows(_p(X), rows, n, row0, _p(piv), _p(U), _p(L11), _p(L))
+    return L
 
 
 def num_threads() -> int:

@@ -671,6 +671,58 @@ double ora_residual(const double* Q, const double* R, const double* X, int64_t m
   return (double)sqrtl(num / den);
 }
 
+/* ---------------------------------------------- pieces for the row-sharded check */
+/* (Used only by tests/test_dist_cpu.py: the oracle-side stages of one rank.  Same
+ * arithmetic as ora_tslu, split at the points where the distributed algorithm exchanges
+ * data.) */
+
+/* GEPP selection on cnt candidate rows (B, cnt x w, overwritten), R#4-R#5 */
+int64_t ora_select(double* B, const int64_t* ids, int64_t cnt, int64_t w, int64_t* out_ids) {
+  return gepp_select(B, ids, cnt, w, out_ids);
+}
+
+/* U rows of one panel from its w pivot rows (prow, w x ncols, pivot order, columns
+ * p0..p0+ncols-1): the elimination of ora_tslu restricted to the pivot rows. */
+void ora_panel_rows(double* prow, int64_t w, int64_t ncols) {
+  for (int64_t k = 0; k < w; k++) {
+    double r = 1.0 / prow[k * ncols + k];
+    for (int64_t t = k + 1; t < w; t++) {
+      double l = prow[t * ncols + k] * r;
+      prow[t * ncols + k] = l;
+      for (int64_t j = k + 1; j < ncols; j++) prow[t * ncols + j] = fma(-l, prow[k * ncols + j], prow[t * ncols + j]);
+    }
+  }
+}
+
+/* eliminate rows (A, rows x n, current values) with the panel pivots k = p0..p0+w-1 of U
+ * (skipping rows flagged in chosen): the elimination loop of ora_tslu. */
+void ora_eliminate_rows(double* A, int64_t rows, int64_t n, int64_t p0, int64_t w, const double* U,
+                        const unsigned char* chosen) {
+  for (int64_t k = p0; k < p0 + w; k++) {
+    double r = 1.0 / U[k * n + k];
+    for (int64_t i = 0; i < rows; i++) {
+      if (chosen && chosen[i]) continue;
+      double* a = A + i * n;
+      double l = a[k] * r;
+      a[k] = l;
+      for (int64_t j = k + 1; j < n; j++) a[j] = fma(-l, U[k * n + j], a[j]);
+    }
+  }
+}
+
+/* L rows of X rows with global ids row0.. (pivot rows take L11 rows) */
+void ora_lfactor_rows(const double* X, int64_t rows, int64_t n, int64_t row0, const int64_t* piv, const double* U,
+                      const double* L11, double* L) {
+  double* rd = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int64_t k = 0; k < n; k++) rd[k] = 1.0 / U[k * n + k];
+  for (int64_t i = 0; i < rows; i++) {
+    int64_t pp = -1;
+    for (int64_t k = 0; k < n; k++) if (piv[k] == row0 + i) pp = k;
+    l_row(X + i * n, n, U, rd, L11, pp, L + i * n);
+  }
+  free(rd);
+}
+
 int ora_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

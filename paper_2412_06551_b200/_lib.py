@@ -80,6 +80,29 @@ def lib():
     L.rlhc_cholesky.argtypes = [P, I64, P, I, P, P]
     L.rlhc_version.restype = ctypes.c_char_p
     L.rlhc_last_error.restype = ctypes.c_char_p
+    # row-sharded building blocks
+    L.rlhc_tslu_local_workspace_size.argtypes = [I64, I64, PC]
+    L.rlhc_tslu_local_workspace_size.restype = SZ
+    L.rlhc_tslu_reduce.argtypes = [P, I64, I64, I64, I64, I64, P, PC, P, P, P, P, SZ, P]
+    L.rlhc_tslu_combine.argtypes = [P, P, P, I64, I64, PC, P, P, P, P, SZ, P]
+    L.rlhc_owned_rows.argtypes = [P, I64, I64, I64, P, P, I64, I64, I64, P, P]
+    L.rlhc_tslu_panel_workspace_size.argtypes = [I64]
+    L.rlhc_tslu_panel_workspace_size.restype = SZ
+    L.rlhc_tslu_panel_factor_rows.argtypes = [P, P, I64, I64, I64, I64, I64, P, P, P, P, SZ, P, P]
+    L.rlhc_tslu_eliminate_workspace_size.argtypes = [I64]
+    L.rlhc_tslu_eliminate_workspace_size.restype = SZ
+    L.rlhc_tslu_eliminate.argtypes = [P, I64, I64, I64, I64, I64, P, P, I64, P, SZ, P]
+    L.rlhc_lfactor_workspace_size.argtypes = [I64, I64]
+    L.rlhc_lfactor_workspace_size.restype = SZ
+    L.rlhc_l11.argtypes = [P, I64, P, P, P, SZ, P]
+    L.rlhc_lfactor.argtypes = [P, I64, I64, I64, I64, P, P, P, P, I64, P, SZ, P]
+    L.rlhc_trmm_upper.argtypes = [P, P, I64, P, P]
+    L.rlhc_cholesky_workspace_size.argtypes = [I64]
+    L.rlhc_cholesky_workspace_size.restype = SZ
+    L.rlhc_cholesky_ws.argtypes = [P, I64, P, I, P, SZ, P, P]
+    for name in ("rlhc_tslu_reduce", "rlhc_tslu_combine", "rlhc_owned_rows", "rlhc_tslu_panel_factor_rows",
+                 "rlhc_tslu_eliminate", "rlhc_l11", "rlhc_lfactor", "rlhc_trmm_upper", "rlhc_cholesky_ws"):
+        getattr(L, name).restype = I
     L.rlhc_launch_count.restype = ctypes.c_uint64
     L.rlhc_stage_timing.argtypes = [I]
     L.rlhc_stage_timing.restype = None
@@ -100,7 +123,11 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_sketch_gauss", "rlhc_sketch_count_workspace_size", "rlhc_sketch_count",
             "rlhc_gram_workspace_size", "rlhc_gram", "rlhc_trsm_apply_workspace_size", "rlhc_trsm_apply",
             "rlhc_hqr_workspace_size", "rlhc_hqr_r", "rlhc_cholesky", "rlhc_version", "rlhc_last_error",
-            "rlhc_launch_count", "rlhc_stage_timing", "rlhc_stage_times", "rlhc_stage_name"]
+            "rlhc_launch_count", "rlhc_stage_timing", "rlhc_stage_times", "rlhc_stage_name",
+            "rlhc_tslu_local_workspace_size", "rlhc_tslu_reduce", "rlhc_tslu_combine", "rlhc_owned_rows",
+            "rlhc_tslu_panel_workspace_size", "rlhc_tslu_panel_factor_rows", "rlhc_tslu_eliminate_workspace_size",
+            "rlhc_tslu_eliminate", "rlhc_lfactor_workspace_size", "rlhc_l11", "rlhc_lfactor", "rlhc_trmm_upper",
+            "rlhc_cholesky_workspace_size", "rlhc_cholesky_ws"]
 NUM_TIMED_STAGES = 11
 
 

@@ -3,9 +3,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace rlhc {
 
 int select_rows(int W);
+void set_last_error(const std::string& msg);
 unsigned long long launch_count();
 
 // tslu.cu
@@ -15,7 +18,8 @@ cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const 
                              int w, int* ids, int* cnt, double* vals, cudaStream_t st);
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
                                      const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
-                                     uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st);
+                                     uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st,
+                                     int packed = 0);
 cudaError_t launch_l11_fixup(double* L11, int n, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, const int64_t* ids, int64_t row0, int cnt, int ncols,
                                double* dst, int64_t ldd, cudaStream_t st);
@@ -41,6 +45,8 @@ size_t rowsolve_partials_bytes(int64_t rows, int n);
 cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
                             double* out, int64_t ldo, const int64_t* piv, const double* L11, double* gpart, double* G,
                             cudaStream_t st);
+cudaError_t launch_pivot_rows(const int64_t* piv, int n, int64_t row0, int64_t rows, const double* L11, double* out,
+                              int64_t ldo, cudaStream_t st);
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st);
 
 // sketch.cu

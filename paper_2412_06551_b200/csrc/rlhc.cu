@@ -15,6 +15,9 @@
 using namespace rlhc;
 
 static thread_local std::string g_last_error;
+namespace rlhc {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace rlhc
 
 static int fail(int code, const char* msg) {
   g_last_error = msg;

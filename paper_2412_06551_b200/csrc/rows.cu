@@ -415,6 +415,13 @@ gram_part_reduce_kernel(const double* __restrict__ part, int nparts, int n, int 
   }
 }
 
+cudaError_t launch_pivot_rows(const int64_t* piv, int n, int64_t row0, int64_t rows, const double* L11, double* out,
+                              int64_t ldo, cudaStream_t st) {
+  note_launch();
+  pivot_rows_kernel<<<n, 64, 0, st>>>(piv, n, row0, rows, L11, out, ldo);
+  return cudaGetLastError();
+}
+
 static size_t rowsolve_smem(int n) {
   const int ncp = (n + 7) & ~7, lds = ncp + 4;
   return ((size_t)ncp * lds + ncp + (size_t)RS_TR * lds) * sizeof(double);

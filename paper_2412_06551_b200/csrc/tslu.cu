@@ -104,9 +104,10 @@ __global__ void __launch_bounds__(512)
 tslu_panel_factor_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                          int n, const int* __restrict__ root_ids, const int* __restrict__ root_cnt, double* __restrict__ U,
                          int64_t* __restrict__ piv, uint8_t* __restrict__ chosen, double* __restrict__ lpanel,
-                         unsigned long long* status) {
+                         unsigned long long* status, int packed) {
   __shared__ double P[64][65];
   __shared__ int ids[64];
+  __shared__ int64_t srow[64];  // row of src holding pivot t (packed: row t)
   const int tid = threadIdx.x;
   if (tid == 0 && root_cnt[0] < w) report(status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + root_cnt[0]);
   for (int t = tid; t < w; t += blockDim.x) {
@@ -115,11 +116,12 @@ tslu_panel_factor_kernel(const double* __restrict__ src, int64_t lds, int64_t ro
     piv[p0 + t] = g;
     int64_t lr = (int64_t)ids[t] - row0;
     if (chosen && lr >= 0 && lr < rows) chosen[lr] = 1;
+    srow[t] = packed ? t : lr;
   }
   __syncthreads();
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
     int t = idx / w, c = idx - t * w;
-    P[t][c] = src[((int64_t)ids[t] - row0) * lds + p0 + c];
+    P[t][c] = src[srow[t] * lds + p0 + c];
   }
   __syncthreads();
   // phase A: right-looking elimination of the w x w block (P[t][t'] <- multiplier for
@@ -160,7 +162,7 @@ tslu_panel_factor_kernel(const double* __restrict__ src, int64_t lds, int64_t ro
 #pragma unroll
     for (int t = 0; t < 64; t++) {
       if (t < w) {
-        double v = src[((int64_t)ids[t] - row0) * lds + j];
+        double v = src[srow[t] * lds + j];
 #pragma unroll
         for (int tp = 0; tp < 64; tp++)
           if (tp < t) v = __fma_rn(-P[t][tp], u[tp], v);
@@ -233,9 +235,10 @@ cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const 
 }
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
                                      const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
-                                     uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st) {
+                                     uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st,
+                                     int packed) {
   note_launch(); tslu_panel_factor_kernel<<<1, 512, 0, st>>>(src, lds, rows, row0, p0, w, n, root_ids, root_cnt, U, piv, chosen,
-                                              lpanel, status);
+                                              lpanel, status, packed);
   return cudaGetLastError();
 }
 cudaError_t launch_l11_fixup(double* L11, int n, cudaStream_t st) {

@@ -50,12 +50,18 @@ def _gen(seed: int, device) -> torch.Generator:
     return g
 
 
+CHUNK = 1 << 16  # rows per independently seeded chunk of A (any aligned row range can be generated alone)
+
+
 def baseline_matrix(m: int, n: int, kappa_exp: float, seed: int, colscale: bool = False, device="cpu",
-                    chunk_rows: int = 1 << 20) -> torch.Tensor:
+                    row0: int = 0, rows: int | None = None) -> torch.Tensor:
     """X = A diag(sigma) V^T (BASELINE.json configs): A iid N(0, 1/m) m x n, V the
     Q factor of an iid N(0,1) n x n matrix, sigma_k = 10^(-kappa_exp k/(n-1)); optional
-    column scaling by 10^u, u ~ U[-3, 3] (cfg3).  Generated in row chunks on `device`."""
+    column scaling by 10^u, u ~ U[-3, 3] (cfg3).  Rows [row0, row0 + rows) of X (default: all),
+    generated on `device`; A's rows come in chunks of CHUNK rows, each from its own seeded
+    stream, so a row shard is bitwise the same rows of the full matrix."""
     dev = torch.device(device)
+    rows = m - row0 if rows is None else rows
     g = _gen(seed, dev)
     Vg = torch.randn(n, n, generator=g, device=dev, dtype=torch.float64)
     V, Rv = torch.linalg.qr(Vg)
@@ -67,12 +73,15 @@ def baseline_matrix(m: int, n: int, kappa_exp: float, seed: int, colscale: bool 
     if colscale:
         u = torch.rand(n, generator=g, device=dev, dtype=torch.float64) * 6.0 - 3.0
         B = B * torch.pow(torch.tensor(10.0, device=dev, dtype=torch.float64), u).unsqueeze(0)
-    X = torch.empty(m, n, device=dev, dtype=torch.float64)
+    X = torch.empty(rows, n, device=dev, dtype=torch.float64)
     scale = 1.0 / math.sqrt(m)
-    for r0 in range(0, m, chunk_rows):
-        r1 = min(m, r0 + chunk_rows)
-        A = torch.randn(r1 - r0, n, generator=g, device=dev, dtype=torch.float64) * scale
-        torch.matmul(A, B, out=X[r0:r1])
+    c_lo, c_hi = row0 // CHUNK, (row0 + rows + CHUNK - 1) // CHUNK
+    for c in range(c_lo, c_hi):
+        gc = _gen(seed * 7919 + 1 + c, dev)
+        a0, a1 = c * CHUNK, min(m, (c + 1) * CHUNK)
+        A = torch.randn(a1 - a0, n, generator=gc, device=dev, dtype=torch.float64) * scale
+        lo, hi = max(a0, row0), min(a1, row0 + rows)
+        torch.matmul(A[lo - a0:hi - a0], B, out=X[lo - row0:hi - row0])
     return X
 
 

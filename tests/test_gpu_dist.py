@@ -1,0 +1,75 @@
+"""GPU checks of the row-sharded path (paper_2412_06551_b200.dist) through the C ABI:
+world size 1 against the single-call pipeline, and world size 2 over gloo (both ranks on
+cuda:0; gloo collectives are host-mediated, so no kernel waits on another rank) against
+the oracle."""
+import os
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def test_world1_matches_single_call(ora):
+    import paper_2412_06551_b200 as rl
+    import synth
+    from paper_2412_06551_b200._lib import TsluCfg
+    from paper_2412_06551_b200.dist import DistPlan
+    for algo, m, n, kw, cfgt in [("sslhc3", 65536, 64, dict(s1=512, s2=128), (256, 2, 64)),
+                                 ("slhc3", 32768, 32, dict(s=64), (512, 2, 32)),
+                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64))]:
+        X = synth.baseline_matrix(m, n, 10, 7, device="cuda")
+        cfg = TsluCfg(*cfgt)
+        plan = DistPlan(algo, m, n, seed=2, cfg=cfg, device="cuda", **kw)
+        Q, R, piv, infos = plan.run(X)
+        assert plan.first_error(infos) == (0, 0, 0)
+        single = (rl.slhc3 if algo == "slhc3" else rl.sslhc3)(X, seed=2, cfg=cfg, **kw)
+        assert torch.equal(piv, single.piv)
+        Rh, Rs = R.cpu().numpy(), single.R.cpu().numpy()
+        assert np.linalg.norm(Rh - Rs) <= 1e-12 * np.linalg.norm(Rs)
+        Qh = Q.cpu().numpy()
+        assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) <= 1e-13 * np.sqrt(n)
+
+
+def _worker(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_2412_06551_b200._lib import TsluCfg
+        from paper_2412_06551_b200.dist import DistPlan
+        m, n = 32768, 48
+        cfg = TsluCfg(256, 2, 48)
+        mloc = m // world
+        X = synth.baseline_matrix(m, n, 9, 4, device="cuda", row0=rank * mloc, rows=mloc)
+        plan = DistPlan("sslhc3", m, n, s1=384, s2=96, seed=6, cfg=cfg, device="cuda")
+        Q, R, piv, infos = plan.run(X)
+        torch.cuda.synchronize()
+        np.savez(out_path + f".{rank}.npz", Q=Q.cpu().numpy(), R=R.cpu().numpy(), piv=piv.cpu().numpy(),
+                 info=np.array(plan.first_error(infos)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_on_one_gpu(ora):
+    import synth
+    d = tempfile.mkdtemp()
+    out = os.path.join(d, "r")
+    mp.spawn(_worker, args=(2, 29700 + os.getpid() % 200, out), nprocs=2, join=True)
+    res = [np.load(out + f".{r}.npz") for r in range(2)]
+    X = synth.baseline_matrix(32768, 48, 9, 4, device="cuda").cpu().numpy()
+    ref = ora.sslhc3(X, 384, 96, 6, 256, 2, 48)
+    for r in res:
+        assert tuple(r["info"]) == (0, 0, 0)
+        assert np.array_equal(r["piv"], ref.piv)
+        assert np.linalg.norm(r["R"] - ref.R) <= 1e-12 * np.linalg.norm(ref.R)
+    Q = np.concatenate([r["Q"] for r in res])
+    assert np.linalg.norm(Q.T @ Q - np.eye(48)) <= 1e-13 * np.sqrt(48)
