@@ -45,6 +45,9 @@ size_t rowsolve_partials_bytes(int64_t rows, int n);
 cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
                             double* out, int64_t ldo, const int64_t* piv, const double* L11, double* gpart, double* G,
                             cudaStream_t st);
+// blocked substitution for any n (rowsolve on 64-column panels + DMMA trailing updates)
+cudaError_t launch_trsm_blocked(const double* A, int64_t lda, int64_t rows, int n, int nsub, const double* T,
+                                int64_t ldt, const double* rdiag, double* out, int64_t ldo, cudaStream_t st);
 cudaError_t launch_pivot_rows(const int64_t* piv, int n, int64_t row0, int64_t rows, const double* L11, double* out,
                               int64_t ldo, cudaStream_t st);
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st);

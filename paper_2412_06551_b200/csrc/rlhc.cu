@@ -211,7 +211,8 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
     if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
     } else {
-      CUDA_TRY(launch_trsm_rows(A, lda, m, ni, ni, T, n, rd, Q, ldq, pp, l11, n, st));
+      CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
+      if (pp) CUDA_TRY(launch_pivot_rows(piv, ni, 0, m, l11, Q, ldq, st));
       if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     }
     return RLHC_OK;
@@ -377,9 +378,9 @@ int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t
   int rc = run_tslu(X, rows, n, ldx, row0, cfg, t, tw, n, piv, U, L11, st);
   if (rc) return rc;
   if (L) {
-    CUDA_TRY(launch_fill_i32(pivpos, rows, -1, st));
-    CUDA_TRY(launch_pivpos(piv, (int)n, row0, rows, pivpos, st));
-    CUDA_TRY(launch_trsm_rows(X, ldx, rows, (int)n, (int)n, U, n, t.rd, L, ldl, pivpos, L11, n, st));
+    (void)pivpos;
+    CUDA_TRY(launch_trsm_blocked(X, ldx, rows, (int)n, (int)n, U, n, t.rd, L, ldl, st));
+    CUDA_TRY(launch_pivot_rows(piv, (int)n, row0, rows, L11, L, ldl, st));
   }
   CUDA_TRY(launch_status_finish(t.status, info, st));
   return RLHC_OK;

@@ -161,6 +161,8 @@ cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int nco
                              int64_t ldt, const double* rdiag, double* out, int64_t ldo, const int* pivpos,
                              const double* L11, int64_t ldl11, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
+  // without a pivot-row override the blocked path (same fma chain, much faster) is used
+  if (!pivpos) return launch_trsm_blocked(A, lda, rows, ncols, nsub, T, ldt, rdiag, out, ldo, st);
   const int ncp = (ncols + 7) & ~7;
   // rows per CTA: keep the tile <= ~100 KB (2 CTAs / SM)
   int nwarp = 4;
@@ -227,7 +229,7 @@ __device__ __forceinline__ void tile_load_async(double* S, int lds, const double
 
 template <bool GRAM>
 __global__ void __launch_bounds__(32 * RS_WARPS, 2)
-rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double* __restrict__ T,
+rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double* __restrict__ T, int64_t ldt,
                 const double* __restrict__ rdiag, double* out, int64_t ldo, double* __restrict__ gpart) {
   extern __shared__ double smem[];
   const int ncp = (n + 7) & ~7;
@@ -236,7 +238,7 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
   double* rd = Tn + ncp * lds;    // 1 / diag(T)
   double* S = rd + ncp;           // RS_TR x lds row tile
   // stage T with async copies (all in flight), then negate in shared memory
-  tile_load_async(Tn, lds, T, n, 0, n, ncp, n, ncp, ((n & 1) == 0) && ((((uintptr_t)T) & 15) == 0));
+  tile_load_async(Tn, lds, T, ldt, 0, n, ncp, n, ncp, ((ldt & 1) == 0) && ((((uintptr_t)T) & 15) == 0));
   cp_async_commit();
   for (int k = threadIdx.x; k < ncp; k += blockDim.x) rd[k] = k < n ? rdiag[k] : 0.0;
   cp_async_wait_all();
@@ -438,15 +440,122 @@ size_t rowsolve_partials_bytes(int64_t rows, int n) {
 }
 
 template <bool GRAM>
-static cudaError_t run_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T,
+static cudaError_t run_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,
                                 const double* rdiag, double* out, int64_t ldo, double* gpart, cudaStream_t st) {
   size_t smem = rowsolve_smem(n);
   cudaError_t e = cudaFuncSetAttribute(rowsolve_kernel<GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   note_launch();
-  rowsolve_kernel<GRAM><<<rowsolve_grid(rows, n), 32 * RS_WARPS, smem, st>>>(A, lda, rows, n, T, rdiag, out, ldo,
-                                                                            gpart);
+  rowsolve_kernel<GRAM><<<rowsolve_grid(rows, n), 32 * RS_WARPS, smem, st>>>(A, lda, rows, n, T, ldt, rdiag, out,
+                                                                            ldo, gpart);
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ blocked TRSM (n > 64)
+// C_out = C_in - A B (rows x N, K <= 64) on DMMA, the chain over k in increasing order:
+// the trailing update of one 64-column panel of the blocked substitution.  Tile 64 x 64,
+// 4 warps (32 x 32 each); A (64 x K) and B (K x 64) staged with cp.async.
+constexpr int GU_T = 64;
+
+__global__ void __launch_bounds__(128)
+gemm_update_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* __restrict__ A,
+                   int64_t lda, const double* __restrict__ B, int64_t ldb, int64_t rows, int K, int N) {
+  constexpr int KC = 32;  // k chunk
+  __shared__ __align__(16) double As[GU_T][KC + 4];
+  __shared__ __align__(16) double Bs[KC][GU_T + 4];
+  const int64_t r0 = (int64_t)blockIdx.x * GU_T;
+  const int c0 = blockIdx.y * GU_T;
+  const int lane = lane_id(), w = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int wi = (w >> 1) * 32, wj = (w & 1) * 32;
+  const bool al_a = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+  const bool al_b = ((ldb & 1) == 0) && ((((uintptr_t)B) & 15) == 0);
+  auto load_chunk = [&](int kc) {
+    for (int idx = threadIdx.x; idx < GU_T * (KC / 2); idx += blockDim.x) {  // A: 64 rows x KC k
+      const int r = idx / (KC / 2), c = 2 * (idx % (KC / 2));
+      const int64_t gr = r0 + r;
+      const int k = kc + c;
+      double* dst = &As[r][c];
+      const double* src = A + gr * lda + k;
+      if (gr < rows && al_a && k + 1 < K) cp_async16(dst, src);
+      else { dst[0] = (gr < rows && k < K) ? src[0] : 0.0; dst[1] = (gr < rows && k + 1 < K) ? src[1] : 0.0; }
+    }
+    for (int idx = threadIdx.x; idx < KC * (GU_T / 2); idx += blockDim.x) {  // B: KC k x 64 columns
+      const int r = idx / (GU_T / 2), c = 2 * (idx % (GU_T / 2));
+      const int k = kc + r;
+      double* dst = &Bs[r][c];
+      const double* src = B + (int64_t)k * ldb + c0 + c;
+      if (k < K && al_b && c0 + c + 1 < N) cp_async16(dst, src);
+      else { dst[0] = (k < K && c0 + c < N) ? src[0] : 0.0; dst[1] = (k < K && c0 + c + 1 < N) ? src[1] : 0.0; }
+    }
+    cp_async_commit();
+  };
+  load_chunk(0);
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int64_t gr = r0 + wi + a * 8 + g;
+      const int c = c0 + wj + b * 8 + 2 * t;
+      acc[a][b][0] = (gr < rows && c < N) ? Cin[gr * ldci + c] : 0.0;
+      acc[a][b][1] = (gr < rows && c + 1 < N) ? Cin[gr * ldci + c + 1] : 0.0;
+    }
+  for (int kc = 0; kc < K; kc += KC) {
+    cp_async_wait_all();
+    __syncthreads();
+    for (int k0 = 0; k0 < KC && kc + k0 < K; k0 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) af[a] = -As[wi + a * 8 + g][k0 + t];
+#pragma unroll
+      for (int b = 0; b < 4; b++) bf[b] = Bs[k0 + t][wj + b * 8 + g];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+    if (kc + KC < K) load_chunk(kc + KC);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int64_t gr = r0 + wi + a * 8 + g;
+      const int c = c0 + wj + b * 8 + 2 * t;
+      if (gr < rows) {
+        if (c < N) Cout[gr * ldco + c] = acc[a][b][0];
+        if (c + 1 < N) Cout[gr * ldco + c + 1] = acc[a][b][1];
+      }
+    }
+}
+
+// out = A T^{-1} (rows x n, substitution, the oracle's fma chain) for any n: panels of 64
+// columns solved by rowsolve_kernel, each followed by the DMMA update of the trailing columns.
+// With nsub < n only the first nsub columns are substituted (the rest receive the updates):
+// the elimination step of a tournament panel.
+cudaError_t launch_trsm_blocked(const double* A, int64_t lda, int64_t rows, int n, int nsub, const double* T,
+                                int64_t ldt, const double* rdiag, double* out, int64_t ldo, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  for (int p0 = 0; p0 < nsub; p0 += 64) {
+    const int w = std::min(64, nsub - p0);
+    const double* src = (p0 == 0) ? A : out;
+    const int64_t lds_ = (p0 == 0) ? lda : ldo;
+    cudaError_t e = run_rowsolve<false>(src + p0, lds_, rows, w, T + (int64_t)p0 * ldt + p0, ldt, rdiag + p0,
+                                        out + p0, ldo, nullptr, st);
+    if (e) return e;
+    const int N = n - p0 - w;
+    if (N > 0) {
+      dim3 grid((unsigned)ceil_div<int64_t>(rows, GU_T), (unsigned)ceil_div(N, GU_T));
+      note_launch();
+      gemm_update_kernel<<<grid, 128, 0, st>>>(src + p0 + w, lds_, out + p0 + w, ldo, out + p0, ldo,
+                                               T + (int64_t)p0 * ldt + p0 + w, ldt, rows, w, N);
+      e = cudaGetLastError();
+      if (e) return e;
+    }
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
@@ -454,8 +563,8 @@ cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, c
                             cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   const bool gram = G != nullptr;
-  cudaError_t e = gram ? run_rowsolve<true>(A, lda, rows, n, T, rdiag, out, ldo, gpart, st)
-                       : run_rowsolve<false>(A, lda, rows, n, T, rdiag, out, ldo, gpart, st);
+  cudaError_t e = gram ? run_rowsolve<true>(A, lda, rows, n, T, n, rdiag, out, ldo, gpart, st)
+                       : run_rowsolve<false>(A, lda, rows, n, T, n, rdiag, out, ldo, gpart, st);
   if (e) return e;
   if (piv) {
     note_launch();
