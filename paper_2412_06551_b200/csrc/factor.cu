@@ -410,21 +410,179 @@ chol_reg_kernel(const double* __restrict__ G, int n, double* __restrict__ R, int
     }
 }
 
-size_t chol_ws_bytes(int n) { return (size_t)n * (n + 1) * sizeof(double); }
+// ------------------------------------------------------------------ blocked Cholesky
+// Single CTA, n <= 128, the matrix in shared memory (row stride ncp + 4).  Blocks of 8:
+//   (1) 8 threads factor the 8 x 8 diagonal block (right-looking, r_kk = sqrt, row scaled by
+//       1/r_kk; a pivot <= 0 or non-finite -> EBREAKDOWN(stage, koff + k));
+//   (2) thread per trailing column solves R_pp^T x = C[p:p+8, j] (8 x 8 forward substitution);
+//   (3) the trailing upper triangle is updated on DMMA: C_ij -= sum_k R_ki R_kj.
+// G is read with row stride ldg and R written with stride ldr (strict lower part 0), so the
+// kernel also serves as the diagonal-block factorization of the 64-blocked large-n path.
+__global__ void __launch_bounds__(256)
+chol_blk_kernel(const double* __restrict__ G, int64_t ldg, int n, double* __restrict__ R, int64_t ldr, int stage,
+                int koff, unsigned long long* status) {
+  extern __shared__ double C[];
+  __shared__ double rdiag_s[8];
+  __shared__ int flag;
+  const int ncp = (n + 7) & ~7;
+  const int ld = ncp + 4;
+  const int lane = lane_id(), wp = warp_id(), nw = blockDim.x >> 5;
+  for (int i = wp; i < ncp; i += nw)
+    for (int j = lane; j < ncp; j += 32) C[i * ld + j] = (i < n && j < n) ? G[(int64_t)i * ldg + j] : (i == j ? 1.0 : 0.0);
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  for (int p = 0; p < ncp; p += 8) {
+    // (1) diagonal block in warp 0: lane l (< 8) holds column p+l of the block in registers,
+    //     rows broadcast by shuffles, static indices throughout
+    if (wp == 0) {
+      const int l = lane & 7;
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; r++) v[r] = C[(p + r) * ld + p + l];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const double d = __shfl_sync(0xffffffffu, v[k], k);
+        if (lane == 0 && (!(d > 0.0) || !isfinite(d)) && p + k < n) {
+          report(status, RLHC_EBREAKDOWN, stage, koff + p + k);
+          flag = 1;
+        }
+        const double rk = __dsqrt_rn(d);
+        const double ri = __drcp_rn(rk);
+        if (l == k) v[k] = rk;
+        else if (l > k) v[k] = __dmul_rn(v[k], ri);
+#pragma unroll
+        for (int r = k + 1; r < 8; r++) {
+          const double rkr = __shfl_sync(0xffffffffu, v[k], r);
+          if (l >= r) v[r] = __fma_rn(-rkr, v[k], v[r]);
+        }
+        if (lane == k) rdiag_s[k] = ri;
+      }
+      if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < 8; r++) C[(p + r) * ld + p + l] = v[r];
+      }
+    }
+    __syncthreads();
+    if (flag) break;
+    // (2) panel rows: R[p:p+8, j] = R_pp^{-T} C[p:p+8, j]
+    for (int j = p + 8 + threadIdx.x; j < ncp; j += blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        double a = C[(p + k) * ld + j];
+#pragma unroll
+        for (int i = 0; i < k; i++) a = __fma_rn(-C[(p + i) * ld + p + k], x[i], a);
+        x[k] = __dmul_rn(a, rdiag_s[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) C[(p + k) * ld + j] = x[k];
+    }
+    __syncthreads();
+    // (3) trailing update on DMMA, 8 x 8 output tiles (I <= J) over the warps
+    const int q0 = p + 8, nt = (ncp - q0) / 8;
+    const int g = lane >> 2, t = lane & 3;
+    for (int tl = wp; tl < nt * nt; tl += nw) {
+      const int I = tl / nt, J = tl - I * nt;
+      if (I > J) continue;
+      const int i0 = q0 + 8 * I, j0 = q0 + 8 * J;
+      double c0 = C[(i0 + g) * ld + j0 + 2 * t], c1 = C[(i0 + g) * ld + j0 + 2 * t + 1];
+#pragma unroll
+      for (int k0 = 0; k0 < 8; k0 += 4) {
+        const double a = -C[(p + k0 + t) * ld + i0 + g];
+        const double b = C[(p + k0 + t) * ld + j0 + g];
+        dmma(c0, c1, a, b);
+      }
+      C[(i0 + g) * ld + j0 + 2 * t] = c0;
+      C[(i0 + g) * ld + j0 + 2 * t + 1] = c1;
+    }
+    __syncthreads();
+  }
+  if (!flag)
+    for (int i = wp; i < n; i += nw)
+      for (int j = lane; j < n; j += 32) R[(int64_t)i * ldr + j] = (j >= i) ? C[i * ld + j] : 0.0;
+}
+
+static size_t chol_blk_smem(int n) {
+  const int ncp = (n + 7) & ~7;
+  return (size_t)ncp * (ncp + 4) * sizeof(double);
+}
+
+static cudaError_t launch_chol_blk(const double* G, int64_t ldg, int n, double* R, int64_t ldr, int stage, int koff,
+                                   unsigned long long* status, cudaStream_t st) {
+  const size_t smem = chol_blk_smem(n);
+  cudaError_t e = cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e) return e;
+  note_launch();
+  chol_blk_kernel<<<1, 256, smem, st>>>(G, ldg, n, R, ldr, stage, koff, status);
+  return cudaGetLastError();
+}
+
+__global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int rows, int cols, double* __restrict__ B,
+                                 int64_t ldb) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? A[(int64_t)r * lda + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) B[(int64_t)c * ldb + r] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void zero_lower_kernel(double* R, int n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n; e += (int64_t)gridDim.x * blockDim.x)
+    if (e / n > e % n) R[e] = 0.0;
+}
+
+// n > 128: 64-column blocks.  Per block: the 64 x 64 diagonal block by chol_blk_kernel,
+// R12^T = C21 R_pp^{-1} (rowsolve on the rows below), R12 = its transpose, and the trailing
+// update C22 -= R12^T R12 on DMMA (gemm_update).  `work` holds the working copy of G (n x n)
+// and the R12^T scratch (n x 64).
+static cudaError_t launch_chol_big(const double* G, int n, double* R, double* work, int stage,
+                                   unsigned long long* status, cudaStream_t st) {
+  double* Cw = work;
+  double* R12t = work + (size_t)n * n;
+  double* rd = R12t + (size_t)n * 64;
+  cudaError_t e = cudaMemcpyAsync(Cw, G, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, st);
+  if (e) return e;
+  e = cudaMemsetAsync(R, 0, (size_t)n * n * 8, st);
+  if (e) return e;
+  for (int p0 = 0; p0 < n; p0 += 64) {
+    const int w = std::min(64, n - p0);
+    e = launch_chol_blk(Cw + (size_t)p0 * n + p0, n, w, R + (size_t)p0 * n + p0, n, stage, p0, status, st);
+    if (e) return e;
+    const int N = n - p0 - w;
+    if (N <= 0) break;
+    e = launch_rdiag(R + (size_t)p0 * n + p0, w, n, rd, stage, status, st);
+    if (e) return e;
+    // R12^T (N x w) = C21 (rows below the block) * R_pp^{-1}
+    e = launch_trsm_blocked(Cw + (size_t)(p0 + w) * n + p0, n, N, w, w, R + (size_t)p0 * n + p0, n, rd, R12t, 64, st);
+    if (e) return e;
+    note_launch();
+    transpose_kernel<<<dim3(ceil_div(w, 32), ceil_div(N, 32)), dim3(32, 8), 0, st>>>(R12t, 64, N, w,
+                                                                                     R + (size_t)p0 * n + p0 + w, n);
+    e = cudaGetLastError();
+    if (e) return e;
+    // C22 -= R12^T R12
+    e = launch_gemm_update(Cw + (size_t)(p0 + w) * n + p0 + w, n, Cw + (size_t)(p0 + w) * n + p0 + w, n, R12t, 64,
+                           R + (size_t)p0 * n + p0 + w, n, N, w, N, st);
+    if (e) return e;
+  }
+  return cudaSuccess;
+}
+
+size_t chol_ws_bytes(int n) {
+  return std::max((size_t)n * (n + 1) * sizeof(double), ((size_t)n * n + (size_t)n * 64 + 64) * sizeof(double));
+}
 
 cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
                         cudaStream_t st) {
-  const size_t need = chol_ws_bytes(n);
-#define CHOL_REG(RR, QC)                                                                  \
-  if (n <= 32 * RR && n <= CH_WARPS * QC) {                                               \
-    note_launch();                                                                        \
-    chol_reg_kernel<RR, QC><<<1, 32 * CH_WARPS, 0, st>>>(G, n, R, stage, status);         \
-    return cudaGetLastError();                                                            \
-  }
-  CHOL_REG(1, 4)
-  CHOL_REG(2, 8)
-  CHOL_REG(4, 16)
-#undef CHOL_REG
+  const size_t need = (size_t)n * (n + 1) * sizeof(double);
+  if (n <= 128) return launch_chol_blk(G, n, n, R, n, stage, 0, status, st);
+  if (work) return launch_chol_big(G, n, R, work, stage, status, st);
   if (need <= 200 * 1024) {
     if (need > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(chol2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);

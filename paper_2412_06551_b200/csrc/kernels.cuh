@@ -45,6 +45,9 @@ size_t rowsolve_partials_bytes(int64_t rows, int n);
 cudaError_t launch_rowsolve(const double* A, int64_t lda, int64_t rows, int n, const double* T, const double* rdiag,
                             double* out, int64_t ldo, const int64_t* piv, const double* L11, double* gpart, double* G,
                             cudaStream_t st);
+// C_out = C_in - A B (rows x N, K <= 64) on DMMA, increasing-k chain
+cudaError_t launch_gemm_update(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                               int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, cudaStream_t st);
 // blocked substitution for any n (rowsolve on 64-column panels + DMMA trailing updates)
 cudaError_t launch_trsm_blocked(const double* A, int64_t lda, int64_t rows, int n, int nsub, const double* T,
                                 int64_t ldt, const double* rdiag, double* out, int64_t ldo, cudaStream_t st);

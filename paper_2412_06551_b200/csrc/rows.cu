@@ -531,6 +531,15 @@ gemm_update_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, 
     }
 }
 
+cudaError_t launch_gemm_update(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                               int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, cudaStream_t st) {
+  if (rows <= 0 || N <= 0) return cudaSuccess;
+  dim3 grid((unsigned)ceil_div<int64_t>(rows, GU_T), (unsigned)ceil_div(N, GU_T));
+  note_launch();
+  gemm_update_kernel<<<grid, 128, 0, st>>>(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N);
+  return cudaGetLastError();
+}
+
 // out = A T^{-1} (rows x n, substitution, the oracle's fma chain) for any n: panels of 64
 // columns solved by rowsolve_kernel, each followed by the DMMA update of the trailing columns.
 // With nsub < n only the first nsub columns are substituted (the rest receive the updates):

@@ -29,7 +29,7 @@ __global__ void k_drcp(int it, double* out) {
 }
 __global__ void k_dsqrt(int it, double* out) {
   double v = threadIdx.x + 1.5;
-  for (int i = 0; i < it; i++) v = __dsqrt_rn(v) + 1.5;
+  for (int i = 0; i < it; i++) v = __dsqrt_rn(v * 3.0 + 0.25) + 1.5;
   if (v == -1) out[0] = v;
 }
 __global__ void k_dfma(int it, double* out) {
@@ -57,6 +57,17 @@ __global__ void k_syncshared(int it, double* out) {  // publish + sync + read (p
   if (v == -1) out[0] = v;
 }
 
+__global__ void k_sqrt_std(int it, double* out) {
+  double v = threadIdx.x + 1.5;
+  for (int i = 0; i < it; i++) v = sqrt(v * 3.0 + 0.25) + 1.5;
+  if (v == -1) out[0] = v;
+}
+__global__ void k_smem_rw(int it, double* out) {  // dependent smem store->load round trips
+  __shared__ double s[64];
+  double v = threadIdx.x;
+  for (int i = 0; i < it; i++) { s[threadIdx.x & 63] = v; __syncwarp(); v = s[(threadIdx.x + 1) & 63] + 1.0; __syncwarp(); }
+  if (v == -1) out[0] = v;
+}
 __global__ void k_dmma_chain(int it, double* out) {
   double c0 = threadIdx.x, c1 = 1.0, a = 0.5, b = 0.25;
   for (int i = 0; i < it; i++)
@@ -109,6 +120,8 @@ int main() {
   run("dsqrt_rn", k_dsqrt, 32);
   run("dfma", k_dfma, 32);
   run("lds chase", k_smem, 32);
+  run("sqrt()", k_sqrt_std, 32);
+  run("smem st/ld rt", k_smem_rw, 32);
   run("dmma chain", k_dmma_chain, 32);
   run("dmma 4chains", k_dmma_4chains, 32);
   run("dmma chain", k_dmma_chain, 256);
