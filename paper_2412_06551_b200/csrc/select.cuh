@@ -1,21 +1,24 @@
 // select.cuh -- the GEPP "select" of one tournament node (R#4-R#5), used by the
 // leaf and node kernels of tslu.cu.
 //
-// Column-owned layout: CTA = NW warps, R = 32*RS candidate rows, panel width W; warp q
-// owns the CW = W/NW panel columns [q*CW, q*CW+CW) of ALL R rows, lane l holds rows
-// {l + 32 s : s < RS}, so a[s][c] = row (l + 32 s), column q*CW + c.
+// Layout: CTA = NW warps, R = 32*RS candidate rows, panel width W, CW = W/NW columns per
+// warp assigned ROUND-ROBIN: warp q owns panel columns {q + NW k : k < CW}; lane l holds
+// rows {l + 32 s : s < RS}, so a[s][k] = row (l + 32 s), column q + NW k.
 //
-// Step t (pivot column t, owned by warp q = t / CW at local column CC):
-//   * after the barrier that published step t-1 (multipliers l, pivot row index), the
-//     owner warp first applies step t-1's update to column CC only, takes the warp-local
-//     argmax of |a[.][CC]| (ties -> smallest global id; no cross-warp reduction), forms
-//     the multipliers a_rt / a_pt and publishes them through shared memory, and only
-//     then applies step t-1's update to its other columns;
-//   * every other warp applies step t-1's update to its columns (the pivot row's values
-//     come from its own registers: select + shuffle from the owning lane);
-//   * ONE __syncthreads per step.
-// The per-element fma chain (increasing step order) is unchanged, so the pivots are
-// bit-identical to the oracle's gepp_select.
+// Pipeline over per-step mbarriers (no CTA-wide barrier inside the elimination).  Step t
+// pivots on column t, owned by warp t % NW at local column K = t / NW.  Every warp, for
+// every step t:
+//   * waits for step t-1's publication (mbarrier t-1), reads its multipliers and pivot row;
+//   * if it owns step t: applies step t-1 to column K first, publishes the updated column,
+//     finds the pivot (warp-local max |a[.][K]|, ties -> smallest global id), publishes
+//     r = 1/pivot and arrives on mbarrier t, then applies step t-1 to its columns > K;
+//   * otherwise applies step t-1 to its columns >= K.
+// Consecutive steps have different owners, so the critical path per step is one column
+// update + one argmax; the bulk update runs in the shadow of the next owner's pivot search.
+// Every warp forms the multipliers l = col * r itself (the oracle's IEEE product).  Every
+// step's column stays in shared memory (W x R doubles): no slot is reused, a producer never
+// waits for a consumer.  The per-element fma chain (increasing step order) is the oracle's,
+// so the pivots are bit-identical to gepp_select.
 #pragma once
 #include <climits>
 
@@ -23,149 +26,252 @@
 
 namespace rlhc {
 
+#ifdef RLHC_SEL_TRACE
+// probe builds only (tools/probe/psel.cu): per-step timestamps in shared memory
+#define SEL_TRACE(idx) \
+  if (lane_id() == 0) sm.trace[(idx)] = clock64();
+#else
+#define SEL_TRACE(idx)
+#endif
+
 template <int W, int NW, int RS>
 struct SelSmem {
-  double l[2][32 * RS];
-  int prow[2];  // candidate index of the pivot row
-  int zero[2];  // zero pivot column (R#5: no update)
+  double col[W][32 * RS];      // pivot column of step t after its update (candidate s*32 + lane)
+  double r[W];                 // |1 / pivot| of step t
+  unsigned long long bar[W];   // mbarrier of step t (32 arrivals: the owner warp)
+  int prow[W];                 // candidate index of the pivot row of step t
+  int zero[W];                 // 1: zero pivot column at step t (R#5: no update); -1: pivot < 0
   int out_src[W];
   int out_id[W];
+#ifdef RLHC_SEL_TRACE
+  long long trace[(W + 1) * 32];
+#endif
 };
 
-// v[c - C_LO] = a[pslot][c] for a warp-uniform runtime slot (compile-time recursion over
-// slots -> a chain of uniform branches, each copying statically indexed registers)
-template <int W, int NW, int RS, int C_LO, int C_HI, int S>
-__device__ __forceinline__ void sel_extract(const double (&a)[RS][W / NW], int pslot, double* v) {
-  if constexpr (S < RS) {
-    if (pslot == S) {
+RLHC_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+RLHC_DEV void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+RLHC_DEV void mbar_arrive(unsigned long long* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+RLHC_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// a[pslot][k] (k compile-time, pslot warp-uniform): log2(RS)-level mux, no branches
+template <int RS, int CW>
+RLHC_DEV double sel_mux(const double (&a)[RS][CW], int k, int pslot) {
+  double m[RS];
 #pragma unroll
-      for (int c = C_LO; c < C_HI; c++) v[c - C_LO] = a[S][c];
-    } else {
-      sel_extract<W, NW, RS, C_LO, C_HI, S + 1>(a, pslot, v);
+  for (int s = 0; s < RS; s++) m[s] = a[s][k];
+#pragma unroll
+  for (int b = 1; b < RS; b <<= 1) {
+    const bool p = (pslot & b) != 0;
+#pragma unroll
+    for (int s = 0; s + b < RS; s += 2 * b) m[s] = p ? m[s + b] : m[s];
+  }
+  return m[0];
+}
+
+// u[k] = a[pslot][k] in lane `plane` for k in [K0, CW) (not yet broadcast: sel_bcast).
+// Only the pivot lane runs the switch: one branch instead of CW muxes.
+#define RLHC_SEL_CASE(S)                                   \
+  case S:                                                  \
+    if constexpr (S < RS) {                                \
+      _Pragma("unroll") for (int k = K0; k < CW; k++) u[k] = a[S][k]; \
+    }                                                      \
+    break;
+template <int RS, int CW, int K0>
+RLHC_DEV void sel_row(const double (&a)[RS][CW], int pslot, int plane, double (&u)[CW]) {
+  static_assert(RS <= 16, "sel_row handles up to 16 slots");
+  if (lane_id() == plane) {
+    switch (pslot) {
+      RLHC_SEL_CASE(0) RLHC_SEL_CASE(1) RLHC_SEL_CASE(2) RLHC_SEL_CASE(3)
+      RLHC_SEL_CASE(4) RLHC_SEL_CASE(5) RLHC_SEL_CASE(6) RLHC_SEL_CASE(7)
+      RLHC_SEL_CASE(8) RLHC_SEL_CASE(9) RLHC_SEL_CASE(10) RLHC_SEL_CASE(11)
+      RLHC_SEL_CASE(12) RLHC_SEL_CASE(13) RLHC_SEL_CASE(14) RLHC_SEL_CASE(15)
+      default: break;
     }
   }
 }
-
-// Apply the published step (par) to columns [c_lo, c_hi) of this warp (compile-time
-// bounds), for the rows still active after removing the pivot row.
-template <int W, int NW, int RS, int C_LO, int C_HI>
-__device__ __forceinline__ void sel_apply(double (&a)[RS][W / NW], unsigned act, int pslot, int plane, int par,
-                                          const SelSmem<W, NW, RS>& sm) {
-  if (C_LO >= C_HI) return;
-  __syncwarp();
-  double u[C_HI > C_LO ? C_HI - C_LO : 1];
+#undef RLHC_SEL_CASE
+template <int CW, int K_LO, int K_HI>
+RLHC_DEV void sel_bcast(double (&u)[CW], int plane) {
 #pragma unroll
-  for (int c = C_LO; c < C_HI; c++) {
-    double v = 0.0;
-#pragma unroll
-    for (int s = 0; s < RS; s++) v = (s == pslot) ? a[s][c] : v;
-    u[c - C_LO] = __shfl_sync(0xffffffffu, v, plane);
-  }
-  // applied to every slot without a branch (keeps the warp converged for the collectives
-  // that follow): rows no longer in the candidate set are never read again
-#pragma unroll
-  for (int s = 0; s < RS; s++) {
-    const double l = sm.l[par][s * 32 + lane_id()];
-#pragma unroll
-    for (int c = C_LO; c < C_HI; c++) a[s][c] = __fma_rn(-l, u[c - C_LO], a[s][c]);
-  }
-  (void)act;
+  for (int k = K_LO; k < K_HI; k++) u[k] = __shfl_sync(0xffffffffu, u[k], plane);
 }
 
-// Argmax + publish for pivot column CC of the calling (owner) warp, step t.
-template <int W, int NW, int RS, int CC>
-__device__ __forceinline__ void sel_pivot(double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int t,
-                                          SelSmem<W, NW, RS>& sm) {
-  const int lane = lane_id();
-  const int par = t & 1;
-  __syncwarp();
-  long long bk = -1ll;
-  int bid = INT_MAX, bs = 0;
+// a[.][k] -= l * u[k] for k in [K_LO, K_HI)
+template <int RS, int CW, int K_LO, int K_HI>
+RLHC_DEV void sel_update(double (&a)[RS][CW], const double (&l)[RS], const double (&u)[CW]) {
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    long long k = ((act >> s) & 1u) ? __double_as_longlong(fabs(a[s][CC])) : -1ll;
-    bool better = k > bk || (k == bk && gid[s] < bid);
-    bk = better ? k : bk; bid = better ? gid[s] : bid; bs = better ? s : bs;
+#pragma unroll
+    for (int k = K_LO; k < K_HI; k++) a[s][k] = __fma_rn(-l[s], u[k], a[s][k]);
   }
-  int hi = (int)(bk >> 32);
-  int mh = __reduce_max_sync(0xffffffffu, hi);
-  unsigned lo = (hi == mh) ? (unsigned)bk : 0u;
-  unsigned ml = __reduce_max_sync(0xffffffffu, lo);
-  bool tie = bk >= 0 && hi == mh && (unsigned)bk == ml;
-  int pid = __reduce_min_sync(0xffffffffu, tie ? bid : INT_MAX);
-  const unsigned wm = __ballot_sync(0xffffffffu, tie && bid == pid);
-  const int plane = __ffs(wm) - 1;
-  double mv = 0.0;
+}
+
+// Pivot search on column K and publication of step t (owner warp only).  Publishes the
+// updated column itself (before the search), |1/pivot| (as soon as the maximum is known)
+// and the pivot's sign; every warp forms l = col * r, the same IEEE product as the oracle.
+template <int W, int NW, int RS, int K>
+RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int t,
+                        SelSmem<W, NW, RS>& sm) {
+  const int lane = lane_id();
 #pragma unroll
-  for (int s = 0; s < RS; s++) mv = (s == bs) ? a[s][CC] : mv;
-  const double pv = __shfl_sync(0xffffffffu, mv, plane);
-  const int pslot = __shfl_sync(0xffffffffu, bs, plane);
-  const bool zero = (mh == 0 && ml == 0u);
-  const double r = zero ? 0.0 : __drcp_rn(pv);  // correctly rounded 1/pv (== IEEE 1.0/pv)
+  for (int s = 0; s < RS; s++) sm.col[t][s * 32 + lane] = a[s][K];
+  // (1) lane-local max of the |a| bit patterns over the active slots (inactive: -1)
+  long long key[RS], m[RS];
+  unsigned negm = 0;
 #pragma unroll
-  for (int s = 0; s < RS; s++) sm.l[par][s * 32 + lane] = zero ? 0.0 : __dmul_rn(a[s][CC], r);
-  if (lane == 0) {
-    sm.prow[par] = pslot * 32 + plane;
-    sm.zero[par] = zero;
-    sm.out_src[t] = pslot * 32 + plane;
+  for (int s = 0; s < RS; s++) {
+    key[s] = __double_as_longlong(fabs(a[s][K]));
+    m[s] = ((act >> s) & 1u) ? key[s] : -1ll;
+    negm |= (a[s][K] < 0.0 ? 1u : 0u) << s;
+  }
+#pragma unroll
+  for (int st = 1; st < RS; st <<= 1) {
+#pragma unroll
+    for (int s = 0; s + st < RS; s += 2 * st) m[s] = m[s + st] > m[s] ? m[s + st] : m[s];
+  }
+  SEL_TRACE(t * 32 + 18)
+  // (2) warp max: hi word, then lo word among the lanes attaining the hi word
+  const int hi = (int)(m[0] >> 32);
+  const int mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)m[0] : 0u);
+  const long long gb = (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
+  const bool zero = (gb == 0);
+  // |1/pivot| in every lane, branch-free, so it overlaps the id reduction (a lane-0 branch
+  // would serialise it into the warp's critical path); the ballot below consumes it
+  const double rabs = __drcp_rn(__longlong_as_double(gb));
+  // (3) smallest global id among the active rows attaining the maximum
+  int id[RS];
+#pragma unroll
+  for (int s = 0; s < RS; s++) id[s] = (((act >> s) & 1u) && key[s] == gb) ? gid[s] : INT_MAX;
+#pragma unroll
+  for (int st = 1; st < RS; st <<= 1) {
+#pragma unroll
+    for (int s = 0; s + st < RS; s += 2 * st) id[s] = min(id[s], id[s + st]);
+  }
+  const int pid = __reduce_min_sync(0xffffffffu, id[0]);
+  // (4) the pivot's lane, slot and sign (global ids are unique)
+  unsigned hm = 0;
+#pragma unroll
+  for (int s = 0; s < RS; s++) hm |= (gid[s] == pid ? 1u : 0u) << s;
+  hm &= act;
+  const unsigned wb = __ballot_sync(0xffffffffu, hm != 0 && rabs != -1.0);  // (rabs >= 0: always true)
+  const unsigned nb = __ballot_sync(0xffffffffu, (hm & negm) != 0);
+  SEL_TRACE(t * 32 + 19)
+  if (hm != 0 && lane == __ffs(wb) - 1) {
+    const int src = (__ffs(hm) - 1) * 32 + lane;
+    sm.prow[t] = src;
+    sm.out_src[t] = src;
     sm.out_id[t] = pid;
   }
+  if (lane == 0) {
+    sm.r[t] = rabs;
+    sm.zero[t] = zero ? 1 : (nb ? -1 : 0);  // 1: zero column; -1: negative pivot
+  }
+  __syncwarp();
+  SEL_TRACE(t * 32 + 20)
+  mbar_arrive(&sm.bar[t]);
 }
 
-// Step t with pivot column (warp q, local column CC): finish step t-1 (delayed update),
-// pivot search for step t, barrier.
-template <int W, int NW, int RS, int CC>
-__device__ __forceinline__ void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int t, int q,
-                                         SelSmem<W, NW, RS>& sm) {
+// Step t (local pivot column K of warp t % NW): consume step t-1, own step t if mine.
+template <int W, int NW, int RS, int K>
+RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int t, bool own,
+                       SelSmem<W, NW, RS>& sm) {
   constexpr int CW = W / NW;
-  const int wp = warp_id();
-  bool prev = false;
-  int pslot = 0, plane = 0, ppar = (t - 1) & 1;
+  const int lane = lane_id();
+  bool upd = false;
+  int pslot = 0, plane = 0;
+  double l[RS], u[CW];
   if (t > 0) {
-    const int prow = sm.prow[ppar];
-    pslot = prow >> 5; plane = prow & 31;
-    if (lane_id() == plane) act &= ~(1u << pslot);  // the pivot row of step t-1 leaves the set
-    prev = !sm.zero[ppar];
+    mbar_wait(&sm.bar[t - 1], 0);
+    SEL_TRACE(t * 32 + warp_id() * 2)
+    const int prow = sm.prow[t - 1];
+    pslot = prow >> 5;
+    plane = prow & 31;
+    const int zf = sm.zero[t - 1];
+    upd = zf != 1;
+    if (upd) {
+      const double r = zf < 0 ? -sm.r[t - 1] : sm.r[t - 1];  // drcp(-x) == -drcp(x)
+#pragma unroll
+      for (int s = 0; s < RS; s++) l[s] = __dmul_rn(sm.col[t - 1][s * 32 + lane], r);
+    }
+    if (lane == plane) act &= ~(1u << pslot);
   }
-  if (wp == q) {
-    // the previous step's update of the pivot column first, then the argmax
-    if (prev) sel_apply<W, NW, RS, CC, CC + 1>(a, act, pslot, plane, ppar, sm);
-    sel_pivot<W, NW, RS, CC>(a, act, gid, t, sm);
-    if (prev) sel_apply<W, NW, RS, CC + 1, CW>(a, act, pslot, plane, ppar, sm);
-  } else if (prev && wp > q) {
-    sel_apply<W, NW, RS, 0, CW>(a, act, pslot, plane, ppar, sm);
+  if (own) {
+    if (upd) {
+      const double uk = __shfl_sync(0xffffffffu, sel_mux<RS, CW>(a, K, pslot), plane);
+#pragma unroll
+      for (int s = 0; s < RS; s++) a[s][K] = __fma_rn(-l[s], uk, a[s][K]);
+    }
+    SEL_TRACE(t * 32 + 16)
+    sel_pivot<W, NW, RS, K>(a, act, gid, t, sm);
+    SEL_TRACE(t * 32 + 17)
+    if (upd) {
+      sel_row<RS, CW, K + 1>(a, pslot, plane, u);
+      sel_bcast<CW, K + 1, CW>(u, plane);
+      sel_update<RS, CW, K + 1, CW>(a, l, u);
+    }
+  } else if (upd) {
+#ifndef RLHC_SEL_NOCONS
+    sel_row<RS, CW, K>(a, pslot, plane, u);
+    sel_bcast<CW, K, CW>(u, plane);
+    sel_update<RS, CW, K, CW>(a, l, u);
+#endif
   }
-  __syncthreads();
+  SEL_TRACE(t * 32 + warp_id() * 2 + 1)
 }
 
-template <int W, int NW, int RS, int CC>
+// Steps t = K*NW + j, j < NW (local pivot column K), then the next group.
+template <int W, int NW, int RS, int K>
 struct SelGroup {
-  static __device__ __forceinline__ void run(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int t0,
-                                             int steps, int q, SelSmem<W, NW, RS>& sm) {
-    if (t0 + CC >= steps) return;
-    sel_step<W, NW, RS, CC>(a, act, gid, t0 + CC, q, sm);
-    SelGroup<W, NW, RS, CC + 1>::run(a, act, gid, t0, steps, q, sm);
+  static RLHC_DEV void run(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int steps,
+                           SelSmem<W, NW, RS>& sm) {
+    if (K * NW >= steps) return;
+    const int q = warp_id();
+#pragma unroll 1
+    for (int j = 0; j < NW; j++) {
+      const int t = K * NW + j;
+      if (t < steps) sel_step<W, NW, RS, K>(a, act, gid, t, j == q, sm);
+    }
+    SelGroup<W, NW, RS, K + 1>::run(a, act, gid, steps, sm);
   }
 };
 template <int W, int NW, int RS>
 struct SelGroup<W, NW, RS, W / NW> {
-  static __device__ __forceinline__ void run(double (&)[RS][W / NW], unsigned&, const int (&)[RS], int, int, int,
-                                             SelSmem<W, NW, RS>&) {}
+  static RLHC_DEV void run(double (&)[RS][W / NW], unsigned&, const int (&)[RS], int, SelSmem<W, NW, RS>&) {}
 };
 
-// GEPP selection (definition: oracle gepp_select / DESIGN.md R#4-R#5).
-// a[s][c]: this lane's values; act: bit s = row (lane + 32 s) is an active candidate;
-// gid[s]: global ids.  Returns the number of steps; sm.out_id / sm.out_src hold the
-// winners (out_src = candidate index lane + 32 s).
+// Initialise the step barriers; call before the candidate loads (gepp_select's first
+// __syncthreads publishes them).
 template <int W, int NW, int RS>
-__device__ __forceinline__ int gepp_select(double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int w,
-                                           SelSmem<W, NW, RS>& sm) {
-  constexpr int CW = W / NW;
+RLHC_DEV void sel_init(SelSmem<W, NW, RS>& sm) {
+  for (int t = threadIdx.x; t < W; t += blockDim.x) mbar_init(&sm.bar[t], 32);
+}
+
+// GEPP selection (definition: oracle gepp_select / DESIGN.md R#4-R#5).
+// a[s][k]: this lane's values (column q + NW k); act: bit s = row (lane + 32 s) is an active
+// candidate; gid[s]: global ids.  Returns the number of steps; sm.out_id / sm.out_src hold
+// the winners (out_src = candidate index lane + 32 s).
+template <int W, int NW, int RS>
+RLHC_DEV int gepp_select(double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int w,
+                         SelSmem<W, NW, RS>& sm) {
+  __syncthreads();  // barrier initialisation visible to every warp
   int c = __popc(act);
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   const int steps = min(c, w);
-#pragma unroll 1
-  for (int q = 0; q * CW < steps; q++) SelGroup<W, NW, RS, 0>::run(a, act, gid, q * CW, steps, q, sm);
+  SelGroup<W, NW, RS, 0>::run(a, act, gid, steps, sm);
   __syncthreads();
   return steps;
 }

@@ -1,13 +1,10 @@
 // tslu.cu -- tournament-pivoted tall-skinny LU "PX = LU"
 // under the pivot contract of DESIGN.md R#3-R#5 (tslu over column panels).
 //
-// One select CTA holds up to R = 32*NW candidate rows of a W-wide panel in REGISTERS
-// (lane = candidate row) and runs GEPP on them.  Per step: one warp argmax (redux.sync
-// on the |a| bit pattern, smallest global id on ties), the warp's winner writes its row
-// to shared memory speculatively, ONE __syncthreads, a cross-warp argmax over the NW
-// slots, then the register-resident rank-1 update.  The register window shifts by one
-// column per step (a[0] is always the current pivot column), so the step loop stays
-// rolled with constant register indices: small code, no local memory.
+// One select CTA holds R = 32*RS candidate rows of a W-wide panel in REGISTERS,
+// column-owned (select.cuh): warp q holds columns [q*W/NW, (q+1)*W/NW) of every candidate
+// row and runs GEPP as a producer/consumer pipeline over per-step mbarriers -- no CTA-wide
+// barrier inside the elimination.
 #include <climits>
 
 #include "common.cuh"
@@ -25,7 +22,9 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals) {
   constexpr int R = 32 * RS, CW = W / NW;
-  __shared__ SelSmem<W, NW, RS> sm;
+  extern __shared__ __align__(16) unsigned char sel_raw[];
+  SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
+  sel_init(sm);
   const int lane = lane_id(), wp = warp_id();
   double a[RS][CW];
   int gid[RS];
@@ -36,9 +35,9 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
     const bool ok = r < rows && !(chosen && chosen[r]);
     act |= (ok ? 1u : 0u) << s;
     gid[s] = (int)(row0 + r);
-    const double* p = src + r * lds + p0 + wp * CW;
+    const double* p = src + r * lds + p0 + wp;
 #pragma unroll
-    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp * CW + c < w) ? p[c] : 0.0;
+    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
   }
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
   int* oi = out_ids + (size_t)blockIdx.x * W;
@@ -61,7 +60,9 @@ tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt,
                  int nslots_in, int arity, int w, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals) {
   constexpr int CW = W / NW;
-  __shared__ SelSmem<W, NW, RS> sm;
+  extern __shared__ __align__(16) unsigned char sel_raw[];
+  SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
+  sel_init(sm);
   const int lane = lane_id(), wp = warp_id();
   const int c0 = blockIdx.x * arity;
   double a[RS][CW];
@@ -76,9 +77,9 @@ tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt,
     act |= (ok ? 1u : 0u) << s;
     const int slot = child * W + e;
     gid[s] = ok ? in_ids[slot] : INT_MAX;
-    const double* p = in_vals + (size_t)(ok ? slot : 0) * W + wp * CW;
+    const double* p = in_vals + (size_t)(ok ? slot : 0) * W + wp;
 #pragma unroll
-    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp * CW + c < w) ? p[c] : 0.0;
+    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
   }
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
   int* oi = out_ids + (size_t)blockIdx.x * W;
@@ -204,14 +205,28 @@ template <int W, int NW, int RS>
 static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st) {
   int nleaves = (int)ceil_div<int64_t>(rows, 32 * RS);
-  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, 0, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals);
+  constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
+  static bool attr = false;  // once per instantiation (idempotent, so a race is harmless)
+  if (!attr) {
+    cudaFuncSetAttribute(tslu_leaf_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals);
   return cudaGetLastError();
 }
 template <int W, int NW, int RS>
 static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity, int w,
                             int* ids, int* cnt, double* vals, cudaStream_t st) {
   int nout = ceil_div(nin, arity);
-  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, 0, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals);
+  constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tslu_leaf_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, smem, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals);
   return cudaGetLastError();
 }
 
