@@ -1,6 +1,8 @@
 // factor.cu -- the small n x n / s x n factorizations (replicated work, no m dependence):
 // HouseholderQR of the sketch (only R kept, H never formed) and Cholesky with
 // breakdown detection.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -246,7 +248,294 @@ hqr_reg_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const do
     }
 }
 
-size_t hqr_ws_bytes(int s, int n) { return ((size_t)s * (n + 1)) * sizeof(double); }
+// ------------------------------------------------------------------ blocked Householder R
+// For sketches that do not fit one CTA's registers (cfg3: 256 x 128, cfg4: 1024 x 512), the
+// LAPACK dgeqrf structure on a row-major working copy Wk (s x n, ld n):
+//   for each panel of HB columns [j0, j0+HB):
+//     hqr_panel_kernel  (1 CTA, 512 threads, lane = row, the (s-j0) x HB panel in registers):
+//       dgeqr2 on the panel (same reflector formulas as above, R#O7); V stays in place below
+//       the diagonal, R on/above it.  The compact-WY factor T (H_0..H_{HB-1} = I - V T V^T)
+//       is built from the SAME block reductions: at step k the reduction that forms
+//       w_c = v_k^T A(:, c) for the panel columns c > k also yields z_j = V(:, j)^T v_k for
+//       j < k, and T(0:k, k) = -tau_k T(0:k, 0:k) z.
+//     hqr_trail_kernel  (1 CTA per 16 trailing columns): Y = V^T A_blk (DMMA, rows split
+//       over warps), Z = T^T Y, A_blk -= V Z (DMMA).
+// The blocked order only re-associates the reflector applications (R agrees with dgeqr2 to
+// rounding; HQR output is tolerance-checked).
+// one transpose-reduce round: CNT live values, exchange half of them across lane bit O
+template <int CNT, int O, int HB>
+RLHC_DEV void hb_round(double (&v)[HB], int lane, int& base) {
+  if constexpr (CNT > 1 && O >= 2) {
+    const bool hi = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < CNT / 2; i++) {
+      const double keep = hi ? v[i + CNT / 2] : v[i];
+      const double send = hi ? v[i] : v[i + CNT / 2];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    base += hi ? CNT / 2 : 0;
+    hb_round<CNT / 2, O / 2, HB>(v, lane, base);
+  } else {
+    // the single live value: reduce over the remaining lane bits O .. 1
+#pragma unroll
+    for (int o = O; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  }
+}
+
+// Block sum of HB values over 16 warps; every thread gets the totals.  Warp stage:
+// transpose-reduce (2 HB - 1 shuffles instead of 5 HB).
+template <int HB>
+RLHC_DEV void hb_block_sum(double (&y)[HB], double (&red)[16][HB + 1], double (&tot)[HB]) {
+  static_assert(HB == 16 || HB == 8, "HB");
+  const int lane = lane_id(), wp = warp_id();
+  int base = 0;
+  hb_round<HB, 16, HB>(y, lane, base);
+  constexpr int LOG = HB == 16 ? 4 : 3;
+  if ((lane & ((32 >> LOG) - 1)) == 0) red[wp][base] = y[0];
+  __syncthreads();
+  if (threadIdx.x < HB) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; w++) sum += red[w][threadIdx.x];
+    tot[threadIdx.x] = sum;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < HB; i++) y[i] = tot[i];
+}
+
+RLHC_DEV double hb_warp_sum(double x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <int RPT, int HB>
+__global__ void __launch_bounds__(512)
+hqr_panel_kernel(double* __restrict__ Wk, int s, int n, int j0, double* __restrict__ Tg,
+                 unsigned long long* status) {
+  __shared__ double red[16][HB + 1];
+  __shared__ double tot[HB];
+  __shared__ double Ts[HB][HB + 1];
+  __shared__ double bc[2];
+  const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
+  const int r = s - j0, nb = min(HB, n - j0);
+  double x[RPT][HB];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int li = tid + 512 * q;
+    const double* p = Wk + (int64_t)(j0 + li) * n + j0;
+#pragma unroll
+    for (int c = 0; c < HB; c++) x[q][c] = (li < r && c < nb) ? p[c] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < HB; k++) {
+    if (k >= nb) break;
+    // (1) sigma = ||A(k+1:, k)||^2, alpha = A(k, k)
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      const int li = tid + 512 * q;
+      if (li > k && li < r) part = __fma_rn(x[q][k], x[q][k], part);
+    }
+    part = hb_warp_sum(part);
+    if (lane == 0) red[wp][0] = part;
+    if (tid == k) bc[0] = x[0][k];
+    __syncthreads();
+    if (tid == 0) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < 16; w++) sum += red[w][0];
+      tot[0] = sum;
+    }
+    __syncthreads();
+    const double alpha = bc[0], xnorm = __dsqrt_rn(tot[0]);
+    double beta = alpha, tau = 0.0, sc = 0.0;
+    if (xnorm != 0.0) {
+      beta = -(alpha >= 0.0 ? 1.0 : -1.0) * hypot(alpha, xnorm);
+      tau = __ddiv_rn(beta - alpha, beta);
+      sc = __ddiv_rn(1.0, alpha - beta);
+    } else if (alpha == 0.0 && tid == 0) {
+      report(status, RLHC_ERANKDEF, RLHC_STAGE_HQR, j0 + k);
+    }
+    // (2) v (1 at row k), R(k, k) = beta; y_c = v^T A(:, c) for every panel column c != k
+    double vv[RPT], y[HB];
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      const int li = tid + 512 * q;
+      vv[q] = (li > k && li < r) ? x[q][k] * sc : (li == k ? 1.0 : 0.0);
+      if (li > k) x[q][k] = vv[q];
+      if (li == k) x[q][k] = beta;
+    }
+#pragma unroll
+    for (int c = 0; c < HB; c++) {
+      double acc = 0.0;
+      if (c != k) {
+#pragma unroll
+        for (int q = 0; q < RPT; q++) acc = __fma_rn(vv[q], x[q][c], acc);
+      }
+      y[c] = acc;
+    }
+    hb_block_sum<HB>(y, red, tot);
+    // (3) trailing panel columns; (4) column k of T from z = y[0:k]
+#pragma unroll
+    for (int c = k + 1; c < HB; c++) {
+      const double tw = tau * y[c];
+#pragma unroll
+      for (int q = 0; q < RPT; q++) x[q][c] = __fma_rn(-vv[q], tw, x[q][c]);
+    }
+    if (tid < k) {
+      double acc = 0.0;
+      for (int p = tid; p < k; p++) acc = __fma_rn(Ts[tid][p], tot[p], acc);  // tot == y (smem copy)
+      Ts[tid][k] = -tau * acc;
+    } else if (tid == k) {
+      Ts[k][k] = tau;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int li = tid + 512 * q;
+    double* p = Wk + (int64_t)(j0 + li) * n + j0;
+    if (li < r)
+#pragma unroll
+      for (int c = 0; c < HB; c++)
+        if (c < nb) p[c] = x[q][c];
+  }
+  for (int e = tid; e < HB * HB; e += blockDim.x) {
+    const int i = e / HB, j = e - i * HB;
+    Tg[e] = (i < nb && j < nb && j >= i) ? Ts[i][j] : 0.0;
+  }
+}
+
+// V(li, p) of the current panel (unit lower trapezoid stored below the diagonal of Wk)
+RLHC_DEV double hb_v(const double* Wk, int n, int j0, int r, int nb, int li, int p) {
+  if (li >= r || p >= nb || li < p) return 0.0;
+  return li == p ? 1.0 : Wk[(int64_t)(j0 + li) * n + j0 + p];
+}
+
+// A(j0:, c0:c0+16) -= V (T^T (V^T A)) for one 16-column block; 8 warps.
+template <int HB>
+__global__ void __launch_bounds__(256)
+hqr_trail_kernel(double* __restrict__ Wk, int s, int n, int j0, const double* __restrict__ Tg) {
+  static_assert(HB == 16 || HB == 8, "panel width");
+  constexpr int MT = HB / 8;  // m-tiles of Y (rows p)
+  __shared__ double Yw[8][HB][17];
+  __shared__ double Zs[HB][17];
+  const int lane = lane_id(), wp = warp_id(), g = lane >> 2, t = lane & 3;
+  const int r = s - j0, nb = min(HB, n - j0);
+  const int c0 = j0 + nb + blockIdx.x * 16;
+  // pass 1: Y = V^T A_blk, k = rows (4 per DMMA), split over warps
+  double acc[MT][2][2];
+#pragma unroll
+  for (int i = 0; i < MT; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 4 * wp; k0 < r; k0 += 32) {
+    const int li = k0 + t;
+    double a[MT], b[2];
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++) a[mt] = hb_v(Wk, n, j0, r, nb, li, mt * 8 + g);
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++) {
+      const int c = c0 + nt * 8 + g;
+      b[nt] = (li < r && c < n) ? Wk[(int64_t)(j0 + li) * n + c] : 0.0;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int nt = 0; nt < 2; nt++) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+#pragma unroll
+  for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++) {
+      Yw[wp][mt * 8 + g][nt * 8 + 2 * t] = acc[mt][nt][0];
+      Yw[wp][mt * 8 + g][nt * 8 + 2 * t + 1] = acc[mt][nt][1];
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < HB * 16; e += blockDim.x) {
+    const int p = e >> 4, c = e & 15;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) sum += Yw[w][p][c];
+    Yw[0][p][c] = sum;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < HB * 16; e += blockDim.x) {
+    const int p = e >> 4, c = e & 15;
+    double z = 0.0;
+    for (int q = 0; q <= p; q++) z = __fma_rn(Tg[q * HB + p], Yw[0][q][c], z);  // (T^T Y)(p, c)
+    Zs[p][c] = z;
+  }
+  __syncthreads();
+  // pass 2: A_blk -= V Z, m = rows (8 per tile), k = p
+  for (int m0 = 8 * wp; m0 < r; m0 += 64) {
+    const int li = m0 + g;
+    double d[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int c = c0 + nt * 8 + 2 * t + e;
+        d[nt][e] = (li < r && c < n) ? Wk[(int64_t)(j0 + li) * n + c] : 0.0;
+      }
+#pragma unroll
+    for (int kk = 0; kk < HB / 4; kk++) {
+      const double a = -hb_v(Wk, n, j0, r, nb, li, 4 * kk + t);
+#pragma unroll
+      for (int nt = 0; nt < 2; nt++) dmma(d[nt][0], d[nt][1], a, Zs[4 * kk + t][nt * 8 + g]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int c = c0 + nt * 8 + 2 * t + e;
+        if (li < r && c < n) Wk[(int64_t)(j0 + li) * n + c] = d[nt][e];
+      }
+  }
+}
+
+__global__ void hqr_copy_kernel(const double* __restrict__ A, int s, int n, int64_t lda, double* __restrict__ Wk) {
+  const int64_t total = (int64_t)s * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    Wk[e] = A[i * lda + j];
+  }
+}
+
+// S = upper n x n of Wk, rows sign-aligned with sgn_ref (R#7)
+__global__ void hqr_finish_kernel(const double* __restrict__ Wk, int n, const double* __restrict__ sgn_ref,
+                                  double* __restrict__ S) {
+  const int i = blockIdx.x;
+  const double d = Wk[(int64_t)i * n + i];
+  const bool flip = sgn_ref && ((d < 0.0) != (sgn_ref[(int64_t)i * n + i] < 0.0));
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double v = (j >= i) ? Wk[(int64_t)i * n + j] : 0.0;
+    S[(int64_t)i * n + j] = flip ? -v : v;
+  }
+}
+
+template <int RPT, int HB>
+static void run_hqr_blocked(const double* A, int s, int n, int64_t lda, const double* sgn_ref, double* S,
+                            double* Wk, double* Tg, unsigned long long* status, cudaStream_t st) {
+  note_launch();
+  hqr_copy_kernel<<<kSMs, 256, 0, st>>>(A, s, n, lda, Wk);
+  for (int j0 = 0; j0 < n; j0 += HB) {
+    note_launch();
+    hqr_panel_kernel<RPT, HB><<<1, 512, 0, st>>>(Wk, s, n, j0, Tg, status);
+    const int rest = n - j0 - HB;
+    if (rest > 0) {
+      note_launch();
+      hqr_trail_kernel<HB><<<ceil_div(rest, 16), 256, 0, st>>>(Wk, s, n, j0, Tg);
+    }
+  }
+  note_launch();
+  hqr_finish_kernel<<<n, 128, 0, st>>>(Wk, n, sgn_ref, S);
+}
+
+size_t hqr_ws_bytes(int s, int n) {
+  return std::max((size_t)s * (n + 1), (size_t)s * n + 16 * 16) * sizeof(double);
+}
 
 cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double* sgn_ref, double* S, double* work,
                        unsigned long long* status, cudaStream_t st) {
@@ -264,6 +553,10 @@ cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double*
   HQR_REG(8, 4)
   HQR_REG(4, 8)
 #undef HQR_REG
+  // blocked path (Wk = work[0 : s*n), T after it)
+  if (s <= 512) { run_hqr_blocked<1, 16>(A, s, n, lda, sgn_ref, S, work, work + (size_t)s * n, status, st); return cudaGetLastError(); }
+  if (s <= 1024) { run_hqr_blocked<2, 16>(A, s, n, lda, sgn_ref, S, work, work + (size_t)s * n, status, st); return cudaGetLastError(); }
+  if (s <= 2048) { run_hqr_blocked<4, 8>(A, s, n, lda, sgn_ref, S, work, work + (size_t)s * n, status, st); return cudaGetLastError(); }
   if (need <= 200 * 1024) {
     if (need > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(hqr2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
