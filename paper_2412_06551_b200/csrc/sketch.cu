@@ -111,16 +111,35 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
     }
 }
 
-__global__ void gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int tjn, int n, int s,
-                                    double* __restrict__ out) {
-  const int64_t total = (int64_t)s * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
-    int tile = (i / ST) * tjn + j / ST;
-    int r = i % ST, c = j % ST;
-    double acc = 0.0;
-    for (int p = 0; p < nsplit; p++) acc += part[((size_t)p * ntiles + tile) * ST * ST + r * ST + c];
-    out[e] = acc;
+// out = sum over the row splits of the partial tiles, in a fixed order: block = 32
+// consecutive partial elements x 8 warps, warp q sums splits [q*per, (q+1)*per) with 8
+// independent accumulators (loads in flight), then the 8 warp sums are combined in order.
+__global__ void __launch_bounds__(256)
+gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int tjn, int n, int s,
+                    double* __restrict__ out) {
+  __shared__ double red[8][32];
+  const int lane = lane_id(), wq = warp_id();
+  const int64_t per_split = (int64_t)ntiles * ST * ST;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int per = (nsplit + 7) / 8;
+  const int p0 = wq * per, p1 = min(nsplit, p0 + per);
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (e < per_split) {
+    const double* p = part + e;
+    int q = p0;
+    for (; q + 8 <= p1; q += 8)
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[u] += p[(size_t)(q + u) * per_split];
+    for (; q < p1; q++) acc[0] += p[(size_t)q * per_split];
+  }
+  red[wq][lane] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  if (wq == 0 && e < per_split) {
+    double v = red[0][lane];
+    for (int q = 1; q < 8; q++) v += red[q][lane];
+    const int tile = (int)(e / (ST * ST)), rc = (int)(e - (int64_t)tile * ST * ST);
+    const int i = (tile / tjn) * ST + rc / ST, j = (tile % tjn) * ST + rc % ST;
+    if (i < s && j < n) out[(int64_t)i * n + j] = v;
   }
 }
 
@@ -131,8 +150,8 @@ cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int 
   note_launch(); gauss_sketch_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  int64_t total = (int64_t)s * n;
-  note_launch(); gauss_reduce_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 2048), 256, 0, st>>>(
+  const int64_t per_split = (int64_t)gg.ti * gg.tj * ST * ST;
+  note_launch(); gauss_reduce_kernel<<<(int)ceil_div<int64_t>(per_split, 32), 256, 0, st>>>(
       part, gg.nsplit, gg.ti * gg.tj, gg.tj, n, s, out);
   return cudaGetLastError();
 }
