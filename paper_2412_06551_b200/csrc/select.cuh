@@ -48,24 +48,6 @@ struct SelSmem {
 #endif
 };
 
-RLHC_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-RLHC_DEV void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-RLHC_DEV void mbar_arrive(unsigned long long* b) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
-}
-RLHC_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
 // a[pslot][k] (k compile-time, pslot warp-uniform): log2(RS)-level mux, no branches
 template <int RS, int CW>
 RLHC_DEV double sel_mux(const double (&a)[RS][CW], int k, int pslot) {

@@ -12,19 +12,35 @@
 namespace rlhc {
 
 // ------------------------------------------------------------------ Gaussian
-constexpr int ST = 64;   // output tile (sketch rows) x (columns)
+// CTA output tile: ST = 64 sketch rows x NT = 32*NTW columns, warps 2 x NTW (32 x 32 each,
+// DMMA m8n8k4 fragments).  Per chunk of SK rows of A: the CTA generates the Omega tile
+// (64 x SK, Philox + Box-Muller, R#19) while the next chunk's A tile streams in with
+// cp.async (double buffer), then the DMMA contraction.  Omega is regenerated once per
+// column tile, so n > 64 uses 256-column tiles (NTW = 8).  (Measured alternatives: 2 CTAs
+// of 64 x 128 per SM, and warp-specialised generator warps feeding compute warps through
+// mbarriers, were both slower: the Box-Muller generation is a latency-bound ~250-
+// instruction chain per pair and needs every warp of the SM to keep up.)
+constexpr int ST = 64;   // output tile rows (sketch rows)
 constexpr int SK = 32;   // rows of A per chunk
 
+static int gauss_ntw(int n) { return n <= 64 ? 2 : 8; }
+
 struct GaussGeom {
-  int ti, tj, nsplit;
+  int ti, tj, nsplit, nt;
   int64_t rows_per_split;
 };
 static GaussGeom gauss_geom(int64_t rows, int n, int s) {
   GaussGeom g;
+  g.nt = 32 * gauss_ntw(n);
   g.ti = ceil_div(s, ST);
-  g.tj = ceil_div(n, ST);
-  int tiles = g.ti * g.tj;
-  int64_t want = std::max<int64_t>(1, (2 * kSMs + tiles - 1) / tiles);
+  g.tj = ceil_div(n, g.nt);
+  const int tiles = g.ti * g.tj;
+  // resident CTAs: 2 per SM (64-column tiles, 128 threads) or 1 (256-column tiles, 512
+  // threads); at least 2 waves, split count rounded so the last wave is (nearly) full
+  const int64_t slots = (g.nt == 64 ? 2 : 1) * (int64_t)kSMs;
+  int64_t want = std::max<int64_t>(1, (2 * slots + tiles - 1) / tiles);
+  const int64_t waves = (want * tiles + slots - 1) / slots;
+  want = std::max<int64_t>(1, waves * slots / tiles);
   int64_t maxs = std::max<int64_t>(1, rows / 128);
   g.nsplit = (int)std::min<int64_t>(want, maxs);
   g.rows_per_split = ceil_div<int64_t>(ceil_div<int64_t>(rows, g.nsplit), SK) * SK;
@@ -33,35 +49,44 @@ static GaussGeom gauss_geom(int64_t rows, int n, int s) {
 }
 size_t gauss_partials_bytes(int64_t rows, int n, int s) {
   GaussGeom g = gauss_geom(rows, n, s);
-  return (size_t)g.nsplit * g.ti * g.tj * ST * ST * sizeof(double);
+  return (size_t)g.nsplit * g.ti * g.tj * ST * g.nt * sizeof(double);
 }
 
-__global__ void __launch_bounds__(128)
+template <int NTW>
+struct GaussSmem {
+  static constexpr int NT = 32 * NTW;
+  double A[2][SK][NT + 4];   // A tile, double-buffered (row pad 4: conflict-free B fragments)
+  double Om[ST][SK + 4];     // Omega tile (row pad 4: conflict-free A fragments)
+};
+
+template <int NTW>
+__global__ void __launch_bounds__(64 * NTW)
 gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
                     uint64_t seed, uint32_t stream_id, int64_t rows_per_split, double* __restrict__ part) {
-  __shared__ double Om[ST][SK + 1];
-  __shared__ __align__(16) double At[SK][ST + 4];
-  const int tile_i = blockIdx.x / ((n + ST - 1) / ST), tile_j = blockIdx.x % ((n + ST - 1) / ST);
-  const int i0 = tile_i * ST, j0 = tile_j * ST;
+  constexpr int NT = 32 * NTW, NTH = 64 * NTW;
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GaussSmem<NTW>& sm = *reinterpret_cast<GaussSmem<NTW>*>(gsm_raw);
+  const int tjn = (n + NT - 1) / NT;
+  const int tile_i = blockIdx.x / tjn, tile_j = blockIdx.x % tjn;
+  const int i0 = tile_i * ST, j0 = tile_j * NT;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
   const int64_t r1 = std::min<int64_t>(rows, r0 + rows_per_split);
   const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)s));
   const int lane = lane_id(), w = warp_id();
   const int g = lane >> 2, t = lane & 3;
-  const int wi = (w >> 1) * 32, wj = (w & 1) * 32;
+  const int wi = (w / NTW) * 32, wj = (w % NTW) * 32;
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; a++)
 #pragma unroll
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
-  for (int64_t k0 = r0; k0 < r1; k0 += SK) {
-    // A tile (SK rows x ST columns): async 16-byte copies issued first, so they are in
-    // flight while this thread generates its share of the Omega tile
-    for (int idx = threadIdx.x; idx < SK * (ST / 2); idx += blockDim.x) {
-      const int kk = idx / (ST / 2), c = 2 * (idx % (ST / 2));
+  // A tile (SK rows x NT columns) of the chunk at k0 into buffer b: 16-byte async copies
+  auto fetch = [&](int64_t k0, int b) {
+    for (int idx = threadIdx.x; idx < SK * (NT / 2); idx += NTH) {
+      const int kk = idx / (NT / 2), c = 2 * (idx % (NT / 2));
       const int64_t gr = k0 + kk;
-      double* dst = &At[kk][c];
+      double* dst = &sm.A[b][kk][c];
       const double* src = A + gr * lda + j0 + c;
       if (gr < r1 && aligned && j0 + c + 1 < n) cp_async16(dst, src);
       else {
@@ -70,8 +95,12 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
       }
     }
     cp_async_commit();
-    // Omega tile: rows i0..i0+63 (pairs i, i+1 share one Philox block), columns k0..k0+31
-    for (int idx = threadIdx.x; idx < (ST / 2) * SK; idx += blockDim.x) {
+  };
+  if (r0 < r1) fetch(r0, 0);
+  int buf = 0;
+  for (int64_t k0 = r0; k0 < r1; k0 += SK, buf ^= 1) {
+    // Omega tile: rows i0..i0+63 (pairs i, i+1 share one Philox block), columns k0..k0+SK-1
+    for (int idx = threadIdx.x; idx < (ST / 2) * SK; idx += NTH) {
       int ip = idx / SK, kk = idx - ip * SK;
       int i = i0 + 2 * ip;
       int64_t gr = k0 + kk;
@@ -81,18 +110,25 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
         z0 = __dmul_rn(z0, scale);
         z1 = (i + 1 < s) ? __dmul_rn(z1, scale) : 0.0;
       }
-      Om[2 * ip][kk] = z0;
-      Om[2 * ip + 1][kk] = z1;
+      sm.Om[2 * ip][kk] = z0;
+      sm.Om[2 * ip + 1][kk] = z1;
     }
-    cp_async_wait_all();
+    // next chunk's A tile into the other buffer (freed by the barrier that ended the
+    // previous iteration), then wait for this chunk's tile only
+    if (k0 + SK < r1) {
+      fetch(k0 + SK, buf ^ 1);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < SK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; a++) af[a] = Om[wi + a * 8 + g][kk + t];
+      for (int a = 0; a < 4; a++) af[a] = sm.Om[wi + a * 8 + g][kk + t];
 #pragma unroll
-      for (int b = 0; b < 4; b++) bf[b] = At[kk + t][wj + b * 8 + g];
+      for (int b = 0; b < 4; b++) bf[b] = sm.A[buf][kk + t][wj + b * 8 + g];
 #pragma unroll
       for (int a = 0; a < 4; a++)
 #pragma unroll
@@ -100,14 +136,14 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
     }
     __syncthreads();
   }
-  double* P = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * ST * ST;
+  double* P = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * ST * NT;
 #pragma unroll
   for (int a = 0; a < 4; a++)
 #pragma unroll
     for (int b = 0; b < 4; b++) {
       int r = wi + a * 8 + g, c = wj + b * 8 + 2 * t;
-      P[r * ST + c] = acc[a][b][0];
-      P[r * ST + c + 1] = acc[a][b][1];
+      P[r * NT + c] = acc[a][b][0];
+      P[r * NT + c + 1] = acc[a][b][1];
     }
 }
 
@@ -115,11 +151,12 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
 // consecutive partial elements x 8 warps, warp q sums splits [q*per, (q+1)*per) with 8
 // independent accumulators (loads in flight), then the 8 warp sums are combined in order.
 __global__ void __launch_bounds__(256)
-gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int tjn, int n, int s,
+gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int tjn, int nt, int n, int s,
                     double* __restrict__ out) {
   __shared__ double red[8][32];
   const int lane = lane_id(), wq = warp_id();
-  const int64_t per_split = (int64_t)ntiles * ST * ST;
+  const int64_t tile_sz = (int64_t)ST * nt;
+  const int64_t per_split = (int64_t)ntiles * tile_sz;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
   const int per = (nsplit + 7) / 8;
   const int p0 = wq * per, p1 = min(nsplit, p0 + per);
@@ -137,8 +174,8 @@ gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int
   if (wq == 0 && e < per_split) {
     double v = red[0][lane];
     for (int q = 1; q < 8; q++) v += red[q][lane];
-    const int tile = (int)(e / (ST * ST)), rc = (int)(e - (int64_t)tile * ST * ST);
-    const int i = (tile / tjn) * ST + rc / ST, j = (tile % tjn) * ST + rc % ST;
+    const int tile = (int)(e / tile_sz), rc = (int)(e - (int64_t)tile * tile_sz);
+    const int i = (tile / tjn) * ST + rc / nt, j = (tile % tjn) * nt + rc % nt;
     if (i < s && j < n) out[(int64_t)i * n + j] = v;
   }
 }
@@ -147,12 +184,26 @@ cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int 
                                 uint32_t stream_id, double* part, double* out, cudaStream_t st) {
   GaussGeom gg = gauss_geom(rows, n, s);
   dim3 grid(gg.ti * gg.tj, gg.nsplit);
-  note_launch(); gauss_sketch_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part);
+  static bool attr = false;  // idempotent, once per process
+  if (!attr) {
+    cudaFuncSetAttribute(gauss_sketch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(GaussSmem<2>));
+    cudaFuncSetAttribute(gauss_sketch_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(GaussSmem<8>));
+    attr = true;
+  }
+  note_launch();
+  if (gg.nt == 64)
+    gauss_sketch_kernel<2><<<grid, 128, sizeof(GaussSmem<2>), st>>>(A, lda, rows, n, row0, s, seed, stream_id,
+                                                                    gg.rows_per_split, part);
+  else
+    gauss_sketch_kernel<8><<<grid, 512, sizeof(GaussSmem<8>), st>>>(A, lda, rows, n, row0, s, seed, stream_id,
+                                                                    gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  const int64_t per_split = (int64_t)gg.ti * gg.tj * ST * ST;
+  const int64_t per_split = (int64_t)gg.ti * gg.tj * ST * gg.nt;
   note_launch(); gauss_reduce_kernel<<<(int)ceil_div<int64_t>(per_split, 32), 256, 0, st>>>(
-      part, gg.nsplit, gg.ti * gg.tj, gg.tj, n, s, out);
+      part, gg.nsplit, gg.ti * gg.tj, gg.tj, gg.nt, n, s, out);
   return cudaGetLastError();
 }
 
