@@ -694,8 +694,11 @@ size_t gram_partials_bytes(int64_t rows, int n) {
 __global__ void __launch_bounds__(128)
 gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int nt, int64_t rows_per_split,
             double* __restrict__ part) {
-  __shared__ __align__(16) double Ai[GK][GT + 4];
-  __shared__ __align__(16) double Aj[GK][GT + 4];
+  // two chunks in flight: the next chunk's column panels stream in (cp.async) while the
+  // current one is contracted
+  extern __shared__ __align__(16) double gram_sm[];
+  double(*Ai)[GK][GT + 4] = reinterpret_cast<double(*)[GK][GT + 4]>(gram_sm);
+  double(*Aj)[GK][GT + 4] = reinterpret_cast<double(*)[GK][GT + 4]>(gram_sm + 2 * GK * (GT + 4));
   // tile index -> (ti, tj), ti <= tj
   int tile = blockIdx.x, ti = 0;
   {
@@ -715,26 +718,49 @@ gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int 
   for (int a = 0; a < 4; a++)
 #pragma unroll
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int64_t k0 = r0; k0 < r1; k0 += GK) {
-    {
-      const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
-      for (int idx = threadIdx.x; idx < GK * (GT / 2); idx += blockDim.x) {
-        const int kk = idx / (GT / 2), c = 2 * (idx % (GT / 2));
-        const int64_t gr = k0 + kk;
-        const bool rok = gr < r1;
+  const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+  // interior chunks (all GK rows in range, both 64-column panels inside n): thread
+  // (warp w, lane) copies rows w + 4j, columns 2*lane, 2*lane+1 of each panel -- no
+  // per-copy index arithmetic or bounds tests
+  const bool cols_full = aligned && i0 + GT <= n && j0 + GT <= n;
+  auto fetch = [&](int64_t k0, int buf) {
+    if (cols_full && k0 + GK <= r1) {
+      const double* pi = A + (k0 + w) * lda + i0 + 2 * lane;
+      const double* pj = A + (k0 + w) * lda + j0 + 2 * lane;
+      const int64_t step = 4 * lda;
 #pragma unroll
-        for (int side = 0; side < 2; side++) {
-          const int cb = side ? j0 : i0;
-          double* dst = side ? &Aj[kk][c] : &Ai[kk][c];
-          const double* src = A + gr * lda + cb + c;
-          if (rok && aligned && cb + c + 1 < n) cp_async16(dst, src);
-          else {
-            dst[0] = (rok && cb + c < n) ? src[0] : 0.0;
-            dst[1] = (rok && cb + c + 1 < n) ? src[1] : 0.0;
-          }
-        }
+      for (int j = 0; j < GK / 4; j++) {
+        cp_async16(&Ai[buf][w + 4 * j][2 * lane], pi + j * step);
+        cp_async16(&Aj[buf][w + 4 * j][2 * lane], pj + j * step);
       }
       cp_async_commit();
+      return;
+    }
+    for (int idx = threadIdx.x; idx < GK * (GT / 2); idx += blockDim.x) {
+      const int kk = idx / (GT / 2), c = 2 * (idx % (GT / 2));
+      const int64_t gr = k0 + kk;
+      const bool rok = gr < r1;
+#pragma unroll
+      for (int side = 0; side < 2; side++) {
+        const int cb = side ? j0 : i0;
+        double* dst = side ? &Aj[buf][kk][c] : &Ai[buf][kk][c];
+        const double* src = A + gr * lda + cb + c;
+        if (rok && aligned && cb + c + 1 < n) cp_async16(dst, src);
+        else {
+          dst[0] = (rok && cb + c < n) ? src[0] : 0.0;
+          dst[1] = (rok && cb + c + 1 < n) ? src[1] : 0.0;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  if (r0 < r1) fetch(r0, 0);
+  int buf = 0;
+  for (int64_t k0 = r0; k0 < r1; k0 += GK, buf ^= 1) {
+    if (k0 + GK < r1) {
+      fetch(k0 + GK, buf ^ 1);
+      cp_async_wait_1();
+    } else {
       cp_async_wait_all();
     }
     __syncthreads();
@@ -742,9 +768,9 @@ gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int 
     for (int kk = 0; kk < GK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; a++) af[a] = Ai[kk + t][wi + a * 8 + g];
+      for (int a = 0; a < 4; a++) af[a] = Ai[buf][kk + t][wi + a * 8 + g];
 #pragma unroll
-      for (int b = 0; b < 4; b++) bf[b] = Aj[kk + t][wj + b * 8 + g];
+      for (int b = 0; b < 4; b++) bf[b] = Aj[buf][kk + t][wj + b * 8 + g];
 #pragma unroll
       for (int a = 0; a < 4; a++)
 #pragma unroll
@@ -783,7 +809,13 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nsplit, 
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st) {
   GramGeom gg = gram_geom(rows, n);
   dim3 grid(gg.ntiles, gg.nsplit);
-  note_launch(); gram_kernel<<<grid, 128, 0, st>>>(A, lda, rows, n, gg.nt, gg.rows_per_split, part);
+  constexpr int smem = 4 * GK * (GT + 4) * (int)sizeof(double);
+  static bool attr = false;  // idempotent
+  if (!attr) {
+    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  note_launch(); gram_kernel<<<grid, 128, smem, st>>>(A, lda, rows, n, gg.nt, gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   int64_t total = (int64_t)n * n;

@@ -82,7 +82,19 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
   // A tile (SK rows x NT columns) of the chunk at k0 into buffer b: 16-byte async copies
+  // interior chunks: thread copies row (tid / (NT/2)) + j*(NTH/(NT/2)), one fixed column
+  // pair -- no per-copy index arithmetic or bounds tests
+  constexpr int RSTEP = NTH / (NT / 2);  // rows covered per pass (NT/2 threads per row)
+  const bool cols_full = aligned && j0 + NT <= n;
   auto fetch = [&](int64_t k0, int b) {
+    if (cols_full && k0 + SK <= r1) {
+      const int rr = threadIdx.x / (NT / 2), cc = 2 * (threadIdx.x % (NT / 2));
+      const double* src = A + (k0 + rr) * lda + j0 + cc;
+#pragma unroll
+      for (int j = 0; j < SK / RSTEP; j++) cp_async16(&sm.A[b][rr + j * RSTEP][cc], src + (int64_t)j * RSTEP * lda);
+      cp_async_commit();
+      return;
+    }
     for (int idx = threadIdx.x; idx < SK * (NT / 2); idx += NTH) {
       const int kk = idx / (NT / 2), c = 2 * (idx % (NT / 2));
       const int64_t gr = k0 + kk;
