@@ -6,10 +6,12 @@ against the roofline (BASELINE.json metric).
 
 One JSON line on rank 0.  A step = one full SLHC3/SSLHC3 call (every stage of
 SURVEY.md 8(a)) on the configuration's synthetic X, resident in HBM.  `value` is the
-algorithmic HBM throughput: the bytes of the 8 required passes over m x n data
-(8 * 8 m n bytes) per second of device time, summed over ranks.
+algorithmic HBM throughput of the whole job: the bytes of the 8 required passes over m x n
+data (8 * 8 m n bytes) per second of device time (max over ranks).
 L2 is flushed between timed steps (a 512 MiB write, outside the timed events).
-N > 1 runs the row-sharded algorithm (paper_2412_06551_b200.dist) with NCCL.
+N > 1 runs the row-sharded algorithm (paper_2412_06551_b200.dist) with NCCL: by default
+weak scaling (every rank holds the config's m rows; --config cfg2 at N = 1 is the
+BASELINE metric workload), --strong keeps the config's m fixed (north star: --config cfg5).
 """
 from __future__ import annotations
 
@@ -30,6 +32,10 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 PEAK_FP64_DMMA_TFLOPS = 37.08  # measured by tools/probe/probe.cu (profiles/r01_probe_fp64_hbm.txt)
+# scalar FP64 FMA (DFMA) peak: measured 36.86 TF/s (same probe); from unit counts
+# 148 SMs x 64 FP64 lanes x 2 flop x 1.965 GHz = 37.2 TF/s
+PEAK_FP64_ALU_TFLOPS = 36.86
+ALU_STAGES = {"tslu"}  # scalar-FMA stages (GEPP select / elimination), not tensor-core work
 
 
 def _peaks():
@@ -103,11 +109,14 @@ class ClockSampler:
 def run_ours(args, cfg: synth.Config, rank: int, world: int):
     import paper_2412_06551_b200 as rl
     from paper_2412_06551_b200 import _lib
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    # RLHC_BENCH_FUNCTIONAL=1: every rank on cuda:0 with gloo -- a functional check of the
+    # N > 1 code path on a one-GPU box, never a timing
+    functional = os.environ.get("RLHC_BENCH_FUNCTIONAL") == "1"
+    dev = torch.device("cuda", 0 if functional else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     if world > 1:
         from paper_2412_06551_b200 import dist as rdist
-        X, plan = rdist.setup_bench(cfg, rank, world, dev)
+        X, plan = rdist.setup_bench(cfg, rank, world, dev, strong=args.strong)
         run = lambda: plan.run(X)  # noqa: E731
     else:
         X = synth.config_matrix(cfg, device=dev)
@@ -147,36 +156,50 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     if code[0] != 0:
         raise RuntimeError(f"timed run failed: info={code}")
 
-    # ---- end to end through the C ABI with host buffers (copies inside the timed region)
-    e2e = None
-    if world == 1:
-        Xh = X.cpu().pin_memory()
-        Qh = torch.empty(cfg.m, cfg.n, dtype=torch.float64).pin_memory()
-        Rh = torch.empty(cfg.n, cfg.n, dtype=torch.float64).pin_memory()
-        Xd = torch.empty_like(X)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot = 0.0
-        for k in range(args.warmup + args.steps):
-            flush.zero_()
-            e0.record(stream)
-            Xd.copy_(Xh, non_blocking=True)
-            r2 = plan.run(Xd)
-            Qh.copy_(r2.Q, non_blocking=True)
-            Rh.copy_(r2.R, non_blocking=True)
-            e1.record(stream)
-            e1.synchronize()
-            if k >= args.warmup:
-                tot += e0.elapsed_time(e1)
-        e2e_ms = tot / args.steps
-        e2e = {"value": 8 * 8.0 * cfg.m * cfg.n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 8 * cfg.m * cfg.n, "d2h_bytes_per_step": 8 * (cfg.m * cfg.n + cfg.n * cfg.n)}
+    # ---- end to end through the public API with host buffers: every step copies this
+    # rank's rows of X from pinned host memory and reads Q (its rows) and R back; device
+    # time, max over ranks
+    m_rows = X.shape[0]
+    Xh = X.cpu().pin_memory()
+    Qh = torch.empty(m_rows, cfg.n, dtype=torch.float64).pin_memory()
+    Rh = torch.empty(cfg.n, cfg.n, dtype=torch.float64).pin_memory()
+    Xd = torch.empty_like(X)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    for k in range(args.warmup + args.steps):
+        flush.zero_()
+        if world > 1:
+            torch.distributed.barrier()
+        e0.record(stream)
+        Xd.copy_(Xh, non_blocking=True)
+        r2 = plan.run(Xd)
+        Qh.copy_(r2.Q, non_blocking=True)
+        Rh.copy_(r2.R, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        if k >= args.warmup:
+            tot += e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot = float(t.item())
+    e2e_ms = tot / args.steps
+    e2e = {"ms_per_step": e2e_ms, "unit": "GB/s", "h2d_bytes_per_step": 8 * m_rows * cfg.n,
+           "d2h_bytes_per_step": 8 * (m_rows * cfg.n + cfg.n * cfg.n), "per": "rank"}
     return ms, stages, launches, clk.summary(), e2e, X
 
 
-def roofline(cfg: synth.Config, stages: dict, world: int):
+def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, m_local: int = 0):
     calls = max(stages.get("calls", 1), 1)
     model = stage_model(cfg)
     hbm, hbm_src = _peaks()
+    if not any(v for k, v in stages.items() if k != "calls"):
+        # N > 1 runs through the per-stage entry points (no stage markers): the whole step
+        # of one rank against its HBM roof (8 passes over its rows)
+        byts = 64.0 * m_local * cfg.n
+        ach = byts / (step_ms * 1e-3) / 1e9
+        return {"kernel": "whole step (per rank)", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": None, "peak_source": hbm_src, "ms": step_ms}
     best = None
     for name, (byts, flops) in model.items():
         t = stages.get(name, 0.0) / calls * 1e-3
@@ -192,6 +215,12 @@ def roofline(cfg: synth.Config, stages: dict, world: int):
         traffic = prof.get(f"{cfg.name}:{name}")
     except Exception:
         pass
+    if name in ALU_STAGES:
+        ach = flops / t / 1e12
+        return {"kernel": name, "bound": "alu", "achieved": ach, "peak": PEAK_FP64_ALU_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / PEAK_FP64_ALU_TFLOPS, "traffic": traffic,
+                "peak_source": "scalar fp64 FMA measured on this pool (profiles/r01_probe_fp64_hbm.txt)",
+                "ms": t * 1e3, "note": "latency-bound tournament (levels x n sequential GEPP steps)"}
     if t_fp >= t_hbm:
         ach = flops / t / 1e12
         return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
@@ -238,24 +267,30 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: fixed global m (the config's), rows split over ranks; default: weak scaling, "
+                         "every rank holds the config's m rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
-    cfg_name = args.config or ("cfg2" if world == 1 else "cfg5")
-    cfg = synth.CONFIGS[cfg_name]
+    cfg = synth.CONFIGS[args.config]
+    strong = args.strong and world > 1
+    m_global = cfg.m if (strong or world == 1) else cfg.m * world
     if world > 1 and not torch.distributed.is_initialized():
-        torch.distributed.init_process_group("nccl" if args.impl == "ours" else "gloo")
-    workload = (f"{cfg.name}: {cfg.algo.upper()} m={cfg.m} n={cfg.n} "
+        functional = os.environ.get("RLHC_BENCH_FUNCTIONAL") == "1"
+        torch.distributed.init_process_group("nccl" if args.impl == "ours" and not functional else "gloo")
+    workload = (f"{cfg.name}: {cfg.algo.upper()} m={m_global} n={cfg.n} "
                 + (f"s={cfg.s}" if cfg.algo == "slhc3" else f"s1={cfg.s1} s2={cfg.s2}")
                 + f" kappa=1e{cfg.kappa_exp}{' colscale' if cfg.colscale else ''} seed={cfg.seed}")
     base = {"metric": f"{cfg.algo.upper()} fp64 QR algorithmic HBM throughput (8 passes of m x n)",
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "m": cfg.m, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "m": m_global, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
                        "kappa": f"1e{cfg.kappa_exp}", "l2": "flushed between steps (512 MiB write)",
-                       "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"}}
+                       "rows_per_gpu": m_global // world,
+                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "1 GPU"}}
     if args.impl == "reference":
         if rank != 0:
             return
@@ -269,10 +304,12 @@ def main():
     if rank != 0:
         return
     per_step = ms / args.steps
-    value = world * 8 * 8.0 * (cfg.m // world if world > 1 else cfg.m) * cfg.n / (per_step * 1e-3) / 1e9
+    value = 8 * 8.0 * m_global * cfg.n / (per_step * 1e-3) / 1e9  # whole job, all ranks
+    e2e["value"] = 8 * 8.0 * m_global * cfg.n / (e2e.pop("ms_per_step") * 1e-3) / 1e9
+    e2e["ms_per_step"] = 8 * 8.0 * m_global * cfg.n / e2e["value"] / 1e6
     line = dict(base, value=value, ms_per_step=per_step, gpu_launches=launches, clocks=clocks,
-                roofline=roofline(cfg, stages, world), e2e=e2e,
-                stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls"})
+                roofline=roofline(cfg, stages, world, per_step, m_global // world), e2e=e2e,
+                stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls" and v})
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, X)
     print(json.dumps(line), flush=True)

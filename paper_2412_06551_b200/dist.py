@@ -293,20 +293,35 @@ class BenchRunner:
         return _DistResult(self.plan, Q, R, piv, infos)
 
 
-def setup_bench(cfg, rank: int, world: int, device):
-    """Weak scaling: every rank holds cfg.m rows, the job factors a (world * cfg.m) x n X."""
+def setup_bench(cfg, rank: int, world: int, device, strong: bool = False):
+    """bench.py's N-GPU workload.  Weak scaling (default): every rank holds cfg.m rows and the
+    job factors a (world * cfg.m) x n X under the single-GPU default contract (rank subtrees
+    of 4^k leaves are complete subtrees of the global arity-4 tree, so the pivots equal a
+    single-GPU run on the whole X).  Strong scaling: the job factors cfg's m x n X, each rank
+    holds m / world rows; arity 2 so that 1/2/4/8 ranks share one tournament."""
     import synth
-    m_global = cfg.m * world
+    m_global = cfg.m if strong else cfg.m * world
+    m_local = m_global // world
     X = synth.baseline_matrix(m_global, cfg.n, cfg.kappa_exp, cfg.seed, cfg.colscale, device=device,
-                              row0=rank * cfg.m, rows=cfg.m)
-    plan = DistPlan(cfg.algo, m_global, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, device=device)
+                              row0=rank * m_local, rows=m_local)
+    tc = dist_default_cfg(m_global, cfg.n, world)
+    if strong:
+        tc = TsluCfg(tc.leaf_rows, 2, tc.panel)
+    plan = DistPlan(cfg.algo, m_global, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, cfg=tc, device=device)
     return X, BenchRunner(plan)
 
 
 def dist_default_cfg(m_global: int, n: int, world: int) -> TsluCfg:
-    """The single-GPU default contract, with arity 2 whenever a power-of-arity local leaf
-    count is needed for some GPU count (so 1/2/4/8 GPUs give identical pivots)."""
+    """The single-GPU default contract (rlhc_default_tslu_cfg) when each rank's leaf count
+    is a power of its arity -- the rank subtrees are then complete subtrees of the global
+    tree and the pivots equal the single-GPU run; otherwise arity 2 (check_shard_contract
+    rejects shards that fit neither)."""
     panel = min(max(n, 1), 64)
     W = kernel_width(panel)
     rows = 256 if W == 64 else 512
-    return TsluCfg(rows, 2, panel)
+    arity = max(2, rows // panel)
+    leaves = (m_global // max(world, 1)) // rows
+    k = round(math.log(leaves, arity)) if leaves > 1 else 0
+    if world > 1 and arity ** k != leaves:
+        arity = 2
+    return TsluCfg(rows, arity, panel)
