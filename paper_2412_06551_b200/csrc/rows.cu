@@ -201,8 +201,9 @@ cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int nco
 //     input once and writes its output once), written as one n x n partial per CTA.
 // out may equal A (each tile is read completely before it is written back).
 constexpr int RS_MAXN = 128;
-constexpr int RS_WARPS = 4;          // warps per CTA
-constexpr int RS_TR = 32 * RS_WARPS; // rows per tile (32 per warp = 4 m8 fragments)
+constexpr int RS_WARPS = 8;          // warps per CTA (2 CTAs per SM)
+constexpr int RS_MF = 2;             // m8 fragments (16 rows) per warp
+constexpr int RS_TR = 8 * RS_MF * RS_WARPS;  // rows per tile
 
 // Asynchronous row-tile load: rows [row_base, row_base + nrows) x columns [0, ncp) of A
 // into S (row stride lds), zero padded beyond `rows` / `ncols`.  Every thread issues all
@@ -227,10 +228,24 @@ __device__ __forceinline__ void tile_load_async(double* S, int lds, const double
   }
 }
 
+#ifdef RLHC_RS_TRACE
+// probe builds only (tools/probe/prs.cu): per-phase timestamps of CTA 0, warp 0
+__device__ long long g_rs_trace[256];
+#define RS_TRACE(i)                                                                   \
+  {                                                                                   \
+    const int rs_i_ = (i);                                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && rs_i_ < 256) g_rs_trace[rs_i_] = clock64(); \
+  }
+#else
+#define RS_TRACE(i)
+#endif
+
 template <bool GRAM>
 __global__ void __launch_bounds__(32 * RS_WARPS, 2)
 rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double* __restrict__ T, int64_t ldt,
                 const double* __restrict__ rdiag, double* out, int64_t ldo, double* __restrict__ gpart) {
+  // 8 warps x 16 rows: the substitution is a chain of dependent DMMA / fma steps per warp,
+  // so throughput comes from the number of warps in flight (16 per SM)
   extern __shared__ double smem[];
   const int ncp = (n + 7) & ~7;
   const int lds = ncp + 4;        // == 4 (mod 16) doubles: conflict-free fragment access
@@ -247,20 +262,24 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
   const int64_t ntiles = ceil_div<int64_t>(rows, RS_TR);
   const int lane = lane_id(), w = warp_id();
   const int g = lane >> 2, t = lane & 3;
-  const int gt = (ncp + 31) / 32;   // 32-wide Gram tiles per side (<= 4)
-  constexpr int GS = GRAM ? 1 : 1;  // one 32x32 Gram tile per warp (fused Gram only for n <= 64)
-  double gacc[4][4][2][GS];
+  // fused Gram (n <= 64): 32 x 32 output tiles of the upper triangle; tile (ti, tj) =
+  // warp w & 3 (index 2, the lower tile, is unused), rows split in halves by w >> 2
+  const int gt = (ncp + 31) / 32;
+  const int gq = w & 3, ghalf = w >> 2;
+  const int gti = gq >> 1, gtj = gq & 1;
+  const bool gwork = GRAM && gti < gt && gtj < gt && gti <= gtj;
+  double gacc[4][4][2];
   if (GRAM) {
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 4; b++)
-#pragma unroll
-        for (int q = 0; q < GS; q++) gacc[a][b][0][q] = gacc[a][b][1][q] = 0.0;
+      for (int b = 0; b < 4; b++) gacc[a][b][0] = gacc[a][b][1] = 0.0;
   }
   const int nc2 = ncp >> 1;  // 16-byte chunks per row
   const bool aligned = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
-  double* Sw = S + (w * 32) * lds;
+  double* Sw = S + (w * 8 * RS_MF) * lds;
+  int trc = 1;
+  RS_TRACE(0)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t rbase = tile * RS_TR;
     __syncthreads();  // previous tile fully consumed
@@ -269,49 +288,54 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
+    RS_TRACE(trc++)
     // ---- substitution, column blocks of 8
     for (int j0 = 0; j0 < ncp; j0 += 8) {
-      double acc[4][2];
+      double acc[RS_MF][2];
 #pragma unroll
-      for (int mf = 0; mf < 4; mf++) {
+      for (int mf = 0; mf < RS_MF; mf++) {
         const double2 c2 = *reinterpret_cast<const double2*>(Sw + (mf * 8 + g) * lds + j0 + 2 * t);
         acc[mf][0] = c2.x; acc[mf][1] = c2.y;
       }
+#pragma unroll 2
       for (int k0 = 0; k0 < j0; k0 += 4) {
         const double b = Tn[(k0 + t) * lds + j0 + g];
 #pragma unroll
-        for (int mf = 0; mf < 4; mf++) dmma(acc[mf][0], acc[mf][1], Sw[(mf * 8 + g) * lds + k0 + t], b);
+        for (int mf = 0; mf < RS_MF; mf++) dmma(acc[mf][0], acc[mf][1], Sw[(mf * 8 + g) * lds + k0 + t], b);
       }
 #pragma unroll
-      for (int mf = 0; mf < 4; mf++)
+      for (int mf = 0; mf < RS_MF; mf++)
         *reinterpret_cast<double2*>(Sw + (mf * 8 + g) * lds + j0 + 2 * t) = make_double2(acc[mf][0], acc[mf][1]);
       __syncwarp();
-      // diagonal 8x8 block: lane = row, static indices:
+      // diagonal 8x8 block: lane = row (16 rows per warp), static indices:
       //   l_k = v_k * (1/T_kk);  v_j = fma(l_k, -T_kj, v_j)  (== fma(-l_k, T_kj, v_j))
-      double* row = Sw + lane * lds + j0;
-      double v[8];
-      {
-        const double2 p0 = reinterpret_cast<const double2*>(row)[0], p1 = reinterpret_cast<const double2*>(row)[1];
-        const double2 p2 = reinterpret_cast<const double2*>(row)[2], p3 = reinterpret_cast<const double2*>(row)[3];
-        v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y; v[4] = p2.x; v[5] = p2.y; v[6] = p3.x; v[7] = p3.y;
-      }
-      const double* Td = Tn + j0 * lds + j0;
-      const int kmax = min(8, n - j0);
-#pragma unroll
-      for (int kk = 0; kk < 8; kk++) {
-        if (kk < kmax) {
-          const double l = __dmul_rn(v[kk], rd[j0 + kk]);
-          v[kk] = l;
-#pragma unroll
-          for (int jj = kk + 1; jj < 8; jj++) v[jj] = __fma_rn(l, Td[kk * lds + jj], v[jj]);
+      if (lane < 8 * RS_MF) {
+        double* row = Sw + lane * lds + j0;
+        double v[8];
+        {
+          const double2 p0 = reinterpret_cast<const double2*>(row)[0], p1 = reinterpret_cast<const double2*>(row)[1];
+          const double2 p2 = reinterpret_cast<const double2*>(row)[2], p3 = reinterpret_cast<const double2*>(row)[3];
+          v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y; v[4] = p2.x; v[5] = p2.y; v[6] = p3.x; v[7] = p3.y;
         }
+        const double* Td = Tn + j0 * lds + j0;
+        const int kmax = min(8, n - j0);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk++) {
+          if (kk < kmax) {
+            const double l = __dmul_rn(v[kk], rd[j0 + kk]);
+            v[kk] = l;
+#pragma unroll
+            for (int jj = kk + 1; jj < 8; jj++) v[jj] = __fma_rn(l, Td[kk * lds + jj], v[jj]);
+          }
+        }
+        reinterpret_cast<double2*>(row)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2*>(row)[1] = make_double2(v[2], v[3]);
+        reinterpret_cast<double2*>(row)[2] = make_double2(v[4], v[5]);
+        reinterpret_cast<double2*>(row)[3] = make_double2(v[6], v[7]);
       }
-      reinterpret_cast<double2*>(row)[0] = make_double2(v[0], v[1]);
-      reinterpret_cast<double2*>(row)[1] = make_double2(v[2], v[3]);
-      reinterpret_cast<double2*>(row)[2] = make_double2(v[4], v[5]);
-      reinterpret_cast<double2*>(row)[3] = make_double2(v[6], v[7]);
       __syncwarp();
     }
+    RS_TRACE(trc++)
     __syncthreads();
     // ---- store the tile (16-byte stores)
     {
@@ -328,47 +352,55 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
           else { if (c < n) dst[0] = v.x; if (c + 1 < n) dst[1] = v.y; }
         }
     }
-    if (GRAM) {
-      // G += tile^T tile on DMMA (rows beyond `rows` are zero-padded)
+    RS_TRACE(trc++)
+    if (gwork) {
+      // G += tile^T tile on DMMA (rows beyond `rows` are zero-padded); this warp: rows
+      // [ghalf * RS_TR/2, (ghalf+1) * RS_TR/2) of its 32 x 32 tile
+      const int i0 = gti * 32, j0 = gtj * 32;
+      const int kb = ghalf * (RS_TR / 2);
+#pragma unroll 2
+      for (int k0 = kb; k0 < kb + RS_TR / 2; k0 += 4) {
+        double af[4], bf[4];
 #pragma unroll
-      for (int q = 0; q < GS; q++) {
-        const int tl = w + q * RS_WARPS;
-        const int ti = tl / gt, tj = tl - ti * gt;
-        if (ti < gt && ti <= tj) {
-          const int i0 = ti * 32, j0 = tj * 32;
-          for (int k0 = 0; k0 < RS_TR; k0 += 4) {
-            double af[4], bf[4];
+        for (int a = 0; a < 4; a++) af[a] = (i0 + a * 8 < ncp) ? S[(k0 + t) * lds + i0 + a * 8 + g] : 0.0;
 #pragma unroll
-            for (int a = 0; a < 4; a++) af[a] = (i0 + a * 8 < ncp) ? S[(k0 + t) * lds + i0 + a * 8 + g] : 0.0;
-#pragma unroll
-            for (int b = 0; b < 4; b++) bf[b] = (j0 + b * 8 < ncp) ? S[(k0 + t) * lds + j0 + b * 8 + g] : 0.0;
-#pragma unroll
-            for (int a = 0; a < 4; a++)
-#pragma unroll
-              for (int b = 0; b < 4; b++) dmma(gacc[a][b][0][q], gacc[a][b][1][q], af[a], bf[b]);
-          }
-        }
-      }
-    }
-  }
-  if (GRAM) {
-    double* P = gpart + (size_t)blockIdx.x * ncp * ncp;
-#pragma unroll
-    for (int q = 0; q < GS; q++) {
-      const int tl = w + q * RS_WARPS;
-      const int ti = tl / gt, tj = tl - ti * gt;
-      if (ti < gt && ti <= tj) {
+        for (int b = 0; b < 4; b++) bf[b] = (j0 + b * 8 < ncp) ? S[(k0 + t) * lds + j0 + b * 8 + g] : 0.0;
 #pragma unroll
         for (int a = 0; a < 4; a++)
 #pragma unroll
-          for (int b = 0; b < 4; b++) {
-            int r = ti * 32 + a * 8 + g, c = tj * 32 + b * 8 + 2 * t;
-            if (r < ncp && c < ncp) {
-              P[r * ncp + c] = gacc[a][b][0][q];
-              P[r * ncp + c + 1] = gacc[a][b][1][q];
-            }
-          }
+          for (int b = 0; b < 4; b++) dmma(gacc[a][b][0], gacc[a][b][1], af[a], bf[b]);
       }
+    }
+  }
+  RS_TRACE(trc++)
+  if (GRAM) {
+    // the two row halves of each tile: half 1 -> shared memory, half 0 adds it (fixed order)
+    __syncthreads();
+    double* Gs = S;  // reuse the tile buffer: 4 tiles x 32 x 33
+    if (gwork && ghalf == 1) {
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int r = a * 8 + g, c = b * 8 + 2 * t;
+          Gs[gq * 32 * 33 + r * 33 + c] = gacc[a][b][0];
+          Gs[gq * 32 * 33 + r * 33 + c + 1] = gacc[a][b][1];
+        }
+    }
+    __syncthreads();
+    if (gwork && ghalf == 0) {
+      double* P = gpart + (size_t)blockIdx.x * ncp * ncp;
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int r = a * 8 + g, c = b * 8 + 2 * t;
+          const int gr = gti * 32 + r, gc = gtj * 32 + c;
+          if (gr < ncp && gc < ncp) {
+            P[gr * ncp + gc] = gacc[a][b][0] + Gs[gq * 32 * 33 + r * 33 + c];
+            P[gr * ncp + gc + 1] = gacc[a][b][1] + Gs[gq * 32 * 33 + r * 33 + c + 1];
+          }
+        }
     }
   }
 }
