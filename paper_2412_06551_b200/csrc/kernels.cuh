@@ -12,10 +12,21 @@ void set_last_error(const std::string& msg);
 unsigned long long launch_count();
 
 // tslu.cu
+// Root-node outputs of a single-panel factorization (the root's GEPP computes them on the
+// way, select.cuh): U written during the select; piv, L11 and 1/diag(U) after it.
+struct RootOut {
+  double* U;       // n x n, ld n (strict lower part pre-zeroed by the caller)
+  int64_t* piv;    // [n] global row ids in pivot order
+  double* L11;     // n x n, ld n: multipliers of the pivot rows, unit diagonal
+  double* rdiag;   // [n] IEEE 1 / U(t, t)
+  unsigned long long* status;
+  int n;
+};
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st);
+                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
+                             const RootOut* root = nullptr);
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
-                             int w, int* ids, int* cnt, double* vals, cudaStream_t st);
+                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* root = nullptr);
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
                                      const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
                                      uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st,

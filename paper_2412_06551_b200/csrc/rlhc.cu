@@ -131,19 +131,25 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
   const bool panels = cfg.panel < n;
   if (panels) CUDA_TRY(cudaMemsetAsync(t.chosen, 0, (size_t)rows, st));
   CUDA_TRY(cudaMemsetAsync(U, 0, (size_t)n * n * sizeof(double), st));  // strict lower part of U is 0
+  // single panel, single process: the root node's GEPP already computes U, the L11
+  // multipliers and 1/diag(U) (same fma chains as the panel elimination), so it emits them
+  const bool root_emit = !panels && row0 == 0;
+  RootOut ro{U, piv, L11, t.rd, t.status, (int)n};
   for (int64_t p0 = 0; p0 < n; p0 += cfg.panel) {
     const int w = (int)std::min<int64_t>(cfg.panel, n - p0);
     const double* src = (p0 == 0) ? X : tw;
     const int64_t lds = (p0 == 0) ? ldx : ldtw;
     CUDA_TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
-                              t.cnt[0], t.vals[0], st));
+                              t.cnt[0], t.vals[0], st, root_emit && nleaves == 1 ? &ro : nullptr));
     int cur = 0, nslots = nleaves;
     while (nslots > 1) {
+      const int nout = (int)ceil_div<int64_t>(nslots, cfg.arity);
       CUDA_TRY(launch_tslu_node(W, t.ids[cur], t.cnt[cur], t.vals[cur], nslots, cfg.arity, w, t.ids[cur ^ 1],
-                                t.cnt[cur ^ 1], t.vals[cur ^ 1], st));
-      nslots = (int)ceil_div<int64_t>(nslots, cfg.arity);
+                                t.cnt[cur ^ 1], t.vals[cur ^ 1], st, root_emit && nout == 1 ? &ro : nullptr));
+      nslots = nout;
       cur ^= 1;
     }
+    if (root_emit) return RLHC_OK;
     CUDA_TRY(launch_tslu_panel_factor(src, lds, rows, row0, (int)p0, w, (int)n, t.ids[cur], t.cnt[cur], U, piv,
                                       panels ? t.chosen : nullptr, nullptr, t.status, st));
     CUDA_TRY(launch_rdiag(U + p0 * n + p0, w, n + 0, t.rd + p0, RLHC_STAGE_LU, t.status, st));

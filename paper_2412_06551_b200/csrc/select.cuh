@@ -23,6 +23,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace rlhc {
 
@@ -43,6 +44,8 @@ struct SelSmem {
   int zero[W];                 // 1: zero pivot column at step t (R#5: no update); -1: pivot < 0
   int out_src[W];
   int out_id[W];
+  double* Uout;                // root emission (single panel): U rows, ld = ldu; else null
+  int ldu;
 #ifdef RLHC_SEL_TRACE
   long long trace[(W + 1) * 32];
 #endif
@@ -161,6 +164,10 @@ RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, const int (
   if (lane == 0) {
     sm.r[t] = rabs;
     sm.zero[t] = zero ? 1 : (nb ? -1 : 0);  // 1: zero column; -1: negative pivot
+    if (sm.Uout) {  // U(t, t) = the pivot itself (|pivot| bits and its sign)
+      const double pv = __longlong_as_double(gb);
+      sm.Uout[(int64_t)t * sm.ldu + t] = nb ? -pv : pv;
+    }
   }
   __syncwarp();
   SEL_TRACE(t * 32 + 20)
@@ -194,6 +201,7 @@ RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[
   if (own) {
     if (upd) {
       const double uk = __shfl_sync(0xffffffffu, sel_mux<RS, CW>(a, K, pslot), plane);
+      u[K] = uk;
 #pragma unroll
       for (int s = 0; s < RS; s++) a[s][K] = __fma_rn(-l[s], uk, a[s][K]);
     }
@@ -211,6 +219,15 @@ RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[
     sel_bcast<CW, K, CW>(u, plane);
     sel_update<RS, CW, K, CW>(a, l, u);
 #endif
+  }
+  // root emission: U(t-1, c) for this warp's columns c > t-1 = the pivot row's values after
+  // t-1 eliminations (the oracle's elimination-among-winners chain, bit for bit)
+  if (upd && sm.Uout && lane < CW - K) {
+    double uv = 0.0;
+#pragma unroll
+    for (int k = K; k < CW; k++) uv = (lane == k - K) ? u[k] : uv;
+    const int c = warp_id() + NW * (K + lane);
+    if (c > t - 1 && c < sm.ldu) sm.Uout[(int64_t)(t - 1) * sm.ldu + c] = uv;  // single panel: w = n = ldu
   }
   SEL_TRACE(t * 32 + warp_id() * 2 + 1)
 }
@@ -238,8 +255,35 @@ struct SelGroup<W, NW, RS, W / NW> {
 // Initialise the step barriers; call before the candidate loads (gepp_select's first
 // __syncthreads publishes them).
 template <int W, int NW, int RS>
-RLHC_DEV void sel_init(SelSmem<W, NW, RS>& sm) {
+RLHC_DEV void sel_init(SelSmem<W, NW, RS>& sm, double* Uout = nullptr, int ldu = 0) {
   for (int t = threadIdx.x; t < W; t += blockDim.x) mbar_init(&sm.bar[t], 32);
+  if (threadIdx.x == 0) {
+    sm.Uout = Uout;
+    sm.ldu = ldu;
+  }
+}
+
+template <int W, int NW, int RS>
+RLHC_DEV void sel_root_finish(const SelSmem<W, NW, RS>& sm, int steps, int w, const RootOut& ro) {
+  if (threadIdx.x == 0 && steps < w) report(ro.status, RLHC_ERANKDEF, RLHC_STAGE_LU, steps);
+  for (int t = threadIdx.x; t < steps; t += blockDim.x) {
+    ro.piv[t] = sm.out_id[t];
+    const int zf = sm.zero[t];
+    if (zf == 1) report(ro.status, RLHC_ERANKDEF, RLHC_STAGE_LU, t);
+    ro.rdiag[t] = zf == 1 ? 0.0 : (zf < 0 ? -sm.r[t] : sm.r[t]);
+  }
+  for (int e = threadIdx.x; e < steps * w; e += blockDim.x) {
+    const int t = e / w, j = e - t * w;
+    double v = 0.0;
+    if (j == t) {
+      v = 1.0;
+    } else if (j < t) {  // l_j of pivot row t: col_j(row) * (1/pivot_j), as every warp formed it
+      const int zf = sm.zero[j];
+      const double r = zf < 0 ? -sm.r[j] : sm.r[j];
+      v = zf == 1 ? 0.0 : __dmul_rn(sm.col[j][sm.out_src[t]], r);
+    }
+    ro.L11[(int64_t)t * ro.n + j] = v;
+  }
 }
 
 // GEPP selection (definition: oracle gepp_select / DESIGN.md R#4-R#5).

@@ -20,11 +20,11 @@ template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
-                 double* __restrict__ out_vals) {
+                 double* __restrict__ out_vals, RootOut root) {
   constexpr int R = 32 * RS, CW = W / NW;
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
-  sel_init(sm);
+  sel_init(sm, root.U, root.n);
   const int lane = lane_id(), wp = warp_id();
   double a[RS][CW];
   int gid[RS];
@@ -40,6 +40,7 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
     for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
   }
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
+  if (root.U) sel_root_finish(sm, steps, w, root);
   int* oi = out_ids + (size_t)blockIdx.x * W;
   double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
@@ -58,11 +59,11 @@ template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt, const double* __restrict__ in_vals,
                  int nslots_in, int arity, int w, int* __restrict__ out_ids, int* __restrict__ out_cnt,
-                 double* __restrict__ out_vals) {
+                 double* __restrict__ out_vals, RootOut root) {
   constexpr int CW = W / NW;
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
-  sel_init(sm);
+  sel_init(sm, root.U, root.n);
   const int lane = lane_id(), wp = warp_id();
   const int c0 = blockIdx.x * arity;
   double a[RS][CW];
@@ -82,6 +83,7 @@ tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt,
     for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
   }
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
+  if (root.U) sel_root_finish(sm, steps, w, root);
   int* oi = out_ids + (size_t)blockIdx.x * W;
   double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
@@ -203,7 +205,8 @@ int select_rows(int W) { return W == 64 ? 256 : 512; }
 
 template <int W, int NW, int RS>
 static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                            const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st) {
+                            const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
+                            const RootOut& root) {
   int nleaves = (int)ceil_div<int64_t>(rows, 32 * RS);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
   static bool attr = false;  // once per instantiation (idempotent, so a race is harmless)
@@ -212,12 +215,13 @@ static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_
     cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals);
+  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals,
+                                                                            root);
   return cudaGetLastError();
 }
 template <int W, int NW, int RS>
 static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity, int w,
-                            int* ids, int* cnt, double* vals, cudaStream_t st) {
+                            int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut& root) {
   int nout = ceil_div(nin, arity);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
   static bool attr = false;
@@ -226,25 +230,29 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
     cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, smem, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals);
+  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, smem, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt,
+                                                                            vals, root);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st) {
+                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
+                             const RootOut* rootp) {
+  const RootOut root = rootp ? *rootp : RootOut{};
   switch (W) {
-    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
-    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
-    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st);
+    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
+    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
+    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
   }
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
-                             int w, int* ids, int* cnt, double* vals, cudaStream_t st) {
+                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* rootp) {
+  const RootOut root = rootp ? *rootp : RootOut{};
   switch (W) {
-    case 16: return run_node<16, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
-    case 32: return run_node<32, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
-    case 64: return run_node<64, 8, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st);
+    case 16: return run_node<16, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
+    case 32: return run_node<32, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
+    case 64: return run_node<64, 8, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
   }
   return cudaErrorInvalidValue;
 }
