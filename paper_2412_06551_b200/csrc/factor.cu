@@ -110,47 +110,41 @@ hqr2_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const doubl
   }
 }
 
-// ------------------------------------------------------------------ register-resident HQR
-// For s <= 32*RR, n <= 16*QC: the s x n matrix lives in REGISTERS of 16 warps: warp w owns
-// columns {w + 16 q : q < QC}, lane l holds rows {l + 32 r : r < RR}; a[r][q].  Step k:
-// the owner of column k forms the reflector (norm by warp reduction), writes v (zeros
-// above row k, 1 at row k) to shared memory and publishes tau; one barrier; every warp
-// applies it to its columns j > k: dot = v . a[:, j] (RR FMAs + warp reduction), a[:, j]
-// -= (tau dot) v.  Look-ahead: the owner of column k+1 applies reflector k to that column
-// first and forms reflector k+1 before its other columns.  No shared-memory traffic on
-// the matrix itself (the smem-resident kernel above is bandwidth bound).
 constexpr int HQ_WARPS = 16;
 
-template <int RR, int QC, int Q>
-__device__ __forceinline__ void hq_get_col(const double (&a)[RR][QC], int q, double (&x)[RR]) {
-  if constexpr (Q < QC) {
-    if (q == Q) {
+// ------------------------------------------------------------------ register-resident HQR
+// For s <= 32*RR, n <= 16*QC the s x n sketch lives in REGISTERS of 16 warps: column j owned
+// by warp j mod 16, lane l holds rows l + 32 r (reflector formulas of R#O7), without CTA
+// barriers (a barrier per step measured ~3000 cycles/step): step k's reflector is published to shared memory
+// (v_k, tau_k) and signalled by mbarrier k.  The owner of column k+1 (another warp) applies
+// reflector k to that column first, forms reflector k+1 and publishes it, then applies k to
+// its later columns; every other warp applies k to its columns as soon as it is published.
+// All reflectors stay in shared memory (n x s doubles), so no slot is reused.
+template <int RR, int QC>
+struct HqpSmem {
+  double v[16 * QC][32 * RR];
+  double tau[16 * QC];
+  double beta[16 * QC];
+  unsigned long long bar[16 * QC];
+};
+
+template <int RR, int QC>
+RLHC_DEV void hqp_apply(double (&a)[RR][QC], int q, const double (&v)[RR], double tau) {
+  double dot = 0.0;
 #pragma unroll
-      for (int r = 0; r < RR; r++) x[r] = a[r][Q];
-    } else {
-      hq_get_col<RR, QC, Q + 1>(a, q, x);
-    }
-  }
-}
-template <int RR, int QC, int Q>
-__device__ __forceinline__ void hq_set_col(double (&a)[RR][QC], int q, const double (&x)[RR]) {
-  if constexpr (Q < QC) {
-    if (q == Q) {
+  for (int r = 0; r < RR; r++) dot = __fma_rn(v[r], a[r][q], dot);
+  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  const double tw = tau * dot;
 #pragma unroll
-      for (int r = 0; r < RR; r++) a[r][Q] = x[r];
-    } else {
-      hq_set_col<RR, QC, Q + 1>(a, q, x);
-    }
-  }
+  for (int r = 0; r < RR; r++) a[r][q] = __fma_rn(-v[r], tw, a[r][q]);
 }
 
 template <int RR, int QC>
 __global__ void __launch_bounds__(32 * HQ_WARPS)
-hqr_reg_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const double* __restrict__ sgn_ref,
-               double* __restrict__ S, unsigned long long* status) {
-  __shared__ double vbuf[2][32 * RR];
-  __shared__ double tauS[2], betaS[HQ_WARPS * QC];
-  __shared__ int flag;
+hqr_pipe_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const double* __restrict__ sgn_ref,
+                double* __restrict__ S, unsigned long long* status) {
+  extern __shared__ __align__(16) unsigned char hq_raw[];
+  HqpSmem<RR, QC>& sm = *reinterpret_cast<HqpSmem<RR, QC>*>(hq_raw);
   const int lane = lane_id(), wp = warp_id();
   double a[RR][QC];
 #pragma unroll
@@ -160,78 +154,73 @@ hqr_reg_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const do
       const int i = lane + 32 * r, j = wp + HQ_WARPS * q;
       a[r][q] = (i < s && j < n) ? A[(int64_t)i * lda + j] : 0.0;
     }
-  if (threadIdx.x == 0) flag = 0;
-  // reflector of column k, owned by this warp at slot q (x = the column's values)
-  auto reflector = [&](int k, int q) {
-    double x[RR];
-    hq_get_col<RR, QC, 0>(a, q, x);
-    double part = 0.0, alpha = 0.0;
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      const int i = lane + 32 * r;
-      if (i > k && i < s) part = __fma_rn(x[r], x[r], part);
-      if (i == k) alpha = x[r];
-    }
-    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    alpha = __shfl_sync(0xffffffffu, alpha, k & 31);
-    const double xnorm = __dsqrt_rn(part);
-    double beta = alpha, tau = 0.0, sc = 0.0;
-    if (xnorm != 0.0) {
-      beta = -(alpha >= 0.0 ? 1.0 : -1.0) * hypot(alpha, xnorm);
-      tau = __ddiv_rn(beta - alpha, beta);
-      sc = __ddiv_rn(1.0, alpha - beta);
-    } else if (alpha == 0.0 && lane == 0) {
-      report(status, RLHC_ERANKDEF, RLHC_STAGE_HQR, k);
-      flag = 1;
-    }
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      const int i = lane + 32 * r;
-      const double v = (i > k) ? x[r] * sc : (i == k ? 1.0 : 0.0);
-      vbuf[k & 1][i] = v;
-      x[r] = (i > k) ? x[r] : (i == k ? beta : x[r]);  // column k of R: beta on the diagonal
-    }
-    hq_set_col<RR, QC, 0>(a, q, x);
-    if (lane == 0) { tauS[k & 1] = tau; betaS[k] = beta; }
-  };
-  // apply reflector k (v in vbuf[k & 1], tau) to this warp's slot q
-  auto apply = [&](int k, int q, const double (&v)[RR], double tau) {
-    double x[RR];
-    hq_get_col<RR, QC, 0>(a, q, x);
-    double dot = 0.0;
-#pragma unroll
-    for (int r = 0; r < RR; r++) dot = __fma_rn(v[r], x[r], dot);
-    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const double tw = tau * dot;
-#pragma unroll
-    for (int r = 0; r < RR; r++) x[r] = __fma_rn(-v[r], tw, x[r]);
-    hq_set_col<RR, QC, 0>(a, q, x);
-  };
+  for (int k = threadIdx.x; k < 16 * QC; k += blockDim.x) mbar_init(&sm.bar[k], 32);
   __syncthreads();
-  if (wp == 0) reflector(0, 0);
-  __syncthreads();
-  for (int k = 0; k < n; k++) {
-    if (flag) break;
-    const double tau = tauS[k & 1];
-    double v[RR];
+  // the warp's last column; it has nothing to do after step last-1
+  const int last = wp + HQ_WARPS * ((n - 1 - wp) / HQ_WARPS);
+  double v[RR], tau = 0.0;
 #pragma unroll
-    for (int r = 0; r < RR; r++) v[r] = vbuf[k & 1][lane + 32 * r];
-    const int jn = k + 1;
-    const bool own_next = jn < n && (jn % HQ_WARPS) == wp;
-    if (own_next) {
-      if (tau != 0.0) apply(k, jn / HQ_WARPS, v, tau);
-      reflector(jn, jn / HQ_WARPS);
-    }
-    if (tau != 0.0) {
+  for (int Q = 0; Q < QC; Q++) {
+#pragma unroll 1
+    for (int jj = 0; jj < HQ_WARPS; jj++) {
+      const int k = Q * HQ_WARPS + jj;  // step k: reflector of column k (owner: warp jj)
+      if (k >= n || wp >= n || k > last) break;
+      if (k > 0) {
+        mbar_wait(&sm.bar[k - 1], 0);
+        tau = sm.tau[k - 1];
 #pragma unroll
-      for (int q = 0; q < QC; q++) {
-        const int j = wp + HQ_WARPS * q;
-        if (j > k && j < n && j != jn) apply(k, q, v, tau);
+        for (int r = 0; r < RR; r++) v[r] = sm.v[k - 1][lane + 32 * r];
+      }
+      if (jj == wp) {
+        // column k = (wp, Q): reflector k-1 first, then form reflector k and publish it
+        if (k > 0 && tau != 0.0) hqp_apply<RR, QC>(a, Q, v, tau);
+        double part = 0.0, alpha = 0.0;
+#pragma unroll
+        for (int r = 0; r < RR; r++) {
+          const int i = lane + 32 * r;
+          if (i > k && i < s) part = __fma_rn(a[r][Q], a[r][Q], part);
+          if (i == k) alpha = a[r][Q];
+        }
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        alpha = __shfl_sync(0xffffffffu, alpha, k & 31);
+        double beta = alpha, tk = 0.0, sc = 0.0;
+        if (part != 0.0) {
+          // beta = -sign(alpha) ||(alpha, x)|| (R#O7; sum of squares already formed, so the
+          // norm is taken directly rather than through hypot)
+          beta = -(alpha >= 0.0 ? 1.0 : -1.0) * __dsqrt_rn(__fma_rn(alpha, alpha, part));
+          tk = __ddiv_rn(beta - alpha, beta);
+          sc = __ddiv_rn(1.0, alpha - beta);
+        } else if (alpha == 0.0 && lane == 0) {
+          report(status, RLHC_ERANKDEF, RLHC_STAGE_HQR, k);
+        }
+#pragma unroll
+        for (int r = 0; r < RR; r++) {
+          const int i = lane + 32 * r;
+          sm.v[k][i] = (i > k) ? a[r][Q] * sc : (i == k ? 1.0 : 0.0);
+          if (i == k) a[r][Q] = beta;
+        }
+        if (lane == 0) {
+          sm.tau[k] = tk;
+          sm.beta[k] = beta;
+        }
+        __syncwarp();
+        mbar_arrive(&sm.bar[k]);
+        // reflector k-1 on this warp's later columns
+        if (k > 0 && tau != 0.0) {
+#pragma unroll
+          for (int q = Q + 1; q < QC; q++)
+            if (wp + HQ_WARPS * q < n) hqp_apply<RR, QC>(a, q, v, tau);
+        }
+      } else if (k > 0 && tau != 0.0) {
+        // reflector k-1 on this warp's columns >= k (column (wp, Q) if wp > jj, and later ones)
+#pragma unroll
+        for (int q = Q; q < QC; q++)
+          if ((q > Q || wp > jj) && wp + HQ_WARPS * q < n) hqp_apply<RR, QC>(a, q, v, tau);
       }
     }
-    __syncthreads();
   }
-  // R = upper n x n part (diag from the reflectors), sign-aligned with sgn_ref
+  __syncthreads();
+  // R = upper n x n part (diag = beta_k), sign-aligned with sgn_ref (R#7)
 #pragma unroll
   for (int r = 0; r < RR; r++)
 #pragma unroll
@@ -239,10 +228,7 @@ hqr_reg_kernel(const double* __restrict__ A, int s, int n, int64_t lda, const do
       const int i = lane + 32 * r, j = wp + HQ_WARPS * q;
       if (i < n && j < n) {
         double val = (j >= i) ? a[r][q] : 0.0;
-        if (sgn_ref) {
-          const double d = betaS[i];
-          if ((d < 0.0) != (sgn_ref[(int64_t)i * n + i] < 0.0)) val = -val;
-        }
+        if (sgn_ref && ((sm.beta[i] < 0.0) != (sgn_ref[(int64_t)i * n + i] < 0.0))) val = -val;
         S[(int64_t)i * n + j] = val;
       }
     }
@@ -543,8 +529,14 @@ cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double*
   const int threads = n >= 512 ? 1024 : 512;
 #define HQR_REG(RR, QC)                                                                            \
   if (s <= 32 * RR && n <= HQ_WARPS * QC) {                                                        \
+    constexpr int smem = (int)sizeof(HqpSmem<RR, QC>);                                             \
+    static bool attr = false;                                                                      \
+    if (!attr) {                                                                                   \
+      cudaFuncSetAttribute(hqr_pipe_kernel<RR, QC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                                 \
+    }                                                                                              \
     note_launch();                                                                                 \
-    hqr_reg_kernel<RR, QC><<<1, 32 * HQ_WARPS, 0, st>>>(A, s, n, lda, sgn_ref, S, status);         \
+    hqr_pipe_kernel<RR, QC><<<1, 32 * HQ_WARPS, smem, st>>>(A, s, n, lda, sgn_ref, S, status);     \
     return cudaGetLastError();                                                                     \
   }
   HQR_REG(1, 1)
