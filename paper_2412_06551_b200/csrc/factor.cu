@@ -611,196 +611,115 @@ chol2_kernel(const double* __restrict__ G, int n, double* __restrict__ R, double
     for (int j = lane; j < n; j += 32) R[(int64_t)i * n + j] = (j >= i) ? C[(int64_t)i * ld + j] : 0.0;
 }
 
-// Register-resident Cholesky for n <= 32*RR (rows) and n <= 8*QC (columns): warp w owns
-// columns {w + 8 q}, lane l holds rows {l + 32 r}.  Step k: the owner of (k, k) forms
-// r_kk (breakdown check) -> barrier -> the holders of row k divide it by r_kk and publish
-// it through shared memory -> barrier -> every lane updates its entries (i, j), k < i <= j:
-// C_ij -= C_ki C_kj.  Same operation order per element as the smem kernel.
-constexpr int CH_WARPS = 8;
+// ------------------------------------------------------------------ pipelined Cholesky
+// n <= 128: G (symmetric) in REGISTERS of 16 warps, column j owned by warp j mod 16, lane l
+// holds rows l + 32 r.  Right-looking, no CTA barriers: the owner of column k applies step
+// k-1 to it, takes d = a_kk (d <= 0 or non-finite -> EBREAKDOWN(stage, koff + k), SPEC
+// S:55), r_kk = sqrt(d), publishes the column l_k = a(:, k) / r_kk (rows > k; r_kk at k) and
+// 1/r_kk through shared memory + mbarrier k, then applies step k-1 to its later columns;
+// every other warp applies a(:, j) -= l_k * l_k(j) to its columns j > k as soon as l_k is
+// published.  R(k, j) = l_k(j) for j >= k; 1/diag(R) is emitted for the substitution passes.
+template <int RR, int QC>
+struct CholSmem {
+  double l[16 * QC][32 * RR];
+  double rinv[16 * QC];
+  unsigned long long bar[16 * QC];
+};
 
 template <int RR, int QC>
-__global__ void __launch_bounds__(32 * CH_WARPS)
-chol_reg_kernel(const double* __restrict__ G, int n, double* __restrict__ R, int stage, unsigned long long* status) {
-  __shared__ double rowk[2][CH_WARPS * QC];
-  __shared__ double rkk[2], rinv[2];
-  __shared__ int flag;
+__global__ void __launch_bounds__(512)
+chol_pipe_kernel(const double* __restrict__ G, int64_t ldg, int n, double* __restrict__ R, int64_t ldr,
+                 double* __restrict__ rdiag, int stage, int koff, unsigned long long* status) {
+  extern __shared__ __align__(16) unsigned char ch_raw[];
+  CholSmem<RR, QC>& sm = *reinterpret_cast<CholSmem<RR, QC>*>(ch_raw);
   const int lane = lane_id(), wp = warp_id();
-  double c[RR][QC];
+  double a[RR][QC];
 #pragma unroll
   for (int r = 0; r < RR; r++)
 #pragma unroll
     for (int q = 0; q < QC; q++) {
-      const int i = lane + 32 * r, j = wp + CH_WARPS * q;
-      c[r][q] = (i < n && j < n) ? G[(int64_t)i * n + j] : 0.0;
+      const int i = lane + 32 * r, j = wp + 16 * q;
+      a[r][q] = (i < n && j < n) ? G[(int64_t)i * ldg + j] : 0.0;
     }
-  if (threadIdx.x == 0) flag = 0;
+  for (int k = threadIdx.x; k < 16 * QC; k += blockDim.x) mbar_init(&sm.bar[k], 32);
   __syncthreads();
-  for (int k = 0; k < n; k++) {
-    const int par = k & 1;
-    const int kr = k >> 5, kq = k / CH_WARPS;
-    if (wp == (k % CH_WARPS) && lane == (k & 31)) {
-      double d = 0.0;
+  const int last = wp < n ? wp + 16 * ((n - 1 - wp) / 16) : -1;
+  double lk[RR];
 #pragma unroll
-      for (int r = 0; r < RR; r++)
+  for (int Q = 0; Q < QC; Q++) {
+#pragma unroll 1
+    for (int jj = 0; jj < 16; jj++) {
+      const int k = Q * 16 + jj;  // step k: column k (owner warp jj)
+      if (k >= n || k > last) break;
+      if (k > 0) {
+        mbar_wait(&sm.bar[k - 1], 0);
 #pragma unroll
-        for (int q = 0; q < QC; q++) d = (r == kr && q == kq) ? c[r][q] : d;
-      if (!(d > 0.0) || !isfinite(d)) { report(status, RLHC_EBREAKDOWN, stage, k); flag = 1; }
-      const double sq = __dsqrt_rn(d);
-      rkk[par] = sq;
-      rinv[par] = __drcp_rn(sq);
-    }
-    __syncthreads();
-    if (flag) break;
-    const double rk = rkk[par], ri_k = rinv[par];
-    if (lane == (k & 31)) {  // holders of row k: scale by 1/r_kk (one IEEE reciprocal per step) and publish
-#pragma unroll
-      for (int r = 0; r < RR; r++)
-        if (r == kr) {
-#pragma unroll
-          for (int q = 0; q < QC; q++) {
-            const int j = wp + CH_WARPS * q;
-            const double v = __dmul_rn(c[r][q], ri_k);
-            if (j == k) c[r][q] = rk;
-            else if (j > k && j < n) c[r][q] = v;
-            if (j > k && j < n) rowk[par][j] = v;
-          }
-        }
-    }
-    __syncthreads();
-    double rj[QC], ri[RR];
-#pragma unroll
-    for (int q = 0; q < QC; q++) {
-      const int j = wp + CH_WARPS * q;
-      rj[q] = (j > k && j < n) ? rowk[par][j] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      const int i = lane + 32 * r;
-      ri[r] = (i > k && i < n) ? rowk[par][i] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < RR; r++)
-#pragma unroll
-      for (int q = 0; q < QC; q++) {
-        const int i = lane + 32 * r, j = wp + CH_WARPS * q;
-        if (i > k && i <= j) c[r][q] = __fma_rn(-ri[r], rj[q], c[r][q]);
+        for (int r = 0; r < RR; r++) lk[r] = sm.l[k - 1][lane + 32 * r];
       }
-  }
+      // a(:, j) -= l_{k-1} * l_{k-1}(j) for this warp's columns j in [q_lo, QC) (j >= k)
+      auto update = [&](int q) {
+        const double s = sm.l[k - 1][wp + 16 * q];
 #pragma unroll
-  for (int r = 0; r < RR; r++)
+        for (int r = 0; r < RR; r++) a[r][q] = __fma_rn(-lk[r], s, a[r][q]);
+      };
+      if (jj == wp) {
+        if (k > 0) update(Q);
+        double d = 0.0;
 #pragma unroll
-    for (int q = 0; q < QC; q++) {
-      const int i = lane + 32 * r, j = wp + CH_WARPS * q;
-      if (i < n && j < n) R[(int64_t)i * n + j] = (j >= i) ? c[r][q] : 0.0;
+        for (int r = 0; r < RR; r++) d = (lane + 32 * r == k) ? a[r][Q] : d;
+        d = __shfl_sync(0xffffffffu, d, k & 31);
+        if (lane == 0 && (!(d > 0.0) || !isfinite(d))) report(status, RLHC_EBREAKDOWN, stage, koff + k);
+        const double rk = __dsqrt_rn(d), ri = __drcp_rn(rk);
+#pragma unroll
+        for (int r = 0; r < RR; r++) {
+          const int i = lane + 32 * r;
+          sm.l[k][i] = (i > k) ? __dmul_rn(a[r][Q], ri) : (i == k ? rk : 0.0);
+        }
+        if (lane == 0) sm.rinv[k] = ri;
+        __syncwarp();
+        mbar_arrive(&sm.bar[k]);
+        if (k > 0) {
+#pragma unroll
+          for (int q = Q + 1; q < QC; q++)
+            if (wp + 16 * q < n) update(q);
+        }
+      } else if (k > 0) {
+#pragma unroll
+        for (int q = Q; q < QC; q++)
+          if ((q > Q || wp > jj) && wp + 16 * q < n) update(q);
+      }
     }
-}
-
-// ------------------------------------------------------------------ blocked Cholesky
-// Single CTA, n <= 128, the matrix in shared memory (row stride ncp + 4).  Blocks of 8:
-//   (1) 8 threads factor the 8 x 8 diagonal block (right-looking, r_kk = sqrt, row scaled by
-//       1/r_kk; a pivot <= 0 or non-finite -> EBREAKDOWN(stage, koff + k));
-//   (2) thread per trailing column solves R_pp^T x = C[p:p+8, j] (8 x 8 forward substitution);
-//   (3) the trailing upper triangle is updated on DMMA: C_ij -= sum_k R_ki R_kj.
-// G is read with row stride ldg and R written with stride ldr (strict lower part 0), so the
-// kernel also serves as the diagonal-block factorization of the 64-blocked large-n path.
-__global__ void __launch_bounds__(256)
-chol_blk_kernel(const double* __restrict__ G, int64_t ldg, int n, double* __restrict__ R, int64_t ldr, int stage,
-                int koff, unsigned long long* status) {
-  extern __shared__ double C[];
-  __shared__ double rdiag_s[8];
-  __shared__ int flag;
-  const int ncp = (n + 7) & ~7;
-  const int ld = ncp + 4;
-  const int lane = lane_id(), wp = warp_id(), nw = blockDim.x >> 5;
-  for (int i = wp; i < ncp; i += nw)
-    for (int j = lane; j < ncp; j += 32) C[i * ld + j] = (i < n && j < n) ? G[(int64_t)i * ldg + j] : (i == j ? 1.0 : 0.0);
-  if (threadIdx.x == 0) flag = 0;
+  }
   __syncthreads();
-  for (int p = 0; p < ncp; p += 8) {
-    // (1) diagonal block in warp 0: lane l (< 8) holds column p+l of the block in registers,
-    //     rows broadcast by shuffles, static indices throughout
-    if (wp == 0) {
-      const int l = lane & 7;
-      double v[8];
-#pragma unroll
-      for (int r = 0; r < 8; r++) v[r] = C[(p + r) * ld + p + l];
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const double d = __shfl_sync(0xffffffffu, v[k], k);
-        if (lane == 0 && (!(d > 0.0) || !isfinite(d)) && p + k < n) {
-          report(status, RLHC_EBREAKDOWN, stage, koff + p + k);
-          flag = 1;
-        }
-        const double rk = __dsqrt_rn(d);
-        const double ri = __drcp_rn(rk);
-        if (l == k) v[k] = rk;
-        else if (l > k) v[k] = __dmul_rn(v[k], ri);
-#pragma unroll
-        for (int r = k + 1; r < 8; r++) {
-          const double rkr = __shfl_sync(0xffffffffu, v[k], r);
-          if (l >= r) v[r] = __fma_rn(-rkr, v[k], v[r]);
-        }
-        if (lane == k) rdiag_s[k] = ri;
-      }
-      if (lane < 8) {
-#pragma unroll
-        for (int r = 0; r < 8; r++) C[(p + r) * ld + p + l] = v[r];
-      }
-    }
-    __syncthreads();
-    if (flag) break;
-    // (2) panel rows: R[p:p+8, j] = R_pp^{-T} C[p:p+8, j]
-    for (int j = p + 8 + threadIdx.x; j < ncp; j += blockDim.x) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        double a = C[(p + k) * ld + j];
-#pragma unroll
-        for (int i = 0; i < k; i++) a = __fma_rn(-C[(p + i) * ld + p + k], x[i], a);
-        x[k] = __dmul_rn(a, rdiag_s[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 8; k++) C[(p + k) * ld + j] = x[k];
-    }
-    __syncthreads();
-    // (3) trailing update on DMMA, 8 x 8 output tiles (I <= J) over the warps
-    const int q0 = p + 8, nt = (ncp - q0) / 8;
-    const int g = lane >> 2, t = lane & 3;
-    for (int tl = wp; tl < nt * nt; tl += nw) {
-      const int I = tl / nt, J = tl - I * nt;
-      if (I > J) continue;
-      const int i0 = q0 + 8 * I, j0 = q0 + 8 * J;
-      double c0 = C[(i0 + g) * ld + j0 + 2 * t], c1 = C[(i0 + g) * ld + j0 + 2 * t + 1];
-#pragma unroll
-      for (int k0 = 0; k0 < 8; k0 += 4) {
-        const double a = -C[(p + k0 + t) * ld + i0 + g];
-        const double b = C[(p + k0 + t) * ld + j0 + g];
-        dmma(c0, c1, a, b);
-      }
-      C[(i0 + g) * ld + j0 + 2 * t] = c0;
-      C[(i0 + g) * ld + j0 + 2 * t + 1] = c1;
-    }
-    __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int k = e / n, j = e - k * n;
+    R[(int64_t)k * ldr + j] = (j >= k) ? sm.l[k][j] : 0.0;
   }
-  if (!flag)
-    for (int i = wp; i < n; i += nw)
-      for (int j = lane; j < n; j += 32) R[(int64_t)i * ldr + j] = (j >= i) ? C[i * ld + j] : 0.0;
+  if (rdiag)
+    for (int k = threadIdx.x; k < n; k += blockDim.x) rdiag[k] = sm.rinv[k];
 }
 
-static size_t chol_blk_smem(int n) {
-  const int ncp = (n + 7) & ~7;
-  return (size_t)ncp * (ncp + 4) * sizeof(double);
-}
-
-static cudaError_t launch_chol_blk(const double* G, int64_t ldg, int n, double* R, int64_t ldr, int stage, int koff,
-                                   unsigned long long* status, cudaStream_t st) {
-  const size_t smem = chol_blk_smem(n);
-  cudaError_t e = cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e) return e;
+template <int RR, int QC>
+static cudaError_t run_chol_pipe(const double* G, int64_t ldg, int n, double* R, int64_t ldr, double* rdiag, int stage,
+                                 int koff, unsigned long long* status, cudaStream_t st) {
+  constexpr int smem = (int)sizeof(CholSmem<RR, QC>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_pipe_kernel<RR, QC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
   note_launch();
-  chol_blk_kernel<<<1, 256, smem, st>>>(G, ldg, n, R, ldr, stage, koff, status);
+  chol_pipe_kernel<RR, QC><<<1, 512, smem, st>>>(G, ldg, n, R, ldr, rdiag, stage, koff, status);
   return cudaGetLastError();
 }
+
+static cudaError_t launch_chol_pipe(const double* G, int64_t ldg, int n, double* R, int64_t ldr, double* rdiag,
+                                    int stage, int koff, unsigned long long* status, cudaStream_t st) {
+  if (n <= 32) return run_chol_pipe<1, 2>(G, ldg, n, R, ldr, rdiag, stage, koff, status, st);
+  if (n <= 64) return run_chol_pipe<2, 4>(G, ldg, n, R, ldr, rdiag, stage, koff, status, st);
+  return run_chol_pipe<4, 8>(G, ldg, n, R, ldr, rdiag, stage, koff, status, st);
+}
+
 
 __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int rows, int cols, double* __restrict__ B,
                                  int64_t ldb) {
@@ -822,7 +741,7 @@ __global__ void zero_lower_kernel(double* R, int n) {
     if (e / n > e % n) R[e] = 0.0;
 }
 
-// n > 128: 64-column blocks.  Per block: the 64 x 64 diagonal block by chol_blk_kernel,
+// n > 128: 64-column blocks.  Per block: the 64 x 64 diagonal block by chol_pipe_kernel,
 // R12^T = C21 R_pp^{-1} (rowsolve on the rows below), R12 = its transpose, and the trailing
 // update C22 -= R12^T R12 on DMMA (gemm_update).  `work` holds the working copy of G (n x n)
 // and the R12^T scratch (n x 64).
@@ -837,7 +756,7 @@ static cudaError_t launch_chol_big(const double* G, int n, double* R, double* wo
   if (e) return e;
   for (int p0 = 0; p0 < n; p0 += 64) {
     const int w = std::min(64, n - p0);
-    e = launch_chol_blk(Cw + (size_t)p0 * n + p0, n, w, R + (size_t)p0 * n + p0, n, stage, p0, status, st);
+    e = launch_chol_pipe(Cw + (size_t)p0 * n + p0, n, w, R + (size_t)p0 * n + p0, n, nullptr, stage, p0, status, st);
     if (e) return e;
     const int N = n - p0 - w;
     if (N <= 0) break;
@@ -864,9 +783,9 @@ size_t chol_ws_bytes(int n) {
 }
 
 cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
-                        cudaStream_t st) {
+                        cudaStream_t st, double* rdiag) {
   const size_t need = (size_t)n * (n + 1) * sizeof(double);
-  if (n <= 128) return launch_chol_blk(G, n, n, R, n, stage, 0, status, st);
+  if (n <= 128) return launch_chol_pipe(G, n, n, R, n, rdiag, stage, 0, status, st);
   if (work) return launch_chol_big(G, n, R, work, stage, status, st);
   if (need <= 200 * 1024) {
     if (need > 48 * 1024) {

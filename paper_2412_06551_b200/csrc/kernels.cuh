@@ -79,8 +79,9 @@ cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int 
 size_t hqr_ws_bytes(int s, int n);
 cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double* sgn_ref, double* S, double* work,
                        unsigned long long* status, cudaStream_t st);
+// R upper with R^T R = G; optionally 1/diag(R) (IEEE reciprocal, == rdiag_kernel's) into rdiag
 cudaError_t launch_chol(const double* G, int n, double* R, double* work, int stage, unsigned long long* status,
-                        cudaStream_t st);
+                        cudaStream_t st, double* rdiag = nullptr);
 size_t chol_ws_bytes(int n);
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);

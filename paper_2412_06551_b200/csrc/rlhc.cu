@@ -245,13 +245,13 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
   mk.mark(6);
   // CholeskyQR2(W): D = chol(G1), V = W D^{-1} (+ G2), J = chol(G2), Q = V J^{-1}
-  CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st));
-  CUDA_TRY(launch_rdiag(a.D, ni, n, a.Di, RLHC_STAGE_SOLVE_D, status, st));
+  CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st, ni <= 128 ? a.Di : nullptr));
+  if (ni > 128) CUDA_TRY(launch_rdiag(a.D, ni, n, a.Di, RLHC_STAGE_SOLVE_D, status, st));
   mk.mark(7);
   if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G))) return rc;
   mk.mark(8);
-  CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st));
-  CUDA_TRY(launch_rdiag(a.J, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
+  CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st, ni <= 128 ? a.Ji : nullptr));
+  if (ni > 128) CUDA_TRY(launch_rdiag(a.J, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
   mk.mark(9);
   if ((rc = solve_pass(Q, ldq, a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
   mk.mark(10);
