@@ -24,7 +24,7 @@ struct RootOut {
 };
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
-                             const RootOut* root = nullptr);
+                             const RootOut* root = nullptr, unsigned long long* finite_status = nullptr);
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
                              int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* root = nullptr);
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,

@@ -125,7 +125,8 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
 // PX = LU on rows x n (global ids row0..): piv, U, L11; the trailing matrix of later
 // panels lives in `tw` (rows x n, ldt).  Returns RLHC_OK or RLHC_ECUDA.
 int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg& cfg,
-             TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st) {
+             TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st,
+             bool check_input = false) {
   const int W = kernel_width(cfg.panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg.leaf_rows);
   const bool panels = cfg.panel < n;
@@ -140,7 +141,8 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
     const double* src = (p0 == 0) ? X : tw;
     const int64_t lds = (p0 == 0) ? ldx : ldtw;
     CUDA_TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
-                              t.cnt[0], t.vals[0], st, root_emit && nleaves == 1 ? &ro : nullptr));
+                              t.cnt[0], t.vals[0], st, root_emit && nleaves == 1 ? &ro : nullptr,
+                              check_input && !panels ? t.status : nullptr));
     int cur = 0, nslots = nleaves;
     while (nslots > 1) {
       const int nout = (int)ceil_div<int64_t>(nslots, cfg.arity);
@@ -203,10 +205,12 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   Marks mk = prof_begin(st);
   mk.mark(0);
   CUDA_TRY(launch_status_init(status, st));
-  CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
+  // input check: a pass of its own, or (one panel) folded into the TSLU leaves' read of X
+  const bool fold_check = cfg.panel >= n;
+  if (!fold_check) CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
   mk.mark(1);
   // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
-  int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st);
+  int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st, fold_check);
   if (rc) return rc;
   CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
   CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));

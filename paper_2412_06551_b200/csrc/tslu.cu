@@ -20,7 +20,7 @@ template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
-                 double* __restrict__ out_vals, RootOut root) {
+                 double* __restrict__ out_vals, RootOut root, unsigned long long* finite_status) {
   constexpr int R = 32 * RS, CW = W / NW;
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
@@ -38,6 +38,17 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
     const double* p = src + r * lds + p0 + wp;
 #pragma unroll
     for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
+  }
+  // single-panel pipelines fold the input check (check_finite_kernel's semantics: the
+  // smallest non-finite element index i*n + j wins) into this pass over X
+  if (finite_status) {
+#pragma unroll
+    for (int s = 0; s < RS; s++)
+#pragma unroll
+      for (int c = 0; c < CW; c++)
+        if (!isfinite(a[s][c]))
+          report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT,
+                 ((int64_t)blockIdx.x * R + s * 32 + lane) * w + wp + NW * c);
   }
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
   if (root.U) sel_root_finish(sm, steps, w, root);
@@ -206,7 +217,7 @@ int select_rows(int W) { return W == 64 ? 256 : 512; }
 template <int W, int NW, int RS>
 static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                             const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
-                            const RootOut& root) {
+                            const RootOut& root, unsigned long long* finite_status) {
   int nleaves = (int)ceil_div<int64_t>(rows, 32 * RS);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
   static bool attr = false;  // once per instantiation (idempotent, so a race is harmless)
@@ -216,7 +227,7 @@ static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_
     attr = true;
   }
   note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals,
-                                                                            root);
+                                                                            root, finite_status);
   return cudaGetLastError();
 }
 template <int W, int NW, int RS>
@@ -237,12 +248,15 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
 
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
-                             const RootOut* rootp) {
+                             const RootOut* rootp, unsigned long long* finite_status) {
   const RootOut root = rootp ? *rootp : RootOut{};
   switch (W) {
-    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
-    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
-    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root);
+    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+                                             finite_status);
+    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+                                             finite_status);
+    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+                                             finite_status);
   }
   return cudaErrorInvalidValue;
 }

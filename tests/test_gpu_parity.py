@@ -160,3 +160,21 @@ def test_end_to_end_vs_oracle(rl, ora, algo, m, n, kexp, colscale, kw):
     assert orth_err(Q) <= 1e-13 * math.sqrt(n)
     assert rel_residual(Q, R, Xh) <= 1e-14 * n
     assert rel_fro(R, ref.R) <= (1e-9 if kexp <= 8 else 1e-12)
+
+
+@pytest.mark.parametrize("algo,m,n,kw", [("slhc3", 4096, 64, dict(s=128)),      # check folded into the leaves
+                                         ("sslhc3", 5000, 100, dict(s1=800, s2=200))])  # separate pass
+def test_nonfinite_input(rl, ora, algo, m, n, kw):
+    """ENONFINITE(stage INPUT, index = smallest i*n + j of a NaN/Inf)."""
+    X = _x(m, n, 8, 23)
+    X[3001, 7] = float("nan")
+    X[777, n - 1] = float("inf")
+    X[2900, 0] = -float("inf")
+    fn = rl.slhc3 if algo == "slhc3" else rl.sslhc3
+    res = fn(X, seed=1, **kw)
+    assert res.info() == (2, 0, 777 * n + n - 1)
+    with pytest.raises(ora.OracleError):
+        if algo == "slhc3":
+            ora.slhc3(X.cpu().numpy(), kw["s"], 1, *rl.default_cfg(m, n).as_tuple())
+        else:
+            ora.sslhc3(X.cpu().numpy(), kw["s1"], kw["s2"], 1, *rl.default_cfg(m, n).as_tuple())
