@@ -178,3 +178,30 @@ def test_nonfinite_input(rl, ora, algo, m, n, kw):
             ora.slhc3(X.cpu().numpy(), kw["s"], 1, *rl.default_cfg(m, n).as_tuple())
         else:
             ora.sslhc3(X.cpu().numpy(), kw["s1"], kw["s2"], 1, *rl.default_cfg(m, n).as_tuple())
+
+
+# ------------------------------------------------------------------ edge cases
+EDGE = [
+    ("slhc3", 300, 1, dict(s=1)),             # n = 1, s = n
+    ("slhc3", 777, 7, dict(s=7)),             # odd n, minimal sketch, one ragged leaf
+    ("slhc3", 64, 64, dict(s=64)),            # square: m = n = s
+    ("sslhc3", 96, 24, dict(s1=96, s2=24)),   # s1 = m, s2 = n
+    ("slhc3", 257, 64, dict(s=128)),          # leaf_rows + 1 rows: two leaves, one of 1 row
+    ("sslhc3", 70000, 64, dict(s1=512, s2=128)),  # ragged last leaf at cfg2's width
+]
+
+
+@pytest.mark.parametrize("algo,m,n,kw", EDGE)
+def test_edge_cases_vs_oracle(rl, ora, algo, m, n, kw):
+    X = _x(m, n, 6, 29)
+    fn = rl.slhc3 if algo == "slhc3" else rl.sslhc3
+    res = fn(X, seed=5, **kw)
+    assert res.info() == (0, 0, 0)
+    c = rl.default_cfg(m, n).as_tuple()
+    Xh = X.cpu().numpy()
+    ref = ora.slhc3(Xh, kw["s"], 5, *c) if algo == "slhc3" else ora.sslhc3(Xh, kw["s1"], kw["s2"], 5, *c)
+    Q, R = res.Q.cpu().numpy(), res.R.cpu().numpy()
+    assert np.array_equal(res.piv.cpu().numpy(), ref.piv)
+    assert orth_err(Q) <= 1e-13 * math.sqrt(n)
+    assert rel_residual(Q, R, Xh) <= 1e-14 * max(n, 1)
+    assert rel_fro(R, ref.R) <= 1e-9
