@@ -711,7 +711,11 @@ static GramGeom gram_geom(int64_t rows, int n) {
   GramGeom g;
   g.nt = ceil_div(n, GT);
   g.ntiles = g.nt * (g.nt + 1) / 2;
-  int64_t want = std::max<int64_t>(1, (2 * kSMs + g.ntiles - 1) / g.ntiles);
+  // 3 resident CTAs per SM (68 KB of shared memory each), split count rounded so the last
+  // wave is (nearly) full
+  const int64_t slots = 3 * (int64_t)kSMs;
+  int64_t want = std::max<int64_t>(1, (slots + g.ntiles - 1) / g.ntiles);
+  want = std::max<int64_t>(1, ((want * g.ntiles + slots - 1) / slots) * slots / g.ntiles);
   int64_t maxs = std::max<int64_t>(1, rows / 256);
   g.nsplit = (int)std::min<int64_t>(want, maxs);
   g.rows_per_split = ceil_div<int64_t>(ceil_div<int64_t>(rows, g.nsplit), GK) * GK;
@@ -723,7 +727,7 @@ size_t gram_partials_bytes(int64_t rows, int n) {
   return (size_t)g.nsplit * g.ntiles * GT * GT * sizeof(double);
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 3)
 gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int nt, int64_t rows_per_split,
             double* __restrict__ part) {
   // two chunks in flight: the next chunk's column panels stream in (cp.async) while the
