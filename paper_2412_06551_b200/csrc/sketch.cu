@@ -326,38 +326,40 @@ __global__ void cs_scatter_kernel(int64_t rows, int s1, const int32_t* __restric
 }
 
 // out[b, :] = sum over the bucket's rows (ascending) of sign * A[row, :]: one warp per
-// bucket, lanes over columns, 4-row prefetch.
-__global__ void cs_apply_kernel(const double* __restrict__ A, int64_t lda, int n, int s1,
-                                const int32_t* __restrict__ perm, const int32_t* __restrict__ start,
-                                const int8_t* __restrict__ sign, double* __restrict__ out) {
-  const int wpb = blockDim.x >> 5;
-  const int b = blockIdx.x * wpb + warp_id();
+// (bucket, 32-column slice), lane = column.  The loads of 8 rows (perm, sign, values) are
+// issued before their 8 additions, which stay in ascending row order (bit-exact sums).
+__global__ void __launch_bounds__(256)
+cs_apply_kernel(const double* __restrict__ A, int64_t lda, int n, int s1, const int32_t* __restrict__ perm,
+                const int32_t* __restrict__ start, const int8_t* __restrict__ sign, double* __restrict__ out) {
+  const int nslice = (n + 31) / 32;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int b = wg / nslice, slice = wg - b * nslice;
   if (b >= s1) return;
-  const int lane = lane_id();
+  const int c = slice * 32 + lane_id();
+  const bool cok = c < n;
   const int p0 = start[b], p1 = start[b + 1];
-  for (int c0 = 0; c0 < n; c0 += 32 * 8) {
-    double acc[8];
+  double acc = 0.0;
+  int p = p0;
+  for (; p + 8 <= p1; p += 8) {
+    int r[8];
+    double v[8];
+    bool ng[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++) acc[q] = 0.0;
-    for (int p = p0; p < p1; p++) {
-      int r = perm[p];
-      const double* row = A + (int64_t)r * lda;
-      bool neg = sign[r] < 0;
+    for (int u = 0; u < 8; u++) r[u] = perm[p + u];
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        int c = c0 + q * 32 + lane;
-        if (c < n) {
-          double v = row[c];
-          acc[q] = neg ? __dadd_rn(acc[q], -v) : __dadd_rn(acc[q], v);
-        }
-      }
+    for (int u = 0; u < 8; u++) {
+      ng[u] = sign[r[u]] < 0;
+      v[u] = cok ? A[(int64_t)r[u] * lda + c] : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      int c = c0 + q * 32 + lane;
-      if (c < n) out[(int64_t)b * n + c] = acc[q];
-    }
+    for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, ng[u] ? -v[u] : v[u]);
   }
+  for (; p < p1; p++) {
+    const int r = perm[p];
+    const double v = cok ? A[(int64_t)r * lda + c] : 0.0;
+    acc = __dadd_rn(acc, sign[r] < 0 ? -v : v);
+  }
+  if (cok) out[(int64_t)b * n + c] = acc;
 }
 
 __global__ void copy_i32_kernel(const int32_t* a, int32_t* b, int64_t cnt) {
@@ -384,7 +386,9 @@ cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int 
   note_launch(); cs_bucket_totals_kernel<<<ceil_div(s1, 256), 256, 0, st>>>(nch, s1, pl.hist, pl.start);
   note_launch(); cs_scan_kernel<<<1, 1024, 0, st>>>(s1, pl.start);
   note_launch(); cs_scatter_kernel<<<nch, 32, hsm, st>>>(rows, s1, pl.bucket, pl.hist, pl.start, pl.perm);
-  note_launch(); cs_apply_kernel<<<ceil_div(s1, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start, pl.sign, out);
+  const int64_t warps = (int64_t)s1 * ((n + 31) / 32);
+  note_launch(); cs_apply_kernel<<<(int)ceil_div<int64_t>(warps, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start,
+                                                                                    pl.sign, out);
   if (bucket_out) note_launch(), copy_i32_kernel<<<256, 256, 0, st>>>(pl.bucket, bucket_out, rows);
   if (sign_out) note_launch(), copy_i8_kernel<<<256, 256, 0, st>>>(pl.sign, sign_out, rows);
   return cudaGetLastError();
