@@ -50,7 +50,8 @@ enum rlhc_code {
   RLHC_ESINGULAR = 4,   /* device: zero / non-finite diagonal of a triangular factor */
   RLHC_EBREAKDOWN = 5,  /* device: Cholesky pivot <= 0 or non-finite (index = k) */
   RLHC_ECUDA = 6,       /* host: CUDA launch error */
-  RLHC_EWORKSPACE = 7   /* host: workspace too small */
+  RLHC_EWORKSPACE = 7,  /* host: workspace too small */
+  RLHC_ENCCL = 8        /* host: NCCL unavailable or an NCCL call failed (_dist entry points) */
 };
 
 enum rlhc_stage {
@@ -209,6 +210,35 @@ int rlhc_lfactor(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t 
 int rlhc_trmm_upper(const double* A, const double* B, int64_t n, double* C, rlhc_stream_t stream);
 size_t rlhc_cholesky_workspace_size(int64_t n);
 int rlhc_cholesky_ws(const double* G, int64_t n, double* Rout, int stage, void* ws, size_t ws_bytes, rlhc_info_t* info,
+                     rlhc_stream_t stream);
+
+/* ------------------------------------------------- row-sharded entry points over NCCL */
+/* SURVEY 8(b) "_dist", 8(e).  The whole SLHC3 / SSLHC3 call on nranks GPUs, one process per
+ * GPU, orchestrated in C on the caller's stream (no host synchronisation): TSLU candidates
+ * all-gathered, pivot rows / sketches / Grams all-reduced (NCCL, SUM), the n x n factors
+ * replicated; DESIGN.md section 7.  NCCL is loaded at run time (dlopen "libnccl.so.2").
+ * Communicator: rank 0 calls rlhc_comm_unique_id (128 bytes), the caller distributes the
+ * bytes (e.g. torch.distributed), every rank calls rlhc_comm_init; nullptr = one rank.
+ * Shards: equal, rank r holds global rows [row0, row0 + m_local), row0 = r * m_local,
+ * m_local a multiple of cfg->leaf_rows and (nranks > 1) m_local / leaf_rows a power of
+ * cfg->arity, so the pivots are those of the single-GPU tournament on the whole X.
+ * Outputs: Q (m_local x n, this rank's rows), R (n x n, replicated), piv (n, global ids,
+ * replicated); info: the first device error in pipeline order (same codes / stages as the
+ * single-GPU call).  Errors: host argument checks -> RLHC_EINVAL / RLHC_EWORKSPACE,
+ * NCCL failures -> RLHC_ENCCL (message in rlhc_last_error). */
+typedef struct rlhc_comm_s* rlhc_comm_t;
+int rlhc_comm_unique_id(void* id_out /* 128 bytes */);
+int rlhc_comm_init(rlhc_comm_t* comm, int nranks, int rank, const void* id /* 128 bytes */);
+int rlhc_comm_destroy(rlhc_comm_t comm);
+size_t rlhc_dist_workspace_size(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2,
+                                const rlhc_tslu_cfg* cfg, int nranks);
+int rlhc_slhc3_dist(const double* X, int64_t m_local, int64_t n, int64_t ldx, int64_t row0, int64_t m_global,
+                    int64_t s, uint64_t seed, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq, double* R,
+                    int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_comm_t comm,
+                    rlhc_stream_t stream);
+int rlhc_sslhc3_dist(const double* X, int64_t m_local, int64_t n, int64_t ldx, int64_t row0, int64_t m_global,
+                     int64_t s1, int64_t s2, uint64_t seed, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq,
+                     double* R, int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_comm_t comm,
                      rlhc_stream_t stream);
 
 /* Library identification and the last host-side error message (thread-local). */

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librlhc.so")
-SOURCES = ["tslu.cu", "rows.cu", "sketch.cu", "small.cu", "factor.cu", "dist_blocks.cu", "rlhc.cu"]
+SOURCES = ["tslu.cu", "rows.cu", "sketch.cu", "small.cu", "factor.cu", "dist_blocks.cu", "dist_c.cu", "rlhc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-                           "-lcudart"])
+                           "-lcudart", "-ldl"])
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

@@ -1,0 +1,373 @@
+// dist_c.cu -- row-sharded SLHC3 / SSLHC3 over NCCL, orchestrated in C (SURVEY 8(b) "_dist"
+// entry points, 8(e)).  Rank r holds global rows [row0, row0 + m_local).  Per call, on the
+// caller's stream, with no host synchronisation:
+//   * PX = LU: per panel, the rank's leaves and local tree levels reduce to ONE tournament
+//     slot (rlhc_tslu_reduce); the slots are all-gathered and every rank runs the remaining
+//     levels (rlhc_tslu_combine) -> identical pivots everywhere; the pivot rows' current
+//     values are assembled by an all-reduce SUM of masked per-rank copies (exact); U rows
+//     follow on every rank; each rank eliminates its own rows.
+//   * L of the local rows, local sketch partials indexed by global row ids -> all-reduce ->
+//     replicated HouseholderQR and Y = S U.
+//   * W = X Y^{-1} + local Gram -> all-reduce -> replicated Cholesky; same for V; Q = V J^{-1}
+//     stays local; R = J (D Y) replicated.
+// The same sequence as paper_2412_06551_b200/dist.py (which drives the stage entry points
+// through torch.distributed and is checked against the oracle on CPU); every arithmetic step
+// is one of the stage entry points.  NCCL is resolved at run time (dlopen "libnccl.so.2":
+// whichever copy the process already has, e.g. PyTorch's), so the library has no link-time
+// NCCL dependency.
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "../../include/rlhc.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rlhc {
+namespace {
+
+// ---- the few NCCL entry points used (the C API is ABI-stable across 2.x)
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef enum { ncclInt32 = 2, ncclFloat64 = 8 } ncclDataType_t;
+typedef enum { ncclSum = 0 } ncclRedOp_t;
+typedef int ncclResult_t;
+
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    auto sym = [&](const char* s) { return dlsym(h, s); };
+    n.GetUniqueId = (decltype(n.GetUniqueId))sym("ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))sym("ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))sym("ncclCommDestroy");
+    n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
+    n.AllGather = (decltype(n.AllGather))sym("ncclAllGather");
+    n.GroupStart = (decltype(n.GroupStart))sym("ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))sym("ncclGroupEnd");
+    n.GetErrorString = (decltype(n.GetErrorString))sym("ncclGetErrorString");
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllReduce && n.AllGather && n.GroupStart &&
+           n.GroupEnd && n.GetErrorString;
+  });
+  return n;
+}
+
+int fail(int code, const char* msg) {
+  set_last_error(msg);
+  return code;
+}
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carve {
+  char* p;
+  size_t used = 0;
+  explicit Carve(void* base) : p((char*)base) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* r = (T*)(p ? p + used : nullptr);
+    used += al(count * sizeof(T));
+    return r;
+  }
+};
+
+int kernel_width(int panel) { return panel <= 16 ? 16 : panel <= 32 ? 32 : 64; }
+
+// first non-OK info of the pipeline, in order (device side: no host synchronisation); the
+// input check reports this rank's local element index, made global with row0 * n
+__global__ void first_info_kernel(const rlhc_info_t* infos, int k, int64_t input_offset, rlhc_info_t* out) {
+  if (threadIdx.x != 0) return;
+  rlhc_info_t r{0, 0, 0};
+  for (int i = 0; i < k; i++)
+    if (infos[i].code != 0) {
+      r = infos[i];
+      if (r.stage == RLHC_STAGE_INPUT) r.index += input_offset;
+      break;
+    }
+  *out = r;
+}
+
+constexpr int kMaxInfos = 64;
+
+struct DistWs {
+  int *slot_ids, *slot_cnt, *all_ids, *all_cnt, *root_ids, *root_cnt;
+  double *slot_vals, *all_vals, *root_vals;
+  uint8_t* chosen;
+  unsigned long long* status;  // input check
+  double *U, *L11, *Xp, *prow, *S, *Y, *D, *J, *N, *G, *Ls, *Lt;
+  rlhc_info_t* infos;
+  void* scratch;
+  size_t scratch_bytes;
+};
+
+size_t scratch_need(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg& cfg,
+                    int nranks) {
+  size_t s = 0;
+  s = std::max(s, rlhc_tslu_local_workspace_size(m_local, 0, &cfg));
+  s = std::max(s, rlhc_tslu_local_workspace_size(0, nranks, &cfg));
+  s = std::max(s, rlhc_tslu_panel_workspace_size(n));
+  s = std::max(s, rlhc_tslu_eliminate_workspace_size(n));
+  s = std::max(s, rlhc_lfactor_workspace_size(m_local, n));
+  s = std::max(s, rlhc_lfactor_workspace_size(n, n));
+  if (algo == RLHC_SLHC3) {
+    s = std::max(s, rlhc_sketch_gauss_workspace_size(m_local, n, s_or_s1));
+    s = std::max(s, rlhc_hqr_workspace_size(s_or_s1, n));
+  } else {
+    s = std::max(s, rlhc_sketch_count_workspace_size(m_local, n, s_or_s1));
+    s = std::max(s, rlhc_sketch_gauss_workspace_size(s_or_s1, n, s2));
+    s = std::max(s, rlhc_hqr_workspace_size(s2, n));
+  }
+  s = std::max(s, rlhc_trsm_apply_workspace_size(m_local, n));
+  s = std::max(s, rlhc_cholesky_workspace_size(n));
+  return s;
+}
+
+void carve_dist(Carve& c, int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg& cfg,
+                int nranks, DistWs& d) {
+  const int W = kernel_width(cfg.panel);
+  d.slot_ids = c.take<int>(W);
+  d.slot_cnt = c.take<int>(1);
+  d.slot_vals = c.take<double>((size_t)W * W);
+  d.all_ids = c.take<int>((size_t)nranks * W);
+  d.all_cnt = c.take<int>(nranks);
+  d.all_vals = c.take<double>((size_t)nranks * W * W);
+  d.root_ids = c.take<int>(W);
+  d.root_cnt = c.take<int>(1);
+  d.root_vals = c.take<double>((size_t)W * W);
+  d.chosen = c.take<uint8_t>((size_t)m_local);
+  d.status = c.take<unsigned long long>(4);
+  double** sq[] = {&d.U, &d.L11, &d.Xp, &d.prow, &d.S, &d.Y, &d.D, &d.J, &d.N, &d.G};
+  for (double** q : sq) *q = c.take<double>((size_t)n * n);
+  const int64_t srows = algo == RLHC_SLHC3 ? s_or_s1 : s2;
+  d.Ls = c.take<double>((size_t)srows * n);
+  d.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
+  d.infos = c.take<rlhc_info_t>(kMaxInfos);
+  d.scratch_bytes = scratch_need(algo, m_local, n, s_or_s1, s2, cfg, nranks);
+  d.scratch = c.take<char>(d.scratch_bytes);
+}
+
+struct DistArgs {
+  int algo;
+  const double* X;
+  int64_t m_local, n, ldx, row0, m_global, s_or_s1, s2;
+  uint64_t seed;
+  rlhc_tslu_cfg cfg;
+  double* Q;
+  int64_t ldq;
+  double* R;
+  int64_t* piv;
+  void* ws;
+  size_t ws_bytes;
+  rlhc_info_t* info;
+};
+
+}  // namespace
+}  // namespace rlhc
+
+using namespace rlhc;
+
+struct rlhc_comm_s {
+  ncclComm_t comm;
+  int nranks, rank;
+};
+
+static int check_dist(const DistArgs& a, int nranks) {
+  if (!a.X || !a.Q || !a.R || !a.piv || !a.ws || !a.info) return fail(RLHC_EINVAL, "null pointer argument");
+  if (a.n < 1 || a.m_local < 1 || a.m_global < a.n) return fail(RLHC_EINVAL, "need m_global >= n >= 1, m_local >= 1");
+  if (a.m_global > 0x7fffffffLL) return fail(RLHC_EINVAL, "m_global must be < 2^31 (int32 row ids)");
+  if (a.ldx < a.n || a.ldq < a.n) return fail(RLHC_EINVAL, "leading dimension < n");
+  if (a.m_local * nranks != a.m_global || a.row0 % a.m_local) return fail(RLHC_EINVAL, "shards must be equal");
+  if (a.m_local % a.cfg.leaf_rows) return fail(RLHC_EINVAL, "m_local must be a multiple of leaf_rows");
+  if (nranks > 1) {
+    int64_t leaves = a.m_local / a.cfg.leaf_rows, p = 1;
+    while (p < leaves) p *= a.cfg.arity;
+    if (p != leaves) return fail(RLHC_EINVAL, "local leaf count must be a power of the arity");
+  }
+  if (a.algo == RLHC_SLHC3 && (a.s_or_s1 < a.n || a.s_or_s1 > a.m_global)) return fail(RLHC_EINVAL, "need n <= s <= m");
+  if (a.algo == RLHC_SSLHC3 && (a.s2 < a.n || a.s_or_s1 < a.s2 || a.s_or_s1 > a.m_global))
+    return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
+  if (((uintptr_t)a.ws) & 255) return fail(RLHC_EINVAL, "workspace must be 256-byte aligned");
+  return RLHC_OK;
+}
+
+#define DTRY(x)                   \
+  do {                            \
+    int rc_ = (x);                \
+    if (rc_ != RLHC_OK) return rc_; \
+  } while (0)
+#define NTRY(x)                                                                      \
+  do {                                                                               \
+    ncclResult_t nr_ = (x);                                                          \
+    if (nr_ != 0) return fail(RLHC_ENCCL, nccl().GetErrorString(nr_));               \
+  } while (0)
+
+static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
+  Nccl& N = nccl();
+  const int nr = comm ? comm->nranks : 1;
+  const int64_t n = a.n, m = a.m_local;
+  const int W = kernel_width(a.cfg.panel);
+  Carve c(a.ws);
+  DistWs d;
+  carve_dist(c, a.algo, m, n, a.s_or_s1, a.s2, a.cfg, nr, d);
+  if (a.ws_bytes < c.used) return fail(RLHC_EWORKSPACE, "workspace too small");
+  void* sc = d.scratch;
+  const size_t scb = d.scratch_bytes;
+  auto allreduce = [&](double* p, size_t count) -> int {
+    if (nr > 1) NTRY(N.AllReduce(p, p, count, ncclFloat64, ncclSum, comm->comm, st));
+    return RLHC_OK;
+  };
+  int ninfo = 0;
+  auto next_info = [&]() { return d.infos + ninfo++; };
+  if (cudaMemsetAsync(d.infos, 0, kMaxInfos * sizeof(rlhc_info_t), st)) return fail(RLHC_ECUDA, "memset");
+  if (cudaMemsetAsync(d.U, 0, (size_t)n * n * sizeof(double), st)) return fail(RLHC_ECUDA, "memset");
+  if (cudaMemsetAsync(d.chosen, 0, (size_t)m, st)) return fail(RLHC_ECUDA, "memset");
+  // finiteness of this rank's rows (stage INPUT), first in pipeline order
+  if (launch_status_init(d.status, st) || launch_check_finite(a.X, m, (int)n, a.ldx, d.status, st) ||
+      launch_status_finish(d.status, next_info(), st))
+    return fail(RLHC_ECUDA, "launch failed");
+  // ---------------- PX = LU (P:279 / P:293), tournament over panels
+  for (int64_t p0 = 0; p0 < n; p0 += a.cfg.panel) {
+    const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
+    const double* src = p0 == 0 ? a.X : a.Q;
+    const int64_t lds = p0 == 0 ? a.ldx : a.ldq;
+    DTRY(rlhc_tslu_reduce(src, lds, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, d.slot_ids, d.slot_cnt,
+                          d.slot_vals, sc, scb, st));
+    const int* root = d.slot_ids;
+    if (nr > 1) {
+      NTRY(N.GroupStart());
+      NTRY(N.AllGather(d.slot_ids, d.all_ids, W, ncclInt32, comm->comm, st));
+      NTRY(N.AllGather(d.slot_cnt, d.all_cnt, 1, ncclInt32, comm->comm, st));
+      NTRY(N.AllGather(d.slot_vals, d.all_vals, (size_t)W * W, ncclFloat64, comm->comm, st));
+      NTRY(N.GroupEnd());
+      DTRY(rlhc_tslu_combine(d.all_ids, d.all_cnt, d.all_vals, nr, w, &a.cfg, d.root_ids, d.root_cnt, d.root_vals, sc,
+                             scb, st));
+      root = d.root_ids;
+    }
+    DTRY(rlhc_owned_rows(src, lds, m, a.row0, root, nullptr, w, p0, n - p0, d.prow, st));
+    DTRY(allreduce(d.prow, (size_t)w * (n - p0)));
+    DTRY(rlhc_tslu_panel_factor_rows(d.prow, root, p0, w, n, a.row0, m, d.U, a.piv, d.chosen, sc, scb, next_info(),
+                                     st));
+    if (p0 + w < n) DTRY(rlhc_tslu_eliminate(src, lds, m, p0, w, n, d.U, a.Q, a.ldq, sc, scb, st));
+  }
+  DTRY(rlhc_owned_rows(a.X, a.ldx, m, a.row0, nullptr, a.piv, n, 0, n, d.Xp, st));
+  DTRY(allreduce(d.Xp, (size_t)n * n));
+  DTRY(rlhc_l11(d.Xp, n, d.U, d.L11, sc, scb, st));
+  DTRY(rlhc_lfactor(a.X, m, n, a.ldx, a.row0, d.U, d.L11, a.piv, a.Q, a.ldq, sc, scb, st));
+  // ---------------- sketch of L (P:280 / P:294): local partials, all-reduced
+  int64_t srows;
+  if (a.algo == RLHC_SLHC3) {
+    srows = a.s_or_s1;
+    DTRY(rlhc_sketch_gauss(a.Q, m, n, a.ldq, a.row0, srows, a.seed, 0, d.Ls, sc, scb, st));
+    DTRY(allreduce(d.Ls, (size_t)srows * n));
+  } else {
+    srows = a.s2;
+    DTRY(rlhc_sketch_count(a.Q, m, n, a.ldq, a.row0, a.s_or_s1, a.seed, d.Lt, nullptr, nullptr, sc, scb, st));
+    DTRY(allreduce(d.Lt, (size_t)a.s_or_s1 * n));
+    DTRY(rlhc_sketch_gauss(d.Lt, a.s_or_s1, n, n, 0, srows, a.seed, 1, d.Ls, sc, scb, st));
+  }
+  // ---------------- [H, S] = HouseholderQR(L_s) (R#7), Y = S U
+  DTRY(rlhc_hqr_r(d.Ls, srows, n, n, d.U, d.S, sc, scb, next_info(), st));
+  DTRY(rlhc_trmm_upper(d.S, d.U, n, d.Y, st));
+  // ---------------- W = X Y^{-1} (+ G1), CholeskyQR2, R = J (D Y)
+  DTRY(rlhc_trsm_apply(a.X, m, n, a.ldx, d.Y, RLHC_SUBST, a.Q, a.ldq, d.G, sc, scb, next_info(), st));
+  DTRY(allreduce(d.G, (size_t)n * n));
+  DTRY(rlhc_cholesky_ws(d.G, n, d.D, RLHC_STAGE_CHOL1, sc, scb, next_info(), st));
+  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.D, RLHC_SUBST, a.Q, a.ldq, d.G, sc, scb, next_info(), st));
+  DTRY(allreduce(d.G, (size_t)n * n));
+  DTRY(rlhc_cholesky_ws(d.G, n, d.J, RLHC_STAGE_CHOL2, sc, scb, next_info(), st));
+  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.J, RLHC_SUBST, a.Q, a.ldq, nullptr, sc, scb, next_info(), st));
+  DTRY(rlhc_trmm_upper(d.D, d.Y, n, d.N, st));
+  DTRY(rlhc_trmm_upper(d.J, d.N, n, a.R, st));
+  note_launch();
+  first_info_kernel<<<1, 32, 0, st>>>(d.infos, ninfo, a.row0 * n, a.info);
+  if (cudaGetLastError()) return fail(RLHC_ECUDA, "launch failed");
+  return RLHC_OK;
+}
+
+extern "C" {
+
+int rlhc_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(RLHC_EINVAL, "null pointer argument");
+  Nccl& N = nccl();
+  if (!N.ok) return fail(RLHC_ENCCL, "libnccl.so.2 not found");
+  NTRY(N.GetUniqueId((ncclUniqueId*)id_out));
+  return RLHC_OK;
+}
+
+int rlhc_comm_init(rlhc_comm_t* comm, int nranks, int rank, const void* id) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(RLHC_EINVAL, "bad arguments");
+  Nccl& N = nccl();
+  if (!N.ok) return fail(RLHC_ENCCL, "libnccl.so.2 not found");
+  rlhc_comm_s* c = new rlhc_comm_s{nullptr, nranks, rank};
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclResult_t r = N.CommInitRank(&c->comm, nranks, uid, rank);
+  if (r != 0) {
+    delete c;
+    return fail(RLHC_ENCCL, N.GetErrorString(r));
+  }
+  *comm = c;
+  return RLHC_OK;
+}
+
+int rlhc_comm_destroy(rlhc_comm_t comm) {
+  if (!comm) return RLHC_OK;
+  Nccl& N = nccl();
+  ncclResult_t r = N.CommDestroy(comm->comm);
+  delete comm;
+  return r == 0 ? RLHC_OK : fail(RLHC_ENCCL, N.GetErrorString(r));
+}
+
+size_t rlhc_dist_workspace_size(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2,
+                                const rlhc_tslu_cfg* cfg, int nranks) {
+  if (!cfg || n < 1 || m_local < 1 || nranks < 1) return 0;
+  if (algo != RLHC_SLHC3 && algo != RLHC_SSLHC3) return 0;
+  Carve c(nullptr);
+  DistWs d;
+  carve_dist(c, algo, m_local, n, s_or_s1, s2, *cfg, nranks, d);
+  return c.used;
+}
+
+int rlhc_slhc3_dist(const double* X, int64_t m_local, int64_t n, int64_t ldx, int64_t row0, int64_t m_global,
+                    int64_t s, uint64_t seed, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq, double* R,
+                    int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_comm_t comm,
+                    rlhc_stream_t stream) {
+  if (!cfg) return fail(RLHC_EINVAL, "null tslu configuration");
+  DistArgs a{RLHC_SLHC3, X, m_local, n, ldx, row0, m_global, s, 0, seed, *cfg, Q, ldq, R, piv, ws, ws_bytes, info};
+  const int nr = comm ? comm->nranks : 1;
+  int rc = check_dist(a, nr);
+  if (rc) return rc;
+  return run_dist(a, comm, (cudaStream_t)stream);
+}
+
+int rlhc_sslhc3_dist(const double* X, int64_t m_local, int64_t n, int64_t ldx, int64_t row0, int64_t m_global,
+                     int64_t s1, int64_t s2, uint64_t seed, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq,
+                     double* R, int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_comm_t comm,
+                     rlhc_stream_t stream) {
+  if (!cfg) return fail(RLHC_EINVAL, "null tslu configuration");
+  DistArgs a{RLHC_SSLHC3, X, m_local, n, ldx, row0, m_global, s1, s2, seed, *cfg, Q, ldq, R, piv, ws, ws_bytes, info};
+  const int nr = comm ? comm->nranks : 1;
+  int rc = check_dist(a, nr);
+  if (rc) return rc;
+  return run_dist(a, comm, (cudaStream_t)stream);
+}
+
+}  // extern "C"

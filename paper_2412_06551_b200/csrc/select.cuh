@@ -118,7 +118,9 @@ RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, const int (
   unsigned negm = 0;
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    key[s] = __double_as_longlong(fabs(a[s][K]));
+    // |a| as the bit pattern with the sign bit cleared: non-negative for every value, NaN
+    // included (after an earlier rank deficiency the trailing matrix can hold NaN)
+    key[s] = __double_as_longlong(a[s][K]) & 0x7fffffffffffffffll;
     m[s] = ((act >> s) & 1u) ? key[s] : -1ll;
     negm |= (a[s][K] < 0.0 ? 1u : 0u) << s;
   }
@@ -160,6 +162,19 @@ RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, const int (
     sm.prow[t] = src;
     sm.out_src[t] = src;
     sm.out_id[t] = pid;
+  }
+  if (wb == 0) {  // unreachable with finite keys; keeps the step well defined regardless
+    const unsigned ab = __ballot_sync(0xffffffffu, act != 0);
+    const int fl = ab ? __ffs(ab) - 1 : 0;
+    if (lane == fl) {
+      const int slot = act ? __ffs(act) - 1 : 0;
+      int g = INT_MAX;
+#pragma unroll
+      for (int s = 0; s < RS; s++) g = (s == slot) ? gid[s] : g;
+      sm.prow[t] = slot * 32 + lane;
+      sm.out_src[t] = slot * 32 + lane;
+      sm.out_id[t] = g;
+    }
   }
   if (lane == 0) {
     sm.r[t] = rabs;

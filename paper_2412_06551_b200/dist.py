@@ -325,3 +325,88 @@ def dist_default_cfg(m_global: int, n: int, world: int) -> TsluCfg:
     if world > 1 and arity ** k != leaves:
         arity = 2
     return TsluCfg(rows, arity, panel)
+
+
+# ---------------------------------------------------------------- C orchestration over NCCL
+class NcclComm:
+    """An NCCL communicator for the C entry points (rlhc_comm_init).  Rank 0's unique id is
+    distributed with torch.distributed (plumbing only); nranks == 1 needs no process group."""
+
+    def __init__(self, group=None):
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            check(lib().rlhc_comm_unique_id(uid))
+        if self.world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            ctypes.memmove(uid, box[0], 128)
+        self.handle = ctypes.c_void_p()
+        check(lib().rlhc_comm_init(ctypes.byref(self.handle), self.world, self.rank, uid))
+
+    def close(self):
+        if self.handle:
+            lib().rlhc_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CDistPlan:
+    """One rank's row-sharded SLHC3 / SSLHC3 through rlhc_slhc3_dist / rlhc_sslhc3_dist: the
+    whole call (tournament, sketches, factorizations, NCCL collectives) in C on the current
+    stream.  Same contract and shard rules as DistPlan."""
+
+    def __init__(self, algo: str, m_global: int, n: int, s: int = 0, s1: int = 0, s2: int = 0, seed: int = 0,
+                 cfg: TsluCfg | None = None, device="cuda", comm: NcclComm | None = None):
+        self.algo, self.n, self.seed, self.s, self.s1, self.s2 = algo, n, seed, s, s1, s2
+        self.comm = comm
+        self.world = comm.world if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        self.m_global, self.m_local = m_global, m_global // self.world
+        self.row0 = self.rank * self.m_local
+        self.cfg = cfg if cfg is not None else dist_default_cfg(m_global, n, self.world)
+        check_shard_contract(m_global, self.m_local, self.world, self.cfg)
+        self.dev = torch.device(device)
+        aid = 0 if algo == "slhc3" else 1
+        nbytes = lib().rlhc_dist_workspace_size(aid, self.m_local, n, s if aid == 0 else s1, s2, ctypes.byref(self.cfg),
+                                                self.world)
+        if nbytes == 0:
+            raise ValueError("unsupported sizes for the distributed entry point")
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.dev)
+        off = (-self.ws.data_ptr()) % 256
+        self.ws_ptr, self.ws_bytes = self.ws.data_ptr() + off, nbytes
+        self.Q = torch.empty(self.m_local, n, dtype=torch.float64, device=self.dev)
+        self.R = torch.empty(n, n, dtype=torch.float64, device=self.dev)
+        self.piv = torch.empty(n, dtype=torch.int64, device=self.dev)
+        self.info_t = torch.zeros(2, dtype=torch.int64, device=self.dev)
+
+    def run(self, X):
+        assert X.shape == (self.m_local, self.n) and X.dtype == torch.float64
+        st = ctypes.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        h = self.comm.handle if self.comm is not None else None
+        common = (ctypes.c_void_p(X.data_ptr()), self.m_local, self.n, X.stride(0), self.row0, self.m_global)
+        tail = (ctypes.c_uint64(self.seed), ctypes.byref(self.cfg), ctypes.c_void_p(self.Q.data_ptr()),
+                self.Q.stride(0), ctypes.c_void_p(self.R.data_ptr()), ctypes.c_void_p(self.piv.data_ptr()),
+                ctypes.c_void_p(self.ws_ptr), self.ws_bytes, ctypes.c_void_p(self.info_t.data_ptr()), h, st)
+        if self.algo == "slhc3":
+            check(lib().rlhc_slhc3_dist(*common, self.s, *tail))
+        else:
+            check(lib().rlhc_sslhc3_dist(*common, self.s1, self.s2, *tail))
+        return _CResult(self)
+
+
+class _CResult:
+    def __init__(self, plan):
+        self.plan, self.Q, self.R, self.piv = plan, plan.Q, plan.R, plan.piv
+
+    def info(self):
+        v = self.plan.info_t.cpu()
+        code = int(v[0] & 0xffffffff)
+        stage = int((v[0] >> 32) & 0xffffffff)
+        return code, stage, int(v[1])

@@ -76,3 +76,25 @@ def test_host_argument_errors(L):
                       ctypes.c_void_p(0x100000), 16, info, None)
     assert rc == _lib.RLHC_EWORKSPACE
     assert L.rlhc_version().startswith(b"rlhc-b200")
+
+
+def test_dist_entry_host_errors():
+    """rlhc_slhc3_dist argument checks are host-side (no GPU needed): bad shards, nulls."""
+    import ctypes
+    from paper_2412_06551_b200 import _lib
+    L = _lib.lib()
+    cfg = _lib.TsluCfg(256, 4, 64)
+    dummy = ctypes.c_void_p(256)
+    info = ctypes.c_void_p(512)
+    # one rank (no communicator) must hold all rows
+    rc = L.rlhc_slhc3_dist(dummy, 4096, 64, 64, 0, 8192, 128, ctypes.c_uint64(1), ctypes.byref(cfg), dummy, 64, dummy,
+                           dummy, dummy, 1 << 30, info, None, None)
+    assert rc == _lib.RLHC_EINVAL and b"shards" in L.rlhc_last_error()
+    rc = L.rlhc_slhc3_dist(None, 4096, 64, 64, 0, 4096, 128, ctypes.c_uint64(1), ctypes.byref(cfg), dummy, 64, dummy,
+                           dummy, dummy, 1 << 30, info, None, None)
+    assert rc == _lib.RLHC_EINVAL
+    # m_local not a multiple of leaf_rows
+    rc = L.rlhc_sslhc3_dist(dummy, 4000, 64, 64, 0, 4000, 512, 128, ctypes.c_uint64(1), ctypes.byref(cfg), dummy, 64,
+                            dummy, dummy, dummy, 1 << 30, info, None, None)
+    assert rc == _lib.RLHC_EINVAL and b"leaf_rows" in L.rlhc_last_error()
+    assert L.rlhc_dist_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(cfg), 8) > 0

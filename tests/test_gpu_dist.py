@@ -73,3 +73,37 @@ def test_two_gloo_ranks_on_one_gpu(ora):
         assert np.linalg.norm(r["R"] - ref.R) <= 1e-12 * np.linalg.norm(ref.R)
     Q = np.concatenate([r["Q"] for r in res])
     assert np.linalg.norm(Q.T @ Q - np.eye(48)) <= 1e-13 * np.sqrt(48)
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_c_dist_entry_matches_single_call(with_comm):
+    """rlhc_slhc3_dist / rlhc_sslhc3_dist (C orchestration, NCCL collectives) on one rank: no
+    communicator, and a real one-rank NCCL communicator; against the single-GPU call."""
+    import paper_2412_06551_b200 as rl
+    import synth
+    from paper_2412_06551_b200._lib import TsluCfg
+    from paper_2412_06551_b200.dist import CDistPlan, NcclComm
+    comm = NcclComm() if with_comm else None
+    for algo, m, n, kw, cfgt in [("slhc3", 65536, 64, dict(s=128), (256, 4, 64)),
+                                 ("sslhc3", 65536, 128, dict(s1=1024, s2=256), (256, 4, 64)),
+                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64))]:
+        X = synth.baseline_matrix(m, n, 12, 8, device="cuda")
+        cfg = TsluCfg(*cfgt)
+        plan = CDistPlan(algo, m, n, seed=3, cfg=cfg, device="cuda", comm=comm, **kw)
+        res = plan.run(X)
+        assert res.info() == (0, 0, 0)
+        single = (rl.slhc3 if algo == "slhc3" else rl.sslhc3)(X, seed=3, cfg=cfg, **kw)
+        assert torch.equal(res.piv, single.piv)
+        Rh, Rs = res.R.cpu().numpy(), single.R.cpu().numpy()
+        assert np.linalg.norm(Rh - Rs) <= 1e-12 * np.linalg.norm(Rs)
+        Qh = res.Q.cpu().numpy()
+        assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) <= 1e-13 * np.sqrt(n)
+        # device errors come back as the first in pipeline order
+        Xd = X.clone()
+        Xd[:, 5] = 0.0
+        assert plan.run(Xd).info()[:2] == (3, 1)  # ERANKDEF, LU
+        Xd[777, 3] = float("nan")
+        assert plan.run(Xd).info() == (2, 0, 777 * n + 3)  # ENONFINITE, INPUT, element index
+        torch.cuda.synchronize()
+    if comm is not None:
+        comm.close()

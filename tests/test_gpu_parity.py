@@ -205,3 +205,18 @@ def test_edge_cases_vs_oracle(rl, ora, algo, m, n, kw):
     assert orth_err(Q) <= 1e-13 * math.sqrt(n)
     assert rel_residual(Q, R, Xh) <= 1e-14 * max(n, 1)
     assert rel_fro(R, ref.R) <= 1e-9
+
+
+@pytest.mark.parametrize("m,n,col", [(16384, 100, 5), (4096, 128, 5), (512, 100, 5), (16384, 100, 70)])
+def test_rank_deficient_multipanel(rl, m, n, col):
+    """A zero column in the first panel leaves NaN in the trailing matrix (the panel's zero
+    pivot); the later panels' tournaments must still be well defined and the call must report
+    ERANKDEF(LU, col), never fault (regression: NaN keys in the pivot search)."""
+    X = _x(m, n, 8, 31)
+    X[:, col] = 0.0
+    piv, U, L11, L, info = rl.getrf_ts(X, cfg=(256, 2, 64), want_L=True)
+    assert info == (3, 1, col)
+    res = rl.sslhc3(X, s1=min(8 * n, m), s2=2 * n, seed=1, cfg=(256, 2, 64))
+    assert res.info() == (3, 1, col)
+    res = rl.slhc3(X, s=2 * n, seed=1)
+    assert res.info()[:2] == (3, 1)
