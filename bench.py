@@ -116,7 +116,7 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     torch.cuda.set_device(dev)
     if world > 1:
         from paper_2412_06551_b200 import dist as rdist
-        X, plan = rdist.setup_bench(cfg, rank, world, dev, strong=args.strong)
+        X, plan = rdist.setup_bench(cfg, rank, world, dev, strong=args.strong, use_c=not functional)
         run = lambda: plan.run(X)  # noqa: E731
     else:
         X = synth.config_matrix(cfg, device=dev)
