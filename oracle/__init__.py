@@ -21,7 +21,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 # error codes / stages, declared independently of include/rlhc.h (SURVEY 8b numbering)
 OK, EINVAL, ENONFINITE, ERANKDEF, ESINGULAR, EBREAKDOWN = 0, 1, 2, 3, 4, 5
-ST_INPUT, ST_LU, ST_SKETCH, ST_HQR, ST_SOLVE_Y, ST_CHOL1, ST_SOLVE_D, ST_CHOL2, ST_SOLVE_J = range(9)
+ST_INPUT, ST_LU, ST_SKETCH, ST_HQR, ST_SOLVE_Y, ST_CHOL1, ST_SOLVE_D, ST_CHOL2, ST_SOLVE_J, ST_CHOL0 = range(10)
 
 
 def build(force: bool = False) -> str:
@@ -76,6 +76,11 @@ def lib():
         L.ora_panel_rows.argtypes = [P, I64, I64]
         L.ora_eliminate_rows.argtypes = [P, I64, I64, I64, I64, P, P]
         L.ora_lfactor_rows.argtypes = [P, I64, I64, I64, P, P, P, P]
+        L.ora_cholqr2.argtypes = [P, I64, I64, I64, P, I64, P, P]
+        L.ora_scholqr3.argtypes = [P, I64, I64, I64, P, I64, P, P]
+        L.ora_scholqr_shift.argtypes = [P, I64, I64]; L.ora_scholqr_shift.restype = D
+        L.ora_luc2.argtypes = [P, I64, I64, I64, I64, I64, I64, P, I64, P, P, P]
+        L.ora_rhc.argtypes = [P, I64, I64, I64, I64, I64, U64, P, I64, P, P]
     return _lib
 
 
@@ -252,6 +257,53 @@ def sslhc3(X, s1: int, s2: int, seed: int, leaf_rows: int, arity: int, panel: in
     n = X.shape[1]
     panel = n if panel is None else panel
     return _run(lib().ora_sslhc3, X, n, (s1, s2, seed, leaf_rows, arity, panel), s2, s1, stages, raise_on_error)
+
+
+# -------------------------------------------------- comparison algorithms
+def _run_simple(call, X, n, raise_on_error: bool):
+    X = _f64(X); m = X.shape[0]
+    Q = np.zeros((m, n)); R = np.zeros((n, n)); piv = np.zeros(n, np.int64)
+    info = _Info()
+    call(X, m, Q, R, piv, info)
+    if raise_on_error:
+        _raise(info)
+    return Result(Q, R, piv, {}, (info.code, info.stage, info.index))
+
+
+def cholqr2(X, raise_on_error: bool = True) -> Result:
+    """CholeskyQR2 (alg:cholqr2, P:36-46)."""
+    n = X.shape[1]
+    return _run_simple(lambda X, m, Q, R, piv, info: lib().ora_cholqr2(_p(X), m, n, n, _p(Q), n, _p(R),
+                                                                      ctypes.byref(info)), X, n, raise_on_error)
+
+
+def scholqr3(X, raise_on_error: bool = True) -> Result:
+    """SCholeskyQR3 (alg:Shifted3), shift of P:984 (R#21)."""
+    n = X.shape[1]
+    return _run_simple(lambda X, m, Q, R, piv, info: lib().ora_scholqr3(_p(X), m, n, n, _p(Q), n, _p(R),
+                                                                       ctypes.byref(info)), X, n, raise_on_error)
+
+
+def scholqr_shift(G, m: int) -> float:
+    G = _f64(G)
+    return lib().ora_scholqr_shift(_p(G), m, G.shape[0])
+
+
+def luc2(X, leaf_rows: int, arity: int, panel: int | None = None, raise_on_error: bool = True) -> Result:
+    """LU-CholeskyQR2 (alg:LU2) under the tournament contract."""
+    n = X.shape[1]
+    panel = n if panel is None else panel
+    return _run_simple(lambda X, m, Q, R, piv, info: lib().ora_luc2(_p(X), m, n, n, leaf_rows, arity, panel, _p(Q), n,
+                                                                   _p(R), _p(piv), ctypes.byref(info)),
+                       X, n, raise_on_error)
+
+
+def rhc(X, s1: int, s2: int, seed: int, raise_on_error: bool = True) -> Result:
+    """Rand.Householder-Cholesky (alg:Rand2), multi-sketch K = Omega_2 Omega_1 X."""
+    n = X.shape[1]
+    return _run_simple(lambda X, m, Q, R, piv, info: lib().ora_rhc(_p(X), m, n, n, s1, s2, ctypes.c_uint64(seed),
+                                                                  _p(Q), n, _p(R), ctypes.byref(info)),
+                       X, n, raise_on_error)
 
 
 def orthogonality(Q) -> float:

@@ -29,7 +29,7 @@
 /* Error model: errors are values, stage-tagged. */
 enum { ORA_OK = 0, ORA_EINVAL = 1, ORA_ENONFINITE = 2, ORA_ERANKDEF = 3, ORA_ESINGULAR = 4, ORA_EBREAKDOWN = 5 };
 enum { ST_INPUT = 0, ST_LU = 1, ST_SKETCH = 2, ST_HQR = 3, ST_SOLVE_Y = 4, ST_CHOL1 = 5, ST_SOLVE_D = 6,
-       ST_CHOL2 = 7, ST_SOLVE_J = 8 };
+       ST_CHOL2 = 7, ST_SOLVE_J = 8, ST_CHOL0 = 9 };
 typedef struct { int32_t code; int32_t stage; int64_t index; } ora_info;
 
 static int set_err(ora_info* info, int code, int stage, int64_t index) {
@@ -639,6 +639,156 @@ int ora_sslhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, i
   rc = lhc_tail(X, m, n, ldx, Lss, s2, U, Q, ldq, R, st, info);
 out:
   free(U); free(L11); free(Lt); free(Lss); free(bucket); free(sign); free(Lrows);
+  return rc;
+}
+
+/* ------------------------------------------------------------ comparison algorithms */
+/* The paper's comparison methods, each step in the paper's order from
+ * the primitives above.  Stage tags: the Cholesky of the preconditioning step is ST_CHOL0,
+ * the CholeskyQR(2) tail uses ST_CHOL1 / ST_CHOL2 like SLHC3. */
+
+/* CholeskyQR (alg:cholqr) in place on the m x n rows of Q: G = Q^T Q (+ shift I),
+ * T = Cholesky(G), Q := Q T^{-1} (substitution). */
+static int cholqr_step(double* Q, int64_t m, int64_t n, int64_t ldq, double* T, double shift, int chol_stage,
+                       int solve_stage, ora_info* info) {
+  double* G = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  ora_gram(Q, m, n, ldq, G);
+  if (shift != 0.0)
+    for (int64_t k = 0; k < n; k++) G[k * n + k] += shift;
+  int rc = ora_chol(G, n, T, chol_stage, info);
+  if (!rc) rc = ora_trsm_right_upper(Q, m, n, ldq, T, Q, ldq, solve_stage, info);
+  free(G);
+  return rc;
+}
+
+static void copy_rows(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq) {
+  for (int64_t i = 0; i < m; i++) memcpy(Q + i * ldq, X + i * ldx, sizeof(double) * (size_t)n);
+}
+
+/* CholeskyQR2 (alg:cholqr2): [W, Y] = CholeskyQR(X), [Q, Z] = CholeskyQR(W), R = Z Y. */
+int ora_cholqr2(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R,
+                ora_info* info) {
+  if (info) { info->code = 0; info->stage = 0; info->index = 0; }
+  if (m < n || n < 1 || ldx < n || ldq < n) return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  int rc = check_finite(X, m, n, ldx, info);
+  if (rc) return rc;
+  size_t nn = (size_t)(n * n);
+  double* Y = (double*)malloc(sizeof(double) * nn);
+  double* Z = (double*)malloc(sizeof(double) * nn);
+  copy_rows(X, m, n, ldx, Q, ldq);
+  rc = cholqr_step(Q, m, n, ldq, Y, 0.0, ST_CHOL0, ST_SOLVE_Y, info);
+  if (!rc) rc = cholqr_step(Q, m, n, ldq, Z, 0.0, ST_CHOL1, ST_SOLVE_D, info);
+  if (!rc) ora_trmm_uu(Z, Y, n, R);
+  free(Y); free(Z);
+  return rc;
+}
+
+/* SCholeskyQR3 (alg:Shifted P:48-59, alg:Shifted3 P:61-71): [W, Y] = SCholeskyQR(X) with
+ * s = 11 (m n u + (n + 1) u) ||X||_g^2 (u = 2^-53; ||X||_g = the largest column
+ * 2-norm, SPEC S:326 -- here sqrt(max diag(X^T X)), R#21), then
+ * [Q, Z] = CholeskyQR2(W) = [W2, D] = CholeskyQR(W), [Q, J] = CholeskyQR(W2), R = J (D Y). */
+double ora_scholqr_shift(const double* G, int64_t m, int64_t n) {
+  double g = 0.0;
+  for (int64_t k = 0; k < n; k++) if (G[k * n + k] > g) g = G[k * n + k];
+  const double u = 0x1p-53;
+  return 11.0 * ((double)m * (double)n * u + (double)(n + 1) * u) * g;
+}
+
+int ora_scholqr3(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R,
+                 ora_info* info) {
+  if (info) { info->code = 0; info->stage = 0; info->index = 0; }
+  if (m < n || n < 1 || ldx < n || ldq < n) return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  int rc = check_finite(X, m, n, ldx, info);
+  if (rc) return rc;
+  size_t nn = (size_t)(n * n);
+  double* G = (double*)malloc(sizeof(double) * nn);
+  double* Y = (double*)malloc(sizeof(double) * nn);
+  double* D = (double*)malloc(sizeof(double) * nn);
+  double* J = (double*)malloc(sizeof(double) * nn);
+  double* N = (double*)malloc(sizeof(double) * nn);
+  ora_gram(X, m, n, ldx, G);
+  const double shift = ora_scholqr_shift(G, m, n);
+  for (int64_t k = 0; k < n; k++) G[k * n + k] += shift;
+  rc = ora_chol(G, n, Y, ST_CHOL0, info);
+  if (!rc) rc = ora_trsm_right_upper(X, m, n, ldx, Y, Q, ldq, ST_SOLVE_Y, info);
+  if (!rc) rc = cholqr_step(Q, m, n, ldq, D, 0.0, ST_CHOL1, ST_SOLVE_D, info);
+  if (!rc) rc = cholqr_step(Q, m, n, ldq, J, 0.0, ST_CHOL2, ST_SOLVE_J, info);
+  if (!rc) { ora_trmm_uu(D, Y, n, N); ora_trmm_uu(J, N, n, R); }
+  free(G); free(Y); free(D); free(J); free(N);
+  return rc;
+}
+
+/* LUC2 (alg:LU P:75-87, alg:LU2 P:89-99): PX = LU (the tournament contract, R#3), G = L^T L,
+ * S = Cholesky(G) ("B" read as G), Y = S U with rows flipped to diag(Y) > 0
+ * (R#23: the unique R with a positive diagonal), W = X Y^{-1}; [Q, Z] = CholeskyQR(W), R = Z Y. */
+int ora_luc2(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t leaf_rows, int64_t arity, int64_t panel,
+             double* Q, int64_t ldq, double* R, int64_t* piv, ora_info* info) {
+  if (info) { info->code = 0; info->stage = 0; info->index = 0; }
+  if (m < n || n < 1 || ldx < n || ldq < n) return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  int rc = check_finite(X, m, n, ldx, info);
+  if (rc) return rc;
+  size_t nn = (size_t)(n * n);
+  double* U = (double*)malloc(sizeof(double) * nn);
+  double* L11 = (double*)malloc(sizeof(double) * nn);
+  double* G = (double*)malloc(sizeof(double) * nn);
+  double* S = (double*)malloc(sizeof(double) * nn);
+  double* Y = (double*)malloc(sizeof(double) * nn);
+  double* Z = (double*)malloc(sizeof(double) * nn);
+  double* Lrows = NULL;
+  rc = ora_tslu(X, m, n, ldx, leaf_rows, arity, panel, piv, U, L11, NULL, info);
+  if (rc) goto out;
+  Lrows = (double*)malloc(sizeof(double) * (size_t)(m * n));
+  ora_lfactor(X, m, n, ldx, piv, U, L11, Lrows);
+  ora_gram(Lrows, m, n, n, G);
+  rc = ora_chol(G, n, S, ST_CHOL0, info);
+  if (rc) goto out;
+  ora_trmm_uu(S, U, n, Y);
+  for (int64_t k = 0; k < n; k++) /* diag(Y) > 0 (the sign of U_kk, R#23) */
+    if (Y[k * n + k] < 0.0)
+      for (int64_t j = 0; j < n; j++) Y[k * n + j] = -Y[k * n + j];
+  rc = ora_trsm_right_upper(X, m, n, ldx, Y, Q, ldq, ST_SOLVE_Y, info);
+  if (rc) goto out;
+  rc = cholqr_step(Q, m, n, ldq, Z, 0.0, ST_CHOL1, ST_SOLVE_D, info);
+  if (!rc) ora_trmm_uu(Z, Y, n, R);
+out:
+  free(U); free(L11); free(G); free(S); free(Y); free(Z); free(Lrows);
+  return rc;
+}
+
+/* RHC (alg:Rand1 P:103-113, alg:Rand2 P:115-127): K = Omega_2 Omega_1 X (CountSketch s1 x m,
+ * stream 2, then Gaussian s2 x s1, stream 1 -- the SSLHC3 sketches applied to X),
+ * [H, Y] = HouseholderQR(K) with rows of Y flipped to a positive diagonal (R#22),
+ * W = X Y^{-1}; [Q, Z] = CholeskyQR(W), R = Z Y. */
+int ora_rhc(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed, double* Q,
+            int64_t ldq, double* R, ora_info* info) {
+  if (info) { info->code = 0; info->stage = 0; info->index = 0; }
+  if (m < n || n < 1 || s2 < n || s1 < s2 || s1 > m || ldx < n || ldq < n)
+    return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  int rc = check_finite(X, m, n, ldx, info);
+  if (rc) return rc;
+  size_t nn = (size_t)(n * n);
+  int32_t* bucket = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+  int8_t* sign = (int8_t*)malloc((size_t)m);
+  double* Kt = (double*)malloc(sizeof(double) * (size_t)(s1 * n));
+  double* K = (double*)malloc(sizeof(double) * (size_t)(s2 * n));
+  double* Xc = (double*)malloc(sizeof(double) * (size_t)(m * n));
+  double* Y = (double*)malloc(sizeof(double) * nn);
+  double* Z = (double*)malloc(sizeof(double) * nn);
+  copy_rows(X, m, n, ldx, Xc, n);
+  ora_cs_hash(seed, 0, m, s1, bucket, sign);
+  ora_cs_apply(Xc, m, n, n, bucket, sign, s1, Kt);
+  ora_sketch_gauss(Kt, s1, n, n, 0, s2, seed, 1u, K);
+  rc = ora_hqr_r(K, s2, n, Y, info);
+  if (rc) goto out;
+  for (int64_t k = 0; k < n; k++)
+    if (Y[k * n + k] < 0.0)
+      for (int64_t j = 0; j < n; j++) Y[k * n + j] = -Y[k * n + j];
+  rc = ora_trsm_right_upper(X, m, n, ldx, Y, Q, ldq, ST_SOLVE_Y, info);
+  if (rc) goto out;
+  rc = cholqr_step(Q, m, n, ldq, Z, 0.0, ST_CHOL1, ST_SOLVE_D, info);
+  if (!rc) ora_trmm_uu(Z, Y, n, R);
+out:
+  free(bucket); free(sign); free(Kt); free(K); free(Xc); free(Y); free(Z);
   return rc;
 }
 
