@@ -16,6 +16,7 @@ BASELINE metric workload), --strong keeps the config's m fixed (north star: --co
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -120,7 +121,11 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
         run = lambda: plan.run(X)  # noqa: E731
     else:
         X = synth.config_matrix(cfg, device=dev)
-        plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, device=dev)
+        if args.method in METHOD_PASSES:
+            s1, s2 = _rhc_sizes(cfg)
+            plan = rl.MethodPlan(args.method, cfg.m, cfg.n, s1=s1, s2=s2, seed=cfg.seed, device=dev)
+        else:
+            plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, device=dev)
         run = lambda: plan.run(X)  # noqa: E731
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -189,14 +194,14 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     return ms, stages, launches, clk.summary(), e2e, X
 
 
-def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, m_local: int = 0):
+def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, m_local: int = 0, passes: int = 8):
     calls = max(stages.get("calls", 1), 1)
     model = stage_model(cfg)
     hbm, hbm_src = _peaks()
     if not any(v for k, v in stages.items() if k != "calls"):
-        # N > 1 runs through the per-stage entry points (no stage markers): the whole step
-        # of one rank against its HBM roof (8 passes over its rows)
-        byts = 64.0 * m_local * cfg.n
+        # N > 1 and the comparison algorithms have no stage markers: the whole step of one
+        # rank against its HBM roof (the algorithmic passes over its rows)
+        byts = passes * 8.0 * m_local * cfg.n
         ach = byts / (step_ms * 1e-3) / 1e9
         return {"kernel": "whole step (per rank)", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": None, "peak_source": hbm_src, "ms": step_ms}
@@ -232,13 +237,18 @@ def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, 
             "traffic": traffic, "peak_source": hbm_src, "ms": t * 1e3}
 
 
-def cpu_baseline(cfg: synth.Config, X: torch.Tensor | None, budget_s: float = 8.0):
+def cpu_baseline(cfg: synth.Config, X: torch.Tensor | None, budget_s: float = 8.0, method: str = "auto"):
     import oracle
     oracle.build()
     Xh = (X.cpu() if X is not None else synth.config_matrix(cfg)).numpy()
     reps, t0 = 0, time.perf_counter()
     while True:
-        if cfg.algo == "slhc3":
+        if method in METHOD_PASSES:
+            s1, s2 = _rhc_sizes(cfg)
+            b, a, p = _default_cfg_tuple(cfg)
+            {"cholqr2": lambda: oracle.cholqr2(Xh), "scholqr3": lambda: oracle.scholqr3(Xh),
+             "luc2": lambda: oracle.luc2(Xh, b, a, p), "rhc": lambda: oracle.rhc(Xh, s1, s2, cfg.seed)}[method]()
+        elif cfg.algo == "slhc3":
             b, a, p = _default_cfg_tuple(cfg)
             oracle.slhc3(Xh, cfg.s, cfg.seed, b, a, p)
         else:
@@ -249,8 +259,24 @@ def cpu_baseline(cfg: synth.Config, X: torch.Tensor | None, budget_s: float = 8.
         if el >= budget_s or reps >= 20:
             break
     per = el / reps
-    return {"value": 8 * 8.0 * cfg.m * cfg.n / per / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+    return {"value": _passes(method) * 8.0 * cfg.m * cfg.n / per / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
             "kind": "oracle", "sample": f"full {cfg.name} ({cfg.m}x{cfg.n}) x{reps}", "s_per_step": per}
+
+
+# the paper's comparison algorithms, 1 GPU: algorithmic passes over m x n
+# data in the paper's order: CholeskyQR = Gram (1 read) + substitution
+# (read + write) = 3; LUC2 = LU (read X, write L) + Gram(L) + W = X Y^-1 + CholeskyQR(W) = 8;
+# RHC = sketch (1) + W = X Y^-1 (2) + CholeskyQR(W) (3) = 6
+METHOD_PASSES = {"cholqr2": 6, "scholqr3": 9, "luc2": 8, "rhc": 6}
+
+
+def _passes(method: str) -> int:
+    return METHOD_PASSES.get(method, 8)
+
+
+def _rhc_sizes(cfg):
+    # RHC's CountSketch / Gaussian sizes: the SSLHC3 ones (s1 = 8n, s2 = 2n, BASELINE.json)
+    return min(cfg.m, cfg.s1 or 8 * cfg.n), cfg.s2 or 2 * cfg.n
 
 
 def _default_cfg_tuple(cfg):
@@ -272,19 +298,35 @@ def main():
                     help="N > 1: fixed global m (the config's), rows split over ranks; default: weak scaling, "
                          "every rank holds the config's m rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kappa-exp", type=int, default=None,
+                    help="override the config's kappa = 1e<k> (default for --method cholqr2: min(k, 6), "
+                         "CholeskyQR2 breaks down once kappa^2 u > 1, P:34)")
+    ap.add_argument("--method", default="auto", choices=["auto"] + sorted(METHOD_PASSES),
+                    help="auto: the config's SLHC3/SSLHC3; else one of the paper's comparison algorithms "
+                         "(1 GPU) on the same X")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
     cfg = synth.CONFIGS[args.config]
+    if args.kappa_exp is not None:
+        cfg = dataclasses.replace(cfg, kappa_exp=args.kappa_exp)
+    elif args.method == "cholqr2" and cfg.kappa_exp > 6:
+        cfg = dataclasses.replace(cfg, kappa_exp=6)
     strong = args.strong and world > 1
     m_global = cfg.m if (strong or world == 1) else cfg.m * world
     if world > 1 and not torch.distributed.is_initialized():
         functional = os.environ.get("RLHC_BENCH_FUNCTIONAL") == "1"
         torch.distributed.init_process_group("nccl" if args.impl == "ours" and not functional else "gloo")
-    workload = (f"{cfg.name}: {cfg.algo.upper()} m={m_global} n={cfg.n} "
-                + (f"s={cfg.s}" if cfg.algo == "slhc3" else f"s1={cfg.s1} s2={cfg.s2}")
+    if args.method != "auto" and world > 1:
+        raise SystemExit("--method: the comparison algorithms run on 1 GPU")
+    algo = cfg.algo if args.method == "auto" else args.method
+    passes = _passes(args.method)
+    s1m, s2m = _rhc_sizes(cfg)
+    sizes = (f"s={cfg.s}" if algo == "slhc3" else f"s1={cfg.s1} s2={cfg.s2}" if algo == "sslhc3"
+             else f"s1={s1m} s2={s2m}" if algo == "rhc" else "")
+    workload = (f"{cfg.name}: {algo.upper()} m={m_global} n={cfg.n}" + (" " + sizes if sizes else "")
                 + f" kappa=1e{cfg.kappa_exp}{' colscale' if cfg.colscale else ''} seed={cfg.seed}")
-    base = {"metric": f"{cfg.algo.upper()} fp64 QR algorithmic HBM throughput (8 passes of m x n)",
+    base = {"metric": f"{algo.upper()} fp64 QR algorithmic HBM throughput ({passes} passes of m x n)",
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "m": m_global, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
@@ -294,7 +336,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_baseline(cfg, None, budget_s=max(5.0, 0.5 * args.steps))
+        cb = cpu_baseline(cfg, None, budget_s=max(5.0, 0.5 * args.steps), method=args.method)
         line = dict(base, impl="reference", value=cb["value"], ms_per_step=cb["s_per_step"] * 1e3,
                     cpu_baseline=cb, e2e={"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                                           "d2h_bytes_per_step": 0}, n_gpus=0)
@@ -304,14 +346,14 @@ def main():
     if rank != 0:
         return
     per_step = ms / args.steps
-    value = 8 * 8.0 * m_global * cfg.n / (per_step * 1e-3) / 1e9  # whole job, all ranks
-    e2e["value"] = 8 * 8.0 * m_global * cfg.n / (e2e.pop("ms_per_step") * 1e-3) / 1e9
-    e2e["ms_per_step"] = 8 * 8.0 * m_global * cfg.n / e2e["value"] / 1e6
+    value = passes * 8.0 * m_global * cfg.n / (per_step * 1e-3) / 1e9  # whole job, all ranks
+    e2e["value"] = passes * 8.0 * m_global * cfg.n / (e2e.pop("ms_per_step") * 1e-3) / 1e9
+    e2e["ms_per_step"] = passes * 8.0 * m_global * cfg.n / e2e["value"] / 1e6
     line = dict(base, value=value, ms_per_step=per_step, gpu_launches=launches, clocks=clocks,
-                roofline=roofline(cfg, stages, world, per_step, m_global // world), e2e=e2e,
+                roofline=roofline(cfg, stages, world, per_step, m_global // world, passes), e2e=e2e,
                 stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls" and v})
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, X)
+        line["cpu_baseline"] = cpu_baseline(cfg, X, method=args.method)
     print(json.dumps(line), flush=True)
 
 

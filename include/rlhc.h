@@ -63,10 +63,13 @@ enum rlhc_stage {
   RLHC_STAGE_CHOL1 = 5,   /* D = chol(W^T W) (P:27-28 inside CholeskyQR2) */
   RLHC_STAGE_SOLVE_D = 6, /* V = W D^{-1} */
   RLHC_STAGE_CHOL2 = 7,   /* J = chol(V^T V) */
-  RLHC_STAGE_SOLVE_J = 8  /* Q = V J^{-1} */
+  RLHC_STAGE_SOLVE_J = 8, /* Q = V J^{-1} */
+  RLHC_STAGE_CHOL0 = 9    /* the preconditioning Cholesky of the comparison methods (below) */
 };
 
 enum rlhc_algo { RLHC_SLHC3 = 0, RLHC_SSLHC3 = 1 };
+/* the paper's comparison algorithms, entry points below */
+enum rlhc_method { RLHC_CHOLQR2 = 2, RLHC_SCHOLQR3 = 3, RLHC_LUC2 = 4, RLHC_RHC = 5 };
 enum rlhc_trsm_mode { RLHC_SUBST = 0, RLHC_INV_GEMM = 1 };
 
 /* Pivot-rule contract of PX = LU (R#3-R#5; the paper only says "P is a
@@ -211,6 +214,33 @@ int rlhc_trmm_upper(const double* A, const double* B, int64_t n, double* C, rlhc
 size_t rlhc_cholesky_workspace_size(int64_t n);
 int rlhc_cholesky_ws(const double* G, int64_t n, double* Rout, int stage, void* ws, size_t ws_bytes, rlhc_info_t* info,
                      rlhc_stream_t stream);
+
+/* ------------------------------------------------- the paper's comparison algorithms */
+/* The methods the paper compares SLHC3 / SSLHC3 against, on the same kernels (SURVEY 8(f)
+ * NEXT-1; oracle: ora_cholqr2 / ora_scholqr3 / ora_luc2 / ora_rhc):
+ *   rlhc_cholqr2   CholeskyQR2 (alg:cholqr2): [W,Y] = CholeskyQR(X), [Q,Z] =
+ *                  CholeskyQR(W), R = Z Y;
+ *   rlhc_scholqr3  SCholeskyQR3 (alg:Shifted3): shifted CholeskyQR with
+ *                  s = 11 (m n u + (n+1) u) ||X||_g^2 (||X||_g = largest column norm,
+ *                  DESIGN.md R#21), then CholeskyQR2;
+ *   rlhc_luc2      LU-CholeskyQR2 (alg:LU2): PX = LU (tournament contract), S =
+ *                  Cholesky(L^T L), Y = S U (diag > 0, R#23), W = X Y^{-1}, CholeskyQR(W);
+ *   rlhc_rhc       Rand.Householder-Cholesky (alg:Rand2): K = Omega_2 Omega_1 X
+ *                  (CountSketch s1 + Gaussian s2, the SSLHC3 streams), Y = HouseholderQR(K)
+ *                  (diag > 0, R#22), W = X Y^{-1}, CholeskyQR(W).
+ * Same conventions as rlhc_slhc3: device pointers, row-major, Q (m x n) must not alias X,
+ * R (n x n, strict lower 0, diag > 0), info = first device error (breakdown of the first
+ * Cholesky: EBREAKDOWN(RLHC_STAGE_CHOL0, k); of the CholeskyQR tail: CHOL1 / CHOL2). */
+size_t rlhc_method_workspace_size(int method, int64_t m, int64_t n, int64_t s1, int64_t s2,
+                                  const rlhc_tslu_cfg* cfg);
+int rlhc_cholqr2(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R, void* ws,
+                 size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+int rlhc_scholqr3(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R, void* ws,
+                  size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+int rlhc_luc2(const double* X, int64_t m, int64_t n, int64_t ldx, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq,
+              double* R, int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
+int rlhc_rhc(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed, double* Q,
+             int64_t ldq, double* R, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream);
 
 /* ------------------------------------------------- row-sharded entry points over NCCL */
 /* SURVEY 8(b) "_dist", 8(e).  The whole SLHC3 / SSLHC3 call on nranks GPUs, one process per

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import (RLHC_INV_GEMM, RLHC_SLHC3, RLHC_SSLHC3, RLHC_SUBST, STAGE_CHOL1, STAGE_CHOL2, Info, RlhcError,
                    TsluCfg, check, lib)
 
-__all__ = ["slhc3", "sslhc3", "getrf_ts", "sketch_gauss", "sketch_count", "gram", "trsm_apply", "hqr_r", "cholesky",
+__all__ = ["slhc3", "sslhc3", "cholqr2", "scholqr3", "luc2", "rhc", "MethodPlan", "getrf_ts", "sketch_gauss", "sketch_count", "gram", "trsm_apply", "hqr_r", "cholesky",
            "default_cfg", "Plan", "RlhcError", "RLHC_SUBST", "RLHC_INV_GEMM", "STAGE_CHOL1", "STAGE_CHOL2"]
 
 
@@ -121,6 +121,67 @@ def sslhc3(X: torch.Tensor, s1: int, s2: int, seed: int = 0, cfg=None) -> Result
     """SSLHC3 (PAPER.md alg:SSLHC3) on a CUDA fp64 row-major X (m x n)."""
     m, n = X.shape
     return Plan("sslhc3", m, n, s1=s1, s2=s2, seed=seed, cfg=cfg, device=X.device).run(X)
+
+
+class MethodPlan:
+    """Reusable call of one of the paper's comparison algorithms:
+    'cholqr2', 'scholqr3', 'luc2' (tournament contract cfg) or 'rhc' (sketch sizes s1, s2)."""
+
+    IDS = {"cholqr2": _lib.RLHC_CHOLQR2, "scholqr3": _lib.RLHC_SCHOLQR3, "luc2": _lib.RLHC_LUC2, "rhc": _lib.RLHC_RHC}
+
+    def __init__(self, method: str, m: int, n: int, s1: int = 0, s2: int = 0, seed: int = 0, cfg=None,
+                 device="cuda"):
+        self.method, self.mid = method, self.IDS[method]
+        self.m, self.n, self.s1, self.s2, self.seed = m, n, s1, s2, seed
+        self.device = torch.device(device)
+        self.cfg = _cfg(cfg, m, n)
+        nbytes = lib().rlhc_method_workspace_size(self.mid, m, n, s1, s2, ctypes.byref(self.cfg))
+        if nbytes == 0:
+            raise RlhcError(_lib.RLHC_EINVAL, "invalid sizes / configuration")
+        self.ws = _ws(nbytes, self.device)
+        self.Q = torch.empty(m, n, dtype=torch.float64, device=self.device)
+        self.R = torch.empty(n, n, dtype=torch.float64, device=self.device)
+        self.piv = torch.empty(n, dtype=torch.int64, device=self.device)
+        self.info_dev = _new_info(self.device)
+
+    def run(self, X: torch.Tensor) -> Result:
+        _need(X, "X")
+        m, n = X.shape
+        assert (m, n) == (self.m, self.n)
+        L = lib()
+        head = (_p(X), m, n, X.stride(0))
+        out = (_p(self.Q), n, _p(self.R))
+        tail = (_p(self.ws), self.ws.numel(), _p(self.info_dev), _stream(self.device))
+        if self.method == "cholqr2":
+            rc = L.rlhc_cholqr2(*head, *out, *tail)
+        elif self.method == "scholqr3":
+            rc = L.rlhc_scholqr3(*head, *out, *tail)
+        elif self.method == "luc2":
+            rc = L.rlhc_luc2(*head, ctypes.byref(self.cfg), *out, _p(self.piv), *tail)
+        else:
+            rc = L.rlhc_rhc(*head, self.s1, self.s2, ctypes.c_uint64(self.seed), *out, *tail)
+        check(rc)
+        return Result(self.Q, self.R, self.piv, self.info_dev)
+
+
+def cholqr2(X: torch.Tensor) -> Result:
+    """CholeskyQR2 (alg:cholqr2, P:36-46)."""
+    return MethodPlan("cholqr2", *X.shape, device=X.device).run(X)
+
+
+def scholqr3(X: torch.Tensor) -> Result:
+    """SCholeskyQR3 (alg:Shifted3; shift P:984)."""
+    return MethodPlan("scholqr3", *X.shape, device=X.device).run(X)
+
+
+def luc2(X: torch.Tensor, cfg=None) -> Result:
+    """LU-CholeskyQR2 (alg:LU2, P:89-99)."""
+    return MethodPlan("luc2", *X.shape, cfg=cfg, device=X.device).run(X)
+
+
+def rhc(X: torch.Tensor, s1: int, s2: int, seed: int = 0) -> Result:
+    """Rand.Householder-Cholesky (alg:Rand2, P:115-127)."""
+    return MethodPlan("rhc", *X.shape, s1=s1, s2=s2, seed=seed, device=X.device).run(X)
 
 
 def getrf_ts(X: torch.Tensor, cfg=None, want_L: bool = False):

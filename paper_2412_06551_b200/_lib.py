@@ -15,14 +15,15 @@ LIB_PATH = os.path.join(_HERE, "librlhc.so")
 (RLHC_OK, RLHC_EINVAL, RLHC_ENONFINITE, RLHC_ERANKDEF, RLHC_ESINGULAR, RLHC_EBREAKDOWN, RLHC_ECUDA, RLHC_EWORKSPACE,
  RLHC_ENCCL) = range(9)
 (STAGE_INPUT, STAGE_LU, STAGE_SKETCH, STAGE_HQR, STAGE_SOLVE_Y, STAGE_CHOL1, STAGE_SOLVE_D, STAGE_CHOL2,
- STAGE_SOLVE_J) = range(9)
+ STAGE_SOLVE_J, STAGE_CHOL0) = range(10)
 RLHC_SLHC3, RLHC_SSLHC3 = 0, 1
+RLHC_CHOLQR2, RLHC_SCHOLQR3, RLHC_LUC2, RLHC_RHC = 2, 3, 4, 5
 RLHC_SUBST, RLHC_INV_GEMM = 0, 1
 
 CODE_NAMES = {0: "OK", 1: "EINVAL", 2: "ENONFINITE", 3: "ERANKDEF", 4: "ESINGULAR", 5: "EBREAKDOWN", 6: "ECUDA",
               7: "EWORKSPACE", 8: "ENCCL"}
 STAGE_NAMES = {0: "INPUT", 1: "LU", 2: "SKETCH", 3: "HQR", 4: "SOLVE_Y", 5: "CHOL1", 6: "SOLVE_D", 7: "CHOL2",
-               8: "SOLVE_J"}
+               8: "SOLVE_J", 9: "CHOL0"}
 
 
 class TsluCfg(ctypes.Structure):
@@ -114,6 +115,15 @@ def lib():
     for name in ("rlhc_slhc3", "rlhc_sslhc3", "rlhc_getrf_ts", "rlhc_sketch_gauss", "rlhc_sketch_count", "rlhc_gram",
                  "rlhc_trsm_apply", "rlhc_hqr_r", "rlhc_cholesky"):
         getattr(L, name).restype = I
+    # the paper's comparison algorithms
+    L.rlhc_method_workspace_size.argtypes = [I, I64, I64, I64, I64, PC]
+    L.rlhc_method_workspace_size.restype = SZ
+    L.rlhc_cholqr2.argtypes = [P, I64, I64, I64, P, I64, P, P, SZ, P, P]
+    L.rlhc_scholqr3.argtypes = [P, I64, I64, I64, P, I64, P, P, SZ, P, P]
+    L.rlhc_luc2.argtypes = [P, I64, I64, I64, PC, P, I64, P, P, P, SZ, P, P]
+    L.rlhc_rhc.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_uint64, P, I64, P, P, SZ, P, P]
+    for name in ("rlhc_cholqr2", "rlhc_scholqr3", "rlhc_luc2", "rlhc_rhc"):
+        getattr(L, name).restype = I
     # row-sharded entry points over NCCL
     L.rlhc_comm_unique_id.argtypes = [P]
     L.rlhc_comm_init.argtypes = [ctypes.POINTER(P), I, I, P]
@@ -140,7 +150,8 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_tslu_panel_workspace_size", "rlhc_tslu_panel_factor_rows", "rlhc_tslu_eliminate_workspace_size",
             "rlhc_tslu_eliminate", "rlhc_lfactor_workspace_size", "rlhc_l11", "rlhc_lfactor", "rlhc_trmm_upper",
             "rlhc_cholesky_workspace_size", "rlhc_cholesky_ws", "rlhc_comm_unique_id", "rlhc_comm_init",
-            "rlhc_comm_destroy", "rlhc_dist_workspace_size", "rlhc_slhc3_dist", "rlhc_sslhc3_dist"]
+            "rlhc_comm_destroy", "rlhc_dist_workspace_size", "rlhc_slhc3_dist", "rlhc_sslhc3_dist",
+            "rlhc_method_workspace_size", "rlhc_cholqr2", "rlhc_scholqr3", "rlhc_luc2", "rlhc_rhc"]
 NUM_TIMED_STAGES = 11
 
 

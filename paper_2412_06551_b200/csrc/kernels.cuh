@@ -85,6 +85,8 @@ cudaError_t launch_chol(const double* G, int n, double* R, double* work, int sta
 size_t chol_ws_bytes(int n);
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);
+cudaError_t launch_shift_diag(double* G, int n, int64_t m, cudaStream_t st);
+cudaError_t launch_flip_neg_rows(double* T, int n, cudaStream_t st);
 cudaError_t launch_status_init(unsigned long long* status, cudaStream_t st);
 cudaError_t launch_status_finish(const unsigned long long* status, void* info, cudaStream_t st);
 cudaError_t launch_fill_i32(int* p, int64_t count, int value, cudaStream_t st);

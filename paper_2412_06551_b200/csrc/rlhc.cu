@@ -268,6 +268,86 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   return RLHC_OK;
 }
 
+// ---- the paper's comparison algorithms on the same kernels (the oracle's
+// ora_cholqr2 / ora_scholqr3 / ora_luc2 / ora_rhc).  Workspace: the SSLHC3 layout with
+// s1 = max(s1, n), s2 = max(s2, n) covers every method.
+int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed,
+               const rlhc_tslu_cfg& cfg, double* Q, int64_t ldq, double* R, int64_t* piv, AlgoWs& a, rlhc_info_t* info,
+               cudaStream_t st) {
+  const int ni = (int)n;
+  unsigned long long* status = a.t.status;
+  CUDA_TRY(launch_status_init(status, st));
+  CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
+  // out = A T^{-1} (substitution, into Q) [+ G = out^T out]
+  auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
+                        const double* l11, double* G) -> int {
+    if (rowsolve_ok(ni)) {
+      CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
+    } else {
+      CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
+      if (pp) CUDA_TRY(launch_pivot_rows(piv, ni, 0, m, l11, Q, ldq, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
+    }
+    return RLHC_OK;
+  };
+  // T = Cholesky(G) with its 1/diag for the next substitution
+  auto chol = [&](double* T, double* rd, int stage) -> int {
+    CUDA_TRY(launch_chol(a.G, ni, T, a.work, stage, status, st, ni <= 128 ? rd : nullptr));
+    const int solve_stage = stage == RLHC_STAGE_CHOL0 ? RLHC_STAGE_SOLVE_Y
+                            : stage == RLHC_STAGE_CHOL1 ? RLHC_STAGE_SOLVE_D : RLHC_STAGE_SOLVE_J;
+    if (ni > 128) CUDA_TRY(launch_rdiag(T, ni, n, rd, solve_stage, status, st));
+    return RLHC_OK;
+  };
+  int rc;
+  if (method == RLHC_CHOLQR2 || method == RLHC_SCHOLQR3) {
+    // [W, Y] = (S)CholeskyQR(X): G = X^T X (+ s I), Y = Cholesky, W = X Y^{-1}
+    CUDA_TRY(launch_gram(X, ldx, m, ni, a.part, a.G, st));
+    if (method == RLHC_SCHOLQR3) CUDA_TRY(launch_shift_diag(a.G, ni, m, st));
+    if ((rc = chol(a.Y, a.rdY, RLHC_STAGE_CHOL0))) return rc;
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
+    if (method == RLHC_CHOLQR2) {  // [Q, Z] = CholeskyQR(W), R = Z Y
+      if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
+      CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, R, st));
+    } else {  // [Q, Z] = CholeskyQR2(W), R = J (D Y)
+      if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G))) return rc;
+      if ((rc = chol(a.J, a.Ji, RLHC_STAGE_CHOL2))) return rc;
+      if ((rc = solve_pass(Q, ldq, a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
+      CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, a.N, st));
+      CUDA_TRY(launch_trmm_uu(a.J, a.N, ni, R, st));
+    }
+  } else if (method == RLHC_LUC2) {
+    // PX = LU, L (into Q), G = L^T L, S = Cholesky(G), Y = S U (diag > 0, R#23), W = X Y^{-1}
+    if ((rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st))) return rc;
+    CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
+    CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+    if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
+    CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
+    if ((rc = chol(a.S, a.Di, RLHC_STAGE_CHOL0))) return rc;
+    CUDA_TRY(launch_trmm_uu(a.S, a.U, ni, a.Y, st));
+    CUDA_TRY(launch_flip_neg_rows(a.Y, ni, st));
+    CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
+    if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
+    CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, R, st));
+  } else {
+    // RHC: K = Omega_2 Omega_1 X, [H, Y] = HouseholderQR(K) (diag > 0, R#22), W = X Y^{-1},
+    // [Q, Z] = CholeskyQR(W), R = Z Y
+    CUDA_TRY(launch_sketch_count(X, ldx, m, ni, 0, (int)s1, seed, a.plan, a.Lt, nullptr, nullptr, st));
+    CUDA_TRY(launch_sketch_gauss(a.Lt, n, s1, ni, 0, (int)s2, seed, 1u, a.part, a.Ls, st));
+    CUDA_TRY(launch_hqr(a.Ls, (int)s2, ni, n, nullptr, a.Y, a.work, status, st));
+    CUDA_TRY(launch_flip_neg_rows(a.Y, ni, st));
+    CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
+    if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
+    CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, R, st));
+  }
+  CUDA_TRY(launch_status_finish(status, info, st));
+  return RLHC_OK;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   const char* pa = (const char*)a;
   const char* pb = (const char*)b;
@@ -311,6 +391,57 @@ size_t rlhc_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   AlgoWs a;
   carve_algo(c, algo, m, n, s_or_s1, s2, cfg, a);
   return c.used;
+}
+
+size_t rlhc_method_workspace_size(int method, int64_t m, int64_t n, int64_t s1, int64_t s2, const rlhc_tslu_cfg* cfgp) {
+  if (method < RLHC_CHOLQR2 || method > RLHC_RHC || n < 1 || m < n) return 0;
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
+  if (!cfg_ok(cfg, n)) return 0;
+  if (method == RLHC_RHC && (s2 < n || s1 < s2 || s1 > m)) return 0;
+  Carver c(nullptr);
+  AlgoWs a;
+  carve_algo(c, RLHC_SSLHC3, m, n, std::max(s1, n), std::max(s2, n), cfg, a);
+  return c.used;
+}
+
+static int method_entry(int method, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2,
+                        uint64_t seed, const rlhc_tslu_cfg* cfgp, double* Q, int64_t ldq, double* R, int64_t* piv,
+                        void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  int rc = check_common(X, m, n, ldx, Q, ldq, R, piv, ws, info);
+  if (rc) return rc;
+  rlhc_tslu_cfg cfg;
+  if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
+  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
+  if (method == RLHC_RHC && (s2 < n || s1 < s2 || s1 > m)) return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
+  size_t need = rlhc_method_workspace_size(method, m, n, s1, s2, &cfg);
+  if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
+  Carver c(ws);
+  AlgoWs a;
+  carve_algo(c, RLHC_SSLHC3, m, n, std::max(s1, n), std::max(s2, n), cfg, a);
+  return run_method(method, X, m, n, ldx, s1, s2, seed, cfg, Q, ldq, R, piv, a, info, (cudaStream_t)stream);
+}
+
+int rlhc_cholqr2(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R, void* ws,
+                 size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  int64_t dummy_piv;
+  return method_entry(RLHC_CHOLQR2, X, m, n, ldx, n, n, 0, nullptr, Q, ldq, R, &dummy_piv, ws, ws_bytes, info, stream);
+}
+int rlhc_scholqr3(const double* X, int64_t m, int64_t n, int64_t ldx, double* Q, int64_t ldq, double* R, void* ws,
+                  size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  int64_t dummy_piv;
+  return method_entry(RLHC_SCHOLQR3, X, m, n, ldx, n, n, 0, nullptr, Q, ldq, R, &dummy_piv, ws, ws_bytes, info,
+                      stream);
+}
+int rlhc_luc2(const double* X, int64_t m, int64_t n, int64_t ldx, const rlhc_tslu_cfg* cfg, double* Q, int64_t ldq,
+              double* R, int64_t* piv, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  return method_entry(RLHC_LUC2, X, m, n, ldx, n, n, 0, cfg, Q, ldq, R, piv, ws, ws_bytes, info, stream);
+}
+int rlhc_rhc(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, int64_t s2, uint64_t seed, double* Q,
+             int64_t ldq, double* R, void* ws, size_t ws_bytes, rlhc_info_t* info, rlhc_stream_t stream) {
+  int64_t dummy_piv;
+  return method_entry(RLHC_RHC, X, m, n, ldx, s1, s2, seed, nullptr, Q, ldq, R, &dummy_piv, ws, ws_bytes, info,
+                      stream);
 }
 
 static int algo_entry(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s_or_s1, int64_t s2,

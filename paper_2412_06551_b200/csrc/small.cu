@@ -63,6 +63,43 @@ cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ comparison-method helpers
+// SCholeskyQR shift (R#21): G += s I with s = 11 (m n u + (n + 1) u) max_k G_kk
+// (||X||_g^2 = the largest squared column norm = the largest diagonal entry of X^T X).
+__global__ void shift_diag_kernel(double* G, int n, int64_t m) {
+  __shared__ double red[32];
+  double g = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) g = fmax(g, G[(int64_t)k * n + k]);
+  for (int o = 16; o; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = g;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    g = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if (threadIdx.x == 0) red[0] = g;
+  }
+  __syncthreads();
+  const double u = 0x1p-53;
+  const double shift = 11.0 * ((double)m * (double)n * u + (double)(n + 1) * u) * red[0];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) G[(int64_t)k * n + k] += shift;
+}
+cudaError_t launch_shift_diag(double* G, int n, int64_t m, cudaStream_t st) {
+  note_launch(); shift_diag_kernel<<<1, 256, 0, st>>>(G, n, m);
+  return cudaGetLastError();
+}
+
+// rows of the upper-triangular T with a negative diagonal negated (diag(T) > 0)
+__global__ void flip_neg_rows_kernel(double* T, int n) {
+  const int k = blockIdx.x;
+  const bool neg = T[(int64_t)k * n + k] < 0.0;
+  if (neg)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) T[(int64_t)k * n + j] = -T[(int64_t)k * n + j];
+}
+cudaError_t launch_flip_neg_rows(double* T, int n, cudaStream_t st) {
+  note_launch(); flip_neg_rows_kernel<<<n, 128, 0, st>>>(T, n);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ upper x upper
 // C = A B for upper-triangular A, B stored with exact zeros below the diagonal: a
 // shared-memory tiled product (16 x 16 tiles, k ascending); the zero parts contribute
