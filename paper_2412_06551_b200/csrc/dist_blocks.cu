@@ -65,12 +65,16 @@ LevelBufs carve_levels(void* ws, int64_t slots, int W) {
   }
   return b;
 }
-// reduce `nslots` slots in buffer `cur` down to one (node levels), returns final buffer index
-int reduce_levels(LevelBufs& b, int cur, int nslots, int arity, int w, int W, cudaStream_t st, int* out_cur) {
+// reduce `nslots` slots in buffer `cur` down to one (node levels), returns final buffer index.
+// rsrc (local rows): the levels read candidate rows from it and only the final slot carries
+// values; else every slot carries values (slots gathered from other ranks)
+int reduce_levels(LevelBufs& b, int cur, int nslots, int arity, int w, int W, cudaStream_t st, int* out_cur,
+                  const RowSrc* rsrc = nullptr) {
   while (nslots > 1) {
-    TRY(launch_tslu_node(W, b.ids[cur], b.cnt[cur], b.vals[cur], nslots, arity, w, b.ids[cur ^ 1], b.cnt[cur ^ 1],
-                         b.vals[cur ^ 1], st));
-    nslots = (nslots + arity - 1) / arity;
+    const int nout = (nslots + arity - 1) / arity;
+    TRY(launch_tslu_node(W, b.ids[cur], b.cnt[cur], rsrc ? nullptr : b.vals[cur], nslots, arity, w, b.ids[cur ^ 1],
+                         b.cnt[cur ^ 1], (rsrc && nout > 1) ? nullptr : b.vals[cur ^ 1], st, nullptr, rsrc));
+    nslots = nout;
     cur ^= 1;
   }
   *out_cur = cur;
@@ -107,9 +111,11 @@ int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0,
   const int W = kw(cfg->panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
   LevelBufs b = carve_levels(ws, nleaves, W);
-  TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0], b.vals[0], st));
+  TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0],
+                       nleaves == 1 ? b.vals[0] : nullptr, st));
+  const RowSrc rsrc{src, lds, row0, (int)p0};
   int cur = 0;
-  int rc = reduce_levels(b, 0, nleaves, cfg->arity, (int)w, W, st, &cur);
+  int rc = reduce_levels(b, 0, nleaves, cfg->arity, (int)w, W, st, &cur, &rsrc);
   if (rc) return rc;
   return copy_slot(b, cur, W, out_ids, out_cnt, out_vals, st);
 }

@@ -25,8 +25,17 @@ struct RootOut {
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
                              const RootOut* root = nullptr, unsigned long long* finite_status = nullptr);
+// Candidate rows of a node: from the slot values (src == nullptr) or, on one process, straight
+// from the panel source by global id: src + (id - row0) * lds + p0 (slots then carry ids only)
+struct RowSrc {
+  const double* src;
+  int64_t lds, row0;
+  int p0;
+};
+// vals may be null (ids-only slots) when the next level reads rows through a RowSrc
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
-                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* root = nullptr);
+                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* root = nullptr,
+                             const RowSrc* rows = nullptr);
 cudaError_t launch_tslu_panel_factor(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w, int n,
                                      const int* root_ids, const int* root_cnt, double* U, int64_t* piv,
                                      uint8_t* chosen, double* lpanel, unsigned long long* status, cudaStream_t st,

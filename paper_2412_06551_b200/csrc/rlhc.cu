@@ -140,14 +140,16 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
     const int w = (int)std::min<int64_t>(cfg.panel, n - p0);
     const double* src = (p0 == 0) ? X : tw;
     const int64_t lds = (p0 == 0) ? ldx : ldtw;
+    // slots carry ids only: every node reads its candidates' rows from src by global id
+    const RowSrc rsrc{src, lds, row0, (int)p0};
     CUDA_TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
-                              t.cnt[0], t.vals[0], st, root_emit && nleaves == 1 ? &ro : nullptr,
+                              t.cnt[0], nullptr, st, root_emit && nleaves == 1 ? &ro : nullptr,
                               check_input && !panels ? t.status : nullptr));
     int cur = 0, nslots = nleaves;
     while (nslots > 1) {
       const int nout = (int)ceil_div<int64_t>(nslots, cfg.arity);
-      CUDA_TRY(launch_tslu_node(W, t.ids[cur], t.cnt[cur], t.vals[cur], nslots, cfg.arity, w, t.ids[cur ^ 1],
-                                t.cnt[cur ^ 1], t.vals[cur ^ 1], st, root_emit && nout == 1 ? &ro : nullptr));
+      CUDA_TRY(launch_tslu_node(W, t.ids[cur], t.cnt[cur], nullptr, nslots, cfg.arity, w, t.ids[cur ^ 1],
+                                t.cnt[cur ^ 1], nullptr, st, root_emit && nout == 1 ? &ro : nullptr, &rsrc));
       nslots = nout;
       cur ^= 1;
     }

@@ -38,12 +38,15 @@ namespace rlhc {
 template <int W, int NW, int RS>
 struct SelSmem {
   double col[W][32 * RS];      // pivot column of step t after its update (candidate s*32 + lane)
+  double col_pad[32 * RS];     // with col: the candidate staging area R x (W + 1) before the select
   double r[W];                 // |1 / pivot| of step t
   unsigned long long bar[W];   // mbarrier of step t (32 arrivals: the owner warp)
   int prow[W];                 // candidate index of the pivot row of step t
   int zero[W];                 // 1: zero pivot column at step t (R#5: no update); -1: pivot < 0
-  int out_src[W];
-  int out_id[W];
+  int out_src[W];              // candidate index of the winner of step t (filled after the loop)
+  int out_id[W];               // its global id
+  int cgid[32 * RS];           // global id of candidate s*32 + lane (node kernel: entry ids first)
+  int perm[32 * RS];           // node kernel: candidate index -> loaded entry (-1: none)
   double* Uout;                // root emission (single panel): U rows, ld = ldu; else null
   int ldu;
 #ifdef RLHC_SEL_TRACE
@@ -105,93 +108,69 @@ RLHC_DEV void sel_update(double (&a)[RS][CW], const double (&l)[RS], const doubl
 }
 
 // Pivot search on column K and publication of step t (owner warp only).  Publishes the
-// updated column itself (before the search), |1/pivot| (as soon as the maximum is known)
-// and the pivot's sign; every warp forms l = col * r, the same IEEE product as the oracle.
+// updated column itself (before the search), |1/pivot| and the pivot's sign; every warp
+// forms l = col * r, the same IEEE product as the oracle.
+//
+// Candidates are held in increasing global-id order (candidate index s*32 + lane: the leaf
+// loads rows in order, the node kernel sorts its candidates), so "the smallest global id
+// among the rows attaining the maximum" (R#4) is the first candidate index attaining it:
+// one ballot per slot, no id reduction.  The maximum of the |a| bit patterns (sign bit
+// cleared: a total order on non-negative doubles that also ranks NaN, which the trailing
+// matrix can hold after a rank deficiency) is taken on the 32-bit halves: the high words,
+// then the low words among the candidates that attain the high maximum.
 template <int W, int NW, int RS, int K>
-RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int t,
-                        SelSmem<W, NW, RS>& sm) {
+RLHC_DEV void sel_pivot(const double (&a)[RS][W / NW], unsigned act, int t, SelSmem<W, NW, RS>& sm) {
   const int lane = lane_id();
 #pragma unroll
   for (int s = 0; s < RS; s++) sm.col[t][s * 32 + lane] = a[s][K];
-  // (1) lane-local max of the |a| bit patterns over the active slots (inactive: -1)
-  long long key[RS], m[RS];
-  unsigned negm = 0;
+  int hi[RS];
+  unsigned lo[RS], negm = 0;
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    // |a| as the bit pattern with the sign bit cleared: non-negative for every value, NaN
-    // included (after an earlier rank deficiency the trailing matrix can hold NaN)
-    key[s] = __double_as_longlong(a[s][K]) & 0x7fffffffffffffffll;
-    m[s] = ((act >> s) & 1u) ? key[s] : -1ll;
+    const int h = __double2hiint(a[s][K]);
+    hi[s] = ((act >> s) & 1u) ? (h & 0x7fffffff) : -1;
+    lo[s] = (unsigned)__double2loint(a[s][K]);
     negm |= (a[s][K] < 0.0 ? 1u : 0u) << s;
   }
+  int mh = hi[0];
 #pragma unroll
-  for (int st = 1; st < RS; st <<= 1) {
-#pragma unroll
-    for (int s = 0; s + st < RS; s += 2 * st) m[s] = m[s + st] > m[s] ? m[s + st] : m[s];
-  }
+  for (int s = 1; s < RS; s++) mh = max(mh, hi[s]);
   SEL_TRACE(t * 32 + 18)
-  // (2) warp max: hi word, then lo word among the lanes attaining the hi word
-  const int hi = (int)(m[0] >> 32);
-  const int mh = __reduce_max_sync(0xffffffffu, hi);
-  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)m[0] : 0u);
-  const long long gb = (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
-  const bool zero = (gb == 0);
-  // |1/pivot| in every lane, branch-free, so it overlaps the id reduction (a lane-0 branch
-  // would serialise it into the warp's critical path); the ballot below consumes it
-  const double rabs = __drcp_rn(__longlong_as_double(gb));
-  // (3) smallest global id among the active rows attaining the maximum
-  int id[RS];
-#pragma unroll
-  for (int s = 0; s < RS; s++) id[s] = (((act >> s) & 1u) && key[s] == gb) ? gid[s] : INT_MAX;
-#pragma unroll
-  for (int st = 1; st < RS; st <<= 1) {
-#pragma unroll
-    for (int s = 0; s + st < RS; s += 2 * st) id[s] = min(id[s], id[s + st]);
-  }
-  const int pid = __reduce_min_sync(0xffffffffu, id[0]);
-  // (4) the pivot's lane, slot and sign (global ids are unique)
-  unsigned hm = 0;
-#pragma unroll
-  for (int s = 0; s < RS; s++) hm |= (gid[s] == pid ? 1u : 0u) << s;
-  hm &= act;
-  const unsigned wb = __ballot_sync(0xffffffffu, hm != 0 && rabs != -1.0);  // (rabs >= 0: always true)
-  const unsigned nb = __ballot_sync(0xffffffffu, (hm & negm) != 0);
+  mh = __reduce_max_sync(0xffffffffu, mh);
   SEL_TRACE(t * 32 + 19)
-  if (hm != 0 && lane == __ffs(wb) - 1) {
-    const int src = (__ffs(hm) - 1) * 32 + lane;
-    sm.prow[t] = src;
-    sm.out_src[t] = src;
-    sm.out_id[t] = pid;
-  }
-  if (wb == 0) {  // unreachable with finite keys; keeps the step well defined regardless
-    const unsigned ab = __ballot_sync(0xffffffffu, act != 0);
-    const int fl = ab ? __ffs(ab) - 1 : 0;
-    if (lane == fl) {
-      const int slot = act ? __ffs(act) - 1 : 0;
-      int g = INT_MAX;
+  unsigned ml = 0;
 #pragma unroll
-      for (int s = 0; s < RS; s++) g = (s == slot) ? gid[s] : g;
-      sm.prow[t] = slot * 32 + lane;
-      sm.out_src[t] = slot * 32 + lane;
-      sm.out_id[t] = g;
-    }
-  }
-  if (lane == 0) {
-    sm.r[t] = rabs;
-    sm.zero[t] = zero ? 1 : (nb ? -1 : 0);  // 1: zero column; -1: negative pivot
-    if (sm.Uout) {  // U(t, t) = the pivot itself (|pivot| bits and its sign)
-      const double pv = __longlong_as_double(gb);
-      sm.Uout[(int64_t)t * sm.ldu + t] = nb ? -pv : pv;
-    }
-  }
-  __syncwarp();
+  for (int s = 0; s < RS; s++) ml = max(ml, hi[s] == mh ? lo[s] : 0u);
+  ml = __reduce_max_sync(0xffffffffu, ml);
   SEL_TRACE(t * 32 + 20)
+  const long long gb = (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
+  // |1/pivot| (independent of which row attains it), branch-free so that it overlaps the
+  // ballots below; exponents outside its window take __drcp_rn after them
+  const double pabs = __longlong_as_double(gb);
+  double rabs = rcp_newton(pabs);
+  // smallest candidate index s*32 + lane attaining the maximum (an active candidate always
+  // does): this lane's first matching slot, then one warp minimum
+  unsigned mm = 0;
+#pragma unroll
+  for (int s = 0; s < RS; s++) mm |= (hi[s] == mh && lo[s] == ml ? 1u : 0u) << s;
+  const int pidx = __reduce_min_sync(0xffffffffu, mm ? (__ffs(mm) - 1) * 32 + lane : INT_MAX);
+  SEL_TRACE(t * 32 + 21)
+  if (!rcp_newton_ok(mh)) rabs = rcp_slow(pabs);  // warp-uniform, rare
+  const bool neg = (negm >> (pidx >> 5)) & 1u;    // meaningful in the pivot's lane
+  if (lane == (pidx & 31)) {
+    sm.prow[t] = pidx;
+    sm.r[t] = rabs;
+    sm.zero[t] = gb == 0 ? 1 : (neg ? -1 : 0);  // 1: zero column (R#5); -1: negative pivot
+  }
+  SEL_TRACE(t * 32 + 22)
   mbar_arrive(&sm.bar[t]);
+  if (lane == (pidx & 31) && sm.Uout)  // root emission: U(t, t) = the pivot (|pivot| and sign)
+    sm.Uout[(int64_t)t * sm.ldu + t] = neg ? -pabs : pabs;
 }
 
 // Step t (local pivot column K of warp t % NW): consume step t-1, own step t if mine.
 template <int W, int NW, int RS, int K>
-RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int t, bool own,
+RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, int t, bool own,
                        SelSmem<W, NW, RS>& sm) {
   constexpr int CW = W / NW;
   const int lane = lane_id();
@@ -221,7 +200,7 @@ RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[
       for (int s = 0; s < RS; s++) a[s][K] = __fma_rn(-l[s], uk, a[s][K]);
     }
     SEL_TRACE(t * 32 + 16)
-    sel_pivot<W, NW, RS, K>(a, act, gid, t, sm);
+    sel_pivot<W, NW, RS, K>(a, act, t, sm);
     SEL_TRACE(t * 32 + 17)
     if (upd) {
       sel_row<RS, CW, K + 1>(a, pslot, plane, u);
@@ -250,21 +229,20 @@ RLHC_DEV void sel_step(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[
 // Steps t = K*NW + j, j < NW (local pivot column K), then the next group.
 template <int W, int NW, int RS, int K>
 struct SelGroup {
-  static RLHC_DEV void run(double (&a)[RS][W / NW], unsigned& act, const int (&gid)[RS], int steps,
-                           SelSmem<W, NW, RS>& sm) {
+  static RLHC_DEV void run(double (&a)[RS][W / NW], unsigned& act, int steps, SelSmem<W, NW, RS>& sm) {
     if (K * NW >= steps) return;
     const int q = warp_id();
 #pragma unroll 1
     for (int j = 0; j < NW; j++) {
       const int t = K * NW + j;
-      if (t < steps) sel_step<W, NW, RS, K>(a, act, gid, t, j == q, sm);
+      if (t < steps) sel_step<W, NW, RS, K>(a, act, t, j == q, sm);
     }
-    SelGroup<W, NW, RS, K + 1>::run(a, act, gid, steps, sm);
+    SelGroup<W, NW, RS, K + 1>::run(a, act, steps, sm);
   }
 };
 template <int W, int NW, int RS>
 struct SelGroup<W, NW, RS, W / NW> {
-  static RLHC_DEV void run(double (&)[RS][W / NW], unsigned&, const int (&)[RS], int, SelSmem<W, NW, RS>&) {}
+  static RLHC_DEV void run(double (&)[RS][W / NW], unsigned&, int, SelSmem<W, NW, RS>&) {}
 };
 
 // Initialise the step barriers; call before the candidate loads (gepp_select's first
@@ -303,16 +281,27 @@ RLHC_DEV void sel_root_finish(const SelSmem<W, NW, RS>& sm, int steps, int w, co
 
 // GEPP selection (definition: oracle gepp_select / DESIGN.md R#4-R#5).
 // a[s][k]: this lane's values (column q + NW k); act: bit s = row (lane + 32 s) is an active
-// candidate; gid[s]: global ids.  Returns the number of steps; sm.out_id / sm.out_src hold
-// the winners (out_src = candidate index lane + 32 s).
+// candidate; gid[s]: global ids, increasing in the candidate index lane + 32 s over the
+// active candidates (the tie rule relies on it).  Returns the number of steps; sm.out_id /
+// sm.out_src hold the winners (out_src = candidate index lane + 32 s).
 template <int W, int NW, int RS>
 RLHC_DEV int gepp_select(double (&a)[RS][W / NW], unsigned act, const int (&gid)[RS], int w,
                          SelSmem<W, NW, RS>& sm) {
+  if (warp_id() == 0) {
+#pragma unroll
+    for (int s = 0; s < RS; s++) sm.cgid[s * 32 + lane_id()] = gid[s];
+  }
   __syncthreads();  // barrier initialisation visible to every warp
   int c = __popc(act);
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   const int steps = min(c, w);
-  SelGroup<W, NW, RS, 0>::run(a, act, gid, steps, sm);
+  SelGroup<W, NW, RS, 0>::run(a, act, steps, sm);
+  __syncthreads();
+  for (int t = threadIdx.x; t < steps; t += blockDim.x) {
+    const int src = sm.prow[t];
+    sm.out_src[t] = src;
+    sm.out_id[t] = sm.cgid[src];
+  }
   __syncthreads();
   return steps;
 }

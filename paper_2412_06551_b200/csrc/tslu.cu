@@ -13,6 +13,52 @@
 
 namespace rlhc {
 
+#ifdef RLHC_TSLU_TRACE
+// probe builds only (tools/probe/ptslu.cu): per-block phase timestamps
+__device__ unsigned long long g_tslu_trace[4096 * 8];
+// distinct trace rows per level of the cfg2 tree (grids of 256, 64, 16, 4, 1 blocks)
+__device__ __forceinline__ int tslu_trace_base(int g) {
+  return g == 256 ? 0 : g == 64 ? 256 : g == 16 ? 320 : g == 4 ? 336 : g == 1 ? 340 : 0;
+}
+#define TSLU_TRACE(k)                                                                     \
+  if (threadIdx.x == 0) {                                                                 \
+    unsigned long long t_;                                                                \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+    g_tslu_trace[(blockIdx.x + tslu_trace_base(gridDim.x)) * 8 + (k)] = t_;               \
+  }
+#else
+#define TSLU_TRACE(k)
+#endif
+
+// Candidate staging: the R x w panel block is read row-contiguously (coalesced) into shared
+// memory -- the step-column area, free until the select starts -- with row stride W + 1
+// (conflict-free column reads), then each warp takes its round-robin columns into registers.
+template <int W, int NW, int RS>
+RLHC_DEV double* sel_stage(SelSmem<W, NW, RS>& sm) { return &sm.col[0][0]; }
+template <int W, int NW, int RS>
+RLHC_DEV void sel_fill(const double* stg, double (&a)[RS][W / NW]) {
+  const int lane = lane_id(), wp = warp_id();
+#pragma unroll
+  for (int s = 0; s < RS; s++)
+#pragma unroll
+    for (int c = 0; c < W / NW; c++) a[s][c] = stg[(s * 32 + lane) * (W + 1) + wp + NW * c];
+}
+// ov (slot values, row stride W) <- the winners' rows: a warp per row, lanes along columns
+template <int W, int NW, typename RowPtr>
+RLHC_DEV void write_slot_rows(double* __restrict__ ov, int steps, int w, RowPtr row_of) {
+  const int lane = lane_id(), wp = warp_id();
+#pragma unroll
+  for (int k = 0; k < (W + NW - 1) / NW; k++) {
+    const int q = wp + NW * k;
+    if (q < steps) {
+      const double* src = row_of(q);
+#pragma unroll
+      for (int c0 = 0; c0 < W; c0 += 32)
+        if (c0 + lane < w) ov[q * W + c0 + lane] = src[c0 + lane];
+    }
+  }
+}
+
 // Leaf select: leaf = global row block [leaf*R, leaf*R + R) of the LOCAL rows
 // (global id = row0 + local row).  src: current values (X for the first panel, the
 // trailing matrix afterwards), panel columns [p0, p0 + w).  Output level slot = leaf.
@@ -21,90 +67,149 @@ __global__ void __launch_bounds__(32 * NW, 1)
 tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals, RootOut root, unsigned long long* finite_status) {
-  constexpr int R = 32 * RS, CW = W / NW;
+  constexpr int R = 32 * RS;
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
+  TSLU_TRACE(0)
   sel_init(sm, root.U, root.n);
-  const int lane = lane_id(), wp = warp_id();
-  double a[RS][CW];
+  const int lane = lane_id();
+  const int64_t rb = (int64_t)blockIdx.x * R;
+  double* stg = sel_stage(sm);
+  // staging: a warp per row, lanes along the columns, every copy in flight at once
+  // (cp.async), rows past the end and columns past w zero-filled
+#pragma unroll 4
+  for (int q = warp_id(); q < R; q += NW) {
+    const int64_t r = rb + q;
+#pragma unroll
+    for (int c0 = 0; c0 < W; c0 += 32) {
+      const int c = c0 + lane;
+      if (c < W) {
+        const bool in = r < rows && c < w;
+        cp_async8(stg + q * (W + 1) + c, in ? src + r * lds + p0 + c : src, in ? 8 : 0);
+      }
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  // single-panel pipelines fold the input check (check_finite_kernel's semantics: the
+  // smallest non-finite element index i*n + j wins) into this pass over X
+  if (finite_status) {
+    for (int idx = threadIdx.x; idx < R * W; idx += blockDim.x) {
+      const int q = idx / W, c = idx - q * W;
+      if (rb + q < rows && c < w && !isfinite(stg[q * (W + 1) + c]))
+        report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, (rb + q) * w + c);
+    }
+  }
   int gid[RS];
   unsigned act = 0;
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    const int64_t r = (int64_t)blockIdx.x * R + s * 32 + lane;
+    const int64_t r = rb + s * 32 + lane;
     const bool ok = r < rows && !(chosen && chosen[r]);
     act |= (ok ? 1u : 0u) << s;
     gid[s] = (int)(row0 + r);
-    const double* p = src + r * lds + p0 + wp;
-#pragma unroll
-    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
   }
-  // single-panel pipelines fold the input check (check_finite_kernel's semantics: the
-  // smallest non-finite element index i*n + j wins) into this pass over X
-  if (finite_status) {
-#pragma unroll
-    for (int s = 0; s < RS; s++)
-#pragma unroll
-      for (int c = 0; c < CW; c++)
-        if (!isfinite(a[s][c]))
-          report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT,
-                 ((int64_t)blockIdx.x * R + s * 32 + lane) * w + wp + NW * c);
-  }
+  double a[RS][W / NW];
+  sel_fill<W, NW, RS>(stg, a);
+  TSLU_TRACE(2)
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
+  TSLU_TRACE(3)
   if (root.U) sel_root_finish(sm, steps, w, root);
   int* oi = out_ids + (size_t)blockIdx.x * W;
-  double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
   for (int e = threadIdx.x; e < W; e += blockDim.x) oi[e] = e < steps ? sm.out_id[e] : -1;
-  for (int idx = threadIdx.x; idx < steps * w; idx += blockDim.x) {
-    int e = idx / w, c = idx - e * w;
-    int64_t rr = (int64_t)blockIdx.x * R + sm.out_src[e];
-    ov[e * W + c] = src[rr * lds + p0 + c];
-  }
+  if (out_vals)
+    write_slot_rows<W, NW>(out_vals + (size_t)blockIdx.x * W * W, steps, w,
+                           [&](int q) { return src + (rb + sm.out_src[q]) * lds + p0; });
+  TSLU_TRACE(4)
 }
 
 // Node select: node = children [node*arity, node*arity + arity) of the level below;
-// candidate index q -> child (q / w), entry (q % w).  Values are the stored current
-// panel values of the candidates (not the eliminated ones).
+// loaded entry j -> child (j / w), entry (j % w).  The entries are sorted by global id into
+// the candidate order (select.cuh's tie rule; slots list their winners in pivot order).
+// Values are the stored current panel values of the candidates (not the eliminated ones).
 template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
 tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt, const double* __restrict__ in_vals,
                  int nslots_in, int arity, int w, int* __restrict__ out_ids, int* __restrict__ out_cnt,
-                 double* __restrict__ out_vals, RootOut root) {
-  constexpr int CW = W / NW;
+                 double* __restrict__ out_vals, RootOut root, RowSrc rsrc) {
+  constexpr int R = 32 * RS;
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
+  TSLU_TRACE(0)
   sel_init(sm, root.U, root.n);
-  const int lane = lane_id(), wp = warp_id();
+  const int lane = lane_id();
   const int c0 = blockIdx.x * arity;
-  double a[RS][CW];
+  // entry ids (INT_MAX: no entry) in cgid, which the select first writes after this
+  // kernel's last read of them (a barrier apart)
+  int* eid = sm.cgid;
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    const int ci = j / w, e = j - ci * w, child = c0 + ci;
+    const bool ok = ci < arity && child < nslots_in && e < in_cnt[child];
+    eid[j] = ok ? in_ids[child * W + e] : INT_MAX;
+    sm.perm[j] = -1;
+  }
+  __syncthreads();
+  // rank of each entry among the valid ones (ids are unique): candidate order = id order
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    const int my = eid[j];
+    if (my == INT_MAX) continue;
+    int rank = 0;
+    const int4* e4 = reinterpret_cast<const int4*>(eid);
+#pragma unroll 8
+    for (int k4 = 0; k4 < R / 4; k4++) {
+      const int4 v = e4[k4];
+      rank += (v.x < my) + (v.y < my) + (v.z < my) + (v.w < my);
+    }
+    sm.perm[rank] = j;
+  }
+  __syncthreads();
+  TSLU_TRACE(1)
   int gid[RS];
   unsigned act = 0;
 #pragma unroll
   for (int s = 0; s < RS; s++) {
-    const int qi = s * 32 + lane;
-    const int ci = qi / w, e = qi - ci * w;
-    const int child = c0 + ci;
-    const bool ok = ci < arity && child < nslots_in && e < in_cnt[child < nslots_in ? child : 0];
-    act |= (ok ? 1u : 0u) << s;
-    const int slot = child * W + e;
-    gid[s] = ok ? in_ids[slot] : INT_MAX;
-    const double* p = in_vals + (size_t)(ok ? slot : 0) * W + wp;
-#pragma unroll
-    for (int c = 0; c < CW; c++) a[s][c] = (ok && wp + NW * c < w) ? p[NW * c] : 0.0;
+    const int j = sm.perm[s * 32 + lane];
+    act |= (j >= 0 ? 1u : 0u) << s;
+    gid[s] = j >= 0 ? eid[j] : INT_MAX;
   }
+  double* stg = sel_stage(sm);
+#pragma unroll 4
+  for (int q = warp_id(); q < R; q += NW) {
+    const int j = sm.perm[q];
+    const int ci = j / w, e = j - ci * w;
+    const double* row = rsrc.src ? rsrc.src + (j >= 0 ? (int64_t)eid[j] - rsrc.row0 : 0) * rsrc.lds + rsrc.p0
+                                 : in_vals + (size_t)((c0 + ci) * W + e) * W;
+#pragma unroll
+    for (int cc = 0; cc < W; cc += 32) {
+      const int c = cc + lane;
+      if (c < W) {
+        const bool in = j >= 0 && c < w;
+        cp_async8(stg + q * (W + 1) + c, in ? row + c : (const double*)in_cnt, in ? 8 : 0);  // 0 bytes: no read
+      }
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  double a[RS][W / NW];
+  sel_fill<W, NW, RS>(stg, a);
+  TSLU_TRACE(2)
   const int steps = gepp_select<W, NW, RS>(a, act, gid, w, sm);
+  TSLU_TRACE(3)
   if (root.U) sel_root_finish(sm, steps, w, root);
   int* oi = out_ids + (size_t)blockIdx.x * W;
-  double* ov = out_vals + (size_t)blockIdx.x * W * W;
   if (threadIdx.x == 0) out_cnt[blockIdx.x] = steps;
   for (int q = threadIdx.x; q < W; q += blockDim.x) oi[q] = q < steps ? sm.out_id[q] : -1;
-  for (int idx = threadIdx.x; idx < steps * w; idx += blockDim.x) {
-    int q = idx / w, c = idx - q * w;
-    const int qi = sm.out_src[q];
-    const int ci = qi / w, e = qi - ci * w;
-    ov[q * W + c] = in_vals[(size_t)((c0 + ci) * W + e) * W + c];
-  }
+  if (out_vals)
+    write_slot_rows<W, NW>(out_vals + (size_t)blockIdx.x * W * W, steps, w, [&](int q) {
+      if (rsrc.src) return rsrc.src + ((int64_t)sm.out_id[q] - rsrc.row0) * rsrc.lds + rsrc.p0;
+      const int j = sm.perm[sm.out_src[q]];
+      const int ci = j / w, e = j - ci * w;
+      return in_vals + (size_t)((c0 + ci) * W + e) * W;
+    });
+  TSLU_TRACE(4)
 }
 
 // Panel factor (single CTA): the root's w winners become pivots p0..p0+w-1.  Their
@@ -232,7 +337,8 @@ static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_
 }
 template <int W, int NW, int RS>
 static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity, int w,
-                            int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut& root) {
+                            int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut& root,
+                            const RowSrc& rsrc) {
   int nout = ceil_div(nin, arity);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
   static bool attr = false;
@@ -242,7 +348,7 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
     attr = true;
   }
   note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, smem, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt,
-                                                                            vals, root);
+                                                                            vals, root, rsrc);
   return cudaGetLastError();
 }
 
@@ -261,12 +367,14 @@ cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tslu_node(int W, const int* in_ids, const int* in_cnt, const double* in_vals, int nin, int arity,
-                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* rootp) {
+                             int w, int* ids, int* cnt, double* vals, cudaStream_t st, const RootOut* rootp,
+                             const RowSrc* rowsp) {
   const RootOut root = rootp ? *rootp : RootOut{};
+  const RowSrc rsrc = rowsp ? *rowsp : RowSrc{};
   switch (W) {
-    case 16: return run_node<16, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
-    case 32: return run_node<32, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
-    case 64: return run_node<64, 8, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root);
+    case 16: return run_node<16, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root, rsrc);
+    case 32: return run_node<32, 8, 16>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root, rsrc);
+    case 64: return run_node<64, 8, 8>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt, vals, st, root, rsrc);
   }
   return cudaErrorInvalidValue;
 }

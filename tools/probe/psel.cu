@@ -56,10 +56,11 @@ int main() {
   for (int s = 0; s < 64; s++) {
     int q = s % NW;
     long long* r = &t[s * 32];
-    // owner: wake (2q), pivot start (16), pivot end (17), done (2q+1)
-    printf("t=%2d own=%d wake=%6lld piv0=%6lld tree=%4lld red=%4lld pub=%4lld arr=%4lld done=%6lld | ", s, q,
-           r[2 * q] ? r[2 * q] - t0 : -1, r[16] - t0, r[18] - r[16], r[19] - r[18], r[20] - r[19], r[17] - r[20],
-           r[2 * q + 1] - t0);
+    // owner: wake (2q), pivot start (16), keys+tree (->18), redux hi (->19), lo (->20),
+    // ballots (->21), publish (->22), pivot end (17), done (2q+1)
+    printf("t=%2d own=%d wake=%6lld piv0=%6lld tree=%4lld rhi=%4lld rlo=%4lld minidx=%4lld pub=%4lld end=%4lld done=%6lld | ",
+           s, q, r[2 * q] ? r[2 * q] - t0 : -1, r[16] - t0, r[18] - r[16], r[19] - r[18], r[20] - r[19],
+           r[21] - r[20], r[22] - r[21], r[17] - r[22], r[2 * q + 1] - t0);
     for (int w = 0; w < NW; w++) printf("%6lld ", r[2 * w + 1] ? r[2 * w + 1] - t0 : -1);
     printf("\n");
   }
