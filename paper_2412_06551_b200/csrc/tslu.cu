@@ -71,6 +71,7 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
   TSLU_TRACE(0)
+  pdl_trigger();
   sel_init(sm, root.U, root.n);
   const int lane = lane_id();
   const int64_t rb = (int64_t)blockIdx.x * R;
@@ -138,7 +139,9 @@ tslu_node_kernel(const int* __restrict__ in_ids, const int* __restrict__ in_cnt,
   extern __shared__ __align__(16) unsigned char sel_raw[];
   SelSmem<W, NW, RS>& sm = *reinterpret_cast<SelSmem<W, NW, RS>*>(sel_raw);
   TSLU_TRACE(0)
+  pdl_trigger();
   sel_init(sm, root.U, root.n);
+  pdl_wait();  // the level below (launched before this one) has completed
   const int lane = lane_id();
   const int c0 = blockIdx.x * arity;
   // entry ids (INT_MAX: no entry) in cgid, which the select first writes after this
@@ -347,9 +350,9 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
     cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  note_launch(); tslu_node_kernel<W, NW, RS><<<nout, 32 * NW, smem, st>>>(in_ids, in_cnt, in_vals, nin, arity, w, ids, cnt,
-                                                                            vals, root, rsrc);
-  return cudaGetLastError();
+  note_launch();
+  return launch_pdl(tslu_node_kernel<W, NW, RS>, dim3(nout), dim3(32 * NW), smem, st, in_ids, in_cnt, in_vals, nin,
+                    arity, w, ids, cnt, vals, root, rsrc);
 }
 
 cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
