@@ -485,44 +485,68 @@ static cudaError_t run_rowsolve(const double* A, int64_t lda, int64_t rows, int 
 
 // ------------------------------------------------------------------ blocked TRSM (n > 64)
 // C_out = C_in - A B (rows x N, K <= 64) on DMMA, the chain over k in increasing order:
-// the trailing update of one 64-column panel of the blocked substitution.  Tile 64 x 64,
-// 4 warps (32 x 32 each); A (64 x K) and B (K x 64) staged with cp.async.
-constexpr int GU_T = 64;
+// Cout = Cin - A B (rows x N, A rows x K, B K x N) on DMMA: the updates of the blocked
+// substitution and factorizations.  Every element is Cin followed by the fma chain over
+// k = 0, 1, ..., K-1 in increasing order (DMMA m8n8k4 == the fma chain k0..k3; zero-padded k
+// leaves the value unchanged), i.e. the substitution's own chain.  CTA tile 128 x 64, 8 warps
+// of 32 x 32, K chunks of 32 double-buffered with cp.async, 2 CTAs per SM.
+constexpr int GS_M = 128, GS_N = 64, GS_K = 32;
+struct GemmSmem {
+  double A[2][GS_M][GS_K + 4];
+  double B[2][GS_K][GS_N + 4];
+};
 
-__global__ void __launch_bounds__(128)
-gemm_update_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* __restrict__ A,
-                   int64_t lda, const double* __restrict__ B, int64_t ldb, int64_t rows, int K, int N) {
-  constexpr int KC = 32;  // k chunk
-  __shared__ __align__(16) double As[GU_T][KC + 4];
-  __shared__ __align__(16) double Bs[KC][GU_T + 4];
-  const int64_t r0 = (int64_t)blockIdx.x * GU_T;
-  const int c0 = blockIdx.y * GU_T;
+__global__ void __launch_bounds__(256, 2)
+gemm_sub_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* __restrict__ A,
+                int64_t lda, const double* __restrict__ B, int64_t ldb, int64_t rows, int K, int N) {
+  extern __shared__ __align__(16) unsigned char gs_raw[];
+  GemmSmem& sm = *reinterpret_cast<GemmSmem*>(gs_raw);
+  const int64_t r0 = (int64_t)blockIdx.x * GS_M;
+  const int c0 = blockIdx.y * GS_N;
   const int lane = lane_id(), w = warp_id();
   const int g = lane >> 2, t = lane & 3;
   const int wi = (w >> 1) * 32, wj = (w & 1) * 32;
   const bool al_a = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
   const bool al_b = ((ldb & 1) == 0) && ((((uintptr_t)B) & 15) == 0);
-  auto load_chunk = [&](int kc) {
-    for (int idx = threadIdx.x; idx < GU_T * (KC / 2); idx += blockDim.x) {  // A: 64 rows x KC k
-      const int r = idx / (KC / 2), c = 2 * (idx % (KC / 2));
+  const bool full_rows = r0 + GS_M <= rows, full_cols = c0 + GS_N <= N;
+  auto load_chunk = [&](int st, int kc) {
+    const bool full_k = kc + GS_K <= K;
+    // A: 128 rows x 32 k = 2048 pairs, 8 per thread
+#pragma unroll
+    for (int i = 0; i < GS_M * GS_K / 2 / 256; i++) {
+      const int idx = threadIdx.x + 256 * i;
+      const int r = idx / (GS_K / 2), c = 2 * (idx % (GS_K / 2));
       const int64_t gr = r0 + r;
       const int k = kc + c;
-      double* dst = &As[r][c];
+      double* dst = &sm.A[st][r][c];
       const double* src = A + gr * lda + k;
-      if (gr < rows && al_a && k + 1 < K) cp_async16(dst, src);
-      else { dst[0] = (gr < rows && k < K) ? src[0] : 0.0; dst[1] = (gr < rows && k + 1 < K) ? src[1] : 0.0; }
+      if (al_a && full_rows && full_k) {
+        cp_async16(dst, src);
+      } else {
+        const bool rok = gr < rows;
+        cp_async8(dst, (rok && k < K) ? src : A, (rok && k < K) ? 8 : 0);
+        cp_async8(dst + 1, (rok && k + 1 < K) ? src + 1 : A, (rok && k + 1 < K) ? 8 : 0);
+      }
     }
-    for (int idx = threadIdx.x; idx < KC * (GU_T / 2); idx += blockDim.x) {  // B: KC k x 64 columns
-      const int r = idx / (GU_T / 2), c = 2 * (idx % (GU_T / 2));
+    // B: 32 k x 64 columns = 1024 pairs, 4 per thread
+#pragma unroll
+    for (int i = 0; i < GS_K * GS_N / 2 / 256; i++) {
+      const int idx = threadIdx.x + 256 * i;
+      const int r = idx / (GS_N / 2), c = 2 * (idx % (GS_N / 2));
       const int k = kc + r;
-      double* dst = &Bs[r][c];
+      double* dst = &sm.B[st][r][c];
       const double* src = B + (int64_t)k * ldb + c0 + c;
-      if (k < K && al_b && c0 + c + 1 < N) cp_async16(dst, src);
-      else { dst[0] = (k < K && c0 + c < N) ? src[0] : 0.0; dst[1] = (k < K && c0 + c + 1 < N) ? src[1] : 0.0; }
+      if (al_b && full_cols && full_k) {
+        cp_async16(dst, src);
+      } else {
+        const bool kok = k < K;
+        cp_async8(dst, (kok && c0 + c < N) ? src : B, (kok && c0 + c < N) ? 8 : 0);
+        cp_async8(dst + 1, (kok && c0 + c + 1 < N) ? src + 1 : B, (kok && c0 + c + 1 < N) ? 8 : 0);
+      }
     }
     cp_async_commit();
   };
-  load_chunk(0);
+  if (K > 0) load_chunk(0, 0);
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; a++)
@@ -533,22 +557,29 @@ gemm_update_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, 
       acc[a][b][0] = (gr < rows && c < N) ? Cin[gr * ldci + c] : 0.0;
       acc[a][b][1] = (gr < rows && c + 1 < N) ? Cin[gr * ldci + c + 1] : 0.0;
     }
-  for (int kc = 0; kc < K; kc += KC) {
-    cp_async_wait_all();
+  int st = 0;
+  for (int kc = 0; kc < K; kc += GS_K) {
+    if (kc + GS_K < K) {
+      load_chunk(st ^ 1, kc + GS_K);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();
-    for (int k0 = 0; k0 < KC && kc + k0 < K; k0 += 4) {
+#pragma unroll
+    for (int k0 = 0; k0 < GS_K; k0 += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; a++) af[a] = -As[wi + a * 8 + g][k0 + t];
+      for (int a = 0; a < 4; a++) af[a] = -sm.A[st][wi + a * 8 + g][k0 + t];
 #pragma unroll
-      for (int b = 0; b < 4; b++) bf[b] = Bs[k0 + t][wj + b * 8 + g];
+      for (int b = 0; b < 4; b++) bf[b] = sm.B[st][k0 + t][wj + b * 8 + g];
 #pragma unroll
       for (int a = 0; a < 4; a++)
 #pragma unroll
         for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
     __syncthreads();
-    if (kc + KC < K) load_chunk(kc + KC);
+    st ^= 1;
   }
 #pragma unroll
   for (int a = 0; a < 4; a++)
@@ -566,9 +597,16 @@ gemm_update_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, 
 cudaError_t launch_gemm_update(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
                                int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, cudaStream_t st) {
   if (rows <= 0 || N <= 0) return cudaSuccess;
-  dim3 grid((unsigned)ceil_div<int64_t>(rows, GU_T), (unsigned)ceil_div(N, GU_T));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(GemmSmem));
+    if (e) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div<int64_t>(rows, GS_M), (unsigned)ceil_div(N, GS_N));
   note_launch();
-  gemm_update_kernel<<<grid, 128, 0, st>>>(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N);
+  gemm_sub_kernel<<<grid, 256, sizeof(GemmSmem), st>>>(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N);
   return cudaGetLastError();
 }
 
@@ -579,23 +617,23 @@ cudaError_t launch_gemm_update(const double* Cin, int64_t ldci, double* Cout, in
 cudaError_t launch_trsm_blocked(const double* A, int64_t lda, int64_t rows, int n, int nsub, const double* T,
                                 int64_t ldt, const double* rdiag, double* out, int64_t ldo, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
+  // left-looking: panel p0 = A(:, p0:p0+w) - out(:, 0:p0) T(0:p0, p0:p0+w) (one GEMM, k in
+  // increasing order -- the same chain as updating panel by panel), then its substitution
   for (int p0 = 0; p0 < nsub; p0 += 64) {
     const int w = std::min(64, nsub - p0);
-    const double* src = (p0 == 0) ? A : out;
-    const int64_t lds_ = (p0 == 0) ? lda : ldo;
-    cudaError_t e = run_rowsolve<false>(src + p0, lds_, rows, w, T + (int64_t)p0 * ldt + p0, ldt, rdiag + p0,
-                                        out + p0, ldo, nullptr, st);
-    if (e) return e;
-    const int N = n - p0 - w;
-    if (N > 0) {
-      dim3 grid((unsigned)ceil_div<int64_t>(rows, GU_T), (unsigned)ceil_div(N, GU_T));
-      note_launch();
-      gemm_update_kernel<<<grid, 128, 0, st>>>(src + p0 + w, lds_, out + p0 + w, ldo, out + p0, ldo,
-                                               T + (int64_t)p0 * ldt + p0 + w, ldt, rows, w, N);
-      e = cudaGetLastError();
+    cudaError_t e;
+    if (p0 > 0) {
+      e = launch_gemm_update(A + p0, lda, out + p0, ldo, out, ldo, T + p0, ldt, rows, p0, w, st);
       if (e) return e;
     }
+    const double* src = (p0 == 0) ? A : out;
+    const int64_t lds_ = (p0 == 0) ? lda : ldo;
+    e = run_rowsolve<false>(src + p0, lds_, rows, w, T + (int64_t)p0 * ldt + p0, ldt, rdiag + p0, out + p0, ldo,
+                            nullptr, st);
+    if (e) return e;
   }
+  // columns past nsub receive the updates of every substituted column
+  if (nsub < n) return launch_gemm_update(A + nsub, lda, out + nsub, ldo, out, ldo, T + nsub, ldt, rows, nsub, n - nsub, st);
   return cudaSuccess;
 }
 
