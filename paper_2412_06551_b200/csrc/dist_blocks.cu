@@ -88,7 +88,8 @@ int copy_slot(LevelBufs& b, int cur, int W, int* out_ids, int* out_cnt, double* 
 }
 bool cfg_valid(const rlhc_tslu_cfg* c, int64_t w) {
   return c && c->panel >= 1 && c->panel <= 64 && w >= 1 && w <= c->panel && c->arity >= 2 &&
-         c->leaf_rows == select_rows(kw(c->panel)) && (int64_t)c->arity * c->panel <= select_rows(kw(c->panel));
+         c->leaf_rows >= 1 && c->leaf_rows <= select_rows(kw(c->panel)) &&
+         (int64_t)c->arity * c->panel <= select_rows(kw(c->panel));
 }
 }  // namespace
 
@@ -111,7 +112,7 @@ int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0,
   const int W = kw(cfg->panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
   LevelBufs b = carve_levels(ws, nleaves, W);
-  TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0],
+  TRY(launch_tslu_leaf(W, cfg->leaf_rows, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0],
                        nleaves == 1 ? b.vals[0] : nullptr, st));
   const RowSrc rsrc{src, lds, row0, (int)p0};
   int cur = 0;

@@ -5,6 +5,8 @@
 
 #include <string>
 
+#include "../../include/rlhc.h"
+
 namespace rlhc {
 
 int select_rows(int W);
@@ -22,7 +24,7 @@ struct RootOut {
   unsigned long long* status;
   int n;
 };
-cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+cudaError_t launch_tslu_leaf(int W, int64_t leaf_rows, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
                              const RootOut* root = nullptr, unsigned long long* finite_status = nullptr);
 // Candidate rows of a node: from the slot values (src == nullptr) or, on one process, straight
@@ -44,6 +46,24 @@ cudaError_t launch_l11_fixup(double* L11, int n, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* src, int64_t lds, const int64_t* ids, int64_t row0, int cnt, int ncols,
                                double* dst, int64_t ldd, cudaStream_t st);
 cudaError_t launch_pivpos(const int64_t* piv, int n, int64_t row0, int64_t rows, int* pivpos, cudaStream_t st);
+
+// tslw.cu: warp-level tournament LU, left-looking 16-column panels (the default contract)
+constexpr int kTslwPanel = 16;
+struct TslwRoot {          // root outputs of one panel (all null below the root)
+  double* U;               // n x n, ld n
+  int64_t* piv;            // [n]
+  double* rd;              // [n] 1 / U(t, t)
+  double* lw;              // 16 x 16: in-panel multipliers of the panel's pivot rows
+  uint8_t* chosen;         // local rows chosen as pivots
+  unsigned long long* status;
+  int64_t row0;
+  int n;
+};
+bool tslw_cfg(const rlhc_tslu_cfg& c);
+size_t tslw_slots(int64_t rows);
+cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
+                     int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
+                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st);
 
 // rows.cu
 cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,

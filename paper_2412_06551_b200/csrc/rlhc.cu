@@ -81,8 +81,9 @@ int kernel_width(int panel) { return panel <= 16 ? 16 : (panel <= 32 ? 32 : 64);
 
 bool cfg_ok(const rlhc_tslu_cfg& c, int64_t n) {
   if (c.panel < 1 || c.panel > 64 || c.panel > n) return false;
+  if (tslw_cfg(c)) return true;
   int W = kernel_width(c.panel);
-  if (c.leaf_rows != select_rows(W)) return false;
+  if (c.leaf_rows < 1 || c.leaf_rows > select_rows(W)) return false;
   if (c.arity < 2 || (int64_t)c.arity * c.panel > select_rows(W)) return false;
   return true;
 }
@@ -106,6 +107,7 @@ struct TsluWs {
   int* cnt[2];
   double* vals[2];
   double* rd;
+  double* lw;
   double* Xp;
 };
 
@@ -114,11 +116,12 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
   int64_t nleaves = ceil_div<int64_t>(rows, cfg.leaf_rows);
   for (int b = 0; b < 2; b++) {
     t.ids[b] = c.take<int>((size_t)nleaves * W);
-    t.cnt[b] = c.take<int>((size_t)nleaves);
+    t.cnt[b] = c.take<int>((size_t)2 * nleaves + 64);  // tslw: packed counts + arrival counters
     t.vals[b] = c.take<double>((size_t)nleaves * W * W);
   }
   t.chosen = c.take<uint8_t>((size_t)rows);
   t.rd = c.take<double>((size_t)n);
+  t.lw = c.take<double>((size_t)kTslwPanel * kTslwPanel);
   t.Xp = c.take<double>((size_t)n * n);
 }
 
@@ -127,6 +130,11 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
 int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg& cfg,
              TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st,
              bool check_input = false) {
+  if (tslw_cfg(cfg)) {  // warp tournament; L (original row order) lands in tw
+    CUDA_TRY(run_tslw(X, ldx, rows, row0, (int)n, cfg.arity, tw, ldtw, piv, U, L11, t.rd, t.lw, t.chosen, t.ids,
+                      t.cnt, t.status, check_input, st));
+    return RLHC_OK;
+  }
   const int W = kernel_width(cfg.panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg.leaf_rows);
   const bool panels = cfg.panel < n;
@@ -142,7 +150,7 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
     const int64_t lds = (p0 == 0) ? ldx : ldtw;
     // slots carry ids only: every node reads its candidates' rows from src by global id
     const RowSrc rsrc{src, lds, row0, (int)p0};
-    CUDA_TRY(launch_tslu_leaf(W, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
+    CUDA_TRY(launch_tslu_leaf(W, cfg.leaf_rows, src, lds, rows, row0, (int)p0, w, panels && p0 > 0 ? t.chosen : nullptr, t.ids[0],
                               t.cnt[0], nullptr, st, root_emit && nleaves == 1 ? &ro : nullptr,
                               check_input && !panels ? t.status : nullptr));
     int cur = 0, nslots = nleaves;
@@ -208,14 +216,17 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   mk.mark(0);
   CUDA_TRY(launch_status_init(status, st));
   // input check: a pass of its own, or (one panel) folded into the TSLU leaves' read of X
-  const bool fold_check = cfg.panel >= n;
+  const bool fold_check = cfg.panel >= n || tslw_cfg(cfg);
   if (!fold_check) CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
   mk.mark(1);
   // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
   int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st, fold_check);
   if (rc) return rc;
-  CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
-  CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+  const bool l_done = tslw_cfg(cfg);  // the warp tournament leaves L in the Q buffer
+  if (!l_done) {
+    CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
+    CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+  }
   mk.mark(2);
   // one streaming pass: out = A T^{-1} (substitution) [+ G = out^T out fused]
   auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
@@ -230,7 +241,7 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
     return RLHC_OK;
   };
   // L in original row order (R#2), into the Q buffer
-  if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
+  if (!l_done && (rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
   mk.mark(3);
   int64_t srows;
   if (algo == RLHC_SLHC3) {  // L_s = Omega L
@@ -321,9 +332,11 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
   } else if (method == RLHC_LUC2) {
     // PX = LU, L (into Q), G = L^T L, S = Cholesky(G), Y = S U (diag > 0, R#23), W = X Y^{-1}
     if ((rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st))) return rc;
-    CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
-    CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
-    if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
+    if (!tslw_cfg(cfg)) {
+      CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
+      CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
+      if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
+    }
     CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, a.G, st));
     if ((rc = chol(a.S, a.Di, RLHC_STAGE_CHOL0))) return rc;
     CUDA_TRY(launch_trmm_uu(a.S, a.U, ni, a.Y, st));
@@ -375,11 +388,10 @@ extern "C" {
 void rlhc_default_tslu_cfg(int64_t m, int64_t n, rlhc_tslu_cfg* cfg) {
   (void)m;
   if (!cfg) return;
-  int panel = (int)std::min<int64_t>(std::max<int64_t>(n, 1), 64);
-  int W = kernel_width(panel);
-  cfg->panel = panel;
-  cfg->leaf_rows = select_rows(W);
-  cfg->arity = std::max(2, select_rows(W) / panel);
+  // the warp tournament (tslw.cu): 16-column panels, 128-row leaves, nodes of 8 children
+  cfg->panel = (int)std::min<int64_t>(std::max<int64_t>(n, 1), kTslwPanel);
+  cfg->leaf_rows = 128;
+  cfg->arity = 8;
 }
 
 size_t rlhc_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg* cfgp) {
@@ -482,7 +494,7 @@ static size_t getrf_carve(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cf
                           int** pivpos) {
   t.status = c.take<unsigned long long>(4);
   carve_tslu(c, rows, n, cfg, t);
-  *tw = cfg.panel < n ? c.take<double>((size_t)rows * n) : nullptr;
+  *tw = (cfg.panel < n || tslw_cfg(cfg)) ? c.take<double>((size_t)rows * n) : nullptr;
   *pivpos = c.take<int>((size_t)rows);
   return c.used;
 }
@@ -517,6 +529,12 @@ int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t
   getrf_carve(c, rows, n, cfg, t, &tw, &pivpos);
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(launch_status_init(t.status, st));
+  if (tslw_cfg(cfg)) {  // input check folded into the leaves; L straight into the caller's buffer
+    int rc = run_tslu(X, rows, n, ldx, row0, cfg, t, L ? L : tw, L ? ldl : n, piv, U, L11, st, true);
+    if (rc) return rc;
+    CUDA_TRY(launch_status_finish(t.status, info, st));
+    return RLHC_OK;
+  }
   CUDA_TRY(launch_check_finite(X, rows, (int)n, ldx, t.status, st));
   int rc = run_tslu(X, rows, n, ldx, row0, cfg, t, tw, n, piv, U, L11, st);
   if (rc) return rc;

@@ -64,7 +64,7 @@ RLHC_DEV void write_slot_rows(double* __restrict__ ov, int steps, int w, RowPtr 
 // trailing matrix afterwards), panel columns [p0, p0 + w).  Output level slot = leaf.
 template <int W, int NW, int RS>
 __global__ void __launch_bounds__(32 * NW, 1)
-tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows_all, int64_t leaf_rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ out_ids, int* __restrict__ out_cnt,
                  double* __restrict__ out_vals, RootOut root, unsigned long long* finite_status) {
   constexpr int R = 32 * RS;
@@ -74,7 +74,8 @@ tslu_leaf_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int6
   pdl_trigger();
   sel_init(sm, root.U, root.n);
   const int lane = lane_id();
-  const int64_t rb = (int64_t)blockIdx.x * R;
+  const int64_t rb = (int64_t)blockIdx.x * leaf_rows;
+  const int64_t rows = rows_all < rb + leaf_rows ? rows_all : rb + leaf_rows;  // end of this leaf
   double* stg = sel_stage(sm);
   // staging: a warp per row, lanes along the columns, every copy in flight at once
   // (cp.async), rows past the end and columns past w zero-filled
@@ -323,10 +324,11 @@ int select_rows(int W) { return W == 64 ? 256 : 512; }
 // (W, NW, RS): W=64 -> 8 warps x 8 cols, 256 rows; W=32 -> 8 x 4, 512 rows; W=16 -> 8 x 2, 512 rows
 
 template <int W, int NW, int RS>
-static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                            const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
+static cudaError_t run_leaf(int64_t leaf_rows, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0,
+                            int w, const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
                             const RootOut& root, unsigned long long* finite_status) {
-  int nleaves = (int)ceil_div<int64_t>(rows, 32 * RS);
+  if (leaf_rows < 1 || leaf_rows > 32 * RS) return cudaErrorInvalidValue;
+  int nleaves = (int)ceil_div<int64_t>(rows, leaf_rows);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
   static bool attr = false;  // once per instantiation (idempotent, so a race is harmless)
   if (!attr) {
@@ -334,7 +336,7 @@ static cudaError_t run_leaf(const double* src, int64_t lds, int64_t rows, int64_
     cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals,
+  note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, leaf_rows, row0, p0, w, chosen, ids, cnt, vals,
                                                                             root, finite_status);
   return cudaGetLastError();
 }
@@ -355,16 +357,16 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
                     arity, w, ids, cnt, vals, root, rsrc);
 }
 
-cudaError_t launch_tslu_leaf(int W, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+cudaError_t launch_tslu_leaf(int W, int64_t leaf_rows, const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                              const uint8_t* chosen, int* ids, int* cnt, double* vals, cudaStream_t st,
                              const RootOut* rootp, unsigned long long* finite_status) {
   const RootOut root = rootp ? *rootp : RootOut{};
   switch (W) {
-    case 16: return run_leaf<16, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+    case 16: return run_leaf<16, 8, 16>(leaf_rows, src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
                                              finite_status);
-    case 32: return run_leaf<32, 8, 16>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+    case 32: return run_leaf<32, 8, 16>(leaf_rows, src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
                                              finite_status);
-    case 64: return run_leaf<64, 8, 8>(src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
+    case 64: return run_leaf<64, 8, 8>(leaf_rows, src, lds, rows, row0, p0, w, chosen, ids, cnt, vals, st, root,
                                              finite_status);
   }
   return cudaErrorInvalidValue;

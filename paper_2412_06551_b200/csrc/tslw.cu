@@ -1,0 +1,900 @@
+// tslw.cu -- warp-level tournament LU "PX = LU" under the
+// pivot contract of DESIGN.md R#3-R#5 with 16-column panels, 128-row leaves and nodes of
+// up to 8 children: the default contract (rlhc_default_tslu_cfg).
+//
+// One WARP runs one tournament node: 128 candidate rows x 16 panel columns in registers,
+// lane = candidate row (4 slots per lane), so a GEPP step needs no communication beyond
+// the warp (three warp reductions for the pivot, the pivot row through 2 KB of per-warp
+// shared memory) and many nodes run side by side on every SM.
+//
+// Panels are LEFT-LOOKING with L kept in the L buffer (the caller's Q buffer in the
+// pipelines): for panel j (columns [p0, p0+16)) the leaf kernel
+//   1. turns the previous panel's Schur values S_{j-1} (kept in L's columns [p0-16, p0))
+//      into L columns by forward substitution with U's diagonal block (in place);
+//   2. forms S_j = X[:, p0:p0+w] - L[:, :p0] U[:p0, p0:p0+w] (fma chain in increasing k)
+//      and stores it in L's columns [p0, p0+w);
+//   3. selects its leaf's 16 winners.
+// Node kernels read their candidates' S_j rows by global id.  The root emits piv, U's
+// diagonal block, 1/diag(U) and the in-panel multipliers; tslw_urows_kernel completes the
+// panel's U rows right of the panel.  After the last panel, tslw_lfinal_kernel converts
+// the last S into L and tslw_fixup_kernel gives the pivot rows their L11 rows.
+// Every element of S, L and U is the oracle's fma chain (oracle ora_tslu / l_row: the
+// elimination and the substitution are the same chain), so piv, U, L11 and L are bit-exact.
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rlhc {
+
+#ifdef RLHC_TSLW_TRACE
+// probe builds only (tools/probe/ptslw.cu): per-warp phase records
+__device__ unsigned long long g_tw[1 << 16][8];
+__device__ unsigned g_twn;
+#define TW_T(v) long long v = clock64(); unsigned long long v##g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v##g));
+#define TW_REC(tag, a, b, c, d)                                                              \
+  if (lane_id() == 0) {                                                                      \
+    unsigned i_ = atomicAdd(&g_twn, 1u);                                                     \
+    if (i_ < (1u << 16)) {                                                                   \
+      g_tw[i_][0] = tag; g_tw[i_][1] = p0; g_tw[i_][2] = gridDim.x; g_tw[i_][3] = a##g;      \
+      g_tw[i_][4] = b - a; g_tw[i_][5] = c - b; g_tw[i_][6] = d - c; g_tw[i_][7] = d##g;     \
+    }                                                                                        \
+  }
+__device__ long long g_stp[64];
+#define TW_STEP(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_stp[i] = clock64();
+#else
+#define TW_T(v)
+#define TW_REC(tag, a, b, c, d)
+#define TW_STEP(i)
+#endif
+
+namespace {
+
+constexpr int WW = kTslwPanel;  // panel width
+constexpr int RS = 4;           // candidate slots per lane
+constexpr int WR = 32 * RS;     // candidate rows per warp (= leaf rows, >= arity * WW)
+constexpr int WPB = 4;          // warps (tournament nodes) per CTA
+
+constexpr int TS = 18;          // row stride (doubles) of the staging tile: 16-byte rows, conflict-free LDS.128 by row
+
+struct WSel {
+  double tile[WR * TS];  // staging of the node's candidate rows (128 x 16)
+  double prow[WW][WW];   // step t: the pivot row (c >= t: U values; c < t: multipliers, root only)
+  double r[WW];          // 1 / pivot of step t
+  int sid[WR];           // global id of candidate c (INT_MAX: none)
+  int win[WW];           // candidate index of the winner of step t
+  int zero[WW];          // 1: zero pivot column at step t (R#5: no update)
+};
+
+// Pivot row of step t (slot ps of the pivot lane), columns [c0, WW) -> dst (c0 even);
+// only the pivot lane runs it.
+#define TSLW_ROW_CASE(S)                                                                      \
+  case S: {                                                                                   \
+    _Pragma("unroll") for (int c = 0; c < WW; c += 2) if (c >= c0)                            \
+      *reinterpret_cast<double2*>(dst + c) = make_double2(a[S][c], a[S][c + 1]);               \
+  } break;
+RLHC_DEV void write_prow(const double (&a)[RS][WW], int ps, double* dst, int c0) {
+  switch (ps) {
+    TSLW_ROW_CASE(0) TSLW_ROW_CASE(1) TSLW_ROW_CASE(2) TSLW_ROW_CASE(3)
+    default: break;
+  }
+}
+#undef TSLW_ROW_CASE
+// Generic GEPP select of one warp (definition: oracle gepp_select, R#4-R#5):
+// any step count, zero pivot columns, reciprocals outside rcp_newton's window.
+// a[s][c]: candidate s*32 + lane, panel column c; candidates are in increasing global-id
+// order over the active ones (bit s of act), so "ties -> smallest id" is "smallest
+// candidate index".  sm.win / sm.prow (whole rows) / sm.r / sm.zero hold the winners.
+// The maximum of |a| is taken on the bit patterns (sign cleared) of the 32-bit halves:
+// high words, then low words among the rows attaining the high maximum.
+RLHC_DEV void wsel_gepp(double (&a)[RS][WW], unsigned act, int steps, WSel& sm) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int t = 0; t < WW; t++) {
+    if (t < steps) {
+      int hi[RS];
+      unsigned lo[RS];
+#pragma unroll
+      for (int s = 0; s < RS; s++) {
+        hi[s] = ((act >> s) & 1u) ? (__double2hiint(a[s][t]) & 0x7fffffff) : -1;
+        lo[s] = (unsigned)__double2loint(a[s][t]);
+      }
+      int mh = max(max(hi[0], hi[1]), max(hi[2], hi[3]));
+      mh = __reduce_max_sync(0xffffffffu, mh);
+      unsigned ml = 0;
+#pragma unroll
+      for (int s = 0; s < RS; s++) ml = max(ml, hi[s] == mh ? lo[s] : 0u);
+      ml = __reduce_max_sync(0xffffffffu, ml);
+      const double pabs = __longlong_as_double((long long)(((unsigned long long)(unsigned)mh << 32) | ml));
+      double rabs = rcp_newton(pabs);
+      unsigned mm = 0;
+#pragma unroll
+      for (int s = 0; s < RS; s++) mm |= (hi[s] == mh && lo[s] == ml ? 1u : 0u) << s;
+      const int pidx = __reduce_min_sync(0xffffffffu, mm ? (__ffs(mm) - 1) * 32 + lane : INT_MAX);
+      const bool zero = (mh | (int)ml) == 0;
+      if (!zero && !rcp_newton_ok(mh)) rabs = rcp_slow(pabs);  // warp-uniform, rare
+      const int ps = pidx >> 5;
+      if (lane == (pidx & 31)) {
+        act &= ~(1u << ps);
+        write_prow(a, ps, &sm.prow[t][0], 0);
+        sm.win[t] = pidx;
+        sm.zero[t] = zero ? 1 : 0;
+      }
+      __syncwarp();
+      if (!zero) {
+        const double r = sm.prow[t][t] < 0.0 ? -rabs : rabs;  // drcp(-x) == -drcp(x)
+        if (lane == 0) sm.r[t] = r;
+        double l[RS];
+#pragma unroll
+        for (int s = 0; s < RS; s++) {
+          l[s] = __dmul_rn(a[s][t], r);
+          a[s][t] = l[s];
+        }
+#pragma unroll
+        for (int c = t + 1; c < WW; c++) {
+          const double u = sm.prow[t][c];
+#pragma unroll
+          for (int s = 0; s < RS; s++) a[s][c] = __fma_rn(-l[s], u, a[s][c]);
+        }
+      } else if (lane == 0) {
+        sm.r[t] = 0.0;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Fast select: 16 full steps as a compact loop (the code stays hot in the instruction
+// cache; a lone warp runs every tournament node on the critical path).  Registers are
+// ROTATED: at step t, a[s][k] holds column t + k, so every index is static.  The update
+// of step t is split: column t + 1 right away (the next pivot search needs it), the
+// other columns at the start of step t + 1, in the shadow of its warp reductions.  The
+// pivot's sign rides on the index reduction (key = candidate index * 2 + sign).  Returns
+// false if a pivot column was zero or a pivot fell outside rcp_newton's window (the
+// caller reruns the generic select).  prow[t][j] = the pivot row's column t + j (rotated).
+// pending update of step t - 1 for rotated columns [K0, K1): a[k] = a[k+1] - l u[k+1]
+template <int K0, int K1>
+RLHC_DEV void wsel_pend(double (&a)[RS][WW], const double (&lp)[RS], const double* up) {
+#pragma unroll
+  for (int k = K0; k < K1; k++) {
+    const double u = up[k + 1];
+#pragma unroll
+    for (int s = 0; s < RS; s++) a[s][k] = __fma_rn(-lp[s], u, a[s][k + 1]);
+  }
+}
+
+// One step; PEND: apply step t - 1's pending update (t > 0), in chunks placed after each
+// warp reduction so that the DFMAs issue in the reductions' latency shadows.
+template <bool PEND>
+RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bool& bad, int t, WSel& sm) {
+  const int lane = lane_id();
+  TW_STEP(t)
+  const double* up = PEND ? &sm.prow[t - 1][0] : nullptr;
+  int hi[RS];
+  unsigned lo[RS];
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    hi[s] = ((act >> s) & 1u) ? (__double2hiint(a[s][0]) & 0x7fffffff) : -1;
+    lo[s] = (unsigned)__double2loint(a[s][0]);
+  }
+  int mh = max(max(hi[0], hi[1]), max(hi[2], hi[3]));
+  mh = __reduce_max_sync(0xffffffffu, mh);
+  if (PEND) wsel_pend<1, 6>(a, lp, up);
+  unsigned ml = 0;
+#pragma unroll
+  for (int s = 0; s < RS; s++) ml = max(ml, hi[s] == mh ? lo[s] : 0u);
+  ml = __reduce_max_sync(0xffffffffu, ml);
+  if (PEND) wsel_pend<6, 10>(a, lp, up);
+  const double rabs = rcp_newton(__longlong_as_double((long long)(((unsigned long long)(unsigned)mh << 32) | ml)));
+  int key = INT_MAX;
+#pragma unroll
+  for (int s = RS - 1; s >= 0; s--)
+    key = (hi[s] == mh && lo[s] == ml) ? (((s * 32 + lane) << 1) | (int)((unsigned)__double2hiint(a[s][0]) >> 31))
+                                       : key;
+  key = __reduce_min_sync(0xffffffffu, key);
+  if (PEND) {
+    wsel_pend<10, WW - 1>(a, lp, up);
+#pragma unroll
+    for (int s = 0; s < RS; s++) a[s][WW - 1] = 0.0;
+  }
+  bad |= (mh | (int)ml) == 0 || !rcp_newton_ok(mh);
+  const int pidx = key >> 1, ps = pidx >> 5, plane = pidx & 31;
+  const double r = (key & 1) ? -rabs : rabs;
+  if (lane == plane) {  // the pivot lane publishes its row
+    act &= ~(1u << ps);
+    write_prow(a, ps, &sm.prow[t][0], 0);
+  }
+  if (lane == 0) {
+    sm.win[t] = pidx;
+    sm.r[t] = r;
+    sm.zero[t] = 0;
+  }
+  __syncwarp();
+  const double u1 = sm.prow[t][1];
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    lp[s] = __dmul_rn(a[s][0], r);
+    a[s][0] = __fma_rn(-lp[s], u1, a[s][1]);
+  }
+}
+
+RLHC_DEV bool wsel_fast(double (&a)[RS][WW], unsigned act, WSel& sm) {
+  bool bad = false;
+  double lp[RS];
+  wsel_step<false>(a, lp, act, bad, 0, sm);
+  // step 0 left columns 2.. unrotated and un-updated: the pending form of steps >= 1
+#pragma unroll 1
+  for (int t = 1; t < WW; t++) wsel_step<true>(a, lp, act, bad, t, sm);
+  __syncwarp();
+  TW_STEP(WW)
+  return !bad;
+}
+
+// Outputs of a node: ids of the winners in pivot order; at the root also piv, chosen,
+// U's diagonal block, 1/diag(U) and rank errors.  rot: prow rows rotated (fast select:
+// U(t, t + j) = prow[t][j]); else prow[t][c] = column c.
+RLHC_DEV void wsel_emit(const WSel& sm, int steps, int w, int slot, int* out_ids, int* out_cnt, const TslwRoot& ro,
+                        int p0, bool rot) {
+  const int lane = lane_id();
+  if (lane == 0) {  // one thread writes the slot: its release (the climb's atomic) covers it
+    out_cnt[slot] = steps;
+    int4* o = reinterpret_cast<int4*>(out_ids + slot * WW);
+#pragma unroll
+    for (int q = 0; q < WW; q += 4) {
+      int v[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = q + j < steps ? sm.sid[sm.win[q + j]] : -1;
+      o[q / 4] = make_int4(v[0], v[1], v[2], v[3]);
+    }
+  }
+  if (!ro.U) return;
+  if (lane == 0 && steps < w) report(ro.status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + steps);
+  if (lane < steps) {
+    const int gid = sm.sid[sm.win[lane]];
+    ro.piv[p0 + lane] = gid;
+    ro.chosen[gid - ro.row0] = 1;
+    ro.rd[p0 + lane] = sm.r[lane];
+    if (sm.zero[lane]) report(ro.status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + lane);
+  }
+  for (int e = lane; e < WW * WW; e += 32) {
+    const int t = e / WW, c = e - t * WW;
+    if (t < steps && c < w && c >= t) ro.U[(int64_t)(p0 + t) * ro.n + p0 + c] = rot ? sm.prow[t][c - t] : sm.prow[t][c];
+  }
+}
+
+// Candidates' rows from the staging tile (row c*TS) -> registers; zero for inactive rows and
+// columns >= w.
+RLHC_DEV void tile_to_regs(const double* tile, int w, double (&a)[RS][WW]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int s = 0; s < RS; s++)
+#pragma unroll
+    for (int c = 0; c < WW; c += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(tile + (s * 32 + lane) * TS + c);
+      a[s][c] = c < w ? v.x : 0.0;
+      a[s][c + 1] = c + 1 < w ? v.y : 0.0;
+    }
+}
+
+// Select on the candidates held in the tile (fast path, else the generic one), then emit.
+RLHC_DEV void select_and_emit(WSel& sm, unsigned act, int w, int slot, int* out_ids, int* out_cnt,
+                              const TslwRoot& ro, int p0) {
+  double a[RS][WW];
+  tile_to_regs(sm.tile, w, a);
+  const int cnt = __reduce_add_sync(0xffffffffu, __popc(act));
+  const int steps = min(cnt, w);
+  bool done = false;
+  if (steps == WW) done = wsel_fast(a, act, sm);
+  if (!done) {
+    if (steps == WW) tile_to_regs(sm.tile, w, a);  // the fast attempt modified a
+    wsel_gepp(a, act, steps, sm);
+  }
+  wsel_emit(sm, steps, w, slot, out_ids, out_cnt, ro, p0, done);
+}
+
+// 16-byte L2 copy (bypasses L1: rows written by other SMs in this kernel); src_bytes < 16
+// zero-fills the rest
+RLHC_DEV void cp_async16_cg(void* smem_ptr, const void* gptr, int src_bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gptr), "r"(src_bytes));
+}
+RLHC_DEV int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// The candidates' S_j rows (global id sm.sid[q], columns [p0, p0+w)) -> tile rows q.
+// v16: rows 16-byte aligned (even ldl, aligned base): 16-byte L2 copies, 4 rows per
+// instruction; else 8-byte L2 loads.
+RLHC_DEV void stage_rows(WSel& sm, int w, const double* Lb, int64_t ldl, int64_t row0, int p0, bool v16) {
+  const int lane = lane_id();
+  if (v16) {
+    const int ch = lane & 7;
+    const int nb = w - 2 * ch;  // valid doubles in this 16-byte chunk
+    const int bytes = nb >= 2 ? 16 : (nb == 1 ? 8 : 0);
+#pragma unroll 8
+    for (int i = 0; i < WR / 4; i++) {
+      const int q = 4 * i + (lane >> 3);
+      const int id = sm.sid[q];
+      const bool ok = id != INT_MAX;
+      cp_async16_cg(sm.tile + q * TS + 2 * ch, ok ? Lb + ((int64_t)id - row0) * ldl + p0 + 2 * ch : Lb,
+                    ok ? bytes : 0);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+  } else {
+    const int c = lane & 15;
+#pragma unroll 8
+    for (int i = 0; i < WR / 2; i++) {
+      const int q = 2 * i + (lane >> 4);
+      const int id = sm.sid[q];
+      sm.tile[q * TS + c] = (id != INT_MAX && c < w) ? __ldcg(Lb + ((int64_t)id - row0) * ldl + p0 + c) : 0.0;
+    }
+  }
+  __syncwarp();
+}
+
+// Schur complement of panel [p0, p0+w), thread per row (CTA = 128 rows):
+//   PRO (p0 > 0): the previous panel's S values (L's columns [p0-16, p0)) -> L by forward
+//   substitution with U's diagonal block (in place; same chain as the select);
+//   S_j = X[:, p0:p0+w] - L[:, :p0] U[:p0, p0:p0+w] (fma chain in increasing k) -> L's
+//   columns [p0, p0+w).  Also the input check of X's panel columns.
+// Row tiles (128 x 16) are staged with coalesced cp.async: X (issued before the wait on
+// the previous kernel: X is never written), S_{j-1}, and L in double-buffered 16-column
+// chunks; every thread then reads its own row from shared memory.
+constexpr int SR = 128;  // rows per Schur CTA
+constexpr int ST = 17;   // tile row stride (doubles): conflict-free LDS.64 by row
+RLHC_DEV void schur_stage(double* tile, const double* base, int64_t ld, int64_t rb, int64_t rows, int col, int w) {
+  const int c = threadIdx.x & 15;
+#pragma unroll
+  for (int j = 0; j < SR / 8; j++) {
+    const int q = (threadIdx.x >> 4) + 8 * j;
+    const bool in = rb + q < rows && c < w;
+    cp_async8(tile + q * ST + c, in ? base + (rb + q) * ld + col + c : base, in ? 8 : 0);
+  }
+}
+__host__ __device__ inline size_t schur_smem(int p0) {
+  return ((size_t)p0 * WW + WW * WW + WW + 4 * SR * ST) * sizeof(double);
+}
+template <bool PRO>
+__global__ void __launch_bounds__(SR)
+tslw_schur_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
+                  int p0, int w, int n, const double* __restrict__ U, const double* __restrict__ rd,
+                  unsigned long long* finite_status) {
+  extern __shared__ __align__(16) double sh[];
+  double* Bx = sh;              // X tile
+  double* Bs = Bx + SR * ST;    // S_{j-1} tile -> L_{j-1}
+  double* Rc = Bs + SR * ST;    // two L chunk tiles
+  double* Ucol = Rc + 2 * SR * ST;  // [p0][WW]: U[k, p0 + c]
+  double* Ublk = Ucol + (size_t)p0 * WW;
+  double* rdp = Ublk + WW * WW;
+  const int64_t rb = (int64_t)blockIdx.x * SR;
+  const int tid = threadIdx.x;
+  schur_stage(Bx, X, ldx, rb, rows, p0, w);
+  cp_async_commit();
+  pdl_trigger();
+  pdl_wait();  // L and U come from the previous kernels
+  const int kold = PRO ? p0 - WW : 0;
+  const int nch = kold / WW;
+  if (PRO) schur_stage(Bs, Lb, ldl, rb, rows, p0 - WW, WW);
+  cp_async_commit();
+  if (nch > 0) schur_stage(Rc, Lb, ldl, rb, rows, 0, WW);
+  cp_async_commit();
+  if (nch > 1) schur_stage(Rc + SR * ST, Lb, ldl, rb, rows, WW, WW);
+  cp_async_commit();
+  for (int e = tid; e < p0 * WW; e += SR) {
+    const int k = e / WW, c = e - k * WW;
+    Ucol[e] = c < w ? U[(int64_t)k * n + p0 + c] : 0.0;
+  }
+  if (PRO) {
+    for (int e = tid; e < WW * WW; e += SR) {
+      const int k = e / WW, c = e - k * WW;
+      Ublk[e] = U[(int64_t)(p0 - WW + k) * n + p0 - WW + c];
+    }
+    if (tid < WW) rdp[tid] = rd[p0 - WW + tid];
+  }
+  asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // X and S_{j-1} (the chunks may be in flight)
+  __syncthreads();
+  const int64_t r = rb + tid;
+  const bool valid = r < rows;
+  double acc[WW];
+#pragma unroll
+  for (int c = 0; c < WW; c++) acc[c] = Bx[tid * ST + c];
+  if (finite_status && valid) {
+#pragma unroll
+    for (int c = 0; c < WW; c++)
+      if (c < w && !isfinite(acc[c])) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, r * n + p0 + c);
+  }
+  if (PRO) {
+    double l[WW];
+#pragma unroll
+    for (int c = 0; c < WW; c++) l[c] = Bs[tid * ST + c];
+#pragma unroll
+    for (int c = 0; c < WW; c++) {
+      double v = l[c];
+#pragma unroll
+      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], Ublk[k * WW + c], v);
+      l[c] = __dmul_rn(v, rdp[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < WW; c++) Bs[tid * ST + c] = l[c];
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < WW; c++) Lb[r * ldl + kold + c] = l[c];
+    }
+  }
+#pragma unroll 1
+  for (int ch = 0; ch < nch; ch++) {
+    if (ch + 1 < nch) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const double* lt = Rc + (ch & 1) * SR * ST + tid * ST;
+    const double* uk = Ucol + ch * WW * WW;
+#pragma unroll
+    for (int k = 0; k < WW; k++) {
+      const double lk = lt[k];
+#pragma unroll
+      for (int c = 0; c < WW; c++) acc[c] = __fma_rn(-lk, uk[k * WW + c], acc[c]);
+    }
+    __syncthreads();
+    if (ch + 2 < nch) schur_stage(Rc + (ch & 1) * SR * ST, Lb, ldl, rb, rows, (ch + 2) * WW, WW);
+    cp_async_commit();
+  }
+  if (PRO) {
+    const double* uk = Ucol + kold * WW;
+#pragma unroll
+    for (int k = 0; k < WW; k++) {
+      const double lk = Bs[tid * ST + k];
+#pragma unroll
+      for (int c = 0; c < WW; c++) acc[c] = __fma_rn(-lk, uk[k * WW + c], acc[c]);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < WW; c++)
+      if (c < w) Lb[r * ldl + p0 + c] = acc[c];
+  }
+}
+
+// The same Schur complement on the FP64 tensor cores, for panels with p0 > 0:
+// CTA = 128 rows x 16 columns, 8 warps of 16 x 16 (2 x 2 DMMA m8n8k4 fragments);
+// acc = X[:, panel]; acc -= L[:, k] U[k, panel] over k = 0 .. kold-1 in 32-wide chunks
+// (double-buffered cp.async), then over the previous panel's 16 columns, whose L values
+// the CTA's first 128 threads compute first (row substitution of S_{j-1}) and publish
+// both to L and to shared memory.  DMMA m8n8k4 is bitwise the fma chain over its 4 k's
+// (profiles/r01_probe_fp64_hbm.txt), so every element is the same increasing-k chain.
+constexpr int SD_M = 128, SD_K = 32;
+struct SchurDSmem {
+  double A[2][SD_M][SD_K + 4];
+  double B[2][SD_K][WW + 4];
+  double Lt[SD_M][WW + 4];   // L_{j-1} of the CTA's rows (A operand of the last chunk)
+  double Ut[WW][WW + 4];     // U[kold + k, p0 + c] (B operand of the last chunk)
+  double Ublk[WW][WW + 1];   // the previous panel's diagonal block
+  double rdp[WW];
+};
+__global__ void __launch_bounds__(256, 2)
+tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
+                       int p0, int w, int n, const double* __restrict__ U, const double* __restrict__ rd,
+                       unsigned long long* finite_status) {
+  extern __shared__ __align__(16) unsigned char sd_raw[];
+  SchurDSmem& sm = *reinterpret_cast<SchurDSmem*>(sd_raw);
+  const int64_t r0 = (int64_t)blockIdx.x * SD_M;
+  const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int kold = p0 - WW;
+  const bool al = ((ldl & 1) == 0) && ((((uintptr_t)Lb) & 15) == 0) && ((n & 1) == 0) && ((((uintptr_t)U) & 15) == 0);
+  // X values of this lane's fragments (X is never written: before the dependency wait)
+  double acc[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t gr = r0 + wp * 16 + a * 8 + g;
+        const int c = b * 8 + 2 * t + h;
+        const double v = (gr < rows && c < w) ? X[gr * ldx + p0 + c] : 0.0;
+        if (finite_status && !isfinite(v)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c);
+        acc[a][b][h] = v;
+      }
+  pdl_trigger();
+  pdl_wait();
+  auto load_chunk = [&](int st, int kc) {
+    // A: 128 rows x 32 k (16-byte pairs, 8 per thread); B: 32 k x 16 columns (1 pair per thread)
+#pragma unroll
+    for (int i = 0; i < SD_M * SD_K / 2 / 256; i++) {
+      const int idx = tid + 256 * i;
+      const int r = idx / (SD_K / 2), c = 2 * (idx % (SD_K / 2));
+      const int64_t gr = r0 + r;
+      const int k = kc + c;
+      double* dst = &sm.A[st][r][c];
+      const double* src = Lb + gr * ldl + k;
+      const bool rok = gr < rows;
+      if (al) {
+        cp_async16_cg(dst, rok && k < kold ? src : Lb, rok && k < kold ? 16 : 0);
+      } else {
+        cp_async8(dst, (rok && k < kold) ? src : Lb, (rok && k < kold) ? 8 : 0);
+        cp_async8(dst + 1, (rok && k + 1 < kold) ? src + 1 : Lb, (rok && k + 1 < kold) ? 8 : 0);
+      }
+    }
+    {
+      const int r = tid / (WW / 2), c = 2 * (tid % (WW / 2));
+      const int k = kc + r;
+      double* dst = &sm.B[st][r][c];
+      const double* src = U + (int64_t)k * n + p0 + c;
+      if (al) {
+        const int nb = (k < kold) ? (c + 1 < w ? 16 : (c < w ? 8 : 0)) : 0;
+        cp_async16_cg(dst, nb ? src : U, nb);
+      } else {
+        cp_async8(dst, (k < kold && c < w) ? src : U, (k < kold && c < w) ? 8 : 0);
+        cp_async8(dst + 1, (k < kold && c + 1 < w) ? src + 1 : U, (k < kold && c + 1 < w) ? 8 : 0);
+      }
+    }
+    cp_async_commit();
+  };
+  if (kold > 0) load_chunk(0, 0);
+  // the previous panel's block, 1/diag, and U[kold.., panel]
+  for (int e = tid; e < WW * WW; e += 256) {
+    const int k = e / WW, c = e - k * WW;
+    sm.Ublk[k][c] = U[(int64_t)(kold + k) * n + kold + c];
+    sm.Ut[k][c] = c < w ? U[(int64_t)(kold + k) * n + p0 + c] : 0.0;
+  }
+  if (tid < WW) sm.rdp[tid] = rd[kold + tid];
+  __syncthreads();
+  if (tid < SD_M) {  // L_{j-1} of row tid: S_{j-1} -> forward substitution (the select's chain)
+    const int64_t gr = r0 + tid;
+    double l[WW];
+#pragma unroll
+    for (int c = 0; c < WW; c++) l[c] = gr < rows ? Lb[gr * ldl + kold + c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < WW; c++) {
+      double v = l[c];
+#pragma unroll
+      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], sm.Ublk[k][c], v);
+      l[c] = __dmul_rn(v, sm.rdp[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < WW; c++) sm.Lt[tid][c] = l[c];
+    if (gr < rows) {
+#pragma unroll
+      for (int c = 0; c < WW; c++) Lb[gr * ldl + kold + c] = l[c];
+    }
+  }
+  int st = 0;
+  for (int kc = 0; kc < kold; kc += SD_K) {
+    if (kc + SD_K < kold) {
+      load_chunk(st ^ 1, kc + SD_K);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < SD_K; k0 += 4) {
+      double af[2], bf[2];
+#pragma unroll
+      for (int a = 0; a < 2; a++) af[a] = -sm.A[st][wp * 16 + a * 8 + g][k0 + t];
+#pragma unroll
+      for (int b = 0; b < 2; b++) bf[b] = sm.B[st][k0 + t][b * 8 + g];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+    st ^= 1;
+  }
+  __syncthreads();  // Lt complete
+#pragma unroll
+  for (int k0 = 0; k0 < WW; k0 += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int a = 0; a < 2; a++) af[a] = -sm.Lt[wp * 16 + a * 8 + g][k0 + t];
+#pragma unroll
+    for (int b = 0; b < 2; b++) bf[b] = sm.Ut[k0 + t][b * 8 + g];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      const int64_t gr = r0 + wp * 16 + a * 8 + g;
+      const int c = b * 8 + 2 * t;
+      if (gr < rows) {
+        if (c < w) Lb[gr * ldl + p0 + c] = acc[a][b][0];
+        if (c + 1 < w) Lb[gr * ldl + p0 + c + 1] = acc[a][b][1];
+      }
+    }
+}
+
+// The tournament of one panel, all levels in one launch.  Warp = leaf (rows
+// [leaf*128, leaf*128 + 128) of the local rows, their S_j rows from L's panel columns);
+// the LAST child to finish a node runs the node (arrival counters, reset by the node's
+// runner for the next panel), up to the root, which emits piv, U's diagonal block and
+// 1/diag(U).  No launch per level, and the select code stays hot in the instruction cache.
+// Slots: level 0 in ids0/cnt0, levels >= 1 packed in idsN/cntN (arrival counters alike).
+__global__ void __launch_bounds__(32 * WPB)
+tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64_t row0, int p0, int w,
+                 const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
+                 int* __restrict__ idsN, int* __restrict__ cntN, int* __restrict__ arrive, int arity, TslwRoot ro) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  WSel& sm = reinterpret_cast<WSel*>(raw)[warp_id()];
+  pdl_trigger();
+  pdl_wait();
+  TW_T(t0)
+  const int lane = lane_id();
+  const int nleaves = (int)ceil_div<int64_t>(rows, WR);
+  const int leaf = blockIdx.x * WPB + warp_id();
+  if (leaf >= nleaves) return;
+  const bool v16 = (ldl & 1) == 0 && (reinterpret_cast<uintptr_t>(Lb) & 15) == 0;
+  const int64_t rb = (int64_t)leaf * WR;
+  unsigned act = 0;
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    const int64_t r = rb + s * 32 + lane;
+    const bool valid = r < rows;
+    sm.sid[s * 32 + lane] = valid ? (int)(row0 + r) : INT_MAX;
+    act |= ((valid && !(chosen && chosen[r])) ? 1u : 0u) << s;
+  }
+  __syncwarp();
+  stage_rows(sm, w, Lb, ldl, row0, p0, v16);
+  TW_T(t1)
+  int nsl = nleaves, slot = leaf;
+  int *oids = ids0, *ocnt = cnt0;
+  const int* cids = nullptr;
+  for (;;) {
+    select_and_emit(sm, act, w, slot, oids, ocnt, nsl == 1 ? ro : TslwRoot{}, p0);
+    if (nsl == 1) break;
+    // climb: the last child of the parent runs it
+    if (cids) arrive += nsl;  // counters of this level's parents follow the previous level's
+    const int parent = slot / arity, nout = (nsl + arity - 1) / arity;
+    const int nchild = min(arity, nsl - parent * arity);
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) old = atom_add_acq_rel_gpu(&arrive[parent], 1);  // releases this slot, acquires the others
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nchild - 1) break;
+    if (lane == 0) arrive[parent] = 0;  // every child has arrived: ready for the next panel
+    const bool first = cids == nullptr;
+    cids = oids;
+    oids = first ? idsN : oids + nsl * WW;
+    ocnt = first ? cntN : ocnt + nsl;
+    // children [parent*arity, +nchild): entry e of child ci at candidate position
+    // ci*16 + (rank of its id within the child): the children cover increasing global
+    // row ranges, so this is increasing-id order
+#pragma unroll
+    for (int s = 0; s < RS; s++) {
+      const int c = s * 32 + lane, ci = c / WW, e = c % WW, child = parent * arity + ci;
+      const int v = ci < nchild ? __ldcg(cids + child * WW + e) : -1;  // -1: no entry
+      const int id = v >= 0 ? v : INT_MAX;
+      int rank = 0;
+#pragma unroll
+      for (int q = 0; q < WW; q++) {
+        const int o = __shfl_sync(0xffffffffu, id, (lane & ~(WW - 1)) | q);
+        rank += (o < id) || (o == id && q < e);
+      }
+      sm.sid[ci * WW + rank] = id;
+    }
+    __syncwarp();
+    act = 0;
+#pragma unroll
+    for (int s = 0; s < RS; s++) act |= (sm.sid[s * 32 + lane] != INT_MAX ? 1u : 0u) << s;
+    stage_rows(sm, w, Lb, ldl, row0, p0, v16);
+    slot = parent;
+    nsl = nout;
+  }
+  TW_T(t2)
+  TW_T(t3)
+  TW_REC(0, t0, t1, t2, t3)
+}
+
+// U rows [p0, p0+w) right of the panel: U[p0+t, c] = X[p_t, c] - sum_{k<p0} L[p_t, k] U[k, c]
+// - sum_{t'<t} l_{t,t'} U[p0+t', c] (the oracle's elimination chain of the pivot row), with
+// the in-panel multipliers l_{t,t'} recomputed from the winners' S_j rows by the same
+// forward substitution (same chain as the select).  CTA: WW x 32 threads (row t, column).
+constexpr int UR_C = 32, UR_K = 32;
+__global__ void __launch_bounds__(WW * UR_C)
+tslw_urows_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Lb, int64_t ldl,
+                  int64_t row0, int p0, int w, int n, const int64_t* __restrict__ piv, double* __restrict__ U,
+                  const double* __restrict__ rd) {
+  __shared__ double Lw[WW][UR_K + 1];
+  __shared__ double Ut[UR_K][UR_C];
+  __shared__ double P[WW][UR_C];
+  __shared__ double lw[WW][WW + 1];
+  __shared__ double Sb[WW][WW + 1];
+  __shared__ double Ub[WW][WW + 1];
+  __shared__ double rdb[WW];
+  __shared__ int64_t prow[WW];
+  pdl_trigger();
+  pdl_wait();
+  const int tx = threadIdx.x % UR_C, t = threadIdx.x / UR_C;
+  const int c = p0 + w + blockIdx.x * UR_C + tx;
+  if (threadIdx.x < WW) {
+    prow[threadIdx.x] = threadIdx.x < w ? piv[p0 + threadIdx.x] - row0 : 0;
+    rdb[threadIdx.x] = threadIdx.x < w ? rd[p0 + threadIdx.x] : 0.0;
+  }
+  {
+    const int q = threadIdx.x % WW, k = threadIdx.x / WW;  // 512 threads cover 16 x 32
+    if (k < WW) Ub[k][q] = (k < w && q < w) ? U[(int64_t)(p0 + k) * n + p0 + q] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < WW * WW) {
+    const int tt = threadIdx.x / WW, q = threadIdx.x % WW;
+    Sb[tt][q] = (tt < w && q < w) ? Lb[prow[tt] * ldl + p0 + q] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < w) {  // multipliers of winner t: S_j row -> substitution with U's block
+    const int tt = threadIdx.x;
+    double l[WW];
+#pragma unroll
+    for (int q = 0; q < WW; q++) l[q] = Sb[tt][q];
+#pragma unroll
+    for (int q = 0; q < WW; q++) {
+      if (q < tt) {
+        double v = l[q];
+#pragma unroll
+        for (int k = 0; k < q; k++) v = __fma_rn(-l[k], Ub[k][q], v);
+        l[q] = __dmul_rn(v, rdb[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < WW; q++) lw[tt][q] = l[q];
+  }
+  double acc = (t < w && c < n) ? X[prow[t] * ldx + c] : 0.0;
+  for (int k0 = 0; k0 < p0; k0 += UR_K) {
+    for (int e = threadIdx.x; e < WW * UR_K; e += blockDim.x) {
+      const int tt = e / UR_K, kk = e - tt * UR_K;
+      Lw[tt][kk] = (tt < w && k0 + kk < p0) ? Lb[prow[tt] * ldl + k0 + kk] : 0.0;
+    }
+    for (int e = threadIdx.x; e < UR_K * UR_C; e += blockDim.x) {
+      const int kk = e / UR_C, x = e - kk * UR_C, cc = p0 + w + blockIdx.x * UR_C + x;
+      Ut[kk][x] = (k0 + kk < p0 && cc < n) ? U[(int64_t)(k0 + kk) * n + cc] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(UR_K, p0 - k0);
+    for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-Lw[t][kk], Ut[kk][tx], acc);
+    __syncthreads();
+  }
+  P[t][tx] = acc;
+  __syncthreads();
+  if (t == 0 && c < n) {
+    double u[WW];
+#pragma unroll
+    for (int tt = 0; tt < WW; tt++) {
+      if (tt < w) {
+        double v = P[tt][tx];
+#pragma unroll
+        for (int q = 0; q < tt; q++) v = __fma_rn(-lw[tt][q], u[q], v);
+        u[tt] = v;
+        U[(int64_t)(p0 + tt) * n + c] = v;
+      }
+    }
+  }
+}
+
+// Last panel: S -> L in place (forward substitution with U's diagonal block).
+__global__ void __launch_bounds__(256)
+tslw_lfinal_kernel(double* __restrict__ Lb, int64_t ldl, int64_t rows, int pl, int wl, int n,
+                   const double* __restrict__ U, const double* __restrict__ rd) {
+  __shared__ double Ub[WW][WW];
+  __shared__ double rdp[WW];
+  pdl_trigger();
+  pdl_wait();
+  for (int e = threadIdx.x; e < WW * WW; e += blockDim.x) {
+    const int k = e / WW, c = e - k * WW;
+    Ub[k][c] = (k < wl && c < wl) ? U[(int64_t)(pl + k) * n + pl + c] : 0.0;
+  }
+  if (threadIdx.x < WW) rdp[threadIdx.x] = threadIdx.x < wl ? rd[pl + threadIdx.x] : 0.0;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double* lr = Lb + r * ldl + pl;
+  double l[WW];
+#pragma unroll
+  for (int c = 0; c < WW; c++) l[c] = c < wl ? lr[c] : 0.0;
+#pragma unroll
+  for (int c = 0; c < WW; c++) {
+    if (c < wl) {
+      double v = l[c];
+#pragma unroll
+      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], Ub[k][c], v);
+      l[c] = __dmul_rn(v, rdp[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < WW; c++)
+    if (c < wl) lr[c] = l[c];
+}
+
+// Pivot row t: L11 row t = its L row in columns < t, 1 on the diagonal, 0 right of it; the
+// same values overwrite its L row (pivot rows take their L11 rows, oracle l_row).
+__global__ void tslw_fixup_kernel(double* __restrict__ Lb, int64_t ldl, int64_t row0, const int64_t* __restrict__ piv,
+                                  int n, double* __restrict__ L11) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  const int64_t r = piv[t] - row0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double v = c < t ? Lb[r * ldl + c] : (c == t ? 1.0 : 0.0);
+    L11[(int64_t)t * n + c] = v;
+    if (c >= t) Lb[r * ldl + c] = v;
+  }
+}
+
+}  // namespace
+
+bool tslw_cfg(const rlhc_tslu_cfg& c) {
+  return c.leaf_rows == WR && c.panel >= 1 && c.panel <= WW && c.arity >= 2 && c.arity * WW <= WR;
+}
+
+size_t tslw_slots(int64_t rows) { return (size_t)ceil_div<int64_t>(rows, WR); }
+
+// PX = LU on rows x n (global ids row0 + local row).  Lb (rows x n, ldl) receives L in
+// original row order (pivot rows: their L11 rows); ids/cnt: two slot buffers of
+// tslw_slots(rows) * 16 ids and counts; chosen: rows bytes; rd: 1/diag(U).
+cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
+                     int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
+                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st) {
+  (void)lw;
+  cudaError_t e;
+  const int nleaves = (int)tslw_slots(rows);
+  // slots: level 0 in ids[0]/cnt[0]; levels >= 1 packed in ids[1]/cnt[1]; the arrival
+  // counters of levels >= 1 follow the packed counts in cnt[1]
+  size_t above = 0;
+  for (int ns = nleaves; ns > 1; ns = ceil_div(ns, arity)) above += ceil_div(ns, arity);
+  int* arrive = cnt[1] + above;
+  if ((e = cudaMemsetAsync(chosen, 0, (size_t)rows, st))) return e;
+  if ((e = cudaMemsetAsync(U, 0, (size_t)n * n * sizeof(double), st))) return e;
+  if ((e = cudaMemsetAsync(arrive, 0, above * sizeof(int), st))) return e;
+  static bool attr = false;
+  if (!attr) {
+    const int mx = 227 * 1024;
+    cudaFuncSetAttribute(tslw_schur_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(tslw_schur_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(tslw_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
+    attr = true;
+  }
+  const TslwRoot root{U, piv, rd, nullptr, chosen, status, row0, n};
+  int pl = 0, wl = 0;
+  for (int p0 = 0; p0 < n; p0 += WW) {
+    const int w = std::min(WW, n - p0);
+    const size_t smem = schur_smem(p0);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const unsigned sgrid = (unsigned)ceil_div<int64_t>(rows, SR);
+    note_launch();
+    e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+                        sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U, (const double*)rd,
+                        check_input ? status : nullptr)
+           : launch_pdl(tslw_schur_kernel<false>, dim3(sgrid), dim3(SR), smem, st, X, ldx, Lb, ldl, rows, p0, w, n,
+                        (const double*)U, (const double*)rd, check_input ? status : nullptr);
+    if (e) return e;
+    note_launch();
+    e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
+                   (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0], cnt[0],
+                   ids[1], cnt[1], arrive, arity, root);
+    if (e) return e;
+    if (p0 + w < n) {
+      note_launch();
+      e = launch_pdl(tslw_urows_kernel, dim3(ceil_div(n - p0 - w, UR_C)), dim3(WW * UR_C), 0, st, X, ldx,
+                     (const double*)Lb, ldl, row0, p0, w, n, (const int64_t*)piv, U, (const double*)rd);
+      if (e) return e;
+    }
+    pl = p0;
+    wl = w;
+  }
+  note_launch();
+  e = launch_pdl(tslw_lfinal_kernel, dim3((unsigned)ceil_div<int64_t>(rows, 256)), dim3(256), 0, st, Lb, ldl, rows, pl,
+                 wl, n, (const double*)U, (const double*)rd);
+  if (e) return e;
+  note_launch();
+  return launch_pdl(tslw_fixup_kernel, dim3(n), dim3(128), 0, st, Lb, ldl, row0, (const int64_t*)piv, n, L11);
+}
+
+}  // namespace rlhc

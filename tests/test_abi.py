@@ -44,15 +44,16 @@ def test_sm100a_cubin(L):
 def test_default_cfg_and_workspace(L):
     from paper_2412_06551_b200 import _lib
     c = _lib.TsluCfg()
-    for (m, n, exp) in [(2048, 16, (512, 32, 16)), (65536, 64, (256, 4, 64)), (1 << 20, 128, (256, 4, 64)),
-                        (262144, 512, (256, 4, 64)), (1000, 40, (256, 6, 40))]:
+    # the warp tournament's contract: 16-column panels, 128-row leaves, nodes of 8 children
+    for (m, n, exp) in [(2048, 16, (128, 8, 16)), (65536, 64, (128, 8, 16)), (1 << 20, 128, (128, 8, 16)),
+                        (262144, 512, (128, 8, 16)), (1000, 40, (128, 8, 16)), (100, 5, (128, 8, 5))]:
         L.rlhc_default_tslu_cfg(m, n, ctypes.byref(c))
         assert c.as_tuple() == exp, (m, n, c.as_tuple())
     assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, None) > 0
     assert L.rlhc_workspace_size(1, 1 << 20, 128, 1024, 256, None) > 0
     assert L.rlhc_workspace_size(0, 65536, 64, 32, 0, None) == 0        # s < n
     assert L.rlhc_workspace_size(1, 65536, 64, 128, 256, None) == 0     # s2 > s1
-    bad = _lib.TsluCfg(100, 4, 64)
+    bad = _lib.TsluCfg(300, 4, 64)  # leaves larger than a select CTA holds
     assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(bad)) == 0
 
 

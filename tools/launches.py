@@ -34,3 +34,6 @@ for k, v in last:
 print(f"calls={len(calls)} kernels/call={len(last)} total={tot/1000:.1f} us")
 for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"  {v/1000:9.1f} us  {100*v/tot:5.1f}%  x{c:<3d} {k}")
+if len(sys.argv) > 2 and sys.argv[2] == "--seq":
+    for k, v in last:
+        print(f"  {v/1000:9.2f} us  {k}")
