@@ -55,7 +55,9 @@ def stage_model(cfg: synth.Config) -> dict:
     srows = cfg.s if cfg.algo == "slhc3" else cfg.s1
     sk_flops = 2.0 * cfg.s * m * n if cfg.algo == "slhc3" else m * n + 2.0 * cfg.s2 * cfg.s1 * n
     return {
-        "check_finite": (M, 0.0), "tslu": (M, m * n * n * 1.0), "lfactor": (2 * M, m * n * n * 1.0),
+        # tslu: the warp tournament reads X and writes L (the L factor is its by-product,
+        # the lfactor stage is empty); m n^2 flop of elimination + the panels' Schur updates
+        "check_finite": (M, 0.0), "tslu": (2 * M, m * n * n * 1.0), "lfactor": (2 * M, m * n * n * 1.0),
         "sketch": (M + 8.0 * srows * n, sk_flops), "hqr_y": (0.0, 2.0 * srows * n * n),
         "solve_w_gram1": (2 * M, m * n * n + tri), "chol1": (0.0, n ** 3 / 3.0),
         "solve_v_gram2": (2 * M, m * n * n + tri), "chol2": (0.0, n ** 3 / 3.0),
@@ -135,12 +137,27 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     code = res.info()
     if code[0] != 0:
         raise RuntimeError(f"warm-up run failed: info={code}")
+    # stage breakdown and kernels per call from direct calls (untimed)
     _lib.lib().rlhc_stage_timing(1)
     _lib.stage_times()  # drain
+    l0 = _lib.lib().rlhc_launch_count()
+    for _ in range(3):
+        flush.zero_()
+        res = run()
+    torch.cuda.synchronize(dev)
+    per_call = (_lib.lib().rlhc_launch_count() - l0) // 3
+    stages = _lib.stage_times()
+    _lib.lib().rlhc_stage_timing(0)
+    # timed steps: one CUDA graph launch per step (rlhc_graph_*, the whole call captured once)
+    use_graph = args.graph and world == 1 and isinstance(plan, rl.Plan)
+    if use_graph:
+        plan.capture(X)
+        run = plan.replay
+        for _ in range(args.warmup):
+            res = run()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    launches0 = _lib.lib().rlhc_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev.index) as clk:
         for k in range(args.steps):
@@ -149,9 +166,7 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
             res = run()
             evs[k][1].record(stream)
         torch.cuda.synchronize(dev)
-    launches = _lib.lib().rlhc_launch_count() - launches0
-    stages = _lib.stage_times()
-    _lib.lib().rlhc_stage_timing(0)
+    launches = per_call * args.steps
     ms = sum(a.elapsed_time(b) for a, b in evs)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -298,6 +313,9 @@ def main():
                     help="N > 1: fixed global m (the config's), rows split over ranks; default: weak scaling, "
                          "every rank holds the config's m rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="time the call as one CUDA graph launch per step (default, N = 1)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--kappa-exp", type=int, default=None,
                     help="override the config's kappa = 1e<k> (default for --method cholqr2: min(k, 6), "
                          "CholeskyQR2 breaks down once kappa^2 u > 1, P:34)")
@@ -332,7 +350,9 @@ def main():
             "config": {"workload": workload, "m": m_global, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
                        "kappa": f"1e{cfg.kappa_exp}", "l2": "flushed between steps (512 MiB write)",
                        "rows_per_gpu": m_global // world,
-                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "1 GPU"}}
+                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "1 GPU",
+                       "launch": ("one CUDA graph per step (rlhc_graph_*)" if args.graph and world == 1
+                                  and args.method in ("auto", "slhc3", "sslhc3") else "stream launches")}}
     if args.impl == "reference":
         if rank != 0:
             return

@@ -275,6 +275,23 @@ int rlhc_sslhc3_dist(const double* X, int64_t m_local, int64_t n, int64_t ldx, i
 const char* rlhc_version(void);
 const char* rlhc_last_error(void);
 
+/* ---------------------------------------------------------------- CUDA graphs */
+/* Launch-latency cut for small problems: capture one
+ * stream-ordered call (rlhc_slhc3, rlhc_sslhc3, a comparison method, a stage entry point)
+ * into a CUDA graph and replay it.  rlhc_graph_begin(stream) starts a thread-local
+ * capture on `stream` (which must not be the legacy default stream); the calls issued on
+ * it are recorded, not run; rlhc_graph_end(stream, &g) instantiates the graph.
+ * rlhc_graph_launch(g, stream) replays it: the same kernels on the same pointers (the
+ * CONTENTS of X may change between replays; sizes, pointers and workspace may not).
+ * Stage timing is suspended while capturing.  Returns RLHC_OK, RLHC_EINVAL (null / no
+ * capture in progress) or RLHC_ECUDA (rlhc_last_error has the CUDA message; a failed
+ * end discards the capture). */
+typedef struct rlhc_graph_s* rlhc_graph_t;
+int rlhc_graph_begin(rlhc_stream_t stream);
+int rlhc_graph_end(rlhc_stream_t stream, rlhc_graph_t* graph);
+int rlhc_graph_launch(rlhc_graph_t graph, rlhc_stream_t stream);
+void rlhc_graph_destroy(rlhc_graph_t graph);
+
 /* ---------------------------------------------------------------- diagnostics */
 /* Number of CUDA kernels this library has launched in the calling process. */
 uint64_t rlhc_launch_count(void);

@@ -110,6 +110,40 @@ class Plan:
         check(rc)
         return Result(self.Q, self.R, self.piv, self.info_dev)
 
+    def capture(self, X: torch.Tensor) -> None:
+        """Record run(X) as a CUDA graph (rlhc_graph_*); replay() then
+        reruns the whole call on X's current contents with one graph launch."""
+        self.run(X)  # first launches (module loading) outside the capture
+        torch.cuda.synchronize(self.device)
+        side = torch.cuda.Stream(device=self.device)
+        with torch.cuda.stream(side):
+            st = _stream(self.device)
+            check(lib().rlhc_graph_begin(st))
+            g = ctypes.c_void_p()
+            try:
+                self.run(X)
+            finally:
+                rc = lib().rlhc_graph_end(st, ctypes.byref(g))
+            check(rc)
+        self.release_graph()
+        self._graph = g
+
+    def replay(self) -> Result:
+        check(lib().rlhc_graph_launch(self._graph, _stream(self.device)))
+        return Result(self.Q, self.R, self.piv, self.info_dev)
+
+    def release_graph(self) -> None:
+        g = getattr(self, "_graph", None)
+        if g is not None and g.value:
+            lib().rlhc_graph_destroy(g)
+        self._graph = None
+
+    def __del__(self):
+        try:
+            self.release_graph()
+        except Exception:
+            pass
+
 
 def slhc3(X: torch.Tensor, s: int, seed: int = 0, cfg=None) -> Result:
     """SLHC3 (PAPER.md alg:SLHC3) on a CUDA fp64 row-major X (m x n)."""

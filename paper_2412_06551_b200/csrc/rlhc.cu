@@ -58,6 +58,8 @@ Marks prof_begin(cudaStream_t st) {
   Marks m;
   std::lock_guard<std::mutex> g(g_prof.mu);
   if (!g_prof.enabled) return m;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return m;
   if (!g_prof.pool.empty()) {
     m.ev = g_prof.pool.back();
     g_prof.pool.pop_back();
@@ -690,5 +692,48 @@ int rlhc_stage_times(double* ms, int max_stages) {
 
 const char* rlhc_stage_name(int k) { return (k >= 0 && k < kStages) ? kStageNames[k] : ""; }
 const char* rlhc_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- CUDA graphs
+struct rlhc_graph_s {
+  cudaGraphExec_t exec;
+};
+
+extern "C" {
+
+int rlhc_graph_begin(rlhc_stream_t stream) {
+  if (!stream) return fail(RLHC_EINVAL, "graph capture needs a non-default stream");
+  CUDA_TRY(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return RLHC_OK;
+}
+
+int rlhc_graph_end(rlhc_stream_t stream, rlhc_graph_t* graph) {
+  if (!stream || !graph) return fail(RLHC_EINVAL, "null argument");
+  *graph = nullptr;
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    g_last_error = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e);
+    return RLHC_ECUDA;
+  }
+  *graph = new rlhc_graph_s{ex};
+  return RLHC_OK;
+}
+
+int rlhc_graph_launch(rlhc_graph_t graph, rlhc_stream_t stream) {
+  if (!graph) return fail(RLHC_EINVAL, "null graph");
+  CUDA_TRY(cudaGraphLaunch(graph->exec, (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+void rlhc_graph_destroy(rlhc_graph_t graph) {
+  if (!graph) return;
+  cudaGraphExecDestroy(graph->exec);
+  delete graph;
+}
 
 }  // extern "C"

@@ -50,7 +50,6 @@ __device__ long long g_stp[64];
 #define TW_STEP(i)
 #endif
 
-namespace {
 
 constexpr int WW = kTslwPanel;  // panel width
 constexpr int RS = 4;           // candidate slots per lane
@@ -827,7 +826,6 @@ __global__ void tslw_fixup_kernel(double* __restrict__ Lb, int64_t ldl, int64_t 
   }
 }
 
-}  // namespace
 
 bool tslw_cfg(const rlhc_tslu_cfg& c) {
   return c.leaf_rows == WR && c.panel >= 1 && c.panel <= WW && c.arity >= 2 && c.arity * WW <= WR;

@@ -220,3 +220,25 @@ def test_rank_deficient_multipanel(rl, m, n, col):
     assert res.info() == (3, 1, col)
     res = rl.slhc3(X, s=2 * n, seed=1)
     assert res.info()[:2] == (3, 1)
+
+
+@pytest.mark.gpu
+def test_graph_replay_bitwise():
+    """rlhc_graph_* (SURVEY 8(f) NEXT-4): one captured call replayed on new contents of X gives
+    bit-for-bit the direct call's Q, R and pivots."""
+    import paper_2412_06551_b200 as rl
+    dev = torch.device("cuda", 0)
+    m, n = 4096, 32
+    X = synth.baseline_matrix(m, n, 10, 5, device=dev)
+    X2 = synth.baseline_matrix(m, n, 12, 6, device=dev)
+    ref = rl.Plan("slhc3", m, n, s=64, seed=3, device=dev)
+    r2 = ref.run(X2)
+    Q2, R2, p2 = r2.Q.clone(), r2.R.clone(), r2.piv.clone()
+    plan = rl.Plan("slhc3", m, n, s=64, seed=3, device=dev)
+    plan.capture(X)
+    X.copy_(X2)  # same buffer, new contents
+    res = plan.replay()
+    torch.cuda.synchronize()
+    assert res.info() == (0, 0, 0)
+    assert torch.equal(res.piv, p2) and torch.equal(res.R, R2) and torch.equal(res.Q, Q2)
+    plan.release_graph()

@@ -44,7 +44,7 @@ def split_stages(call):
         base = name.split("<")[0]
         if base in ("status_init_kernel", "check_finite_kernel"):
             stage = "check_finite"
-        elif base.startswith("tslu_") or base in ("gather_rows_kernel", "l11_fixup_kernel", "trsm_rows_kernel") \
+        elif base.startswith(("tslu_", "tslw_", "<unnamed>::tslw_")) or base in ("gather_rows_kernel", "l11_fixup_kernel", "trsm_rows_kernel") \
                 and stage in ("check_finite", "tslu"):
             stage = "tslu"
             seen_tslu = True
