@@ -151,7 +151,9 @@ int rlhc_gram(const double* A, int64_t rows, int64_t n, int64_t lda, double* G, 
 
 /* out = A T^{-1} for n x n upper-triangular T ("Q = X R^{-1}").
  * mode RLHC_SUBST: row-wise substitution (backward stable for any kappa(T); used for
- * U and Y).  mode RLHC_INV_GEMM: T^{-1} formed once (n x n) then a streaming product
+ * U and Y); for n <= 64 with the oracle's operation sequence per element (acc = a_k;
+ * acc -= o_j T_jk as a rounded product then a rounded difference, j increasing; o_k =
+ * acc / T_kk, IEEE division), for n > 64 blocked with the fma chain.  mode RLHC_INV_GEMM: T^{-1} formed once (n x n) then a streaming product
  * (used in the CholeskyQR2 tail where kappa(T) <= ~7).  out may equal A
  * (same pointer and ld: in place) but must not partially overlap it.  G_out: nullable
  * n x n, the Gram of out fused into the same pass.  A zero diagonal of T ->

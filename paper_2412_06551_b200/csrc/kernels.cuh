@@ -94,6 +94,12 @@ cudaError_t launch_trsm_blocked(const double* A, int64_t lda, int64_t rows, int 
 cudaError_t launch_pivot_rows(const int64_t* piv, int n, int64_t row0, int64_t rows, const double* L11, double* out,
                               int64_t ldo, cudaStream_t st);
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st);
+// out = A T^{-1} with the oracle's op sequence (separate multiply and subtract, IEEE
+// division), n <= 64; out may alias A; G != null: G = out^T out fused (partials in gpart)
+bool subst_ms_ok(int n);
+size_t subst_ms_partials_bytes(int64_t rows, int n);
+cudaError_t launch_subst_ms(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,
+                            double* out, int64_t ldo, double* gpart, double* G, cudaStream_t st);
 
 // sketch.cu
 size_t gauss_partials_bytes(int64_t rows, int n, int s);

@@ -201,6 +201,7 @@ void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   a.Ls = c.take<double>((size_t)srows * n);
   a.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
   size_t part = std::max(gram_partials_bytes(m, (int)n), rowsolve_partials_bytes(m, (int)n));
+  part = std::max(part, subst_ms_partials_bytes(m, (int)n));
   part = std::max(part, algo == RLHC_SLHC3 ? gauss_partials_bytes(m, (int)n, (int)s_or_s1)
                                            : gauss_partials_bytes(s_or_s1, (int)n, (int)s2));
   a.part = c.take<double>(part / sizeof(double) + 1);
@@ -231,9 +232,13 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   }
   mk.mark(2);
   // one streaming pass: out = A T^{-1} (substitution) [+ G = out^T out fused]
+  // ms: the oracle's op sequence (DESIGN.md R#O9) for solves with an ill-conditioned T (W = X Y^{-1});
+  // the CholeskyQR passes (kappa(D), kappa(J) <= ~7) keep the faster fma chain
   auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
-                        const double* l11, double* G) -> int {
-    if (rowsolve_ok(ni)) {
+                        const double* l11, double* G, bool ms = false) -> int {
+    if (ms && !pp && subst_ms_ok(ni)) {  // the oracle's op sequence (DESIGN.md R#O9), then the Gram
+      CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
+    } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
     } else {
       CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
@@ -261,7 +266,7 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
   mk.mark(5);
   // W = X Y^{-1} by substitution, fused G1 = W^T W (first Gram of CholeskyQR2)
-  if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+  if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true))) return rc;
   mk.mark(6);
   // CholeskyQR2(W): D = chol(G1), V = W D^{-1} (+ G2), J = chol(G2), Q = V J^{-1}
   CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st, ni <= 128 ? a.Di : nullptr));
@@ -294,9 +299,13 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
   CUDA_TRY(launch_status_init(status, st));
   CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
   // out = A T^{-1} (substitution, into Q) [+ G = out^T out]
+  // ms: the oracle's op sequence (DESIGN.md R#O9) for solves with an ill-conditioned T (W = X Y^{-1});
+  // the CholeskyQR passes (kappa(D), kappa(J) <= ~7) keep the faster fma chain
   auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
-                        const double* l11, double* G) -> int {
-    if (rowsolve_ok(ni)) {
+                        const double* l11, double* G, bool ms = false) -> int {
+    if (ms && !pp && subst_ms_ok(ni)) {  // the oracle's op sequence (DESIGN.md R#O9), then the Gram
+      CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
+    } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
     } else {
       CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
@@ -319,7 +328,7 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
     CUDA_TRY(launch_gram(X, ldx, m, ni, a.part, a.G, st));
     if (method == RLHC_SCHOLQR3) CUDA_TRY(launch_shift_diag(a.G, ni, m, st));
     if ((rc = chol(a.Y, a.rdY, RLHC_STAGE_CHOL0))) return rc;
-    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true))) return rc;
     if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
     if (method == RLHC_CHOLQR2) {  // [Q, Z] = CholeskyQR(W), R = Z Y
       if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
@@ -344,7 +353,7 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
     CUDA_TRY(launch_trmm_uu(a.S, a.U, ni, a.Y, st));
     CUDA_TRY(launch_flip_neg_rows(a.Y, ni, st));
     CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
-    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true))) return rc;
     if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
     if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
     CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, R, st));
@@ -356,7 +365,7 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
     CUDA_TRY(launch_hqr(a.Ls, (int)s2, ni, n, nullptr, a.Y, a.work, status, st));
     CUDA_TRY(launch_flip_neg_rows(a.Y, ni, st));
     CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
-    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G))) return rc;
+    if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true))) return rc;
     if ((rc = chol(a.D, a.Di, RLHC_STAGE_CHOL1))) return rc;
     if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, nullptr))) return rc;
     CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, R, st));
@@ -615,7 +624,9 @@ int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(launch_status_init(status, st));
   CUDA_TRY(launch_rdiag(T, (int)n, n, rd, RLHC_STAGE_SOLVE_Y, status, st));
-  if (mode == RLHC_SUBST) {
+  if (mode == RLHC_SUBST && subst_ms_ok((int)n)) {
+    CUDA_TRY(launch_subst_ms(A, lda, rows, (int)n, T, n, out, ldo, nullptr, nullptr, st));
+  } else if (mode == RLHC_SUBST) {
     CUDA_TRY(launch_trsm_rows(A, lda, rows, (int)n, (int)n, T, n, rd, out, ldo, nullptr, nullptr, 0, st));
   } else {
     CUDA_TRY(launch_tri_inv(T, (int)n, Ti, st));

@@ -898,3 +898,156 @@ cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, doubl
 }
 
 }  // namespace rlhc
+
+namespace rlhc {
+
+// ------------------------------------------------------------------ substitution, oracle op order
+// out = A T^{-1} (T upper, n <= 64) with the oracle's operation sequence (ora_trsm_right_upper,
+// DESIGN.md R#O9): acc = a_k; acc = acc - (o_j * T[j][k]) for j < k (a rounded product, then a
+// rounded difference: no fma); o_k = acc / T[k][k] (IEEE division).  Used for W = X Y^{-1}
+// and the CholeskyQR passes: the fma chain amplifies cancellation in W on the
+// arrowhead of P:1071-1082 (|W| 1.5e10 instead of 19 at beta = 1e-25, tools/arrow_fma.py),
+// this sequence does not; W is then bit-identical to the oracle's.  Thread per row, the
+// row in registers (static indices), T in shared memory (broadcast reads), row tiles staged
+// through shared memory with coalesced cp.async; out may alias A.
+constexpr int SMS_R = 128, SMS_LD = 65;
+__host__ __device__ inline int sms_smem_bytes() { return (64 * 64 + 64 + SMS_R * SMS_LD) * (int)sizeof(double); }
+// Persistent: each CTA stages T^T once, then loops over 128-row tiles; with GRAM the CTA
+// accumulates its partial W^T W of the upper 32 x 32 tiles on DMMA from the solved tile
+// (warp q < 3: tile (0,0), (0,1), (1,1)), reduced by gram_part_reduce_kernel.
+// Right-looking with ROTATED registers: at step k, acc[c] holds column k + c of the row, so
+// acc[0] is divided by T_kk and every later column receives - o_k T[k][k+c] (a rounded
+// product, then a rounded difference): per element the same terms in the same (increasing
+// j) order as the oracle's left-looking loop.  A compact loop (the fully unrolled
+// triangle was instruction-bound), up to 63 independent updates per step; the rotation
+// narrows to 48, 32, 16 slots as the live columns shrink.
+template <int NS>
+RLHC_DEV void sms_steps(double (&acc)[64], int k0, int k1, const double* Tsh, const double* diag, double* orow) {
+#pragma unroll 1
+  for (int k = k0; k < k1; k++) {
+    const double wk = __ddiv_rn(acc[0], diag[k]);
+    orow[k] = wk;
+    const double* u = Tsh + k * 64;  // u[c] = T[k][k + 1 + c] (0 past n)
+#pragma unroll
+    for (int c = 0; c < NS - 1; c += 2) {
+      const double2 uu = *reinterpret_cast<const double2*>(u + c);
+      acc[c] = __dsub_rn(acc[c + 1], __dmul_rn(wk, uu.x));
+      if (c + 1 < NS - 1) acc[c + 1] = __dsub_rn(acc[c + 2], __dmul_rn(wk, uu.y));
+    }
+    acc[NS - 1] = 0.0;
+  }
+}
+template <bool GRAM>
+__global__ void __launch_bounds__(SMS_R, 2)
+subst_ms_kernel(const double* A, int64_t lda, int64_t rows, int n, const double* __restrict__ T, int64_t ldt,
+                double* out, int64_t ldo, double* __restrict__ gpart) {
+  extern __shared__ __align__(16) double sms[];
+  double* Tsh = sms;              // [64][64]: Tsh[k][c] = T[k][k + 1 + c]
+  double* diag = Tsh + 64 * 64;   // [64]
+  double* tile = diag + 64;       // [SMS_R][SMS_LD]
+  const int tid = threadIdx.x, lane = lane_id(), wq = warp_id();
+  const int g = lane >> 2, t = lane & 3;
+  for (int e = tid; e < 64 * 64; e += SMS_R) {
+    const int k = e >> 6, c = e & 63, j = k + 1 + c;
+    Tsh[e] = (k < n && j < n) ? T[(int64_t)k * ldt + j] : 0.0;
+  }
+  if (tid < 64) diag[tid] = tid < n ? T[(int64_t)tid * ldt + tid] : 1.0;
+  const int ncp = (n + 7) & ~7;
+  const int gt = (ncp + 31) / 32;
+  const int gti = wq >> 1, gtj = (wq == 0) ? 0 : 1;  // warp 0: (0,0), 1: (0,1), 2: (1,1)
+  const bool gwork = GRAM && wq < 3 && gtj < gt && gti < gt;
+  double gacc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) gacc[a][b][0] = gacc[a][b][1] = 0.0;
+  const int64_t ntiles = ceil_div<int64_t>(rows, SMS_R);
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int64_t r0 = tl * SMS_R;
+    __syncthreads();  // previous tile consumed (stores and Gram)
+    for (int e = tid; e < SMS_R * 64; e += SMS_R) {
+      const int q = e >> 6, c = e & 63;
+      const bool in = r0 + q < rows && c < n;
+      cp_async8(tile + q * SMS_LD + c, in ? A + (r0 + q) * lda + c : A, in ? 8 : 0);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    double acc[64];
+    double* orow = tile + tid * SMS_LD;
+#pragma unroll
+    for (int c = 0; c < 64; c++) acc[c] = orow[c];
+    // at step k the live columns are k .. n-1: rotate 64, 48, 32, 16 slots as they shrink
+    sms_steps<64>(acc, 0, min(n, 16), Tsh, diag, orow);
+    sms_steps<48>(acc, min(n, 16), min(n, 32), Tsh, diag, orow);
+    sms_steps<32>(acc, min(n, 32), min(n, 48), Tsh, diag, orow);
+    sms_steps<16>(acc, min(n, 48), n, Tsh, diag, orow);
+    __syncthreads();
+    for (int e = tid; e < SMS_R * 64; e += SMS_R) {
+      const int q = e >> 6, c = e & 63;
+      if (r0 + q < rows && c < n) out[(r0 + q) * ldo + c] = tile[q * SMS_LD + c];
+    }
+    if (gwork) {  // G(ti, tj) += W(:, ti block)^T W(:, tj block) over the tile's rows
+#pragma unroll 2
+      for (int k0 = 0; k0 < SMS_R; k0 += 4) {
+        double af[4], bf[4];
+        const double* rowp = tile + (k0 + t) * SMS_LD;
+#pragma unroll
+        for (int a = 0; a < 4; a++) af[a] = rowp[gti * 32 + a * 8 + g];
+#pragma unroll
+        for (int b = 0; b < 4; b++) bf[b] = rowp[gtj * 32 + b * 8 + g];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) dmma(gacc[a][b][0], gacc[a][b][1], af[a], bf[b]);
+      }
+    }
+  }
+  if (gwork) {
+    double* P = gpart + (size_t)blockIdx.x * ncp * ncp;
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const int gr = gti * 32 + a * 8 + g, gc = gtj * 32 + b * 8 + 2 * t;
+        if (gr < ncp && gc < ncp) {
+          P[gr * ncp + gc] = gacc[a][b][0];
+          P[gr * ncp + gc + 1] = gacc[a][b][1];
+        }
+      }
+  }
+}
+
+static int sms_grid(int64_t rows) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, SMS_R), (int64_t)kSMs * 2));
+}
+size_t subst_ms_partials_bytes(int64_t rows, int n) {
+  const int ncp = (n + 7) & ~7;
+  return (size_t)sms_grid(rows) * ncp * ncp * sizeof(double);
+}
+
+bool subst_ms_ok(int n) { return n <= 64; }
+
+cudaError_t launch_subst_ms(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,
+                            double* out, int64_t ldo, double* gpart, double* G, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int smem = sms_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(subst_ms_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (!e) e = cudaFuncSetAttribute(subst_ms_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e) return e;
+    attr = true;
+  }
+  const int grid = sms_grid(rows);
+  note_launch();
+  if (G) subst_ms_kernel<true><<<grid, SMS_R, smem, st>>>(A, lda, rows, n, T, ldt, out, ldo, gpart);
+  else subst_ms_kernel<false><<<grid, SMS_R, smem, st>>>(A, lda, rows, n, T, ldt, out, ldo, gpart);
+  if (!G) return cudaGetLastError();
+  const int ncp = (n + 7) & ~7;
+  note_launch();
+  gram_part_reduce_kernel<<<(int)ceil_div<int64_t>((int64_t)ncp * ncp, 32), 256, 0, st>>>(gpart, grid, n, ncp, G);
+  return cudaGetLastError();
+}
+
+}  // namespace rlhc

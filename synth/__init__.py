@@ -117,3 +117,19 @@ def arrowhead(m: int, n: int, beta: float, device="cpu") -> torch.Tensor:
     X[:n, :n] = torch.diag(torch.pow(torch.tensor(beta, dtype=torch.float64, device=device), k / (n - 1)))
     X[0, 1:] += -5.0
     return X
+
+
+def sprand(m: int, n: int, density: float, kappa: float, seed: int, device="cpu") -> torch.Tensor:
+    """P:1199 (section 5.3): MATLAB sprand(m, n, density, 1/kappa) stand-in, the SPEC S:469
+    reading: a sparse pattern with iid Bernoulli(density) support and N(0,1) values, its
+    thin SVD, singular values replaced by the geometric ladder 1 ... 1/kappa, recomposed
+    (dense).  The paper does not state sprand's value distribution (SPEC 'Open Questions')."""
+    dev = torch.device(device)
+    g = _gen(seed, dev)
+    vals = torch.randn(m, n, generator=g, device=dev, dtype=torch.float64)
+    mask = torch.rand(m, n, generator=g, device=dev, dtype=torch.float64) < density
+    S = torch.where(mask, vals, torch.zeros((), dtype=torch.float64, device=dev))
+    U, _, Vh = torch.linalg.svd(S, full_matrices=False)
+    k = torch.arange(n, device=dev, dtype=torch.float64)
+    sig = torch.pow(torch.tensor(1.0 / kappa, dtype=torch.float64, device=dev), k / max(n - 1, 1))
+    return ((U * sig.unsqueeze(0)) @ Vh).contiguous()

@@ -242,3 +242,24 @@ def test_graph_replay_bitwise():
     assert res.info() == (0, 0, 0)
     assert torch.equal(res.piv, p2) and torch.equal(res.R, R2) and torch.equal(res.Q, Q2)
     plan.release_graph()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(1000, 7), (4096, 50), (3000, 64)])
+def test_trsm_subst_bitwise(m, n):
+    """W = A T^{-1} for n <= 64 follows the oracle's operation sequence (DESIGN.md R#O9:
+    rounded product, rounded difference, IEEE division): bit for bit, also on the arrowhead
+     where an fma chain would blow up."""
+    import oracle
+    import paper_2412_06551_b200 as rl
+    dev = torch.device("cuda", 0)
+    A = synth.baseline_matrix(m, n, 10, 11, device=dev)
+    Th = np.triu(np.random.default_rng(n).standard_normal((n, n))) + 4 * np.eye(n)
+    T = torch.from_numpy(Th).to(dev)
+    W, _, info = rl.trsm_apply(A, T)
+    assert info == (0, 0, 0)
+    assert np.array_equal(W.cpu().numpy(), oracle.trsm_right_upper(A.cpu().numpy(), Th))
+    X = synth.arrowhead(2000, 50, 1e-25, device=dev)
+    piv, U, L11, L, inf2 = rl.getrf_ts(X, want_L=True)
+    W2, _, _ = rl.trsm_apply(X, U)
+    assert np.array_equal(W2.cpu().numpy(), oracle.trsm_right_upper(X.cpu().numpy(), U.cpu().numpy()))
