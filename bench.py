@@ -127,7 +127,8 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
             s1, s2 = _rhc_sizes(cfg)
             plan = rl.MethodPlan(args.method, cfg.m, cfg.n, s1=s1, s2=s2, seed=cfg.seed, device=dev)
         else:
-            plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, device=dev)
+            tcfg = (cfg.m, 2, min(16, cfg.n)) if args.pivot == "gepp" else None  # one leaf = exact GEPP
+            plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, cfg=tcfg, device=dev)
         run = lambda: plan.run(X)  # noqa: E731
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -316,6 +317,8 @@ def main():
     ap.add_argument("--graph", dest="graph", action="store_true", default=True,
                     help="time the call as one CUDA graph launch per step (default, N = 1)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--pivot", default="tournament", choices=["tournament", "gepp"],
+                    help="pivot contract: the default tournament (CALU) or exact GEPP (one leaf, SURVEY 8(f) NEXT-2)")
     ap.add_argument("--kappa-exp", type=int, default=None,
                     help="override the config's kappa = 1e<k> (default for --method cholqr2: min(k, 6), "
                          "CholeskyQR2 breaks down once kappa^2 u > 1, P:34)")

@@ -59,11 +59,17 @@ struct TslwRoot {          // root outputs of one panel (all null below the root
   int64_t row0;
   int n;
 };
-bool tslw_cfg(const rlhc_tslu_cfg& c);
+// the warp kernels run this contract (tournament (128, <= 8, 16) or one leaf = exact GEPP)
+bool tslw_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
+bool tslg_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
 size_t tslw_slots(int64_t rows);
+// exact GEPP mode (one leaf of all rows): workspace of the panel's working copy
+size_t tslg_ws_bytes(int64_t rows);
+// gepp_ws != null: exact GEPP (one leaf holding every row) instead of the tournament
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
-                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st);
+                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st,
+                     void* gepp_ws = nullptr);
 
 // rows.cu
 cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,

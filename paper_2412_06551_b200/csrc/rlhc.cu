@@ -81,9 +81,9 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int kernel_width(int panel) { return panel <= 16 ? 16 : (panel <= 32 ? 32 : 64); }
 
-bool cfg_ok(const rlhc_tslu_cfg& c, int64_t n) {
+bool cfg_ok(const rlhc_tslu_cfg& c, int64_t m, int64_t n) {
   if (c.panel < 1 || c.panel > 64 || c.panel > n) return false;
-  if (tslw_cfg(c)) return true;
+  if (tslw_cfg(c, m, n)) return true;
   int W = kernel_width(c.panel);
   if (c.leaf_rows < 1 || c.leaf_rows > select_rows(W)) return false;
   if (c.arity < 2 || (int64_t)c.arity * c.panel > select_rows(W)) return false;
@@ -111,6 +111,7 @@ struct TsluWs {
   double* rd;
   double* lw;
   double* Xp;
+  void* gepp;  // exact GEPP mode: the panel's working copy
 };
 
 void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, TsluWs& t) {
@@ -124,6 +125,7 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
   t.chosen = c.take<uint8_t>((size_t)rows);
   t.rd = c.take<double>((size_t)n);
   t.lw = c.take<double>((size_t)kTslwPanel * kTslwPanel);
+  t.gepp = tslg_cfg(cfg, rows, n) ? (void*)c.take<char>(tslg_ws_bytes(rows)) : nullptr;
   t.Xp = c.take<double>((size_t)n * n);
 }
 
@@ -132,9 +134,9 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
 int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg& cfg,
              TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st,
              bool check_input = false) {
-  if (tslw_cfg(cfg)) {  // warp tournament; L (original row order) lands in tw
+  if (tslw_cfg(cfg, rows, n)) {  // warp tournament (or exact GEPP); L (original row order) lands in tw
     CUDA_TRY(run_tslw(X, ldx, rows, row0, (int)n, cfg.arity, tw, ldtw, piv, U, L11, t.rd, t.lw, t.chosen, t.ids,
-                      t.cnt, t.status, check_input, st));
+                      t.cnt, t.status, check_input, st, t.gepp));
     return RLHC_OK;
   }
   const int W = kernel_width(cfg.panel);
@@ -219,13 +221,13 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   mk.mark(0);
   CUDA_TRY(launch_status_init(status, st));
   // input check: a pass of its own, or (one panel) folded into the TSLU leaves' read of X
-  const bool fold_check = cfg.panel >= n || tslw_cfg(cfg);
+  const bool fold_check = cfg.panel >= n || tslw_cfg(cfg, m, n);
   if (!fold_check) CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
   mk.mark(1);
   // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
   int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st, fold_check);
   if (rc) return rc;
-  const bool l_done = tslw_cfg(cfg);  // the warp tournament leaves L in the Q buffer
+  const bool l_done = tslw_cfg(cfg, m, n);  // the warp tournament leaves L in the Q buffer
   if (!l_done) {
     CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
     CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
@@ -343,7 +345,7 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
   } else if (method == RLHC_LUC2) {
     // PX = LU, L (into Q), G = L^T L, S = Cholesky(G), Y = S U (diag > 0, R#23), W = X Y^{-1}
     if ((rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st))) return rc;
-    if (!tslw_cfg(cfg)) {
+    if (!tslw_cfg(cfg, m, n)) {
       CUDA_TRY(launch_fill_i32(a.pivpos, m, -1, st));
       CUDA_TRY(launch_pivpos(piv, ni, 0, m, a.pivpos, st));
       if ((rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
@@ -408,7 +410,7 @@ void rlhc_default_tslu_cfg(int64_t m, int64_t n, rlhc_tslu_cfg* cfg) {
 size_t rlhc_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg* cfgp) {
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
-  if (n < 1 || m < n || !cfg_ok(cfg, n)) return 0;
+  if (n < 1 || m < n || !cfg_ok(cfg, m, n)) return 0;
   if (algo == RLHC_SLHC3 && (s_or_s1 < n || s_or_s1 > m)) return 0;
   if (algo == RLHC_SSLHC3 && (s2 < n || s_or_s1 < s2 || s_or_s1 > m)) return 0;
   if (algo != RLHC_SLHC3 && algo != RLHC_SSLHC3) return 0;
@@ -422,7 +424,7 @@ size_t rlhc_method_workspace_size(int method, int64_t m, int64_t n, int64_t s1, 
   if (method < RLHC_CHOLQR2 || method > RLHC_RHC || n < 1 || m < n) return 0;
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
-  if (!cfg_ok(cfg, n)) return 0;
+  if (!cfg_ok(cfg, m, n)) return 0;
   if (method == RLHC_RHC && (s2 < n || s1 < s2 || s1 > m)) return 0;
   Carver c(nullptr);
   AlgoWs a;
@@ -437,7 +439,7 @@ static int method_entry(int method, const double* X, int64_t m, int64_t n, int64
   if (rc) return rc;
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
-  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
+  if (!cfg_ok(cfg, m, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
   if (method == RLHC_RHC && (s2 < n || s1 < s2 || s1 > m)) return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
   size_t need = rlhc_method_workspace_size(method, m, n, s1, s2, &cfg);
   if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
@@ -476,7 +478,7 @@ static int algo_entry(int algo, const double* X, int64_t m, int64_t n, int64_t l
   if (rc) return rc;
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(m, n, &cfg);
-  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
+  if (!cfg_ok(cfg, m, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration (see rlhc_default_tslu_cfg)");
   if (algo == RLHC_SLHC3 && (s_or_s1 < n || s_or_s1 > m)) return fail(RLHC_EINVAL, "need n <= s <= m");
   if (algo == RLHC_SSLHC3 && (s2 < n || s_or_s1 < s2 || s_or_s1 > m))
     return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
@@ -505,7 +507,7 @@ static size_t getrf_carve(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cf
                           int** pivpos) {
   t.status = c.take<unsigned long long>(4);
   carve_tslu(c, rows, n, cfg, t);
-  *tw = (cfg.panel < n || tslw_cfg(cfg)) ? c.take<double>((size_t)rows * n) : nullptr;
+  *tw = (cfg.panel < n || tslw_cfg(cfg, rows, n)) ? c.take<double>((size_t)rows * n) : nullptr;
   *pivpos = c.take<int>((size_t)rows);
   return c.used;
 }
@@ -513,7 +515,7 @@ static size_t getrf_carve(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cf
 size_t rlhc_getrf_ts_workspace_size(int64_t rows, int64_t n, const rlhc_tslu_cfg* cfgp) {
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(rows, n, &cfg);
-  if (n < 1 || rows < n || !cfg_ok(cfg, n)) return 0;
+  if (n < 1 || rows < n || !cfg_ok(cfg, rows, n)) return 0;
   Carver c(nullptr);
   TsluWs t;
   double* tw;
@@ -530,7 +532,7 @@ int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t
   if (rows > 0x7fffffffLL) return fail(RLHC_EINVAL, "rows must be < 2^31");
   rlhc_tslu_cfg cfg;
   if (cfgp) cfg = *cfgp; else rlhc_default_tslu_cfg(rows, n, &cfg);
-  if (!cfg_ok(cfg, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration");
+  if (!cfg_ok(cfg, rows, n)) return fail(RLHC_EINVAL, "unsupported tslu configuration");
   size_t need = rlhc_getrf_ts_workspace_size(rows, n, &cfg);
   if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
   Carver c(ws);
@@ -540,7 +542,7 @@ int rlhc_getrf_ts(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t
   getrf_carve(c, rows, n, cfg, t, &tw, &pivpos);
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(launch_status_init(t.status, st));
-  if (tslw_cfg(cfg)) {  // input check folded into the leaves; L straight into the caller's buffer
+  if (tslw_cfg(cfg, rows, n)) {  // input check folded into the leaves; L straight into the caller's buffer
     int rc = run_tslu(X, rows, n, ldx, row0, cfg, t, L ? L : tw, L ? ldl : n, piv, U, L11, st, true);
     if (rc) return rc;
     CUDA_TRY(launch_status_finish(t.status, info, st));

@@ -23,8 +23,12 @@
 #include <algorithm>
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rlhc {
 
@@ -827,19 +831,150 @@ __global__ void tslw_fixup_kernel(double* __restrict__ Lb, int64_t ldl, int64_t 
 }
 
 
-bool tslw_cfg(const rlhc_tslu_cfg& c) {
-  return c.leaf_rows == WR && c.panel >= 1 && c.panel <= WW && c.arity >= 2 && c.arity * WW <= WR;
+// ------------------------------------------------------------------ exact GEPP mode
+// One leaf holding every row (leaf_rows >= rows): the tournament of a
+// panel is plain GEPP on all remaining rows (oracle gepp_select with one candidate set),
+// i.e. exact partial pivoting with ties to the smallest row id.  One cooperative launch per
+// panel, thread per row (grid-strided): each step t updates the working copy Sw of the
+// panel's Schur values with step t-1 (the select's own ops: l = a * (1/pivot), a[c] =
+// fma(-l, u[c], a[c])), then the grid finds the pivot in two atomic rounds -- the largest
+// |a| bit pattern, then the smallest row among the rows attaining it -- and the owner
+// publishes the pivot row.  Three grid barriers per step.
+struct TslgScratch {
+  unsigned long long gmax[WW];
+  unsigned int gidx[WW];
+  double prow[WW][WW];
+  double r[WW];
+};
+__global__ void __launch_bounds__(256)
+tslg_kernel(const double* __restrict__ Lb, int64_t ldl, double* __restrict__ Sw, int64_t rows, int64_t row0, int p0,
+            int w, uint8_t* __restrict__ chosen, TslgScratch* sc, TslwRoot ro) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long bkey[8];
+  __shared__ unsigned int bidx[8];
+  __shared__ double up[WW];
+  __shared__ double rprev;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = lane_id(), wq = warp_id();
+  if (tid0 == 0) {
+    for (int t = 0; t < WW; t++) {
+      sc->gmax[t] = 0ull;
+      sc->gidx[t] = 0xffffffffu;
+    }
+  }
+  grid.sync();
+  for (int t = 0; t < w; t++) {
+    if (threadIdx.x < WW) up[threadIdx.x] = t > 0 ? sc->prow[t - 1][threadIdx.x] : 0.0;
+    if (threadIdx.x == 0) rprev = t > 0 ? sc->r[t - 1] : 0.0;
+    __syncthreads();
+    unsigned long long best = 0;
+    unsigned int bi = 0xffffffffu;
+    for (int64_t r = tid0; r < rows; r += nthr) {
+      if (__ldcg(chosen + r)) continue;  // set by another SM during this launch
+      double v[WW];
+      if (t == 0) {
+#pragma unroll
+        for (int c = 0; c < WW; c++) v[c] = c < w ? Lb[r * ldl + p0 + c] : 0.0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < WW; c++) v[c] = Sw[r * WW + c];
+        if (rprev != 0.0) {  // step t-1 was not a zero column (R#5 has no update)
+          double l = 0.0;
+#pragma unroll
+          for (int c = 0; c < WW; c++)
+            if (c == t - 1) l = __dmul_rn(v[c], rprev);
+#pragma unroll
+          for (int c = 0; c < WW; c++) {
+            if (c == t - 1) v[c] = l;
+            else if (c >= t) v[c] = __fma_rn(-l, up[c], v[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < WW; c++) Sw[r * WW + c] = v[c];
+      double vt = 0.0;
+#pragma unroll
+      for (int c = 0; c < WW; c++)
+        if (c == t) vt = v[c];
+      const unsigned long long key = (unsigned long long)__double_as_longlong(vt) & 0x7fffffffffffffffull;
+      if (key > best || bi == 0xffffffffu) {  // rows ascend: the first of equal keys is kept
+        best = key;
+        bi = (unsigned int)r;
+      }
+    }
+    // block maximum of the key, then the grid's
+    unsigned long long k = best;
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, k, o);
+      k = x > k ? x : k;
+    }
+    if (lane == 0) bkey[wq] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); q++) m = bkey[q] > m ? bkey[q] : m;
+      atomicMax(&sc->gmax[t], m);
+    }
+    grid.sync();
+    // the smallest row attaining the maximum (ties -> smallest id, R#4)
+    const unsigned long long gm = sc->gmax[t];
+    unsigned int cand = (bi != 0xffffffffu && best == gm) ? bi : 0xffffffffu;
+    for (int o = 16; o; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+    if (lane == 0) bidx[wq] = cand;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int m = 0xffffffffu;
+      for (int q = 0; q < (int)(blockDim.x >> 5); q++) m = min(m, bidx[q]);
+      if (m != 0xffffffffu) atomicMin(&sc->gidx[t], m);
+    }
+    grid.sync();
+    const unsigned int p = sc->gidx[t];
+    if (tid0 == 0) {  // publish the pivot row (after t updates), 1/pivot; root outputs
+      const bool zero = gm == 0 || p == 0xffffffffu;
+      const unsigned int pp = p == 0xffffffffu ? 0u : p;
+      double pv = 0.0;
+      for (int c = 0; c < WW; c++) {
+        const double x = __ldcg(Sw + (int64_t)pp * WW + c);
+        sc->prow[t][c] = x;
+        if (c == t) pv = x;
+      }
+      const double rr = zero ? 0.0 : __drcp_rn(pv);
+      sc->r[t] = rr;
+      chosen[pp] = 1;
+      ro.piv[p0 + t] = row0 + pp;
+      ro.rd[p0 + t] = rr;
+      if (zero) report(ro.status, RLHC_ERANKDEF, RLHC_STAGE_LU, p0 + t);
+      for (int c = t; c < w; c++) ro.U[(int64_t)(p0 + t) * ro.n + p0 + c] = __ldcg(Sw + (int64_t)pp * WW + c);
+    }
+    grid.sync();
+  }
 }
+
+// The warp kernels use 16-column panels: the contract's panel must be 16, or n when n < 16.
+bool tslw_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n) {
+  if (!(c.panel == WW || (c.panel == n && n < WW))) return false;
+  if (c.leaf_rows >= m && c.arity >= 2) return true;  // exact GEPP mode (one leaf)
+  return c.leaf_rows == WR && c.arity >= 2 && c.arity * WW <= WR;
+}
+bool tslg_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n) { return tslw_cfg(c, m, n) && c.leaf_rows >= m; }
 
 size_t tslw_slots(int64_t rows) { return (size_t)ceil_div<int64_t>(rows, WR); }
 
 // PX = LU on rows x n (global ids row0 + local row).  Lb (rows x n, ldl) receives L in
 // original row order (pivot rows: their L11 rows); ids/cnt: two slot buffers of
 // tslw_slots(rows) * 16 ids and counts; chosen: rows bytes; rd: 1/diag(U).
+size_t tslg_ws_bytes(int64_t rows) { return (size_t)rows * WW * sizeof(double) + sizeof(TslgScratch) + 256; }
+
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
-                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st) {
+                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st,
+                     void* gepp_ws) {
   (void)lw;
+  double* Sw = gepp_ws ? reinterpret_cast<double*>(gepp_ws) : nullptr;  // exact GEPP mode (one leaf)
+  TslgScratch* gsc = gepp_ws ? reinterpret_cast<TslgScratch*>(reinterpret_cast<char*>(gepp_ws) +
+                                                               (((size_t)rows * WW * sizeof(double) + 255) & ~(size_t)255))
+                             : nullptr;
   cudaError_t e;
   const int nleaves = (int)tslw_slots(rows);
   // slots: level 0 in ids[0]/cnt[0]; levels >= 1 packed in ids[1]/cnt[1]; the arrival
@@ -873,11 +1008,27 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
            : launch_pdl(tslw_schur_kernel<false>, dim3(sgrid), dim3(SR), smem, st, X, ldx, Lb, ldl, rows, p0, w, n,
                         (const double*)U, (const double*)rd, check_input ? status : nullptr);
     if (e) return e;
-    note_launch();
-    e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
-                   (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0], cnt[0],
-                   ids[1], cnt[1], arrive, arity, root);
-    if (e) return e;
+    if (Sw) {  // exact GEPP: one cooperative launch per panel
+      static int per_sm = 0;
+      if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tslg_kernel, 256, 0);
+      const int gridg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, 256),
+                                                                    (int64_t)kSMs * std::max(per_sm, 1)));
+      const double* Lbc = Lb;
+      int p0v = p0, wv = w;
+      int64_t rowsv = rows, row0v = row0, ldlv = ldl;
+      TslwRoot rootv = root;
+      void* args[] = {(void*)&Lbc, (void*)&ldlv, (void*)&Sw, (void*)&rowsv, (void*)&row0v, (void*)&p0v, (void*)&wv,
+                      (void*)&chosen, (void*)&gsc, (void*)&rootv};
+      note_launch();
+      e = cudaLaunchCooperativeKernel((const void*)tslg_kernel, dim3(gridg), dim3(256), args, 0, st);
+      if (e) return e;
+    } else {
+      note_launch();
+      e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
+                     (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0],
+                     cnt[0], ids[1], cnt[1], arrive, arity, root);
+      if (e) return e;
+    }
     if (p0 + w < n) {
       note_launch();
       e = launch_pdl(tslw_urows_kernel, dim3(ceil_div(n - p0 - w, UR_C)), dim3(WW * UR_C), 0, st, X, ldx,

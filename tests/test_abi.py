@@ -53,6 +53,8 @@ def test_default_cfg_and_workspace(L):
     assert L.rlhc_workspace_size(1, 1 << 20, 128, 1024, 256, None) > 0
     assert L.rlhc_workspace_size(0, 65536, 64, 32, 0, None) == 0        # s < n
     assert L.rlhc_workspace_size(1, 65536, 64, 128, 256, None) == 0     # s2 > s1
+    # exact GEPP: one leaf holding every row
+    assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(_lib.TsluCfg(65536, 2, 16))) > 0
     bad = _lib.TsluCfg(300, 4, 64)  # leaves larger than a select CTA holds
     assert L.rlhc_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(bad)) == 0
 

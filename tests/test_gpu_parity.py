@@ -60,6 +60,10 @@ LU_CASES = [
     (2048, 16, None), (5000, 16, None), (65536, 64, None), (10000, 40, None), (3000, 33, None),
     (4100, 100, None), (20000, 128, None), (9000, 200, None), (6000, 64, (256, 2, 64)), (8192, 32, (512, 8, 32)),
     (300, 64, None), (64, 64, None),
+    # exact GEPP (one leaf holding every row)
+    (4096, 50, (4096, 2, 16)), (3000, 64, (3000, 2, 16)), (2000, 5, (2000, 2, 5)), (400000, 24, (400000, 2, 16)),
+    # an 8-wide panel at 128-row leaves runs on the CTA kernels (not the warp kernels' 16-wide panels)
+    (5000, 40, (128, 8, 8)),
 ]
 
 
@@ -263,3 +267,19 @@ def test_trsm_subst_bitwise(m, n):
     piv, U, L11, L, inf2 = rl.getrf_ts(X, want_L=True)
     W2, _, _ = rl.trsm_apply(X, U)
     assert np.array_equal(W2.cpu().numpy(), oracle.trsm_right_upper(X.cpu().numpy(), U.cpu().numpy()))
+
+
+def test_exact_gepp_pivots_match_lapack(rl):
+    """The one-leaf contract is exact partial pivoting: the GPU's pivot order is LAPACK
+    dgetrf's row interchanges (scipy lu_factor) on a Gaussian matrix."""
+    import scipy.linalg as sl
+    from paper_2412_06551_b200._lib import TsluCfg
+    m, n = 5000, 40
+    X = torch.randn(m, n, dtype=torch.float64, device=DEV, generator=torch.Generator(device=DEV).manual_seed(5))
+    piv, U, L11, L, info = rl.getrf_ts(X, cfg=TsluCfg(m, 2, 16))
+    assert info == (0, 0, 0)
+    _, ipiv = sl.lu_factor(X.cpu().numpy())
+    perm = np.arange(m)
+    for k, p in enumerate(ipiv):
+        perm[[k, p]] = perm[[p, k]]
+    assert np.array_equal(piv.cpu().numpy(), perm[:n])
