@@ -267,6 +267,23 @@ RLHC_DEV void wsel_emit(const WSel& sm, int steps, int w, int slot, int* out_ids
   }
 }
 
+// Forward substitution of one row over a 16-column block, RIGHT-looking: l[k] = acc_k *
+// rd(k), then acc_c -= l[k] u(k, c) for c > k.  Per element these are the fma chain over k
+// in increasing order and the final product of the left-looking loop (the select's own ops),
+// but the critical path is 16 steps instead of 120 dependent fmas.  Columns >= lim untouched.
+template <typename UF, typename RF>
+RLHC_DEV void subst_row_rl(double (&l)[WW], int lim, UF u, RF rd) {
+#pragma unroll
+  for (int k = 0; k < WW; k++) {
+    if (k < lim) {
+      l[k] = __dmul_rn(l[k], rd(k));
+#pragma unroll
+      for (int c = k + 1; c < WW; c++)
+        if (c < lim) l[c] = __fma_rn(-l[k], u(k, c), l[c]);
+    }
+  }
+}
+
 // Candidates' rows from the staging tile (row c*TS) -> registers; zero for inactive rows and
 // columns >= w.
 RLHC_DEV void tile_to_regs(const double* tile, int w, double (&a)[RS][WW]) {
@@ -415,13 +432,7 @@ tslw_schur_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict_
     double l[WW];
 #pragma unroll
     for (int c = 0; c < WW; c++) l[c] = Bs[tid * ST + c];
-#pragma unroll
-    for (int c = 0; c < WW; c++) {
-      double v = l[c];
-#pragma unroll
-      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], Ublk[k * WW + c], v);
-      l[c] = __dmul_rn(v, rdp[c]);
-    }
+    subst_row_rl(l, WW, [&](int k, int c) { return Ublk[k * WW + c]; }, [&](int k) { return rdp[k]; });
 #pragma unroll
     for (int c = 0; c < WW; c++) Bs[tid * ST + c] = l[c];
     if (valid) {
@@ -455,10 +466,17 @@ tslw_schur_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict_
       for (int c = 0; c < WW; c++) acc[c] = __fma_rn(-lk, uk[k * WW + c], acc[c]);
     }
   }
-  if (valid) {
+  // S_j through the X tile (this thread's row), stored coalesced
 #pragma unroll
-    for (int c = 0; c < WW; c++)
-      if (c < w) Lb[r * ldl + p0 + c] = acc[c];
+  for (int c = 0; c < WW; c++) Bx[tid * ST + c] = acc[c];
+  __syncthreads();
+  {
+    const int c = tid & 15;
+#pragma unroll
+    for (int j = 0; j < SR / 8; j++) {
+      const int q = (tid >> 4) + 8 * j;
+      if (rb + q < rows && c < w) Lb[(rb + q) * ldl + p0 + c] = Bx[q * ST + c];
+    }
   }
 }
 
@@ -538,6 +556,17 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     }
     cp_async_commit();
   };
+  // S_{j-1} of the CTA's rows -> Lt (coalesced, 16 threads per row), then the first L chunk
+  {
+    const int c = tid & 15;
+#pragma unroll
+    for (int j = 0; j < SD_M / 16; j++) {
+      const int q = (tid >> 4) + 16 * j;
+      const bool in = r0 + q < rows;
+      cp_async8(&sm.Lt[q][c], in ? Lb + (r0 + q) * ldl + kold + c : Lb, in ? 8 : 0);
+    }
+    cp_async_commit();
+  }
   if (kold > 0) load_chunk(0, 0);
   // the previous panel's block, 1/diag, and U[kold.., panel]
   for (int e = tid; e < WW * WW; e += 256) {
@@ -546,25 +575,16 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     sm.Ut[k][c] = c < w ? U[(int64_t)(kold + k) * n + p0 + c] : 0.0;
   }
   if (tid < WW) sm.rdp[tid] = rd[kold + tid];
+  if (kold > 0) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
+  else cp_async_wait_all();
   __syncthreads();
   if (tid < SD_M) {  // L_{j-1} of row tid: S_{j-1} -> forward substitution (the select's chain)
-    const int64_t gr = r0 + tid;
     double l[WW];
 #pragma unroll
-    for (int c = 0; c < WW; c++) l[c] = gr < rows ? Lb[gr * ldl + kold + c] : 0.0;
-#pragma unroll
-    for (int c = 0; c < WW; c++) {
-      double v = l[c];
-#pragma unroll
-      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], sm.Ublk[k][c], v);
-      l[c] = __dmul_rn(v, sm.rdp[c]);
-    }
+    for (int c = 0; c < WW; c++) l[c] = sm.Lt[tid][c];
+    subst_row_rl(l, WW, [&](int k, int c) { return sm.Ublk[k][c]; }, [&](int k) { return sm.rdp[k]; });
 #pragma unroll
     for (int c = 0; c < WW; c++) sm.Lt[tid][c] = l[c];
-    if (gr < rows) {
-#pragma unroll
-      for (int c = 0; c < WW; c++) Lb[gr * ldl + kold + c] = l[c];
-    }
   }
   int st = 0;
   for (int kc = 0; kc < kold; kc += SD_K) {
@@ -591,6 +611,14 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     st ^= 1;
   }
   __syncthreads();  // Lt complete
+  {  // L_{j-1} to L (coalesced)
+    const int c = tid & 15;
+#pragma unroll
+    for (int j = 0; j < SD_M / 16; j++) {
+      const int q = (tid >> 4) + 16 * j;
+      if (r0 + q < rows) Lb[(r0 + q) * ldl + kold + c] = sm.Lt[q][c];
+    }
+  }
 #pragma unroll
   for (int k0 = 0; k0 < WW; k0 += 4) {
     double af[2], bf[2];
@@ -603,17 +631,25 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
 #pragma unroll
       for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
   }
+  // S_j through shared memory (the first A buffer is free), stored coalesced
+  double* So = &sm.A[0][0][0];  // [SD_M][SD_K + 4]
 #pragma unroll
   for (int a = 0; a < 2; a++)
 #pragma unroll
     for (int b = 0; b < 2; b++) {
-      const int64_t gr = r0 + wp * 16 + a * 8 + g;
-      const int c = b * 8 + 2 * t;
-      if (gr < rows) {
-        if (c < w) Lb[gr * ldl + p0 + c] = acc[a][b][0];
-        if (c + 1 < w) Lb[gr * ldl + p0 + c + 1] = acc[a][b][1];
-      }
+      const int rr = wp * 16 + a * 8 + g, c = b * 8 + 2 * t;
+      So[rr * (SD_K + 4) + c] = acc[a][b][0];
+      So[rr * (SD_K + 4) + c + 1] = acc[a][b][1];
     }
+  __syncthreads();
+  {
+    const int c = tid & 15;
+#pragma unroll
+    for (int j = 0; j < SD_M / 16; j++) {
+      const int q = (tid >> 4) + 16 * j;
+      if (r0 + q < rows && c < w) Lb[(r0 + q) * ldl + p0 + c] = So[q * (SD_K + 4) + c];
+    }
+  }
 }
 
 // The tournament of one panel, all levels in one launch.  Warp = leaf (rows
@@ -737,15 +773,7 @@ tslw_urows_kernel(const double* __restrict__ X, int64_t ldx, const double* __res
     double l[WW];
 #pragma unroll
     for (int q = 0; q < WW; q++) l[q] = Sb[tt][q];
-#pragma unroll
-    for (int q = 0; q < WW; q++) {
-      if (q < tt) {
-        double v = l[q];
-#pragma unroll
-        for (int k = 0; k < q; k++) v = __fma_rn(-l[k], Ub[k][q], v);
-        l[q] = __dmul_rn(v, rdb[q]);
-      }
-    }
+    subst_row_rl(l, tt, [&](int k, int q) { return Ub[k][q]; }, [&](int k) { return rdb[k]; });
 #pragma unroll
     for (int q = 0; q < WW; q++) lw[tt][q] = l[q];
   }
@@ -787,32 +815,44 @@ tslw_lfinal_kernel(double* __restrict__ Lb, int64_t ldl, int64_t rows, int pl, i
                    const double* __restrict__ U, const double* __restrict__ rd) {
   __shared__ double Ub[WW][WW];
   __shared__ double rdp[WW];
+  __shared__ double tile[256 * ST];
   pdl_trigger();
   pdl_wait();
+  const int64_t rb = (int64_t)blockIdx.x * 256;
+  // the CTA's 256 rows x wl columns, coalesced (16 threads per row)
+  {
+    const int c = threadIdx.x & 15;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int q = (threadIdx.x >> 4) + 16 * j;
+      const bool in = rb + q < rows && c < wl;
+      cp_async8(tile + q * ST + c, in ? Lb + (rb + q) * ldl + pl + c : Lb, in ? 8 : 0);
+    }
+    cp_async_commit();
+  }
   for (int e = threadIdx.x; e < WW * WW; e += blockDim.x) {
     const int k = e / WW, c = e - k * WW;
     Ub[k][c] = (k < wl && c < wl) ? U[(int64_t)(pl + k) * n + pl + c] : 0.0;
   }
   if (threadIdx.x < WW) rdp[threadIdx.x] = threadIdx.x < wl ? rd[pl + threadIdx.x] : 0.0;
+  cp_async_wait_all();
   __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  double* lr = Lb + r * ldl + pl;
   double l[WW];
+  double* row = tile + threadIdx.x * ST;
 #pragma unroll
-  for (int c = 0; c < WW; c++) l[c] = c < wl ? lr[c] : 0.0;
+  for (int c = 0; c < WW; c++) l[c] = row[c];
+  subst_row_rl(l, wl, [&](int k, int c) { return Ub[k][c]; }, [&](int k) { return rdp[k]; });
 #pragma unroll
-  for (int c = 0; c < WW; c++) {
-    if (c < wl) {
-      double v = l[c];
+  for (int c = 0; c < WW; c++) row[c] = l[c];
+  __syncthreads();
+  {
+    const int c = threadIdx.x & 15;
 #pragma unroll
-      for (int k = 0; k < c; k++) v = __fma_rn(-l[k], Ub[k][c], v);
-      l[c] = __dmul_rn(v, rdp[c]);
+    for (int j = 0; j < 16; j++) {
+      const int q = (threadIdx.x >> 4) + 16 * j;
+      if (rb + q < rows && c < wl) Lb[(rb + q) * ldl + pl + c] = tile[q * ST + c];
     }
   }
-#pragma unroll
-  for (int c = 0; c < WW; c++)
-    if (c < wl) lr[c] = l[c];
 }
 
 // Pivot row t: L11 row t = its L row in columns < t, 1 on the diagonal, 0 right of it; the
