@@ -170,7 +170,9 @@ RLHC_DEV void wsel_pend(double (&a)[RS][WW], const double (&lp)[RS], const doubl
 
 // One step; PEND: apply step t - 1's pending update (t > 0), in chunks placed after each
 // warp reduction so that the DFMAs issue in the reductions' latency shadows.
-template <bool PEND>
+// KMAX: the pending update writes slots [1, KMAX) only (at step t the live columns are
+// t .. 15, i.e. slots 0 .. 15 - t: KMAX = 16 - t is enough, so the rotation narrows).
+template <bool PEND, int KMAX = WW - 1>
 RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bool& bad, int t, WSel& sm) {
   const int lane = lane_id();
   TW_STEP(t)
@@ -184,12 +186,12 @@ RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bo
   }
   int mh = max(max(hi[0], hi[1]), max(hi[2], hi[3]));
   mh = __reduce_max_sync(0xffffffffu, mh);
-  if (PEND) wsel_pend<1, 6>(a, lp, up);
+  if (PEND) wsel_pend<1, (KMAX < 6 ? KMAX : 6)>(a, lp, up);
   unsigned ml = 0;
 #pragma unroll
   for (int s = 0; s < RS; s++) ml = max(ml, hi[s] == mh ? lo[s] : 0u);
   ml = __reduce_max_sync(0xffffffffu, ml);
-  if (PEND) wsel_pend<6, 10>(a, lp, up);
+  if (PEND) wsel_pend<(KMAX < 6 ? KMAX : 6), (KMAX < 10 ? KMAX : 10)>(a, lp, up);
   const double rabs = rcp_newton(__longlong_as_double((long long)(((unsigned long long)(unsigned)mh << 32) | ml)));
   int key = INT_MAX;
 #pragma unroll
@@ -198,9 +200,11 @@ RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bo
                                        : key;
   key = __reduce_min_sync(0xffffffffu, key);
   if (PEND) {
-    wsel_pend<10, WW - 1>(a, lp, up);
+    wsel_pend<(KMAX < 10 ? KMAX : 10), KMAX>(a, lp, up);
+    if (KMAX == WW - 1) {
 #pragma unroll
-    for (int s = 0; s < RS; s++) a[s][WW - 1] = 0.0;
+      for (int s = 0; s < RS; s++) a[s][WW - 1] = 0.0;
+    }
   }
   bad |= (mh | (int)ml) == 0 || !rcp_newton_ok(mh);
   const int pidx = key >> 1, ps = pidx >> 5, plane = pidx & 31;
@@ -229,7 +233,13 @@ RLHC_DEV bool wsel_fast(double (&a)[RS][WW], unsigned act, WSel& sm) {
   wsel_step<false>(a, lp, act, bad, 0, sm);
   // step 0 left columns 2.. unrotated and un-updated: the pending form of steps >= 1
 #pragma unroll 1
-  for (int t = 1; t < WW; t++) wsel_step<true>(a, lp, act, bad, t, sm);
+  for (int t = 1; t < 4; t++) wsel_step<true, WW - 1>(a, lp, act, bad, t, sm);
+#pragma unroll 1
+  for (int t = 4; t < 8; t++) wsel_step<true, 12>(a, lp, act, bad, t, sm);
+#pragma unroll 1
+  for (int t = 8; t < 12; t++) wsel_step<true, 8>(a, lp, act, bad, t, sm);
+#pragma unroll 1
+  for (int t = 12; t < WW; t++) wsel_step<true, 4>(a, lp, act, bad, t, sm);
   __syncwarp();
   TW_STEP(WW)
   return !bad;
