@@ -68,8 +68,8 @@ size_t tslg_ws_bytes(int64_t rows);
 // gepp_ws != null: exact GEPP (one leaf holding every row) instead of the tournament
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
-                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st,
-                     void* gepp_ws = nullptr);
+                     int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
+                     cudaStream_t st, void* gepp_ws = nullptr);
 
 // rows.cu
 cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,

@@ -136,7 +136,7 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
              bool check_input = false) {
   if (tslw_cfg(cfg, rows, n)) {  // warp tournament (or exact GEPP); L (original row order) lands in tw
     CUDA_TRY(run_tslw(X, ldx, rows, row0, (int)n, cfg.arity, tw, ldtw, piv, U, L11, t.rd, t.lw, t.chosen, t.ids,
-                      t.cnt, t.status, check_input, st, t.gepp));
+                      t.cnt, t.vals, t.status, check_input, st, t.gepp));
     return RLHC_OK;
   }
   const int W = kernel_width(cfg.panel);

@@ -46,12 +46,23 @@ __device__ unsigned g_twn;
     }                                                                                        \
   }
 __device__ long long g_stp[64];
+// per level of the climbing warp: select start/end, arrival done, node staged (globaltimer ns)
+__device__ unsigned long long g_lv[1 << 14][6];
+__device__ unsigned g_lvn;
+#define TW_G(v) unsigned long long v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+#define TW_LV(lev, a, b, c, d)                                                              \
+  if (lane_id() == 0) {                                                                     \
+    unsigned i_ = atomicAdd(&g_lvn, 1u);                                                    \
+    if (i_ < (1u << 14)) { g_lv[i_][0] = p0; g_lv[i_][1] = lev; g_lv[i_][2] = a; g_lv[i_][3] = b; g_lv[i_][4] = c; g_lv[i_][5] = d; } \
+  }
 #define TW_STEP(i) \
   if (blockIdx.x == 0 && threadIdx.x == 0) g_stp[i] = clock64();
 #else
 #define TW_T(v)
 #define TW_REC(tag, a, b, c, d)
 #define TW_STEP(i)
+#define TW_G(v)
+#define TW_LV(lev, a, b, c, d)
 #endif
 
 
@@ -66,8 +77,9 @@ struct WSel {
   double tile[WR * TS];  // staging of the node's candidate rows (128 x 16)
   double prow[WW][WW];   // step t: the pivot row (c >= t: U values; c < t: multipliers, root only)
   double r[WW];          // 1 / pivot of step t
-  int sid[WR];           // global id of candidate c (INT_MAX: none)
-  int win[WW];           // candidate index of the winner of step t
+  int sid[WR];           // global id of candidate (tile row) c (INT_MAX: none)
+  int rank[WR];          // position of candidate c in increasing-id order (the tie-break key)
+  int win[WW];           // candidate (tile row) of the winner of step t
   int zero[WW];          // 1: zero pivot column at step t (R#5: no update)
 };
 
@@ -92,7 +104,7 @@ RLHC_DEV void write_prow(const double (&a)[RS][WW], int ps, double* dst, int c0)
 // candidate index".  sm.win / sm.prow (whole rows) / sm.r / sm.zero hold the winners.
 // The maximum of |a| is taken on the bit patterns (sign cleared) of the 32-bit halves:
 // high words, then low words among the rows attaining the high maximum.
-RLHC_DEV void wsel_gepp(double (&a)[RS][WW], unsigned act, int steps, WSel& sm) {
+RLHC_DEV void wsel_gepp(double (&a)[RS][WW], unsigned act, int steps, const int (&rk)[RS], WSel& sm) {
   const int lane = lane_id();
 #pragma unroll
   for (int t = 0; t < WW; t++) {
@@ -112,17 +124,19 @@ RLHC_DEV void wsel_gepp(double (&a)[RS][WW], unsigned act, int steps, WSel& sm) 
       ml = __reduce_max_sync(0xffffffffu, ml);
       const double pabs = __longlong_as_double((long long)(((unsigned long long)(unsigned)mh << 32) | ml));
       double rabs = rcp_newton(pabs);
-      unsigned mm = 0;
+      int kr = INT_MAX;  // smallest rank (= smallest id) among this lane's rows attaining the maximum
 #pragma unroll
-      for (int s = 0; s < RS; s++) mm |= (hi[s] == mh && lo[s] == ml ? 1u : 0u) << s;
-      const int pidx = __reduce_min_sync(0xffffffffu, mm ? (__ffs(mm) - 1) * 32 + lane : INT_MAX);
+      for (int s = 0; s < RS; s++) kr = (hi[s] == mh && lo[s] == ml) ? min(kr, rk[s]) : kr;
+      const int prank = __reduce_min_sync(0xffffffffu, kr);
       const bool zero = (mh | (int)ml) == 0;
       if (!zero && !rcp_newton_ok(mh)) rabs = rcp_slow(pabs);  // warp-uniform, rare
-      const int ps = pidx >> 5;
-      if (lane == (pidx & 31)) {
+      int ps = -1;
+#pragma unroll
+      for (int s = 0; s < RS; s++) ps = rk[s] == prank ? s : ps;
+      if (ps >= 0) {  // the pivot's lane
         act &= ~(1u << ps);
         write_prow(a, ps, &sm.prow[t][0], 0);
-        sm.win[t] = pidx;
+        sm.win[t] = ps * 32 + lane;
         sm.zero[t] = zero ? 1 : 0;
       }
       __syncwarp();
@@ -173,7 +187,8 @@ RLHC_DEV void wsel_pend(double (&a)[RS][WW], const double (&lp)[RS], const doubl
 // KMAX: the pending update writes slots [1, KMAX) only (at step t the live columns are
 // t .. 15, i.e. slots 0 .. 15 - t: KMAX = 16 - t is enough, so the rotation narrows).
 template <bool PEND, int KMAX = WW - 1>
-RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bool& bad, int t, WSel& sm) {
+RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bool& bad, int t, const int (&rk)[RS],
+                        WSel& sm) {
   const int lane = lane_id();
   TW_STEP(t)
   const double* up = PEND ? &sm.prow[t - 1][0] : nullptr;
@@ -196,8 +211,7 @@ RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bo
   int key = INT_MAX;
 #pragma unroll
   for (int s = RS - 1; s >= 0; s--)
-    key = (hi[s] == mh && lo[s] == ml) ? (((s * 32 + lane) << 1) | (int)((unsigned)__double2hiint(a[s][0]) >> 31))
-                                       : key;
+    key = (hi[s] == mh && lo[s] == ml) ? ((rk[s] << 1) | (int)((unsigned)__double2hiint(a[s][0]) >> 31)) : key;
   key = __reduce_min_sync(0xffffffffu, key);
   if (PEND) {
     wsel_pend<(KMAX < 10 ? KMAX : 10), KMAX>(a, lp, up);
@@ -207,14 +221,17 @@ RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bo
     }
   }
   bad |= (mh | (int)ml) == 0 || !rcp_newton_ok(mh);
-  const int pidx = key >> 1, ps = pidx >> 5, plane = pidx & 31;
+  const int prank = key >> 1;
   const double r = (key & 1) ? -rabs : rabs;
-  if (lane == plane) {  // the pivot lane publishes its row
+  int ps = -1;
+#pragma unroll
+  for (int s = 0; s < RS; s++) ps = rk[s] == prank ? s : ps;
+  if (ps >= 0) {  // the pivot lane publishes its row
     act &= ~(1u << ps);
     write_prow(a, ps, &sm.prow[t][0], 0);
+    sm.win[t] = ps * 32 + lane;
   }
   if (lane == 0) {
-    sm.win[t] = pidx;
     sm.r[t] = r;
     sm.zero[t] = 0;
   }
@@ -227,19 +244,19 @@ RLHC_DEV void wsel_step(double (&a)[RS][WW], double (&lp)[RS], unsigned& act, bo
   }
 }
 
-RLHC_DEV bool wsel_fast(double (&a)[RS][WW], unsigned act, WSel& sm) {
+RLHC_DEV bool wsel_fast(double (&a)[RS][WW], unsigned act, const int (&rk)[RS], WSel& sm) {
   bool bad = false;
   double lp[RS];
-  wsel_step<false>(a, lp, act, bad, 0, sm);
+  wsel_step<false>(a, lp, act, bad, 0, rk, sm);
   // step 0 left columns 2.. unrotated and un-updated: the pending form of steps >= 1
 #pragma unroll 1
-  for (int t = 1; t < 4; t++) wsel_step<true, WW - 1>(a, lp, act, bad, t, sm);
+  for (int t = 1; t < 4; t++) wsel_step<true, WW - 1>(a, lp, act, bad, t, rk, sm);
 #pragma unroll 1
-  for (int t = 4; t < 8; t++) wsel_step<true, 12>(a, lp, act, bad, t, sm);
+  for (int t = 4; t < 8; t++) wsel_step<true, 12>(a, lp, act, bad, t, rk, sm);
 #pragma unroll 1
-  for (int t = 8; t < 12; t++) wsel_step<true, 8>(a, lp, act, bad, t, sm);
+  for (int t = 8; t < 12; t++) wsel_step<true, 8>(a, lp, act, bad, t, rk, sm);
 #pragma unroll 1
-  for (int t = 12; t < WW; t++) wsel_step<true, 4>(a, lp, act, bad, t, sm);
+  for (int t = 12; t < WW; t++) wsel_step<true, 4>(a, lp, act, bad, t, rk, sm);
   __syncwarp();
   TW_STEP(WW)
   return !bad;
@@ -248,18 +265,20 @@ RLHC_DEV bool wsel_fast(double (&a)[RS][WW], unsigned act, WSel& sm) {
 // Outputs of a node: ids of the winners in pivot order; at the root also piv, chosen,
 // U's diagonal block, 1/diag(U) and rank errors.  rot: prow rows rotated (fast select:
 // U(t, t + j) = prow[t][j]); else prow[t][c] = column c.
-RLHC_DEV void wsel_emit(const WSel& sm, int steps, int w, int slot, int* out_ids, int* out_cnt, const TslwRoot& ro,
-                        int p0, bool rot) {
+RLHC_DEV void wsel_emit(const WSel& sm, int steps, int w, int slot, int* out_ids, int* out_cnt, double* out_vals,
+                        const TslwRoot& ro, int p0, bool rot) {
   const int lane = lane_id();
-  if (lane == 0) {  // one thread writes the slot: its release (the climb's atomic) covers it
-    out_cnt[slot] = steps;
-    int4* o = reinterpret_cast<int4*>(out_ids + slot * WW);
+  // the slot: every lane writes a part; the climb's __syncwarp orders these writes before
+  // lane 0's release (atom.acq_rel.gpu is cumulative), as a CTA barrier before one thread's
+  // release publishes the whole CTA's writes
+  if (lane == 0) out_cnt[slot] = steps;
+  if (lane < WW) out_ids[slot * WW + lane] = lane < steps ? sm.sid[sm.win[lane]] : -1;
+  if (out_vals && !ro.U) {  // the winners' (original) panel rows: the parent reads them in one pass
+    double2* ov = reinterpret_cast<double2*>(out_vals + (size_t)slot * WW * WW);
 #pragma unroll
-    for (int q = 0; q < WW; q += 4) {
-      int v[4];
-#pragma unroll
-      for (int j = 0; j < 4; j++) v[j] = q + j < steps ? sm.sid[sm.win[q + j]] : -1;
-      o[q / 4] = make_int4(v[0], v[1], v[2], v[3]);
+    for (int j = 0; j < WW * WW / 2 / 32; j++) {
+      const int e = j * 32 + lane, q = e / (WW / 2), c = e % (WW / 2);
+      if (q < steps) ov[e] = reinterpret_cast<const double2*>(sm.tile + sm.win[q] * TS)[c];
     }
   }
   if (!ro.U) return;
@@ -309,19 +328,22 @@ RLHC_DEV void tile_to_regs(const double* tile, int w, double (&a)[RS][WW]) {
 }
 
 // Select on the candidates held in the tile (fast path, else the generic one), then emit.
-RLHC_DEV void select_and_emit(WSel& sm, unsigned act, int w, int slot, int* out_ids, int* out_cnt,
+RLHC_DEV void select_and_emit(WSel& sm, unsigned act, int w, int slot, int* out_ids, int* out_cnt, double* out_vals,
                               const TslwRoot& ro, int p0) {
   double a[RS][WW];
+  int rk[RS];
+#pragma unroll
+  for (int s = 0; s < RS; s++) rk[s] = sm.rank[s * 32 + lane_id()];
   tile_to_regs(sm.tile, w, a);
   const int cnt = __reduce_add_sync(0xffffffffu, __popc(act));
   const int steps = min(cnt, w);
   bool done = false;
-  if (steps == WW) done = wsel_fast(a, act, sm);
+  if (steps == WW) done = wsel_fast(a, act, rk, sm);
   if (!done) {
     if (steps == WW) tile_to_regs(sm.tile, w, a);  // the fast attempt modified a
-    wsel_gepp(a, act, steps, sm);
+    wsel_gepp(a, act, steps, rk, sm);
   }
-  wsel_emit(sm, steps, w, slot, out_ids, out_cnt, ro, p0, done);
+  wsel_emit(sm, steps, w, slot, out_ids, out_cnt, out_vals, ro, p0, done);
 }
 
 // 16-byte L2 copy (bypasses L1: rows written by other SMs in this kernel); src_bytes < 16
@@ -671,7 +693,8 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
 __global__ void __launch_bounds__(32 * WPB)
 tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
-                 int* __restrict__ idsN, int* __restrict__ cntN, int* __restrict__ arrive, int arity, TslwRoot ro) {
+                 int* __restrict__ idsN, int* __restrict__ cntN, double* __restrict__ vals0,
+                 double* __restrict__ valsN, int* __restrict__ arrive, int arity, TslwRoot ro) {
   extern __shared__ __align__(16) unsigned char raw[];
   WSel& sm = reinterpret_cast<WSel*>(raw)[warp_id()];
   pdl_trigger();
@@ -689,6 +712,7 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
     const int64_t r = rb + s * 32 + lane;
     const bool valid = r < rows;
     sm.sid[s * 32 + lane] = valid ? (int)(row0 + r) : INT_MAX;
+    sm.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
     act |= ((valid && !(chosen && chosen[r])) ? 1u : 0u) << s;
   }
   __syncwarp();
@@ -696,10 +720,18 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
   TW_T(t1)
   int nsl = nleaves, slot = leaf;
   int *oids = ids0, *ocnt = cnt0;
+  double* ovals = vals0;
   const int* cids = nullptr;
+  const double* cvals = nullptr;
+  int lev = 0;
   for (;;) {
-    select_and_emit(sm, act, w, slot, oids, ocnt, nsl == 1 ? ro : TslwRoot{}, p0);
-    if (nsl == 1) break;
+    TW_G(ga)
+    select_and_emit(sm, act, w, slot, oids, ocnt, ovals, nsl == 1 ? ro : TslwRoot{}, p0);
+    TW_G(gb)
+    if (nsl == 1) {
+      TW_LV(lev, ga, gb, gb, gb)
+      break;
+    }
     // climb: the last child of the parent runs it
     if (cids) arrive += nsl;  // counters of this level's parents follow the previous level's
     const int parent = slot / arity, nout = (nsl + arity - 1) / arity;
@@ -708,15 +740,33 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
     int old = 0;
     if (lane == 0) old = atom_add_acq_rel_gpu(&arrive[parent], 1);  // releases this slot, acquires the others
     old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != nchild - 1) break;
+    TW_G(gc)
+    if (old != nchild - 1) {
+      TW_LV(lev + 100, ga, gb, gc, gc)
+      break;
+    }
     if (lane == 0) arrive[parent] = 0;  // every child has arrived: ready for the next panel
     const bool first = cids == nullptr;
     cids = oids;
+    cvals = ovals;
     oids = first ? idsN : oids + nsl * WW;
     ocnt = first ? cntN : ocnt + nsl;
-    // children [parent*arity, +nchild): entry e of child ci at candidate position
-    // ci*16 + (rank of its id within the child): the children cover increasing global
-    // row ranges, so this is increasing-id order
+    ovals = first ? valsN : ovals + (size_t)nsl * WW * WW;
+    // children [parent*arity, +nchild): entry e of child ci -> tile row ci*16 + e, its ids and
+    // (original) panel rows loaded in one pass (L2: written by other SMs in this launch)
+    {
+      const int ch = lane & 7;
+#pragma unroll 8
+      for (int i = 0; i < WR / 4; i++) {
+        const int q = 4 * i + (lane >> 3), ci = q / WW, e = q % WW;
+        const bool ok = ci < nchild;
+        cp_async16_cg(sm.tile + q * TS + 2 * ch,
+                      ok ? cvals + ((size_t)(parent * arity + ci) * WW + e) * WW + 2 * ch : cvals, ok ? 16 : 0);
+      }
+      cp_async_commit();
+    }
+    // rank = position in increasing-id order: the children cover increasing global row
+    // ranges, so rank = ci*16 + (rank of the id within its child)
 #pragma unroll
     for (int s = 0; s < RS; s++) {
       const int c = s * 32 + lane, ci = c / WW, e = c % WW, child = parent * arity + ci;
@@ -728,13 +778,17 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
         const int o = __shfl_sync(0xffffffffu, id, (lane & ~(WW - 1)) | q);
         rank += (o < id) || (o == id && q < e);
       }
-      sm.sid[ci * WW + rank] = id;
+      sm.sid[c] = id;
+      sm.rank[c] = ci * WW + rank;
     }
-    __syncwarp();
     act = 0;
 #pragma unroll
     for (int s = 0; s < RS; s++) act |= (sm.sid[s * 32 + lane] != INT_MAX ? 1u : 0u) << s;
-    stage_rows(sm, w, Lb, ldl, row0, p0, v16);
+    cp_async_wait_all();
+    __syncwarp();
+    TW_G(gd)
+    TW_LV(lev, ga, gb, gc, gd)
+    lev++;
     slot = parent;
     nsl = nout;
   }
@@ -1018,8 +1072,8 @@ size_t tslg_ws_bytes(int64_t rows) { return (size_t)rows * WW * sizeof(double) +
 
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
-                     int* ids[2], int* cnt[2], unsigned long long* status, bool check_input, cudaStream_t st,
-                     void* gepp_ws) {
+                     int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
+                     cudaStream_t st, void* gepp_ws) {
   (void)lw;
   double* Sw = gepp_ws ? reinterpret_cast<double*>(gepp_ws) : nullptr;  // exact GEPP mode (one leaf)
   TslgScratch* gsc = gepp_ws ? reinterpret_cast<TslgScratch*>(reinterpret_cast<char*>(gepp_ws) +
@@ -1076,7 +1130,7 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
       note_launch();
       e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
                      (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0],
-                     cnt[0], ids[1], cnt[1], arrive, arity, root);
+                     cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity, root);
       if (e) return e;
     }
     if (p0 + w < n) {

@@ -29,15 +29,19 @@ int main(int argc, char** argv) {
   uint8_t* chosen; cudaMalloc(&chosen, m);
   unsigned long long* status; cudaMalloc(&status, 8); cudaMemset(status, 0xff, 8);
   int *ids[2], *cnt[2];
+  double* vals[2];
   size_t ns = tslw_slots(m);
-  for (int k = 0; k < 2; k++) { cudaMalloc(&ids[k], ns * 16 * 4); cudaMalloc(&cnt[k], ns * 4); }
+  for (int k = 0; k < 2; k++) {
+    cudaMalloc(&ids[k], ns * 16 * 4); cudaMalloc(&cnt[k], (2 * ns + 64) * 4); cudaMalloc(&vals[k], ns * 256 * 8);
+  }
   cudaStream_t st; cudaStreamCreate(&st);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 4; rep++) {
     unsigned z = 0;
     cudaMemcpyToSymbol(g_twn, &z, 4);
+    cudaMemcpyToSymbol(g_lvn, &z, 4);
     cudaEventRecord(e0, st);
-    run_tslw(X, n, m, 0, n, 8, Lb, n, piv, U, L11, rd, lw, chosen, ids, cnt, status, true, st);
+    run_tslw(X, n, m, 0, n, 8, Lb, n, piv, U, L11, rd, lw, chosen, ids, cnt, vals, status, true, st);
     cudaEventRecord(e1, st);
     cudaStreamSynchronize(st);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -63,6 +67,21 @@ int main(int argc, char** argv) {
     for (auto* r : v) { s0 = std::min(s0, r[3]); e = std::max(e, r[7]); a += r[4]; b += r[5]; am = std::max(am, (double)r[4]); bm = std::max(bm, (double)r[5]); }
     printf("p0 %3llu warps %5zu: start %8.2f end %8.2f us | phase1 cycles mean %7.0f max %7.0f | select+climb mean %7.0f max %7.0f\n",
            k, v.size(), (s0 - T0) * 1e-3, (e - T0) * 1e-3, a / v.size(), am, b / v.size(), bm);
+  }
+  unsigned nl; cudaMemcpyFromSymbol(&nl, g_lvn, 4);
+  std::vector<unsigned long long> lv((size_t)std::min(nl, 1u << 14) * 6);
+  cudaMemcpyFromSymbol(lv.data(), g_lv, lv.size() * 8);
+  std::map<std::pair<unsigned long long, unsigned long long>, std::vector<unsigned long long*>> lg;
+  for (size_t i = 0; i < lv.size() / 6; i++) lg[{lv[i * 6], lv[i * 6 + 1]}].push_back(&lv[i * 6]);
+  for (auto& [k, v] : lg) {
+    double sel = 0, arr = 0, stg = 0, sm = 0, am = 0, gm = 0;
+    for (auto* r : v) {
+      sel += r[3] - r[2]; arr += r[4] - r[3]; stg += r[5] - r[4];
+      sm = std::max(sm, (double)(r[3] - r[2])); am = std::max(am, (double)(r[4] - r[3])); gm = std::max(gm, (double)(r[5] - r[4]));
+    }
+    printf("p0 %3llu level %3llu warps %5zu: select %.2f (max %.2f) us, emit+arrive %.2f (max %.2f), node load %.2f (max %.2f)\n",
+           k.first, k.second, v.size(), sel / v.size() * 1e-3, sm * 1e-3, arr / v.size() * 1e-3, am * 1e-3,
+           stg / v.size() * 1e-3, gm * 1e-3);
   }
   return 0;
 }
