@@ -73,7 +73,7 @@ constexpr int WPB = 4;          // warps (tournament nodes) per CTA
 
 constexpr int TS = 18;          // row stride (doubles) of the staging tile: 16-byte rows, conflict-free LDS.128 by row
 
-struct WSel {
+struct alignas(16) WSel {
   double tile[WR * TS];  // staging of the node's candidate rows (128 x 16)
   double prow[WW][WW];   // step t: the pivot row (c >= t: U values; c < t: multipliers, root only)
   double r[WW];          // 1 / pivot of step t
@@ -361,7 +361,8 @@ RLHC_DEV int atom_add_acq_rel_gpu(int* p, int v) {
 // The candidates' S_j rows (global id sm.sid[q], columns [p0, p0+w)) -> tile rows q.
 // v16: rows 16-byte aligned (even ldl, aligned base): 16-byte L2 copies, 4 rows per
 // instruction; else 8-byte L2 loads.
-RLHC_DEV void stage_rows(WSel& sm, int w, const double* Lb, int64_t ldl, int64_t row0, int p0, bool v16) {
+RLHC_DEV void stage_rows(WSel& sm, int w, const double* Lb, int64_t ldl, int64_t row0, int p0, bool v16,
+                          bool wait = true) {
   const int lane = lane_id();
   if (v16) {
     const int ch = lane & 7;
@@ -376,6 +377,7 @@ RLHC_DEV void stage_rows(WSel& sm, int w, const double* Lb, int64_t ldl, int64_t
                     ok ? bytes : 0);
     }
     cp_async_commit();
+    if (!wait) return;
     cp_async_wait_all();
   } else {
     const int c = lane & 15;
@@ -710,13 +712,20 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
 #pragma unroll
   for (int s = 0; s < RS; s++) {
     const int64_t r = rb + s * 32 + lane;
-    const bool valid = r < rows;
-    sm.sid[s * 32 + lane] = valid ? (int)(row0 + r) : INT_MAX;
+    sm.sid[s * 32 + lane] = r < rows ? (int)(row0 + r) : INT_MAX;
     sm.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
-    act |= ((valid && !(chosen && chosen[r])) ? 1u : 0u) << s;
   }
   __syncwarp();
-  stage_rows(sm, w, Lb, ldl, row0, p0, v16);
+  stage_rows(sm, w, Lb, ldl, row0, p0, v16, false);  // in flight while the flags load
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    const int64_t r = rb + s * 32 + lane;
+    act |= ((r < rows && !(chosen && chosen[r])) ? 1u : 0u) << s;
+  }
+  if (v16) {
+    cp_async_wait_all();
+    __syncwarp();
+  }
   TW_T(t1)
   int nsl = nleaves, slot = leaf;
   int *oids = ids0, *ocnt = cnt0;
