@@ -53,14 +53,14 @@ struct LevelBufs {
   double* vals[2];
 };
 size_t level_bytes(int64_t slots, int W) {
-  return 2 * (al(slots * W * 4) + al(slots * 4) + al(slots * W * W * 8));
+  return 2 * (al(slots * W * 4) + al((2 * slots + 64) * 4) + al(slots * W * W * 8));
 }
 LevelBufs carve_levels(void* ws, int64_t slots, int W) {
   LevelBufs b;
   char* p = (char*)ws;
   for (int k = 0; k < 2; k++) {
     b.ids[k] = (int*)p; p += al(slots * W * 4);
-    b.cnt[k] = (int*)p; p += al(slots * 4);
+    b.cnt[k] = (int*)p; p += al((2 * slots + 64) * 4);  // warp tree: counts + arrival counters
     b.vals[k] = (double*)p; p += al(slots * W * W * 8);
   }
   return b;
@@ -112,6 +112,12 @@ int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0,
   const int W = kw(cfg->panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
   LevelBufs b = carve_levels(ws, nleaves, W);
+  if (cfg->leaf_rows == 128 && cfg->arity >= 2 && cfg->arity <= 8 && w <= 16) {
+    // the warp tournament (the default contract): every local level in one launch
+    TRY(run_tslw_local_tree(src, lds, rows, row0, (int)p0, (int)w, chosen, cfg->arity, b.ids, b.cnt, b.vals, out_ids,
+                            out_cnt, out_vals, st));
+    return RLHC_OK;
+  }
   TRY(launch_tslu_leaf(W, cfg->leaf_rows, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0],
                        nleaves == 1 ? b.vals[0] : nullptr, st));
   const RowSrc rsrc{src, lds, row0, (int)p0};

@@ -63,6 +63,10 @@ struct TslwRoot {          // root outputs of one panel (all null below the root
 bool tslw_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
 bool tslg_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
 size_t tslw_slots(int64_t rows);
+// row-sharded local tree of the warp contract down to one slot (rlhc_tslu_reduce)
+cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+                                const uint8_t* chosen, int arity, int* ids[2], int* cnt[2], double* vals[2],
+                                int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st);
 // exact GEPP mode (one leaf of all rows): workspace of the panel's working copy
 size_t tslg_ws_bytes(int64_t rows);
 // gepp_ws != null: exact GEPP (one leaf holding every row) instead of the tournament

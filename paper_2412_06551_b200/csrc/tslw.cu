@@ -1079,6 +1079,41 @@ size_t tslw_slots(int64_t rows) { return (size_t)ceil_div<int64_t>(rows, WR); }
 // tslw_slots(rows) * 16 ids and counts; chosen: rows bytes; rd: 1/diag(U).
 size_t tslg_ws_bytes(int64_t rows) { return (size_t)rows * WW * sizeof(double) + sizeof(TslgScratch) + 256; }
 
+// The row-sharded path's local tournament (rlhc_tslu_reduce under the warp contract): the
+// tree kernel on this rank's rows of the panel source `src` (current panel values, columns
+// [p0, p0+w)), every local level down to ONE slot, no root outputs; the top slot (ids,
+// count, the winners' panel rows) is copied to out_*.  cnt[1] holds the packed counts of the
+// levels >= 1 followed by their arrival counters.
+cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
+                                const uint8_t* chosen, int arity, int* ids[2], int* cnt[2], double* vals[2],
+                                int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st) {
+  cudaError_t e;
+  const int nleaves = (int)tslw_slots(rows);
+  size_t above = 0, top = 0;  // packed slots of the levels >= 1; offset of the top level
+  for (int ns = nleaves; ns > 1; ns = ceil_div(ns, arity)) {
+    top = above;
+    above += ceil_div(ns, arity);
+  }
+  int* arrive = cnt[1] + above;
+  if (above && (e = cudaMemsetAsync(arrive, 0, above * sizeof(int), st))) return e;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tslw_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  note_launch();
+  e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st, src, lds,
+                 rows, row0, p0, w, chosen, ids[0], cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity,
+                 TslwRoot{});
+  if (e) return e;
+  const int* tid = nleaves == 1 ? ids[0] : ids[1] + top * WW;
+  const int* tcnt = nleaves == 1 ? cnt[0] : cnt[1] + top;
+  const double* tval = nleaves == 1 ? vals[0] : vals[1] + top * WW * WW;
+  if ((e = cudaMemcpyAsync(out_ids, tid, WW * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(out_cnt, tcnt, sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  return cudaMemcpyAsync(out_vals, tval, (size_t)WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
+}
+
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
                      int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
