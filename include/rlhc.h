@@ -206,6 +206,26 @@ size_t rlhc_tslu_eliminate_workspace_size(int64_t n);
 int rlhc_tslu_eliminate(const double* src, int64_t lds, int64_t rows, int64_t p0, int64_t w, int64_t n,
                         const double* U, double* dst, int64_t ldd, void* ws, size_t ws_bytes, rlhc_stream_t stream);
 /* L11 from the pivot rows of X (n x n, pivot order) and U; L of this rank's rows. */
+/* Left-looking blocks of the warp contract (leaf_rows 128, 16-column panels; DESIGN.md
+ * section 7), row-sharded: L is this rank's rows x n L buffer (the Q buffer).
+ * rlhc_tslw_schur: panel [p0, p0+16) of this rank's rows.  p0 > 0: L's columns [p0-16, p0)
+ *   (the previous panel's Schur values) become L by forward substitution with U's diagonal
+ *   block; then L[:, p0:p0+w) = X[:, p0:p0+w) - L[:, :p0] U[:p0, p0:p0+w) (fma chain in
+ *   increasing k, bit-identical to the single-process pipeline).  U: n x n, rows < p0 final.
+ * rlhc_tslw_owned_rows: T (cnt x (n-p0), ld n-p0) = the current rows of the panel's winners
+ *   ids[0..cnt) (global ids) over columns [p0, n) for the winners this rank owns, 0 for the
+ *   others (an all-reduce sum gives every row exactly); input of rlhc_tslu_panel_factor_rows.
+ * rlhc_tslw_finish: after the last panel: its Schur values become L, and this rank's pivot
+ *   rows take their L11 rows (unit diagonal, zeros right of it).  L then equals the
+ *   single-process rlhc_getrf_ts L rows of this rank.
+ * All asynchronous on `stream`; EINVAL for bad sizes. */
+int rlhc_tslw_schur(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl, int64_t p0,
+                    const double* U, rlhc_stream_t stream);
+int rlhc_tslw_owned_rows(const double* X, int64_t ldx, const double* L, int64_t ldl, int64_t rows, int64_t row0,
+                         const int* ids, int64_t cnt, int64_t p0, int64_t n, const double* U, double* T,
+                         rlhc_stream_t stream);
+int rlhc_tslw_finish(double* L, int64_t ldl, int64_t rows, int64_t row0, int64_t n, const double* U,
+                     const int64_t* piv, rlhc_stream_t stream);
 size_t rlhc_lfactor_workspace_size(int64_t rows, int64_t n);
 int rlhc_l11(const double* Xp, int64_t n, const double* U, double* L11, void* ws, size_t ws_bytes,
              rlhc_stream_t stream);

@@ -55,6 +55,9 @@ def lib():
     P, I64, U64, U32, SZ, I = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
                                ctypes.c_int)
     PC = ctypes.POINTER(TsluCfg)
+    L.rlhc_tslw_schur.argtypes = [P, I64, I64, I64, P, I64, I64, P, P]
+    L.rlhc_tslw_owned_rows.argtypes = [P, I64, P, I64, I64, I64, P, I64, I64, I64, P, P, P]
+    L.rlhc_tslw_finish.argtypes = [P, I64, I64, I64, I64, P, P, P]
     L.rlhc_graph_begin.argtypes = [P]
     L.rlhc_graph_end.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
     L.rlhc_graph_launch.argtypes = [P, P]
@@ -157,7 +160,8 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_cholesky_workspace_size", "rlhc_cholesky_ws", "rlhc_comm_unique_id", "rlhc_comm_init",
             "rlhc_comm_destroy", "rlhc_dist_workspace_size", "rlhc_slhc3_dist", "rlhc_sslhc3_dist",
             "rlhc_method_workspace_size", "rlhc_cholqr2", "rlhc_scholqr3", "rlhc_luc2", "rlhc_rhc",
-            "rlhc_graph_begin", "rlhc_graph_end", "rlhc_graph_launch", "rlhc_graph_destroy"]
+            "rlhc_graph_begin", "rlhc_graph_end", "rlhc_graph_launch", "rlhc_graph_destroy",
+            "rlhc_tslw_schur", "rlhc_tslw_owned_rows", "rlhc_tslw_finish"]
 NUM_TIMED_STAGES = 11
 
 

@@ -199,6 +199,32 @@ int rlhc_tslu_eliminate(const double* src, int64_t lds, int64_t rows, int64_t p0
   return RLHC_OK;
 }
 
+int rlhc_tslw_schur(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl, int64_t p0,
+                    const double* U, rlhc_stream_t stream) {
+  if (!X || !L || !U || rows < 1 || n < 1 || ldx < n || ldl < n || p0 < 0 || p0 >= n || p0 % 16)
+    return fail(RLHC_EINVAL, "bad arguments");
+  TRY(launch_tslw_schur(X, ldx, L, ldl, rows, (int)p0, (int)std::min<int64_t>(16, n - p0), (int)n, U,
+                        (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+int rlhc_tslw_owned_rows(const double* X, int64_t ldx, const double* L, int64_t ldl, int64_t rows, int64_t row0,
+                         const int* ids, int64_t cnt, int64_t p0, int64_t n, const double* U, double* T,
+                         rlhc_stream_t stream) {
+  if (!X || !L || !ids || !U || !T || rows < 0 || n < 1 || cnt < 0 || cnt > 16 || p0 < 0 || p0 >= n)
+    return fail(RLHC_EINVAL, "bad arguments");
+  if (cnt == 0) return RLHC_OK;
+  TRY(launch_tslw_owned(X, ldx, L, ldl, rows, row0, ids, (int)cnt, (int)p0, (int)n, U, T, (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
+int rlhc_tslw_finish(double* L, int64_t ldl, int64_t rows, int64_t row0, int64_t n, const double* U,
+                     const int64_t* piv, rlhc_stream_t stream) {
+  if (!L || !U || !piv || rows < 1 || n < 1 || ldl < n) return fail(RLHC_EINVAL, "bad arguments");
+  TRY(launch_tslw_finish(L, ldl, rows, row0, (int)n, U, piv, (cudaStream_t)stream));
+  return RLHC_OK;
+}
+
 size_t rlhc_lfactor_workspace_size(int64_t rows, int64_t n) {
   return al(256) + al((size_t)n * 8) + al(rowsolve_partials_bytes(std::max<int64_t>(rows, n), (int)n));
 }

@@ -244,7 +244,34 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
       launch_status_finish(d.status, next_info(), st))
     return fail(RLHC_ECUDA, "launch failed");
   // ---------------- PX = LU (P:279 / P:293), tournament over panels
-  for (int64_t p0 = 0; p0 < n; p0 += a.cfg.panel) {
+  // the warp contract (leaf 128, 16-column panels): left-looking panels with the single-process
+  // pipeline's arithmetic -- this rank's Schur complement of the panel into Q, the local
+  // tournament (one launch), the gathered top levels, the winners' current rows from their
+  // owners (all-reduced), their elimination -> U rows; L is left in Q
+  const bool warp = a.cfg.leaf_rows == 128 && a.cfg.arity >= 2 && a.cfg.arity <= 8 && a.cfg.panel == 16 && n > 16;
+  for (int64_t p0 = 0; warp && p0 < n; p0 += a.cfg.panel) {
+    const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
+    DTRY(rlhc_tslw_schur(a.X, m, n, a.ldx, a.Q, a.ldq, p0, d.U, st));
+    DTRY(rlhc_tslu_reduce(a.Q, a.ldq, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, d.slot_ids, d.slot_cnt,
+                          d.slot_vals, sc, scb, st));
+    const int* root = d.slot_ids;
+    if (nr > 1) {
+      NTRY(N.GroupStart());
+      NTRY(N.AllGather(d.slot_ids, d.all_ids, W, ncclInt32, comm->comm, st));
+      NTRY(N.AllGather(d.slot_cnt, d.all_cnt, 1, ncclInt32, comm->comm, st));
+      NTRY(N.AllGather(d.slot_vals, d.all_vals, (size_t)W * W, ncclFloat64, comm->comm, st));
+      NTRY(N.GroupEnd());
+      DTRY(rlhc_tslu_combine(d.all_ids, d.all_cnt, d.all_vals, nr, w, &a.cfg, d.root_ids, d.root_cnt, d.root_vals, sc,
+                             scb, st));
+      root = d.root_ids;
+    }
+    DTRY(rlhc_tslw_owned_rows(a.X, a.ldx, a.Q, a.ldq, m, a.row0, root, w, p0, n, d.U, d.prow, st));
+    DTRY(allreduce(d.prow, (size_t)w * (n - p0)));
+    DTRY(rlhc_tslu_panel_factor_rows(d.prow, root, p0, w, n, a.row0, m, d.U, a.piv, d.chosen, sc, scb, next_info(),
+                                     st));
+  }
+  if (warp) DTRY(rlhc_tslw_finish(a.Q, a.ldq, m, a.row0, n, d.U, a.piv, st));
+  for (int64_t p0 = 0; !warp && p0 < n; p0 += a.cfg.panel) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
     const double* src = p0 == 0 ? a.X : a.Q;
     const int64_t lds = p0 == 0 ? a.ldx : a.ldq;
@@ -267,10 +294,12 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
                                      st));
     if (p0 + w < n) DTRY(rlhc_tslu_eliminate(src, lds, m, p0, w, n, d.U, a.Q, a.ldq, sc, scb, st));
   }
-  DTRY(rlhc_owned_rows(a.X, a.ldx, m, a.row0, nullptr, a.piv, n, 0, n, d.Xp, st));
-  DTRY(allreduce(d.Xp, (size_t)n * n));
-  DTRY(rlhc_l11(d.Xp, n, d.U, d.L11, sc, scb, st));
-  DTRY(rlhc_lfactor(a.X, m, n, a.ldx, a.row0, d.U, d.L11, a.piv, a.Q, a.ldq, sc, scb, st));
+  if (!warp) {
+    DTRY(rlhc_owned_rows(a.X, a.ldx, m, a.row0, nullptr, a.piv, n, 0, n, d.Xp, st));
+    DTRY(allreduce(d.Xp, (size_t)n * n));
+    DTRY(rlhc_l11(d.Xp, n, d.U, d.L11, sc, scb, st));
+    DTRY(rlhc_lfactor(a.X, m, n, a.ldx, a.row0, d.U, d.L11, a.piv, a.Q, a.ldq, sc, scb, st));
+  }
   // ---------------- sketch of L (P:280 / P:294): local partials, all-reduced
   int64_t srows;
   if (a.algo == RLHC_SLHC3) {

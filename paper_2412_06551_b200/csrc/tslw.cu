@@ -608,7 +608,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     sm.Ublk[k][c] = U[(int64_t)(kold + k) * n + kold + c];
     sm.Ut[k][c] = c < w ? U[(int64_t)(kold + k) * n + p0 + c] : 0.0;
   }
-  if (tid < WW) sm.rdp[tid] = rd[kold + tid];
+  if (tid < WW) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
   if (kold > 0) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
   else cp_async_wait_all();
   __syncthreads();
@@ -907,7 +907,9 @@ tslw_lfinal_kernel(double* __restrict__ Lb, int64_t ldl, int64_t rows, int pl, i
     const int k = e / WW, c = e - k * WW;
     Ub[k][c] = (k < wl && c < wl) ? U[(int64_t)(pl + k) * n + pl + c] : 0.0;
   }
-  if (threadIdx.x < WW) rdp[threadIdx.x] = threadIdx.x < wl ? rd[pl + threadIdx.x] : 0.0;
+  if (threadIdx.x < WW)
+    rdp[threadIdx.x] = threadIdx.x >= wl ? 0.0
+                       : rd ? rd[pl + threadIdx.x] : __ddiv_rn(1.0, U[(int64_t)(pl + threadIdx.x) * (n + 1)]);
   cp_async_wait_all();
   __syncthreads();
   double l[WW];
@@ -930,17 +932,56 @@ tslw_lfinal_kernel(double* __restrict__ Lb, int64_t ldl, int64_t rows, int pl, i
 
 // Pivot row t: L11 row t = its L row in columns < t, 1 on the diagonal, 0 right of it; the
 // same values overwrite its L row (pivot rows take their L11 rows, oracle l_row).
+// (Row-sharded: rows = this rank's row count; other ranks' pivot rows are skipped; L11 may be null.)
 __global__ void tslw_fixup_kernel(double* __restrict__ Lb, int64_t ldl, int64_t row0, const int64_t* __restrict__ piv,
-                                  int n, double* __restrict__ L11) {
+                                  int n, double* __restrict__ L11, int64_t rows) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
   const int64_t r = piv[t] - row0;
+  if (r < 0 || r >= rows) return;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     const double v = c < t ? Lb[r * ldl + c] : (c == t ? 1.0 : 0.0);
-    L11[(int64_t)t * n + c] = v;
+    if (L11) L11[(int64_t)t * n + c] = v;
     if (c >= t) Lb[r * ldl + c] = v;
   }
+}
+
+// Row-sharded TSLU (the warp contract): the current rows of the panel's winners that this
+// rank owns, T[e][c - p0] = X[id_e, c] - sum_{k<p0} L[id_e, k] U[k, c] for c in [p0, n) (the
+// fma chain of tslw_urows_kernel's first phase); 0 for winners owned by other ranks, so the
+// all-reduced sum is every winner's row exactly.  CTA: 16 winners x 32 columns.
+__global__ void __launch_bounds__(WW * 32)
+tslw_owned_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Lb, int64_t ldl,
+                  int64_t rows, int64_t row0, const int* __restrict__ ids, int cnt, int p0, int n,
+                  const double* __restrict__ U, double* __restrict__ T) {
+  __shared__ double Lw[WW][33];
+  __shared__ double Ut[32][32];
+  __shared__ int64_t lr[WW];
+  const int tx = threadIdx.x % 32, t = threadIdx.x / 32;
+  const int c = p0 + blockIdx.x * 32 + tx;
+  if (threadIdx.x < WW) {
+    const int64_t r = threadIdx.x < cnt ? (int64_t)ids[threadIdx.x] - row0 : -1;
+    lr[threadIdx.x] = (r >= 0 && r < rows) ? r : -1;
+  }
+  __syncthreads();
+  const bool mine = t < cnt && lr[t] >= 0;
+  double acc = (mine && c < n) ? X[lr[t] * ldx + c] : 0.0;
+  for (int k0 = 0; k0 < p0; k0 += 32) {
+    for (int e = threadIdx.x; e < WW * 32; e += blockDim.x) {
+      const int tt = e / 32, kk = e % 32;
+      Lw[tt][kk] = (lr[tt] >= 0 && tt < cnt && k0 + kk < p0) ? Lb[lr[tt] * ldl + k0 + kk] : 0.0;
+    }
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+      const int kk = e / 32, x = e % 32, cc = p0 + blockIdx.x * 32 + x;
+      Ut[kk][x] = (k0 + kk < p0 && cc < n) ? U[(int64_t)(k0 + kk) * n + cc] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(32, p0 - k0);
+    for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-Lw[t][kk], Ut[kk][tx], acc);
+    __syncthreads();
+  }
+  if (t < cnt && c < n) T[(int64_t)t * (n - p0) + (c - p0)] = mine ? acc : 0.0;
 }
 
 
@@ -1191,7 +1232,43 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
                  wl, n, (const double*)U, (const double*)rd);
   if (e) return e;
   note_launch();
-  return launch_pdl(tslw_fixup_kernel, dim3(n), dim3(128), 0, st, Lb, ldl, row0, (const int64_t*)piv, n, L11);
+  return launch_pdl(tslw_fixup_kernel, dim3(n), dim3(128), 0, st, Lb, ldl, row0, (const int64_t*)piv, n, L11, rows);
+}
+
+// ------------------------------------------------------------------ row-sharded TSLU blocks
+cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
+                              const double* U, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tslw_schur_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
+    attr = true;
+  }
+  note_launch();
+  if (p0 == 0)
+    return launch_pdl(tslw_schur_kernel<false>, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), schur_smem(0), st,
+                      X, ldx, Lb, ldl, rows, 0, w, n, U, (const double*)nullptr, (unsigned long long*)nullptr);
+  return launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+                    sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, U, (const double*)nullptr,
+                    (unsigned long long*)nullptr);
+}
+
+cudaError_t launch_tslw_owned(const double* X, int64_t ldx, const double* Lb, int64_t ldl, int64_t rows, int64_t row0,
+                              const int* ids, int cnt, int p0, int n, const double* U, double* T, cudaStream_t st) {
+  note_launch();
+  tslw_owned_kernel<<<ceil_div(n - p0, 32), WW * 32, 0, st>>>(X, ldx, Lb, ldl, rows, row0, ids, cnt, p0, n, U, T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tslw_finish(double* Lb, int64_t ldl, int64_t rows, int64_t row0, int n, const double* U,
+                               const int64_t* piv, cudaStream_t st) {
+  const int pl = ((n - 1) / WW) * WW, wl = n - pl;
+  note_launch();
+  cudaError_t e = launch_pdl(tslw_lfinal_kernel, dim3((unsigned)ceil_div<int64_t>(rows, 256)), dim3(256), 0, st, Lb,
+                             ldl, rows, pl, wl, n, U, (const double*)nullptr);
+  if (e) return e;
+  note_launch();
+  return launch_pdl(tslw_fixup_kernel, dim3(n), dim3(128), 0, st, Lb, ldl, row0, piv, n, (double*)nullptr, rows);
 }
 
 }  // namespace rlhc

@@ -94,6 +94,25 @@ class CudaBackend:
                                                  _p(ws), ws.numel(), _p(info), self._st()))
         return info
 
+    # -- left-looking blocks of the warp contract (leaf 128, 16-column panels)
+    def warp_contract(self):
+        c = self.cfg
+        return c.leaf_rows == 128 and 2 <= c.arity <= 8 and c.panel == 16
+
+    def tslw_schur(self, X, L, p0, U):
+        check(self.L.rlhc_tslw_schur(_p(X), X.shape[0], X.shape[1], X.stride(0), _p(L), L.stride(0), p0, _p(U),
+                                     self._st()))
+
+    def tslw_owned_rows(self, X, L, row0, ids, p0, U):
+        n = X.shape[1]
+        out = torch.empty(ids.numel(), n - p0, dtype=torch.float64, device=self.dev)
+        check(self.L.rlhc_tslw_owned_rows(_p(X), X.stride(0), _p(L), L.stride(0), X.shape[0], row0, _p(ids),
+                                          ids.numel(), p0, n, _p(U), _p(out), self._st()))
+        return out
+
+    def tslw_finish(self, L, row0, U, piv):
+        check(self.L.rlhc_tslw_finish(_p(L), L.stride(0), L.shape[0], row0, L.shape[1], _p(U), _p(piv), self._st()))
+
     def eliminate(self, src, p0, w, n, U, dst):
         ws = self._ws(self.L.rlhc_tslu_eliminate_workspace_size(n))
         check(self.L.rlhc_tslu_eliminate(_p(src), src.stride(0), src.shape[0], p0, w, n, _p(U), _p(dst),
@@ -228,7 +247,25 @@ class DistPlan:
         U = B.zeros(n, n)
         piv = B.zeros(n, dtype=torch.int64)
         chosen = B.zeros(m, dtype=torch.uint8)
-        for p0 in range(0, n, cfg.panel):
+        if getattr(B, "warp_contract", lambda: False)() and n > 16:
+            # left-looking panels (the single-process pipeline's arithmetic): this rank's Schur
+            # complement of the panel into Q, the local tournament, the gathered top levels, the
+            # winners' current rows from their owners (all-reduced), their elimination -> U rows
+            for p0 in range(0, n, cfg.panel):
+                w = min(cfg.panel, n - p0)
+                B.tslw_schur(X, Q, p0, U)
+                ids, cnt, vals = B.tslu_reduce(Q, self.row0, p0, w, chosen if p0 > 0 else None)
+                if self.world > 1:
+                    ids, cnt, vals = B.tslu_combine(self._allgather(ids), self._allgather(cnt),
+                                                    self._allgather(vals), w)
+                root = ids[0, :w].contiguous()
+                prow = self._allreduce(B.tslw_owned_rows(X, Q, self.row0, root, p0, U))
+                infos.append(B.panel_factor_rows(prow, root, p0, w, n, self.row0, m, U, piv, chosen))
+            B.tslw_finish(Q, self.row0, U, piv)
+            L = Q
+        else:
+            L = None
+        for p0 in (range(0, n, cfg.panel) if L is None else ()):
             w = min(cfg.panel, n - p0)
             src = X if p0 == 0 else Q
             ids, cnt, vals = B.tslu_reduce(src, self.row0, p0, w, chosen if p0 > 0 else None)
@@ -239,9 +276,10 @@ class DistPlan:
             infos.append(B.panel_factor_rows(prow, root, p0, w, n, self.row0, m, U, piv, chosen))
             if p0 + w < n:
                 B.eliminate(src, p0, w, n, U, Q)
-        Xp = self._allreduce(B.owned_rows(X, self.row0, piv, 0, n))
-        L11 = B.l11(Xp, U)
-        L = B.lfactor(X, self.row0, U, L11, piv, Q)
+        if L is None:
+            Xp = self._allreduce(B.owned_rows(X, self.row0, piv, 0, n))
+            L11 = B.l11(Xp, U)
+            L = B.lfactor(X, self.row0, U, L11, piv, Q)
         # ---------------- sketch of L (P:280 / P:294), all-reduced partials
         if self.algo == "slhc3":
             Ls = self._allreduce(B.sketch_gauss(L, self.row0, self.s, self.seed, 0))

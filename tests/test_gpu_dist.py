@@ -24,7 +24,10 @@ def test_world1_matches_single_call(ora):
     from paper_2412_06551_b200.dist import DistPlan
     for algo, m, n, kw, cfgt in [("sslhc3", 65536, 64, dict(s1=512, s2=128), (256, 2, 64)),
                                  ("slhc3", 32768, 32, dict(s=64), (512, 2, 32)),
-                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64))]:
+                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64)),
+                                 # the default (warp) contract: left-looking row-sharded panels
+                                 ("slhc3", 65536, 64, dict(s=128), (128, 8, 16)),
+                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (128, 8, 16))]:
         X = synth.baseline_matrix(m, n, 10, 7, device="cuda")
         cfg = TsluCfg(*cfgt)
         plan = DistPlan(algo, m, n, seed=2, cfg=cfg, device="cuda", **kw)
@@ -38,7 +41,7 @@ def test_world1_matches_single_call(ora):
         assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) <= 1e-13 * np.sqrt(n)
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, cfgt):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -46,8 +49,8 @@ def _worker(rank, world, port, out_path):
         import synth
         from paper_2412_06551_b200._lib import TsluCfg
         from paper_2412_06551_b200.dist import DistPlan
-        m, n = 32768, 48
-        cfg = TsluCfg(256, 2, 48)
+        m, n = (32768 if cfgt[0] == 256 else 131072), 48  # rank subtrees complete (512 = 8^3 leaves)
+        cfg = TsluCfg(*cfgt)
         mloc = m // world
         X = synth.baseline_matrix(m, n, 9, 4, device="cuda", row0=rank * mloc, rows=mloc)
         plan = DistPlan("sslhc3", m, n, s1=384, s2=96, seed=6, cfg=cfg, device="cuda")
@@ -59,14 +62,15 @@ def _worker(rank, world, port, out_path):
         dist.destroy_process_group()
 
 
-def test_two_gloo_ranks_on_one_gpu(ora):
+@pytest.mark.parametrize("cfgt", [(256, 2, 48), (128, 8, 16)])
+def test_two_gloo_ranks_on_one_gpu(ora, cfgt):
     import synth
     d = tempfile.mkdtemp()
     out = os.path.join(d, "r")
-    mp.spawn(_worker, args=(2, 29700 + os.getpid() % 200, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, 29700 + os.getpid() % 200 + cfgt[0] % 7, out, cfgt), nprocs=2, join=True)
     res = [np.load(out + f".{r}.npz") for r in range(2)]
-    X = synth.baseline_matrix(32768, 48, 9, 4, device="cuda").cpu().numpy()
-    ref = ora.sslhc3(X, 384, 96, 6, 256, 2, 48)
+    X = synth.baseline_matrix(32768 if cfgt[0] == 256 else 131072, 48, 9, 4, device="cuda").cpu().numpy()
+    ref = ora.sslhc3(X, 384, 96, 6, *cfgt)
     for r in res:
         assert tuple(r["info"]) == (0, 0, 0)
         assert np.array_equal(r["piv"], ref.piv)
@@ -86,7 +90,9 @@ def test_c_dist_entry_matches_single_call(with_comm):
     comm = NcclComm() if with_comm else None
     for algo, m, n, kw, cfgt in [("slhc3", 65536, 64, dict(s=128), (256, 4, 64)),
                                  ("sslhc3", 65536, 128, dict(s1=1024, s2=256), (256, 4, 64)),
-                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64))]:
+                                 ("sslhc3", 16384, 100, dict(s1=800, s2=200), (256, 2, 64)),
+                                 ("slhc3", 65536, 64, dict(s=128), (128, 8, 16)),
+                                 ("sslhc3", 65536, 128, dict(s1=1024, s2=256), (128, 8, 16))]:
         X = synth.baseline_matrix(m, n, 12, 8, device="cuda")
         cfg = TsluCfg(*cfgt)
         plan = CDistPlan(algo, m, n, seed=3, cfg=cfg, device="cuda", comm=comm, **kw)

@@ -56,9 +56,10 @@ def split_stages(call):
             stage = "hqr_y"
         elif base.startswith("chol") or base in ("transpose_kernel", "zero_lower_kernel"):
             stage = {"solve_w_gram1": "chol1", "solve_v_gram2": "chol2"}.get(stage, stage)
-        elif base in ("rowsolve_kernel", "gemm_update_kernel", "gram_kernel", "gram_reduce_kernel",
+        elif base in ("rowsolve_kernel", "subst_ms_kernel", "gemm_update_kernel", "gram_kernel", "gram_reduce_kernel",
                       "gram_part_reduce_kernel", "pivot_rows_kernel"):
-            if base == "rowsolve_kernel" or (base == "gemm_update_kernel" and stage in ("hqr_y", "chol1", "chol2")):
+            if base in ("rowsolve_kernel", "subst_ms_kernel") or \
+                    (base == "gemm_update_kernel" and stage in ("hqr_y", "chol1", "chol2")):
                 if stage in ("hqr_y",):
                     stage = "solve_w_gram1"
                 elif stage == "chol1":
