@@ -391,16 +391,11 @@ RLHC_DEV void stage_rows(WSel& sm, int w, const double* Lb, int64_t ldl, int64_t
   __syncwarp();
 }
 
-// Schur complement of panel [p0, p0+w), thread per row (CTA = 128 rows):
-//   PRO (p0 > 0): the previous panel's S values (L's columns [p0-16, p0)) -> L by forward
-//   substitution with U's diagonal block (in place; same chain as the select);
-//   S_j = X[:, p0:p0+w] - L[:, :p0] U[:p0, p0:p0+w] (fma chain in increasing k) -> L's
-//   columns [p0, p0+w).  Also the input check of X's panel columns.
-// Row tiles (128 x 16) are staged with coalesced cp.async: X (issued before the wait on
-// the previous kernel: X is never written), S_{j-1}, and L in double-buffered 16-column
-// chunks; every thread then reads its own row from shared memory.
-constexpr int SR = 128;  // rows per Schur CTA
-constexpr int ST = 17;   // tile row stride (doubles): conflict-free LDS.64 by row
+// First panel (p0 = 0): its Schur values are X's panel columns -- the copy into L's columns
+// [0, w) with the input check of those columns.  CTA = 128 rows, coalesced staging through
+// shared memory both ways (X is never written: its load is issued before the dependency wait).
+constexpr int SR = 128;  // rows per CTA
+constexpr int ST = 17;   // tile row stride (doubles)
 RLHC_DEV void schur_stage(double* tile, const double* base, int64_t ld, int64_t rb, int64_t rows, int col, int w) {
   const int c = threadIdx.x & 15;
 #pragma unroll
@@ -410,107 +405,29 @@ RLHC_DEV void schur_stage(double* tile, const double* base, int64_t ld, int64_t 
     cp_async8(tile + q * ST + c, in ? base + (rb + q) * ld + col + c : base, in ? 8 : 0);
   }
 }
-__host__ __device__ inline size_t schur_smem(int p0) {
-  return ((size_t)p0 * WW + WW * WW + WW + 4 * SR * ST) * sizeof(double);
-}
-template <bool PRO>
 __global__ void __launch_bounds__(SR)
-tslw_schur_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
-                  int p0, int w, int n, const double* __restrict__ U, const double* __restrict__ rd,
-                  unsigned long long* finite_status) {
-  extern __shared__ __align__(16) double sh[];
-  double* Bx = sh;              // X tile
-  double* Bs = Bx + SR * ST;    // S_{j-1} tile -> L_{j-1}
-  double* Rc = Bs + SR * ST;    // two L chunk tiles
-  double* Ucol = Rc + 2 * SR * ST;  // [p0][WW]: U[k, p0 + c]
-  double* Ublk = Ucol + (size_t)p0 * WW;
-  double* rdp = Ublk + WW * WW;
+tslw_schur0_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
+                   int w, int n, unsigned long long* finite_status) {
+  __shared__ double Bx[SR * ST];
   const int64_t rb = (int64_t)blockIdx.x * SR;
   const int tid = threadIdx.x;
-  schur_stage(Bx, X, ldx, rb, rows, p0, w);
+  schur_stage(Bx, X, ldx, rb, rows, 0, w);
   cp_async_commit();
   pdl_trigger();
-  pdl_wait();  // L and U come from the previous kernels
-  const int kold = PRO ? p0 - WW : 0;
-  const int nch = kold / WW;
-  if (PRO) schur_stage(Bs, Lb, ldl, rb, rows, p0 - WW, WW);
-  cp_async_commit();
-  if (nch > 0) schur_stage(Rc, Lb, ldl, rb, rows, 0, WW);
-  cp_async_commit();
-  if (nch > 1) schur_stage(Rc + SR * ST, Lb, ldl, rb, rows, WW, WW);
-  cp_async_commit();
-  for (int e = tid; e < p0 * WW; e += SR) {
-    const int k = e / WW, c = e - k * WW;
-    Ucol[e] = c < w ? U[(int64_t)k * n + p0 + c] : 0.0;
-  }
-  if (PRO) {
-    for (int e = tid; e < WW * WW; e += SR) {
-      const int k = e / WW, c = e - k * WW;
-      Ublk[e] = U[(int64_t)(p0 - WW + k) * n + p0 - WW + c];
-    }
-    if (tid < WW) rdp[tid] = rd[p0 - WW + tid];
-  }
-  asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // X and S_{j-1} (the chunks may be in flight)
+  pdl_wait();  // L may still be read by the previous call's last kernels
+  cp_async_wait_all();
   __syncthreads();
   const int64_t r = rb + tid;
-  const bool valid = r < rows;
-  double acc[WW];
-#pragma unroll
-  for (int c = 0; c < WW; c++) acc[c] = Bx[tid * ST + c];
-  if (finite_status && valid) {
+  if (finite_status && r < rows) {
 #pragma unroll
     for (int c = 0; c < WW; c++)
-      if (c < w && !isfinite(acc[c])) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, r * n + p0 + c);
+      if (c < w && !isfinite(Bx[tid * ST + c])) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, r * n + c);
   }
-  if (PRO) {
-    double l[WW];
+  const int c = tid & 15;
 #pragma unroll
-    for (int c = 0; c < WW; c++) l[c] = Bs[tid * ST + c];
-    subst_row_rl(l, WW, [&](int k, int c) { return Ublk[k * WW + c]; }, [&](int k) { return rdp[k]; });
-#pragma unroll
-    for (int c = 0; c < WW; c++) Bs[tid * ST + c] = l[c];
-    if (valid) {
-#pragma unroll
-      for (int c = 0; c < WW; c++) Lb[r * ldl + kold + c] = l[c];
-    }
-  }
-#pragma unroll 1
-  for (int ch = 0; ch < nch; ch++) {
-    if (ch + 1 < nch) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-    const double* lt = Rc + (ch & 1) * SR * ST + tid * ST;
-    const double* uk = Ucol + ch * WW * WW;
-#pragma unroll
-    for (int k = 0; k < WW; k++) {
-      const double lk = lt[k];
-#pragma unroll
-      for (int c = 0; c < WW; c++) acc[c] = __fma_rn(-lk, uk[k * WW + c], acc[c]);
-    }
-    __syncthreads();
-    if (ch + 2 < nch) schur_stage(Rc + (ch & 1) * SR * ST, Lb, ldl, rb, rows, (ch + 2) * WW, WW);
-    cp_async_commit();
-  }
-  if (PRO) {
-    const double* uk = Ucol + kold * WW;
-#pragma unroll
-    for (int k = 0; k < WW; k++) {
-      const double lk = Bs[tid * ST + k];
-#pragma unroll
-      for (int c = 0; c < WW; c++) acc[c] = __fma_rn(-lk, uk[k * WW + c], acc[c]);
-    }
-  }
-  // S_j through the X tile (this thread's row), stored coalesced
-#pragma unroll
-  for (int c = 0; c < WW; c++) Bx[tid * ST + c] = acc[c];
-  __syncthreads();
-  {
-    const int c = tid & 15;
-#pragma unroll
-    for (int j = 0; j < SR / 8; j++) {
-      const int q = (tid >> 4) + 8 * j;
-      if (rb + q < rows && c < w) Lb[(rb + q) * ldl + p0 + c] = Bx[q * ST + c];
-    }
+  for (int j = 0; j < SR / 8; j++) {
+    const int q = (tid >> 4) + 8 * j;
+    if (rb + q < rows && c < w) Lb[(rb + q) * ldl + c] = Bx[q * ST + c];
   }
 }
 
@@ -1177,8 +1094,6 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   static bool attr = false;
   if (!attr) {
     const int mx = 227 * 1024;
-    cudaFuncSetAttribute(tslw_schur_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(tslw_schur_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(tslw_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
     attr = true;
@@ -1187,15 +1102,12 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
     const int w = std::min(WW, n - p0);
-    const size_t smem = schur_smem(p0);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    const unsigned sgrid = (unsigned)ceil_div<int64_t>(rows, SR);
     note_launch();
     e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                         sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U, (const double*)rd,
                         check_input ? status : nullptr)
-           : launch_pdl(tslw_schur_kernel<false>, dim3(sgrid), dim3(SR), smem, st, X, ldx, Lb, ldl, rows, p0, w, n,
-                        (const double*)U, (const double*)rd, check_input ? status : nullptr);
+           : launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx, Lb,
+                        ldl, rows, w, n, check_input ? status : nullptr);
     if (e) return e;
     if (Sw) {  // exact GEPP: one cooperative launch per panel
       static int per_sm = 0;
@@ -1240,14 +1152,13 @@ cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t 
                               const double* U, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tslw_schur_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
     attr = true;
   }
   note_launch();
   if (p0 == 0)
-    return launch_pdl(tslw_schur_kernel<false>, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), schur_smem(0), st,
-                      X, ldx, Lb, ldl, rows, 0, w, n, U, (const double*)nullptr, (unsigned long long*)nullptr);
+    return launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx, Lb,
+                      ldl, rows, w, n, (unsigned long long*)nullptr);
   return launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                     sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, U, (const double*)nullptr,
                     (unsigned long long*)nullptr);
