@@ -123,11 +123,22 @@ cudaError_t launch_subst_ms(const double* A, int64_t lda, int64_t rows, int n, c
 // sketch.cu
 size_t gauss_partials_bytes(int64_t rows, int n, int s);
 cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s, uint64_t seed,
-                                uint32_t stream_id, double* part, double* out, cudaStream_t st);
+                                uint32_t stream_id, double* part, double* out, cudaStream_t st,
+                                const double* Om = nullptr);
+// Omega stored (s x cols, ld omega_ld(cols)) for the OMEM sketch; generated off the critical path
+int64_t omega_ld(int64_t cols);
+size_t omega_bytes(int64_t s, int64_t cols);
+cudaError_t launch_omega_gen(uint64_t seed, uint32_t stream_id, int s, int64_t cols, int64_t row0, double* Om,
+                             cudaStream_t st);
 size_t cs_plan_bytes(int64_t rows, int s1);
 cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s1,
                                 uint64_t seed, void* plan_ws, double* out, int32_t* bucket_out, int8_t* sign_out,
                                 cudaStream_t st);
+// the two halves of launch_sketch_count: the plan (hash, histogram, scan, scatter) depends
+// only on the seed and sizes, so it can run off the critical path; apply gathers the buckets
+cudaError_t launch_cs_plan(int64_t rows, int64_t row0, int s1, uint64_t seed, void* plan_ws, cudaStream_t st);
+cudaError_t launch_cs_apply(const double* A, int64_t lda, int64_t rows, int n, int s1, void* plan_ws, double* out,
+                            cudaStream_t st);
 
 // small.cu
 size_t hqr_ws_bytes(int s, int n);

@@ -189,6 +189,58 @@ struct AlgoWs {
   double *U, *L11, *S, *Y, *G, *D, *Di, *J, *Ji, *N, *rdY;
   double *Lt, *Ls, *part, *work;
   void* plan;
+  double* Om;  // the stored Gaussian sketch (nullptr: generated inside the sketch kernel)
+};
+
+// Omega (and the CountSketch plan) depend only on the seed and the sizes: they are produced
+// on a side stream forked at the start of the call, overlapping the latency-bound TSLU, and
+// joined before the sketch.  Bounded so that huge sketches keep the in-kernel generator.
+constexpr size_t kOmegaStoreMax = size_t(4) << 30;
+// SLHC3 stores Omega only for n > 256, where the in-kernel generator would redo it for
+// every 256-column tile; below that the side-stream generator costs the TSLU more than it
+// saves the sketch (cfg2: TSLU +45 us, sketch -35 us).  RLHC_OMEGA_STORE=0/1 overrides
+// (measurement knob).
+static size_t omega_store_bytes(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2) {
+  static const int force = [] {
+    const char* e = getenv("RLHC_OMEGA_STORE");
+    return e ? atoi(e) : -1;
+  }();
+  const bool want = force >= 0 ? force != 0 : (algo == RLHC_SSLHC3 || n > 256);
+  const size_t b = algo == RLHC_SLHC3 ? omega_bytes(s_or_s1, m) : omega_bytes(s2, s_or_s1);
+  return want && b <= kOmegaStoreMax ? b : 0;
+}
+
+// one non-blocking side stream and a fork/join event pair per host thread and device
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static cudaError_t side_stream(SideStream** out) {
+  static thread_local std::array<SideStream, 64> per_dev;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  SideStream& ss = per_dev[dev];
+  if (!ss.s) {
+    if ((e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking))) return e;
+    if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming))) return e;
+  }
+  *out = &ss;
+  return cudaSuccess;
+}
+// joins the side stream back into `st` on every exit path (a capture must not end forked)
+struct SideJoin {
+  cudaStream_t st = nullptr;
+  SideStream* ss = nullptr;
+  cudaError_t join() {
+    if (!ss) return cudaSuccess;
+    SideStream* p = ss;
+    ss = nullptr;
+    return cudaStreamWaitEvent(st, p->join, 0);
+  }
+  ~SideJoin() { join(); }
 };
 
 void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg& cfg,
@@ -210,6 +262,8 @@ void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   size_t work = std::max(hqr_ws_bytes((int)srows, (int)n), chol_ws_bytes((int)n));
   a.work = c.take<double>(work / sizeof(double) + 1);
   a.plan = algo == RLHC_SSLHC3 ? (void*)c.take<char>(cs_plan_bytes(m, (int)s_or_s1)) : nullptr;
+  const size_t ob = omega_store_bytes(algo, m, n, s_or_s1, s2);
+  a.Om = ob ? c.take<double>(ob / sizeof(double)) : nullptr;
 }
 
 int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s_or_s1, int64_t s2, uint64_t seed,
@@ -220,6 +274,23 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   Marks mk = prof_begin(st);
   mk.mark(0);
   CUDA_TRY(launch_status_init(status, st));
+  // side stream: Omega (SLHC3: s x m; SSLHC3: s2 x s1) and the CountSketch plan
+  SideJoin side;
+  if (a.Om) {
+    SideStream* ss = nullptr;
+    CUDA_TRY(side_stream(&ss));
+    CUDA_TRY(cudaEventRecord(ss->fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    side.st = st;
+    side.ss = ss;
+    if (algo == RLHC_SLHC3) {
+      CUDA_TRY(launch_omega_gen(seed, 0u, (int)s_or_s1, m, 0, a.Om, ss->s));
+    } else {
+      CUDA_TRY(launch_cs_plan(m, 0, (int)s_or_s1, seed, a.plan, ss->s));
+      CUDA_TRY(launch_omega_gen(seed, 1u, (int)s2, s_or_s1, 0, a.Om, ss->s));
+    }
+    CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+  }
   // input check: a pass of its own, or (one panel) folded into the TSLU leaves' read of X
   const bool fold_check = cfg.panel >= n || tslw_cfg(cfg, m, n);
   if (!fold_check) CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
@@ -253,13 +324,15 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   if (!l_done && (rc = solve_pass(X, ldx, a.U, a.t.rd, a.pivpos, a.L11, nullptr))) return rc;
   mk.mark(3);
   int64_t srows;
+  CUDA_TRY(side.join());
   if (algo == RLHC_SLHC3) {  // L_s = Omega L
     srows = s_or_s1;
-    CUDA_TRY(launch_sketch_gauss(Q, ldq, m, ni, 0, (int)srows, seed, 0u, a.part, a.Ls, st));
+    CUDA_TRY(launch_sketch_gauss(Q, ldq, m, ni, 0, (int)srows, seed, 0u, a.part, a.Ls, st, a.Om));
   } else {                   // L_t = Omega_1 L, L_ss = Omega_2 L_t
     srows = s2;
-    CUDA_TRY(launch_sketch_count(Q, ldq, m, ni, 0, (int)s_or_s1, seed, a.plan, a.Lt, nullptr, nullptr, st));
-    CUDA_TRY(launch_sketch_gauss(a.Lt, n, s_or_s1, ni, 0, (int)s2, seed, 1u, a.part, a.Ls, st));
+    if (a.Om) CUDA_TRY(launch_cs_apply(Q, ldq, m, ni, (int)s_or_s1, a.plan, a.Lt, st));
+    else CUDA_TRY(launch_sketch_count(Q, ldq, m, ni, 0, (int)s_or_s1, seed, a.plan, a.Lt, nullptr, nullptr, st));
+    CUDA_TRY(launch_sketch_gauss(a.Lt, n, s_or_s1, ni, 0, (int)s2, seed, 1u, a.part, a.Ls, st, a.Om));
   }
   mk.mark(4);
   // [H, S] = HouseholderQR(L_s), sign(S_kk) = sign(U_kk) (R#7); Y = S U

@@ -52,20 +52,40 @@ size_t gauss_partials_bytes(int64_t rows, int n, int s) {
   return (size_t)g.nsplit * g.ti * g.tj * ST * g.nt * sizeof(double);
 }
 
-template <int NTW>
+template <int NTW, bool OMEM>
 struct GaussSmem {
   static constexpr int NT = 32 * NTW;
-  double A[2][SK][NT + 4];   // A tile, double-buffered (row pad 4: conflict-free B fragments)
-  double Om[ST][SK + 4];     // Omega tile (row pad 4: conflict-free A fragments)
+  double A[2][SK][NT + 4];            // A tile, double-buffered (row pad 4: conflict-free B fragments)
+  double Om[OMEM ? 2 : 1][ST][SK + 4];  // Omega tile (row pad 4: conflict-free A fragments)
 };
 
-template <int NTW>
+// Omega (s x cols, entries of stream `stream_id` scaled by 1/sqrt(s), exactly the values
+// gauss_sketch_kernel generates) written to Om (row-major, ld ldom, rows rounded up to
+// even; the pad row is zero).  Launched on a side stream so that the Box-Muller work
+// overlaps the latency-bound TSLU; the sketch then streams Omega from HBM (OMEM).
+__global__ void __launch_bounds__(256)
+omega_gen_kernel(uint64_t seed, uint32_t stream_id, int s, int64_t cols, int64_t row0, double* __restrict__ Om,
+                 int64_t ldom) {
+  const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)s));
+  const int64_t total = (int64_t)((s + 1) / 2) * cols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ip = idx / cols, r = idx - ip * cols;
+    double z0, z1;
+    gauss_pair(seed, (uint64_t)(row0 + r), (uint32_t)ip, stream_id, &z0, &z1);
+    Om[(2 * ip) * ldom + r] = __dmul_rn(z0, scale);
+    Om[(2 * ip + 1) * ldom + r] = (2 * ip + 1 < s) ? __dmul_rn(z1, scale) : 0.0;
+  }
+}
+
+template <int NTW, bool OMEM>
 __global__ void __launch_bounds__(64 * NTW)
 gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
-                    uint64_t seed, uint32_t stream_id, int64_t rows_per_split, double* __restrict__ part) {
+                    uint64_t seed, uint32_t stream_id, int64_t rows_per_split, double* __restrict__ part,
+                    const double* __restrict__ Omg, int64_t ldom) {
   constexpr int NT = 32 * NTW, NTH = 64 * NTW;
   extern __shared__ __align__(16) unsigned char gsm_raw[];
-  GaussSmem<NTW>& sm = *reinterpret_cast<GaussSmem<NTW>*>(gsm_raw);
+  GaussSmem<NTW, OMEM>& sm = *reinterpret_cast<GaussSmem<NTW, OMEM>*>(gsm_raw);
   const int tjn = (n + NT - 1) / NT;
   const int tile_i = blockIdx.x / tjn, tile_j = blockIdx.x % tjn;
   const int i0 = tile_i * ST, j0 = tile_j * NT;
@@ -86,7 +106,23 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
   // pair -- no per-copy index arithmetic or bounds tests
   constexpr int RSTEP = NTH / (NT / 2);  // rows covered per pass (NT/2 threads per row)
   const bool cols_full = aligned && j0 + NT <= n;
+  const int s_even = (s + 1) & ~1;  // rows of the stored Omega
   auto fetch = [&](int64_t k0, int b) {
+    if (OMEM) {  // Omega tile rows i0..i0+63, columns k0..k0+SK-1 (zero outside s_even x r1)
+      if (k0 + SK <= r1 && i0 + ST <= s_even) {
+        const int rr = threadIdx.x / (SK / 2), cc = 2 * (threadIdx.x % (SK / 2));
+        constexpr int OSTEP = NTH / (SK / 2);
+#pragma unroll
+        for (int j = 0; j < ST / OSTEP; j++)
+          cp_async16(&sm.Om[b][rr + j * OSTEP][cc], Omg + (int64_t)(i0 + rr + j * OSTEP) * ldom + k0 + cc);
+      } else {
+        for (int idx = threadIdx.x; idx < ST * SK; idx += NTH) {
+          const int ii = idx / SK, kk = idx - ii * SK;
+          const bool in = i0 + ii < s_even && k0 + kk < r1;
+          sm.Om[b][ii][kk] = in ? Omg[(int64_t)(i0 + ii) * ldom + k0 + kk] : 0.0;
+        }
+      }
+    }
     if (cols_full && k0 + SK <= r1) {
       const int rr = threadIdx.x / (NT / 2), cc = 2 * (threadIdx.x % (NT / 2));
       const double* src = A + (k0 + rr) * lda + j0 + cc;
@@ -112,7 +148,7 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
   int buf = 0;
   for (int64_t k0 = r0; k0 < r1; k0 += SK, buf ^= 1) {
     // Omega tile: rows i0..i0+63 (pairs i, i+1 share one Philox block), columns k0..k0+SK-1
-    for (int idx = threadIdx.x; idx < (ST / 2) * SK; idx += NTH) {
+    for (int idx = threadIdx.x; !OMEM && idx < (ST / 2) * SK; idx += NTH) {
       int ip = idx / SK, kk = idx - ip * SK;
       int i = i0 + 2 * ip;
       int64_t gr = k0 + kk;
@@ -122,8 +158,8 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
         z0 = __dmul_rn(z0, scale);
         z1 = (i + 1 < s) ? __dmul_rn(z1, scale) : 0.0;
       }
-      sm.Om[2 * ip][kk] = z0;
-      sm.Om[2 * ip + 1][kk] = z1;
+      sm.Om[0][2 * ip][kk] = z0;
+      sm.Om[0][2 * ip + 1][kk] = z1;
     }
     // next chunk's A tile into the other buffer (freed by the barrier that ended the
     // previous iteration), then wait for this chunk's tile only
@@ -138,7 +174,7 @@ gauss_sketch_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int
     for (int kk = 0; kk < SK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; a++) af[a] = sm.Om[wi + a * 8 + g][kk + t];
+      for (int a = 0; a < 4; a++) af[a] = sm.Om[OMEM ? buf : 0][wi + a * 8 + g][kk + t];
 #pragma unroll
       for (int b = 0; b < 4; b++) bf[b] = sm.A[buf][kk + t][wj + b * 8 + g];
 #pragma unroll
@@ -192,25 +228,51 @@ gauss_reduce_kernel(const double* __restrict__ part, int nsplit, int ntiles, int
   }
 }
 
-cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s, uint64_t seed,
-                                uint32_t stream_id, double* part, double* out, cudaStream_t st) {
-  GaussGeom gg = gauss_geom(rows, n, s);
-  dim3 grid(gg.ti * gg.tj, gg.nsplit);
-  static bool attr = false;  // idempotent, once per process
+int64_t omega_ld(int64_t cols) { return (cols + 3) & ~(int64_t)3; }
+size_t omega_bytes(int64_t s, int64_t cols) { return (size_t)((s + 1) & ~(int64_t)1) * omega_ld(cols) * sizeof(double); }
+
+cudaError_t launch_omega_gen(uint64_t seed, uint32_t stream_id, int s, int64_t cols, int64_t row0, double* Om,
+                             cudaStream_t st) {
+  const int64_t total = (int64_t)((s + 1) / 2) * cols;
+  if (total == 0) return cudaSuccess;
+  // full occupancy: fewer generator CTAs per SM only stretch its overlap with the TSLU
+  // (measured cfg4a TSLU +2.2 ms at 1 CTA/SM, +1.4 ms at 8)
+  static const int per_sm = [] {
+    const char* e = getenv("RLHC_OMEGA_CTAS");
+    return e ? atoi(e) : 8;
+  }();
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), (int64_t)per_sm * kSMs);
+  note_launch(); omega_gen_kernel<<<grid, 256, 0, st>>>(seed, stream_id, s, cols, row0, Om, omega_ld(cols));
+  return cudaGetLastError();
+}
+
+template <int NTW, bool OMEM>
+static void gauss_launch(dim3 grid, const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
+                         uint64_t seed, uint32_t stream_id, int64_t rps, double* part, const double* Om,
+                         int64_t ldom, cudaStream_t st) {
+  static bool attr = false;  // idempotent, once per process and instantiation
   if (!attr) {
-    cudaFuncSetAttribute(gauss_sketch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(GaussSmem<2>));
-    cudaFuncSetAttribute(gauss_sketch_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(GaussSmem<8>));
+    cudaFuncSetAttribute(gauss_sketch_kernel<NTW, OMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(GaussSmem<NTW, OMEM>));
     attr = true;
   }
+  gauss_sketch_kernel<NTW, OMEM><<<grid, 64 * NTW, sizeof(GaussSmem<NTW, OMEM>), st>>>(
+      A, lda, rows, n, row0, s, seed, stream_id, rps, part, Om, ldom);
+}
+
+cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s, uint64_t seed,
+                                uint32_t stream_id, double* part, double* out, cudaStream_t st, const double* Om) {
+  GaussGeom gg = gauss_geom(rows, n, s);
+  dim3 grid(gg.ti * gg.tj, gg.nsplit);
+  const int64_t ldom = omega_ld(rows);
   note_launch();
-  if (gg.nt == 64)
-    gauss_sketch_kernel<2><<<grid, 128, sizeof(GaussSmem<2>), st>>>(A, lda, rows, n, row0, s, seed, stream_id,
-                                                                    gg.rows_per_split, part);
-  else
-    gauss_sketch_kernel<8><<<grid, 512, sizeof(GaussSmem<8>), st>>>(A, lda, rows, n, row0, s, seed, stream_id,
-                                                                    gg.rows_per_split, part);
+  if (gg.nt == 64) {
+    if (Om) gauss_launch<2, true>(grid, A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part, Om, ldom, st);
+    else gauss_launch<2, false>(grid, A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part, Om, ldom, st);
+  } else {
+    if (Om) gauss_launch<8, true>(grid, A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part, Om, ldom, st);
+    else gauss_launch<8, false>(grid, A, lda, rows, n, row0, s, seed, stream_id, gg.rows_per_split, part, Om, ldom, st);
+  }
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   const int64_t per_split = (int64_t)gg.ti * gg.tj * ST * gg.nt;
@@ -369,9 +431,7 @@ __global__ void copy_i8_kernel(const int8_t* a, int8_t* b, int64_t cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s1,
-                                uint64_t seed, void* plan_ws, double* out, int32_t* bucket_out, int8_t* sign_out,
-                                cudaStream_t st) {
+cudaError_t launch_cs_plan(int64_t rows, int64_t row0, int s1, uint64_t seed, void* plan_ws, cudaStream_t st) {
   CsPlan pl = carve_plan(plan_ws, rows, s1);
   int nch = (int)ceil_div<int64_t>(rows, CS_CHUNK);
   size_t hsm = (size_t)s1 * sizeof(int);
@@ -386,9 +446,25 @@ cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int 
   note_launch(); cs_bucket_totals_kernel<<<ceil_div(s1, 256), 256, 0, st>>>(nch, s1, pl.hist, pl.start);
   note_launch(); cs_scan_kernel<<<1, 1024, 0, st>>>(s1, pl.start);
   note_launch(); cs_scatter_kernel<<<nch, 32, hsm, st>>>(rows, s1, pl.bucket, pl.hist, pl.start, pl.perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cs_apply(const double* A, int64_t lda, int64_t rows, int n, int s1, void* plan_ws, double* out,
+                            cudaStream_t st) {
+  CsPlan pl = carve_plan(plan_ws, rows, s1);
   const int64_t warps = (int64_t)s1 * ((n + 31) / 32);
   note_launch(); cs_apply_kernel<<<(int)ceil_div<int64_t>(warps, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start,
                                                                                     pl.sign, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_count(const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s1,
+                                uint64_t seed, void* plan_ws, double* out, int32_t* bucket_out, int8_t* sign_out,
+                                cudaStream_t st) {
+  cudaError_t e = launch_cs_plan(rows, row0, s1, seed, plan_ws, st);
+  if (e) return e;
+  if ((e = launch_cs_apply(A, lda, rows, n, s1, plan_ws, out, st))) return e;
+  CsPlan pl = carve_plan(plan_ws, rows, s1);
   if (bucket_out) note_launch(), copy_i32_kernel<<<256, 256, 0, st>>>(pl.bucket, bucket_out, rows);
   if (sign_out) note_launch(), copy_i8_kernel<<<256, 256, 0, st>>>(pl.sign, sign_out, rows);
   return cudaGetLastError();

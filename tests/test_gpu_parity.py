@@ -142,6 +142,7 @@ E2E = [
     ("sslhc3", 30000, 40, 15, True, dict(s1=320, s2=80)),
     ("sslhc3", 65536, 128, 10, False, dict(s1=1024, s2=256)),
     ("slhc3", 3000, 100, 8, False, dict(s=200)),
+    ("slhc3", 4000, 300, 6, False, dict(s=600)),                # n > 256: Omega stored (side stream)
 ]
 
 
