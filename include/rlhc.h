@@ -298,6 +298,27 @@ const char* rlhc_version(void);
 const char* rlhc_last_error(void);
 
 /* ---------------------------------------------------------------- CUDA graphs */
+/* ---- Host-buffer pipeline (end to end through the C ABI).
+ * `count` independent problems of one shape, inputs and outputs in HOST memory: problem i
+ * factors X_host[i] (m x n, row-major, ld n) with seed seeds[i] by SLHC3 (algo RLHC_SLHC3,
+ * s_or_s1 = s) or SSLHC3 (RLHC_SSLHC3, s_or_s1 = s1, s2) exactly as
+ * rlhc_slhc3 / rlhc_sslhc3 do, and writes Q_host[i] (m x n, ld n), R_host[i] (n x n),
+ * piv_host[i] (n int64, the array or an entry may be NULL) and info_host[i].
+ * Device copies are double-buffered inside `ws`: the host->device copy of problem i+1 and the
+ * device->host copies of problem i-1 run on two library-internal copy streams while problem i
+ * computes on `stream`.  Host buffers (info_host and piv_host included) should be pinned
+ * (cudaHostAlloc / cudaHostRegister): a copy into pageable memory blocks the enqueueing thread.  The call only enqueues; `stream` completes after the last copy, so
+ * synchronise it before reading the host outputs.  ws: device memory of
+ * rlhc_host_pipeline_workspace_size bytes, 256-byte aligned, owned by the caller, not to be
+ * used concurrently by another call.  Errors: RLHC_EINVAL (sizes, pointers, configuration),
+ * RLHC_EWORKSPACE, RLHC_ECUDA; numerical outcomes per problem in info_host[i]. */
+size_t rlhc_host_pipeline_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2,
+                                         const rlhc_tslu_cfg* cfg);
+int rlhc_host_pipeline(int algo, int64_t count, const double* const* X_host, int64_t m, int64_t n, int64_t s_or_s1,
+                       int64_t s2, const uint64_t* seeds, const rlhc_tslu_cfg* cfg, double* const* Q_host,
+                       double* const* R_host, int64_t* const* piv_host, rlhc_info_t* info_host, void* ws,
+                       size_t ws_bytes, rlhc_stream_t stream);
+
 /* Launch-latency cut for small problems: capture one
  * stream-ordered call (rlhc_slhc3, rlhc_sslhc3, a comparison method, a stage entry point)
  * into a CUDA graph and replay it.  rlhc_graph_begin(stream) starts a thread-local

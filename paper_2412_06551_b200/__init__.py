@@ -157,6 +157,49 @@ def sslhc3(X: torch.Tensor, s1: int, s2: int, seed: int = 0, cfg=None) -> Result
     return Plan("sslhc3", m, n, s1=s1, s2=s2, seed=seed, cfg=cfg, device=X.device).run(X)
 
 
+class HostPipeline:
+    """Host-buffer pipeline (rlhc_host_pipeline): independent SLHC3 / SSLHC3 problems of one
+    shape from host X to host Q, R, piv, info, with the host->device copy of the next problem
+    and the device->host copy of the previous one overlapping the current computation."""
+
+    def __init__(self, algo: str, m: int, n: int, s: int = 0, s1: int = 0, s2: int = 0, cfg=None, device="cuda"):
+        self.algo = RLHC_SLHC3 if algo == "slhc3" else RLHC_SSLHC3
+        self.m, self.n = m, n
+        self.a, self.b = (s, 0) if self.algo == RLHC_SLHC3 else (s1, s2)
+        self.device = torch.device(device)
+        self.cfg = _cfg(cfg, m, n)
+        nbytes = lib().rlhc_host_pipeline_workspace_size(self.algo, m, n, self.a, self.b, ctypes.byref(self.cfg))
+        if nbytes == 0:
+            raise RlhcError(_lib.RLHC_EINVAL, "invalid sizes / configuration")
+        self.ws = _ws(nbytes, self.device)
+
+    def run(self, Xs, seeds, Qs, Rs, pivs=None) -> torch.Tensor:
+        """Enqueue len(Xs) problems; Xs, Qs, Rs (and pivs) are host tensors (pinned for overlap).
+        Returns the infos as a pinned (count, 2) int64 host tensor, valid after
+        torch.cuda.synchronize(): use infos() for (code, stage, index) tuples."""
+        cnt = len(Xs)
+        for t in list(Xs) + list(Qs) + list(Rs):
+            if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous():
+                raise RlhcError(_lib.RLHC_EINVAL, "host buffers must be contiguous float64 CPU tensors")
+        ptrs = lambda ts: (ctypes.c_void_p * cnt)(*[t.data_ptr() for t in ts])  # noqa: E731
+        xs, qs, rs = ptrs(Xs), ptrs(Qs), ptrs(Rs)
+        ps = ptrs(pivs) if pivs is not None else None
+        sd = (ctypes.c_uint64 * cnt)(*seeds)
+        self._keep = (xs, qs, rs, ps, sd)  # alive until the copies ran
+        self.info = torch.zeros(max(cnt, 1), 2, dtype=torch.int64).pin_memory()  # rlhc_info_t[cnt]
+        check(lib().rlhc_host_pipeline(self.algo, cnt, xs, self.m, self.n, self.a, self.b, sd, ctypes.byref(self.cfg),
+                                       qs, rs, ps, self.info.data_ptr(), _p(self.ws), self.ws.numel(),
+                                       _stream(self.device)))
+        return self.info
+
+    def infos(self) -> list:
+        """(code, stage, index) per problem of the last run (after synchronising)."""
+        out = []
+        for w0, idx in self.info.tolist():
+            out.append((w0 & 0xFFFFFFFF, (w0 >> 32) & 0xFFFFFFFF, idx))
+        return out
+
+
 class MethodPlan:
     """Reusable call of one of the paper's comparison algorithms:
     'cholqr2', 'scholqr3', 'luc2' (tournament contract cfg) or 'rhc' (sketch sizes s1, s2)."""

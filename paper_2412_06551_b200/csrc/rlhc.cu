@@ -575,6 +575,107 @@ int rlhc_sslhc3(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t s1, 
   return algo_entry(RLHC_SSLHC3, X, m, n, ldx, s1, s2, seed, cfg, Q, ldq, R, piv, ws, ws_bytes, info, stream);
 }
 
+// ---- host-buffer pipeline: count independent problems streamed through double-buffered
+// device copies (H2D of i+1 and D2H of i-1 on internal copy streams while i computes)
+struct HostPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+};
+static cudaError_t host_pipe(HostPipe** out) {
+  static thread_local std::array<HostPipe, 64> per_dev;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  HostPipe& hp = per_dev[dev];
+  if (!hp.h2d) {
+    if ((e = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking))) return e;
+    if ((e = cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking))) return e;
+    for (int b = 0; b < 2; b++) {
+      if ((e = cudaEventCreateWithFlags(&hp.ev_h2d[b], cudaEventDisableTiming))) return e;
+      if ((e = cudaEventCreateWithFlags(&hp.ev_comp[b], cudaEventDisableTiming))) return e;
+      if ((e = cudaEventCreateWithFlags(&hp.ev_d2h[b], cudaEventDisableTiming))) return e;
+    }
+  }
+  *out = &hp;
+  return cudaSuccess;
+}
+struct PipeWs {
+  void* algo_ws;
+  size_t algo_bytes;
+  double *X[2], *Q[2], *R[2];
+  int64_t* piv[2];
+  rlhc_info_t* info[2];
+};
+static size_t pipe_carve(void* ws, int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2,
+                         const rlhc_tslu_cfg* cfg, PipeWs& p) {
+  p.algo_bytes = rlhc_workspace_size(algo, m, n, s_or_s1, s2, cfg);
+  if (!p.algo_bytes) return 0;
+  Carver c(ws);
+  p.algo_ws = c.take<char>(p.algo_bytes);
+  for (int b = 0; b < 2; b++) {
+    p.X[b] = c.take<double>((size_t)m * n);
+    p.Q[b] = c.take<double>((size_t)m * n);
+    p.R[b] = c.take<double>((size_t)n * n);
+    p.piv[b] = c.take<int64_t>((size_t)n);
+    p.info[b] = c.take<rlhc_info_t>(1);
+  }
+  return c.used;
+}
+
+size_t rlhc_host_pipeline_workspace_size(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2,
+                                         const rlhc_tslu_cfg* cfg) {
+  PipeWs p;
+  return pipe_carve(nullptr, algo, m, n, s_or_s1, s2, cfg, p);
+}
+
+int rlhc_host_pipeline(int algo, int64_t count, const double* const* X_host, int64_t m, int64_t n, int64_t s_or_s1,
+                       int64_t s2, const uint64_t* seeds, const rlhc_tslu_cfg* cfg, double* const* Q_host,
+                       double* const* R_host, int64_t* const* piv_host, rlhc_info_t* info_host, void* ws,
+                       size_t ws_bytes, rlhc_stream_t stream) {
+  if (algo != RLHC_SLHC3 && algo != RLHC_SSLHC3) return fail(RLHC_EINVAL, "unknown algorithm");
+  if (count < 0 || (count > 0 && (!X_host || !seeds || !Q_host || !R_host || !info_host || !ws)))
+    return fail(RLHC_EINVAL, "null pointer argument");
+  PipeWs p;
+  const size_t need = pipe_carve(nullptr, algo, m, n, s_or_s1, s2, cfg, p);
+  if (!need) return fail(RLHC_EINVAL, "invalid sizes");
+  if (ws_bytes < need) return fail(RLHC_EWORKSPACE, "workspace too small");
+  pipe_carve(ws, algo, m, n, s_or_s1, s2, cfg, p);
+  HostPipe* hp = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(host_pipe(&hp));
+  const size_t xb = (size_t)m * n * sizeof(double), rb = (size_t)n * n * sizeof(double);
+  // the copy streams start after the work already queued on `stream`
+  CUDA_TRY(cudaEventRecord(hp->ev_d2h[0], st));
+  CUDA_TRY(cudaStreamWaitEvent(hp->h2d, hp->ev_d2h[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->ev_d2h[0], 0));
+  for (int64_t i = 0; i < count; i++) {
+    const int b = (int)(i & 1);
+    if (!X_host[i] || !Q_host[i] || !R_host[i]) return fail(RLHC_EINVAL, "null pointer argument");
+    if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(hp->h2d, hp->ev_comp[b], 0));  // X[b] consumed by i-2
+    CUDA_TRY(cudaMemcpyAsync(p.X[b], X_host[i], xb, cudaMemcpyHostToDevice, hp->h2d));
+    CUDA_TRY(cudaEventRecord(hp->ev_h2d[b], hp->h2d));
+    CUDA_TRY(cudaStreamWaitEvent(st, hp->ev_h2d[b], 0));
+    if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(st, hp->ev_d2h[b], 0));  // Q[b], R[b] drained for i-2
+    int rc = algo_entry(algo, p.X[b], m, n, n, s_or_s1, s2, seeds[i], cfg, p.Q[b], n, p.R[b], p.piv[b], p.algo_ws,
+                        p.algo_bytes, p.info[b], stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(hp->ev_comp[b], st));
+    CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->ev_comp[b], 0));
+    CUDA_TRY(cudaMemcpyAsync(Q_host[i], p.Q[b], xb, cudaMemcpyDeviceToHost, hp->d2h));
+    CUDA_TRY(cudaMemcpyAsync(R_host[i], p.R[b], rb, cudaMemcpyDeviceToHost, hp->d2h));
+    if (piv_host && piv_host[i])
+      CUDA_TRY(cudaMemcpyAsync(piv_host[i], p.piv[b], (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToHost, hp->d2h));
+    CUDA_TRY(cudaMemcpyAsync(info_host + i, p.info[b], sizeof(rlhc_info_t), cudaMemcpyDeviceToHost, hp->d2h));
+    CUDA_TRY(cudaEventRecord(hp->ev_d2h[b], hp->d2h));
+  }
+  // `stream` completes after the last device-to-host copy
+  for (int64_t i = std::max<int64_t>(0, count - 2); i < count; i++)
+    CUDA_TRY(cudaStreamWaitEvent(st, hp->ev_d2h[i & 1], 0));
+  if (count == 0) CUDA_TRY(cudaStreamWaitEvent(st, hp->ev_d2h[0], 0));
+  return RLHC_OK;
+}
+
 // ---------------------------------------------------------------- per-stage
 static size_t getrf_carve(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, TsluWs& t, double** tw,
                           int** pivpos) {

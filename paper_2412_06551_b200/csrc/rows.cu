@@ -911,7 +911,21 @@ namespace rlhc {
 // row in registers (static indices), T in shared memory (broadcast reads), row tiles staged
 // through shared memory with coalesced cp.async; out may alias A.
 constexpr int SMS_R = 128, SMS_LD = 65;
-__host__ __device__ inline int sms_smem_bytes() { return (64 * 64 + 64 + SMS_R * SMS_LD) * (int)sizeof(double); }
+__host__ __device__ inline int sms_smem_bytes() { return (64 * 64 + 128 + SMS_R * SMS_LD) * (int)sizeof(double); }
+// a / b correctly rounded (== __ddiv_rn) from y = RN(1/b): q0 = RN(a y) is within 1.5 ulp of
+// a/b, one residual step q1 = q0 + (a - b q0) y brings it within 1 ulp, and by Markstein's
+// theorem (y within 1/2 ulp of 1/b, q1 within 1 ulp of a/b, r1 = a - b q1 exact) the second
+// step RN(q1 + r1 y) is RN(a/b).  Five dependent FP64 ops instead of the library sequence;
+// away from the exponent range where the theorem's no-underflow/overflow premise holds
+// (and for a zero quotient, to keep the sign of zero) the library division is used.
+RLHC_DEV double div_by_rcp(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double q1 = __fma_rn(__fma_rn(-b, q0, a), y, q0);
+  const double q2 = __fma_rn(__fma_rn(-b, q1, a), y, q1);
+  const double aa = fabs(a), aq = fabs(q2);
+  if (aa >= 0x1p-900 && aa <= 0x1p+900 && aq >= 0x1p-900 && aq <= 0x1p+900) return q2;
+  return __ddiv_rn(a, b);
+}
 // Persistent: each CTA stages T^T once, then loops over 128-row tiles; with GRAM the CTA
 // accumulates its partial W^T W of the upper 32 x 32 tiles on DMMA from the solved tile
 // (warp q < 3: tile (0,0), (0,1), (1,1)), reduced by gram_part_reduce_kernel.
@@ -925,7 +939,7 @@ template <int NS>
 RLHC_DEV void sms_steps(double (&acc)[64], int k0, int k1, const double* Tsh, const double* diag, double* orow) {
 #pragma unroll 1
   for (int k = k0; k < k1; k++) {
-    const double wk = __ddiv_rn(acc[0], diag[k]);
+    const double wk = div_by_rcp(acc[0], diag[k], diag[64 + k]);
     orow[k] = wk;
     const double* u = Tsh + k * 64;  // u[c] = T[k][k + 1 + c] (0 past n)
 #pragma unroll
@@ -943,15 +957,22 @@ subst_ms_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
                 double* out, int64_t ldo, double* __restrict__ gpart) {
   extern __shared__ __align__(16) double sms[];
   double* Tsh = sms;              // [64][64]: Tsh[k][c] = T[k][k + 1 + c]
-  double* diag = Tsh + 64 * 64;   // [64]
-  double* tile = diag + 64;       // [SMS_R][SMS_LD]
+  double* diag = Tsh + 64 * 64;   // [128]: T_kk, then RN(1 / T_kk)
+  double* tile = diag + 128;      // [SMS_R][SMS_LD]
   const int tid = threadIdx.x, lane = lane_id(), wq = warp_id();
   const int g = lane >> 2, t = lane & 3;
-  for (int e = tid; e < 64 * 64; e += SMS_R) {
+  for (int e = tid; e < 64 * 64; e += SMS_R) {  // all loads in flight (cp.async, zero fill)
     const int k = e >> 6, c = e & 63, j = k + 1 + c;
-    Tsh[e] = (k < n && j < n) ? T[(int64_t)k * ldt + j] : 0.0;
+    const bool in = k < n && j < n;
+    cp_async8(Tsh + e, in ? T + (int64_t)k * ldt + j : T, in ? 8 : 0);
   }
-  if (tid < 64) diag[tid] = tid < n ? T[(int64_t)tid * ldt + tid] : 1.0;
+  cp_async_commit();
+  if (tid < 64) {  // diag[k] = T_kk, diag[64 + k] = RN(1 / T_kk) (NaN outside div_by_rcp's range)
+    const double d = tid < n ? T[(int64_t)tid * ldt + tid] : 1.0;
+    const double ad = fabs(d);
+    diag[tid] = d;
+    diag[64 + tid] = (ad >= 0x1p-900 && ad <= 0x1p+900) ? __drcp_rn(d) : __longlong_as_double(0x7ff8000000000000LL);
+  }
   const int ncp = (n + 7) & ~7;
   const int gt = (ncp + 31) / 32;
   const int gti = wq >> 1, gtj = (wq == 0) ? 0 : 1;  // warp 0: (0,0), 1: (0,1), 2: (1,1)

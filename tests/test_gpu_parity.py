@@ -270,6 +270,28 @@ def test_trsm_subst_bitwise(m, n):
     assert np.array_equal(W2.cpu().numpy(), oracle.trsm_right_upper(X.cpu().numpy(), U.cpu().numpy()))
 
 
+@pytest.mark.gpu
+def test_trsm_subst_bitwise_wide_exponents():
+    """The substitution's division (reciprocal + two residual steps, the library division
+    outside 2^-900..2^900 and for zero quotients) is IEEE division bit for bit: diagonal and
+    rows scaled over 10^-300..10^300, exact zeros, quotients that underflow and overflow."""
+    import oracle
+    import paper_2412_06551_b200 as rl
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(99)
+    m, n = 4096, 48
+    Ah = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-300, 300, (m, 1))
+    Ah[::7, 3] = 0.0
+    Ah[5::11, :] *= 1e-20
+    Th = np.triu(rng.standard_normal((n, n))) * 1e-3 + np.diag(10.0 ** rng.uniform(-30, 30, n))
+    W, _, info = rl.trsm_apply(torch.from_numpy(Ah).to(dev), torch.from_numpy(Th).to(dev))
+    ref = oracle.trsm_right_upper(Ah, Th)
+    got = W.cpu().numpy()
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin)
+    assert np.array_equal(got[fin], ref[fin])
+
+
 def test_exact_gepp_pivots_match_lapack(rl):
     """The one-leaf contract is exact partial pivoting: the GPU's pivot order is LAPACK
     dgetrf's row interchanges (scipy lu_factor) on a Gaussian matrix."""
@@ -284,3 +306,27 @@ def test_exact_gepp_pivots_match_lapack(rl):
     for k, p in enumerate(ipiv):
         perm[[k, p]] = perm[[p, k]]
     assert np.array_equal(piv.cpu().numpy(), perm[:n])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo,m,n,kw", [("slhc3", 20000, 64, dict(s=128)),
+                                         ("sslhc3", 30000, 40, dict(s1=320, s2=80))])
+def test_host_pipeline_matches_device_calls(rl, algo, m, n, kw):
+    """rlhc_host_pipeline: host X -> host Q, R, piv, info for several problems with the
+    copies overlapping the computation; every problem bit-identical to the device-buffer call."""
+    dev = torch.device("cuda", 0)
+    cnt = 5
+    Xs = [_x(m, n, 8, 40 + i).cpu().pin_memory() for i in range(cnt)]
+    Qs = [torch.empty(m, n, dtype=torch.float64).pin_memory() for _ in range(cnt)]
+    Rs = [torch.empty(n, n, dtype=torch.float64).pin_memory() for _ in range(cnt)]
+    ps = [torch.empty(n, dtype=torch.int64).pin_memory() for _ in range(cnt)]
+    seeds = [7 + 3 * i for i in range(cnt)]
+    hp = rl.HostPipeline(algo, m, n, device=dev, **kw)
+    hp.run(Xs, seeds, Qs, Rs, ps)
+    torch.cuda.synchronize(dev)
+    assert hp.infos() == [(0, 0, 0)] * cnt
+    fn = rl.slhc3 if algo == "slhc3" else rl.sslhc3
+    for i in range(cnt):
+        res = fn(Xs[i].to(dev), seed=seeds[i], **kw)
+        assert torch.equal(res.Q.cpu(), Qs[i]) and torch.equal(res.R.cpu(), Rs[i])
+        assert torch.equal(res.piv.cpu(), ps[i])
