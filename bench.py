@@ -214,12 +214,13 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     if world == 1 and isinstance(plan, rl.Plan):
         hp = rl.HostPipeline(cfg.algo, m_rows, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, cfg=tcfg, device=dev)
         Qh2 = torch.empty_like(Qh).pin_memory()
-        Qs = [Qh if k % 2 == 0 else Qh2 for k in range(args.steps)]
-        Rs = [Rh] * args.steps
+        nq = max(args.steps, args.warmup)
+        Qs = [Qh if k % 2 == 0 else Qh2 for k in range(nq)]
+        Rs = [Rh] * nq
         hp.run([Xh] * args.warmup, [cfg.seed] * args.warmup, Qs[:args.warmup], Rs[:args.warmup])
         torch.cuda.synchronize(dev)
         e0.record(stream)
-        hp.run([Xh] * args.steps, [cfg.seed] * args.steps, Qs, Rs)
+        hp.run([Xh] * args.steps, [cfg.seed] * args.steps, Qs[:args.steps], Rs[:args.steps])
         e1.record(stream)
         e1.synchronize()
         bad = [c for c in hp.infos() if c[0] != 0]

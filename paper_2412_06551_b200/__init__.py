@@ -178,6 +178,8 @@ class HostPipeline:
         Returns the infos as a pinned (count, 2) int64 host tensor, valid after
         torch.cuda.synchronize(): use infos() for (code, stage, index) tuples."""
         cnt = len(Xs)
+        if len(seeds) != cnt or len(Qs) != cnt or len(Rs) != cnt or (pivs is not None and len(pivs) != cnt):
+            raise RlhcError(_lib.RLHC_EINVAL, "Xs, seeds, Qs, Rs (and pivs) must have the same length")
         for t in list(Xs) + list(Qs) + list(Rs):
             if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous():
                 raise RlhcError(_lib.RLHC_EINVAL, "host buffers must be contiguous float64 CPU tensors")
