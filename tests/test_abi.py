@@ -101,3 +101,20 @@ def test_dist_entry_host_errors():
                             dummy, dummy, dummy, 1 << 30, info, None, None)
     assert rc == _lib.RLHC_EINVAL and b"leaf_rows" in L.rlhc_last_error()
     assert L.rlhc_dist_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(cfg), 8) > 0
+
+
+def test_host_pipeline_host_checks(L):
+    """rlhc_host_pipeline: workspace = the algorithm's plus two device copies of X, Q, R, piv,
+    info; invalid algorithm / sizes / pointers are host errors (no device call)."""
+    from paper_2412_06551_b200 import _lib
+    m, n, s = 4096, 32, 64
+    cfg = _lib.TsluCfg()
+    L.rlhc_default_tslu_cfg(m, n, ctypes.byref(cfg))
+    algo_ws = L.rlhc_workspace_size(0, m, n, s, 0, ctypes.byref(cfg))
+    ws = L.rlhc_host_pipeline_workspace_size(0, m, n, s, 0, ctypes.byref(cfg))
+    assert ws >= algo_ws + 2 * 8 * (2 * m * n + n * n + n)
+    assert L.rlhc_host_pipeline_workspace_size(0, m, n, n - 1, 0, ctypes.byref(cfg)) == 0  # s < n
+    assert L.rlhc_host_pipeline(7, 0, None, m, n, s, 0, None, ctypes.byref(cfg), None, None, None, None, None,
+                                0, None) == _lib.RLHC_EINVAL
+    assert L.rlhc_host_pipeline(0, 1, None, m, n, s, 0, None, ctypes.byref(cfg), None, None, None, None, None,
+                                0, None) == _lib.RLHC_EINVAL
