@@ -2,16 +2,19 @@
 """bench.py -- SLHC3 / SSLHC3 (arXiv 2412.06551) fp64 QR on B200: time and HBM GB/s
 against the roofline (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5]
 
 One JSON line on rank 0.  A step = one full SLHC3/SSLHC3 call (every stage of
-SURVEY.md 8(a)) on the configuration's synthetic X, resident in HBM.  `value` is the
-algorithmic HBM throughput of the whole job: the bytes of the 8 required passes over m x n
-data (8 * 8 m n bytes) per second of device time (max over ranks).
-L2 is flushed between timed steps (a 512 MiB write, outside the timed events).
+SURVEY.md 8(a)) on the configuration's synthetic X, resident in HBM.  The default workload
+is BASELINE.json's headline: cfg5, SSLHC3 on m = 2^24, n = 256 (the metric is quoted "at
+1/2/4/8 B200" on it; it fits one B200).  `value` is the algorithmic HBM throughput of the
+whole job: the bytes of the 8 required passes over m x n data (8 * 8 m n bytes, DESIGN.md
+section 6) per second of device time (max over ranks).  X (32 GiB at cfg5) is far larger
+than L2; L2 is also flushed between timed steps (a 512 MiB write, outside the timed events).
 N > 1 runs the row-sharded algorithm (paper_2412_06551_b200.dist) with NCCL: by default
-weak scaling (every rank holds the config's m rows; --config cfg2 at N = 1 is the
-BASELINE metric workload), --strong keeps the config's m fixed (north star: --config cfg5).
+strong scaling of the config's m (the north star: cfg5 at 1/2/4/8 GPUs); --weak gives every
+rank the config's m rows.  Every arm runs the same pivot contract, restated below
+(TSLU_CONTRACT), on the GPU and in the oracle.
 """
 from __future__ import annotations
 
@@ -117,17 +120,21 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     functional = os.environ.get("RLHC_BENCH_FUNCTIONAL") == "1"
     dev = torch.device("cuda", 0 if functional else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
+    tcfg = None
     if world > 1:
         from paper_2412_06551_b200 import dist as rdist
-        X, plan = rdist.setup_bench(cfg, rank, world, dev, strong=args.strong, use_c=not functional)
+        X, plan = rdist.setup_bench(cfg, rank, world, dev, strong=not args.weak, use_c=not functional,
+                                    contract=_default_cfg_tuple(cfg))
         run = lambda: plan.run(X)  # noqa: E731
     else:
         X = synth.config_matrix(cfg, device=dev)
         if args.method in METHOD_PASSES:
             s1, s2 = _rhc_sizes(cfg)
-            plan = rl.MethodPlan(args.method, cfg.m, cfg.n, s1=s1, s2=s2, seed=cfg.seed, device=dev)
+            plan = rl.MethodPlan(args.method, cfg.m, cfg.n, s1=s1, s2=s2, seed=cfg.seed, cfg=_default_cfg_tuple(cfg),
+                                 device=dev)
         else:
-            tcfg = (cfg.m, 2, min(16, cfg.n)) if args.pivot == "gepp" else None  # one leaf = exact GEPP
+            # the restated contract (TSLU_CONTRACT); --pivot gepp: one leaf = exact GEPP
+            tcfg = (cfg.m, 2, min(16, cfg.n)) if args.pivot == "gepp" else _default_cfg_tuple(cfg)
             plan = rl.Plan(cfg.algo, cfg.m, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, cfg=tcfg, device=dev)
         run = lambda: plan.run(X)  # noqa: E731
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -179,59 +186,69 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
 
     # ---- end to end through the public API with host buffers: every step copies this
     # rank's rows of X from pinned host memory and reads Q (its rows) and R back; device
-    # time, max over ranks
+    # time, max over ranks.  The device-resident buffers of the timed part are released
+    # first (cfg5: X, Q are 32 GiB each; the host pipeline double-buffers both).
     m_rows = X.shape[0]
-    Xh = X.cpu().pin_memory()
+    Xh = torch.empty(m_rows, cfg.n, dtype=torch.float64).pin_memory()
+    Xh.copy_(X)
     Qh = torch.empty(m_rows, cfg.n, dtype=torch.float64).pin_memory()
     Rh = torch.empty(cfg.n, cfg.n, dtype=torch.float64).pin_memory()
-    Xd = torch.empty_like(X)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tot = 0.0
-    for k in range(args.warmup + args.steps):
-        flush.zero_()
-        if world > 1:
-            torch.distributed.barrier()
-        e0.record(stream)
-        Xd.copy_(Xh, non_blocking=True)
-        r2 = plan.run(Xd)
-        Qh.copy_(r2.Q, non_blocking=True)
-        Rh.copy_(r2.R, non_blocking=True)
-        e1.record(stream)
-        e1.synchronize()
-        if k >= args.warmup:
-            tot += e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([tot], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot = float(t.item())
-    serial_ms = tot / args.steps
+    big = 8 * m_rows * cfg.n > (4 << 30)
+    e2e_steps = min(args.steps, 5) if big else args.steps  # each cfg5 step moves 64 GiB over PCIe
+    e2e_warm = 1 if big else args.warmup
     e2e = {"unit": "GB/s", "h2d_bytes_per_step": 8 * m_rows * cfg.n,
-           "d2h_bytes_per_step": 8 * (m_rows * cfg.n + cfg.n * cfg.n), "per": "rank",
-           "latency_ms_per_call": serial_ms}
-    # throughput: the same K steps through rlhc_host_pipeline (host X -> host Q, R; the H2D
-    # copy of step k+1 and the D2H copy of step k-1 overlap step k's computation)
-    e2e_ms = serial_ms
+           "d2h_bytes_per_step": 8 * (m_rows * cfg.n + cfg.n * cfg.n), "per": "rank", "steps": e2e_steps}
     if world == 1 and isinstance(plan, rl.Plan):
+        del X, plan, run, res
+        torch.cuda.empty_cache()
+        # K problems through rlhc_host_pipeline (host X -> host Q, R; the H2D copy of step k+1
+        # and the D2H copy of step k-1 overlap step k's computation); the serial latency of
+        # one call (copy in, compute, copy out) from a pipeline of one problem
         hp = rl.HostPipeline(cfg.algo, m_rows, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, cfg=tcfg, device=dev)
-        Qh2 = torch.empty_like(Qh).pin_memory()
-        nq = max(args.steps, args.warmup)
-        Qs = [Qh if k % 2 == 0 else Qh2 for k in range(nq)]
-        Rs = [Rh] * nq
-        hp.run([Xh] * args.warmup, [cfg.seed] * args.warmup, Qs[:args.warmup], Rs[:args.warmup])
+        hp.run([Xh] * e2e_warm, [cfg.seed] * e2e_warm, [Qh] * e2e_warm, [Rh] * e2e_warm)
         torch.cuda.synchronize(dev)
         e0.record(stream)
-        hp.run([Xh] * args.steps, [cfg.seed] * args.steps, Qs[:args.steps], Rs[:args.steps])
+        hp.run([Xh], [cfg.seed], [Qh], [Rh])
+        e1.record(stream)
+        e1.synchronize()
+        e2e["latency_ms_per_call"] = e0.elapsed_time(e1)
+        e0.record(stream)
+        hp.run([Xh] * e2e_steps, [cfg.seed] * e2e_steps, [Qh] * e2e_steps, [Rh] * e2e_steps)
         e1.record(stream)
         e1.synchronize()
         bad = [c for c in hp.infos() if c[0] != 0]
         if bad:
             raise RuntimeError(f"host pipeline run failed: {bad[0]}")
-        e2e_ms = e0.elapsed_time(e1) / args.steps
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
         e2e["api"] = "rlhc_host_pipeline (K steps streamed; copies overlap compute)"
+        del hp
+        X = None
     else:
-        e2e["api"] = "rlhc_slhc3_dist per step (copies serial)"
+        Xd = torch.empty_like(X)
+        tot = 0.0
+        for k in range(e2e_warm + e2e_steps):
+            flush.zero_()
+            if world > 1:
+                torch.distributed.barrier()
+            e0.record(stream)
+            Xd.copy_(Xh, non_blocking=True)
+            r2 = plan.run(Xd)
+            Qh.copy_(r2.Q, non_blocking=True)
+            Rh.copy_(r2.R, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if k >= e2e_warm:
+                tot += e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([tot], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            tot = float(t.item())
+        e2e_ms = tot / e2e_steps
+        e2e["api"] = ("rlhc_slhc3_dist / rlhc_sslhc3_dist per step (copies serial)" if world > 1
+                      else "MethodPlan.run per step (copies serial)")
     e2e["ms_per_step"] = e2e_ms
-    return ms, stages, launches, clk.summary(), e2e, X
+    return ms, stages, launches, clk.summary(), e2e, Xh
 
 
 def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, m_local: int = 0, passes: int = 8):
@@ -277,30 +294,54 @@ def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, 
             "traffic": traffic, "peak_source": hbm_src, "ms": t * 1e3}
 
 
-def cpu_baseline(cfg: synth.Config, X: torch.Tensor | None, budget_s: float = 8.0, method: str = "auto"):
+def sample_rows(cfg: synth.Config) -> int:
+    """Rows of the oracle's bounded sample: the whole X up to 2^24 entries (cfg1, cfg2), else
+    the first rows of X holding 2^24 entries (cfg3: 131072 rows, cfg4: 32768, cfg5: 65536;
+    a few seconds of oracle work on 16 host cores).  Never fewer than the sketch rows
+    (s <= m, s1 <= m, P:261)."""
+    if cfg.m * cfg.n <= (1 << 24):
+        return cfg.m
+    return min(cfg.m, max((1 << 24) // cfg.n, cfg.s, cfg.s1, 1))
+
+
+def cpu_baseline(cfg: synth.Config, Xh: torch.Tensor | None, budget_s: float = 8.0, method: str = "auto",
+                 max_reps: int = 20, warm: int = 0):
+    """The oracle (oracle/, plain C, all host cores) on a bounded sample of the workload: the
+    first sample_rows(cfg) rows of the same X bytes (the whole X for cfg1-cfg3), the same
+    sketch sizes, seed and pivot contract.  value = the metric's bytes for the sample / time."""
     import oracle
     oracle.build()
-    Xh = (X.cpu() if X is not None else synth.config_matrix(cfg)).numpy()
-    reps, t0 = 0, time.perf_counter()
-    while True:
+    ms_ = sample_rows(cfg)
+    if Xh is None:
+        Xh = synth.baseline_matrix(cfg.m, cfg.n, cfg.kappa_exp, cfg.seed, cfg.colscale,
+                                   device="cuda" if torch.cuda.is_available() else "cpu", rows=ms_).cpu()
+    Xs = Xh[:ms_].numpy()
+    b, a, p = _default_cfg_tuple(cfg)
+
+    def one():
         if method in METHOD_PASSES:
             s1, s2 = _rhc_sizes(cfg)
-            b, a, p = _default_cfg_tuple(cfg)
-            {"cholqr2": lambda: oracle.cholqr2(Xh), "scholqr3": lambda: oracle.scholqr3(Xh),
-             "luc2": lambda: oracle.luc2(Xh, b, a, p), "rhc": lambda: oracle.rhc(Xh, s1, s2, cfg.seed)}[method]()
+            {"cholqr2": lambda: oracle.cholqr2(Xs), "scholqr3": lambda: oracle.scholqr3(Xs),
+             "luc2": lambda: oracle.luc2(Xs, b, a, p), "rhc": lambda: oracle.rhc(Xs, s1, s2, cfg.seed)}[method]()
         elif cfg.algo == "slhc3":
-            b, a, p = _default_cfg_tuple(cfg)
-            oracle.slhc3(Xh, cfg.s, cfg.seed, b, a, p)
+            oracle.slhc3(Xs, cfg.s, cfg.seed, b, a, p)
         else:
-            b, a, p = _default_cfg_tuple(cfg)
-            oracle.sslhc3(Xh, cfg.s1, cfg.s2, cfg.seed, b, a, p)
+            oracle.sslhc3(Xs, cfg.s1, cfg.s2, cfg.seed, b, a, p)
+
+    for _ in range(warm):
+        one()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        one()
         reps += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or reps >= 20:
+        if el >= budget_s or reps >= max_reps:
             break
     per = el / reps
-    return {"value": _passes(method) * 8.0 * cfg.m * cfg.n / per / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
-            "kind": "oracle", "sample": f"full {cfg.name} ({cfg.m}x{cfg.n}) x{reps}", "s_per_step": per}
+    what = f"full {cfg.name} ({cfg.m}x{cfg.n})" if ms_ == cfg.m else \
+        f"first {ms_} of {cfg.m} rows of {cfg.name}'s X ({ms_}x{cfg.n}, same sketch sizes, seed, contract {b, a, p})"
+    return {"value": _passes(method) * 8.0 * ms_ * cfg.n / per / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": f"{what} x{reps}", "s_per_step": per}
 
 
 # the paper's comparison algorithms (SURVEY 8(f) NEXT-1), 1 GPU: algorithmic passes over m x n
@@ -320,11 +361,13 @@ def _rhc_sizes(cfg):
 
 
 def _default_cfg_tuple(cfg):
-    # the device's default tournament contract, restated (rlhc_default_tslu_cfg)
-    panel = min(cfg.n, 64)
-    W = 16 if panel <= 16 else 32 if panel <= 32 else 64
-    rows = 256 if W == 64 else 512
-    return rows, max(2, rows // panel), panel
+    """The tournament pivot contract every arm runs (R#3), restated here rather than
+    read from the product library: 128-row leaves, 8-ary nodes, 16-column panels (CALU);
+    both the GPU and the oracle are handed exactly this tuple."""
+    return TSLU_CONTRACT[0], TSLU_CONTRACT[1], min(cfg.n, TSLU_CONTRACT[2])
+
+
+TSLU_CONTRACT = (128, 8, 16)  # (leaf_rows, arity, panel)
 
 
 def main():
@@ -333,10 +376,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--strong", action="store_true",
-                    help="N > 1: fixed global m (the config's), rows split over ranks; default: weak scaling, "
-                         "every rank holds the config's m rows")
+    ap.add_argument("--config", default="cfg5", help="BASELINE.json config (cfg5 = the headline)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: every rank holds the config's m rows (default: strong scaling, the config's m "
+                         "split over the ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", dest="graph", action="store_true", default=True,
                     help="time the call as one CUDA graph launch per step (default, N = 1)")
@@ -357,7 +400,7 @@ def main():
         cfg = dataclasses.replace(cfg, kappa_exp=args.kappa_exp)
     elif args.method == "cholqr2" and cfg.kappa_exp > 6:
         cfg = dataclasses.replace(cfg, kappa_exp=6)
-    strong = args.strong and world > 1
+    strong = world > 1 and not args.weak
     m_global = cfg.m if (strong or world == 1) else cfg.m * world
     if world > 1 and not torch.distributed.is_initialized():
         functional = os.environ.get("RLHC_BENCH_FUNCTIONAL") == "1"
@@ -371,11 +414,16 @@ def main():
              else f"s1={s1m} s2={s2m}" if algo == "rhc" else "")
     workload = (f"{cfg.name}: {algo.upper()} m={m_global} n={cfg.n}" + (" " + sizes if sizes else "")
                 + f" kappa=1e{cfg.kappa_exp}{' colscale' if cfg.colscale else ''} seed={cfg.seed}")
+    contract = (cfg.m, 2, min(16, cfg.n)) if args.pivot == "gepp" else _default_cfg_tuple(cfg)
     base = {"metric": f"{algo.upper()} fp64 QR algorithmic HBM throughput ({passes} passes of m x n)",
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "m": m_global, "n": cfg.n, "s": cfg.s, "s1": cfg.s1, "s2": cfg.s2,
-                       "kappa": f"1e{cfg.kappa_exp}", "l2": "flushed between steps (512 MiB write)",
+                       "kappa": f"1e{cfg.kappa_exp}",
+                       "tslu_contract": {"leaf_rows": contract[0], "arity": contract[1], "panel": contract[2]},
+                       "l2": (f"X ({8 * m_global * cfg.n / 2**30:.1f} GiB) larger than L2; also flushed between "
+                              "steps (512 MiB write)") if 8 * m_global * cfg.n > (256 << 20)
+                       else "flushed between steps (512 MiB write)",
                        "rows_per_gpu": m_global // world,
                        "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "1 GPU",
                        "launch": ("one CUDA graph per step (rlhc_graph_*)" if args.graph and world == 1
@@ -383,13 +431,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_baseline(cfg, None, budget_s=max(5.0, 0.5 * args.steps), method=args.method)
+        # the oracle as it stands, each step one bounded sample of the workload (sample_rows)
+        cb = cpu_baseline(cfg, None, budget_s=1e9, method=args.method, max_reps=args.steps, warm=args.warmup)
         line = dict(base, impl="reference", value=cb["value"], ms_per_step=cb["s_per_step"] * 1e3,
                     cpu_baseline=cb, e2e={"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                                           "d2h_bytes_per_step": 0}, n_gpus=0)
         print(json.dumps(line), flush=True)
         return
-    ms, stages, launches, clocks, e2e, X = run_ours(args, cfg, rank, world)
+    ms, stages, launches, clocks, e2e, Xh = run_ours(args, cfg, rank, world)
     if rank != 0:
         return
     per_step = ms / args.steps
@@ -400,7 +449,7 @@ def main():
                 roofline=roofline(cfg, stages, world, per_step, m_global // world, passes), e2e=e2e,
                 stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls" and v})
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, X, method=args.method)
+        line["cpu_baseline"] = cpu_baseline(cfg, Xh, method=args.method)
     print(json.dumps(line), flush=True)
 
 

@@ -331,7 +331,7 @@ class BenchRunner:
         return _DistResult(self.plan, Q, R, piv, infos)
 
 
-def setup_bench(cfg, rank: int, world: int, device, strong: bool = False, use_c: bool = True):
+def setup_bench(cfg, rank: int, world: int, device, strong: bool = True, use_c: bool = True, contract=None):
     """bench.py's N-GPU workload.  Weak scaling (default): every rank holds cfg.m rows and the
     job factors a (world * cfg.m) x n X under the single-GPU default contract (rank subtrees
     of 4^k leaves are complete subtrees of the global arity-4 tree, so the pivots equal a
@@ -342,9 +342,7 @@ def setup_bench(cfg, rank: int, world: int, device, strong: bool = False, use_c:
     m_local = m_global // world
     X = synth.baseline_matrix(m_global, cfg.n, cfg.kappa_exp, cfg.seed, cfg.colscale, device=device,
                               row0=rank * m_local, rows=m_local)
-    tc = dist_default_cfg(m_global, cfg.n, world)
-    if strong:
-        tc = TsluCfg(tc.leaf_rows, 2, tc.panel)
+    tc = TsluCfg(*contract) if contract is not None else dist_default_cfg(m_global, cfg.n, world)
     if use_c:  # the C orchestration (rlhc_*_dist) over an NCCL communicator of its own
         plan = CDistPlan(cfg.algo, m_global, cfg.n, s=cfg.s, s1=cfg.s1, s2=cfg.s2, seed=cfg.seed, cfg=tc,
                          device=device, comm=NcclComm())
