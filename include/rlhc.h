@@ -64,7 +64,9 @@ enum rlhc_stage {
   RLHC_STAGE_SOLVE_D = 6, /* V = W D^{-1} */
   RLHC_STAGE_CHOL2 = 7,   /* J = chol(V^T V) */
   RLHC_STAGE_SOLVE_J = 8, /* Q = V J^{-1} */
-  RLHC_STAGE_CHOL0 = 9    /* the preconditioning Cholesky of the comparison methods (below) */
+  RLHC_STAGE_CHOL0 = 9,   /* the preconditioning Cholesky of the comparison methods (below) */
+  RLHC_STAGE_COMM = 10    /* row-sharded calls: a replicated input differing across ranks
+                             (RLHC_DIST_CHECK=1 debug check; code RLHC_ENCCL, index = count) */
 };
 
 enum rlhc_algo { RLHC_SLHC3 = 0, RLHC_SSLHC3 = 1 };
@@ -187,6 +189,16 @@ size_t rlhc_tslu_local_workspace_size(int64_t rows, int64_t nslots_in, const rlh
 int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
                      const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals,
                      void* ws, size_t ws_bytes, rlhc_stream_t stream);
+/* the same down to `nslots_out` slots: the rank's rows are nslots_out complete subtrees of
+ * the global tree (leaves / nslots_out a power of the arity), written as
+ * consecutive slots out_ids[nslots_out * W], out_cnt[nslots_out], out_vals[nslots_out * W * W]
+ * in global order.  RLHC_EINVAL when the leaf count does not split that way. */
+int rlhc_tslu_reduce_to(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
+                        const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids,
+                        int* out_cnt, double* out_vals, void* ws, size_t ws_bytes, rlhc_stream_t stream);
+/* the number of slots a rank of `rows_local` rows reduces to under the contract: the leaf
+ * count divided by the largest power of the arity dividing it (1 when it is a power). */
+int64_t rlhc_tslu_local_slots(int64_t rows_local, const rlhc_tslu_cfg* cfg);
 /* the tree levels above `nslots` consecutive slots (e.g. the all-gathered rank roots). */
 int rlhc_tslu_combine(const int* in_ids, const int* in_cnt, const double* in_vals, int64_t nslots, int64_t w,
                       const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals, void* ws, size_t ws_bytes,

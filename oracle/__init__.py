@@ -28,10 +28,21 @@ def build(force: bool = False) -> str:
     """Compile the oracle (gcc, fp64, no fp contraction, OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+        # -mfma only lets fma() compile to the instruction (it is exact either way); with
+        # -ffp-contract=off no a*b+c is ever contracted, so the arithmetic is unchanged
+        isa = ["-mfma", "-mavx2"] if _host_has_fma() else []
+        subprocess.check_call(["gcc", "-O3", "-ffp-contract=off", "-fno-fast-math", *isa, "-fopenmp", "-fPIC",
                                "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
+
+
+def _host_has_fma() -> bool:
+    try:
+        return any(" fma " in f" {ln.split(":", 1)[1]} " and " avx2 " in f" {ln.split(":", 1)[1]} "
+                   for ln in open("/proc/cpuinfo") if ln.startswith("flags"))
+    except OSError:
+        return False
 
 
 class _Info(ctypes.Structure):
@@ -43,6 +54,8 @@ class _Stages(ctypes.Structure):
 
 
 _lib = None
+_ROWS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double))
+_QROWS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double))
 
 
 def lib():
@@ -81,6 +94,8 @@ def lib():
         L.ora_scholqr_shift.argtypes = [P, I64, I64]; L.ora_scholqr_shift.restype = D
         L.ora_luc2.argtypes = [P, I64, I64, I64, I64, I64, I64, P, I64, P, P, P]
         L.ora_rhc.argtypes = [P, I64, I64, I64, I64, I64, U64, P, I64, P, P]
+        L.ora_lhc3_chunked.argtypes = [ctypes.c_int, I64, I64, I64, I64, U64, I64, I64, I64, I64, _ROWS_FN, _QROWS_FN,
+                                       P, P, P, P, P]
     return _lib
 
 
@@ -257,6 +272,51 @@ def sslhc3(X, s1: int, s2: int, seed: int, leaf_rows: int, arity: int, panel: in
     n = X.shape[1]
     panel = n if panel is None else panel
     return _run(lib().ora_sslhc3, X, n, (s1, s2, seed, leaf_rows, arity, panel), s2, s1, stages, raise_on_error)
+
+
+def lhc3_chunked(algo: str, m: int, n: int, get_rows, s_or_s1: int, s2: int, seed: int, leaf_rows: int, arity: int,
+                 panel: int, chunk_rows: int = 65536, put_q=None, stages: bool = False,
+                 raise_on_error: bool = True) -> Result:
+    """SLHC3 / SSLHC3 with X streamed in row chunks (ora_lhc3_chunked; cfg5 does not fit the
+    in-memory oracle): get_rows(row0, rows) -> (rows x n) float64 array of X's rows;
+    put_q(row0, Q_rows) (optional) receives Q's rows.  Bit-identical to slhc3 / sslhc3.
+    Result.Q is None."""
+    sslhc = algo == "sslhc3"
+    R = np.zeros((n, n)); piv = np.zeros(n, np.int64); info = _Info()
+    err = []
+
+    def _get(user, row0, rows, buf):
+        try:
+            a = np.ascontiguousarray(get_rows(int(row0), int(rows)), dtype=np.float64)
+            assert a.shape == (rows, n), a.shape
+            ctypes.memmove(buf, a.ctypes.data, a.nbytes)
+        except BaseException as e:  # noqa: BLE001 -- reported after the call
+            err.append(e)
+
+    def _put(user, row0, rows, buf):
+        try:
+            put_q(int(row0), np.ctypeslib.as_array(buf, shape=(int(rows), n)).copy())
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    cb_get = _ROWS_FN(_get)
+    cb_put = _QROWS_FN(_put) if put_q is not None else _QROWS_FN()
+    st = _Stages(); arrs = {}
+    if stages:
+        srows = s2 if sslhc else s_or_s1
+        for k in _STAGE_SHAPES:
+            if k == "Lt" and not sslhc:
+                continue
+            shape = (srows, n) if k == "Ls" else (s_or_s1, n) if k == "Lt" else (n, n)
+            arrs[k] = np.zeros(shape)
+            setattr(st, k, arrs[k].ctypes.data)
+    lib().ora_lhc3_chunked(1 if sslhc else 0, m, n, s_or_s1, s2, ctypes.c_uint64(seed), leaf_rows, arity, panel,
+                           chunk_rows, cb_get, cb_put, None, _p(R), _p(piv), ctypes.byref(st), ctypes.byref(info))
+    if err:
+        raise err[0]
+    if raise_on_error:
+        _raise(info)
+    return Result(None, R, piv, arrs, (info.code, info.stage, info.index))
 
 
 # -------------------------------------------------- comparison algorithms (SURVEY 8(f) NEXT-1)

@@ -873,6 +873,463 @@ void ora_lfactor_rows(const double* X, int64_t rows, int64_t n, int64_t row0, co
   free(rd);
 }
 
+/* ------------------------------------------------ row-chunked SLHC3 / SSLHC3 (cfg5) */
+/* The same algorithm, step for step and bit for bit, as ora_slhc3 / ora_sslhc3 above, for
+ * X too large to hold twice in host RAM (cfg5: 2^24 x 256 = 32 GiB; SURVEY 8(c) "processes X
+ * in row chunks").  X is never stored: get(user, row0, rows, buf) delivers rows
+ * [row0, row0 + rows) (rows x n, row-major) whenever a pass needs them, and put (optional)
+ * receives the rows of Q.  Host memory is O(chunk_rows * n + n^2 + s1 * n + tree), where the
+ * tree holds at most arity pending nodes of w winners per level.
+ *
+ * Every value is the one the in-memory oracle computes:
+ *  - TSLU (R#3-R#5): per panel, the leaves' candidate values are the rows'
+ *    Schur complements at the panel start, recomputed from the X row by the elimination's own
+ *    per-element fma chain (l = a_k * (1/U_kk), a_j = fma(-l, U_kj, a_j), k increasing) --
+ *    the right-looking update of ora_tslu applies exactly this sequence to every element.
+ *    Nodes are formed as leaves stream in (arity consecutive children; the trailing partial
+ *    group of a level closes when the stream ends), so the tree is ora_tslu's tree.  Pivot
+ *    row k's U / L11 row is its X row run through pivots 0..k-1 by the same chain.
+ *  - L rows by l_row (ora_lfactor), CountSketch in ascending rows (ora_cs_apply), the
+ *    Gaussian sketch with ora_sketch_gauss's fixed 64-way row partition.
+ *  - W = X Y^-1, V = W D^-1, Q = V J^-1 recomputed per chunk by ora_trsm_right_upper (row
+ *    independent); the Grams with ora_gram's 64-row partials combined by its pairwise tree
+ *    (a binary-counter stack: merging equal-size neighbours left + right, folding the rest
+ *    from the right at the end reproduces ora_gram's step-doubling sums exactly).
+ * chunk_rows must be a positive multiple of leaf_rows and of 64. */
+typedef void (*ora_rows_fn)(void* user, int64_t row0, int64_t rows, double* buf);
+typedef void (*ora_qrows_fn)(void* user, int64_t row0, int64_t rows, const double* Q);
+
+typedef struct { int64_t cnt; int64_t ids[64]; double* vals; } ck_node; /* winners + panel-start values */
+
+typedef struct {
+  int64_t w, arity, nlev;
+  ck_node* pend;       /* [lev * arity + i] */
+  int64_t* npend;      /* pending children per level */
+  int64_t* total;      /* nodes ever pushed per level */
+  ck_node root;
+  int have_root;
+} ck_tree;
+
+static void ck_node_free(ck_node* nd) { free(nd->vals); nd->vals = NULL; nd->cnt = 0; }
+
+/* GEPP over the stacked children (their order = global order), winners keep their values */
+static ck_node ck_combine(const ck_node* ch, int64_t nch, int64_t w) {
+  int64_t tot = 0;
+  for (int64_t c = 0; c < nch; c++) tot += ch[c].cnt;
+  ck_node out; out.cnt = 0; out.vals = (double*)malloc(sizeof(double) * (size_t)(w * w > 0 ? w * w : 1));
+  int64_t* ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(tot > 0 ? tot : 1));
+  double* V = (double*)malloc(sizeof(double) * (size_t)((tot > 0 ? tot : 1) * w));
+  double* B = (double*)malloc(sizeof(double) * (size_t)((tot > 0 ? tot : 1) * w));
+  int64_t q = 0;
+  for (int64_t c = 0; c < nch; c++)
+    for (int64_t e = 0; e < ch[c].cnt; e++, q++) {
+      ids[q] = ch[c].ids[e];
+      memcpy(V + q * w, ch[c].vals + e * w, sizeof(double) * (size_t)w);
+    }
+  memcpy(B, V, sizeof(double) * (size_t)(tot * w));
+  out.cnt = gepp_select(B, ids, tot, w, out.ids);
+  for (int64_t t = 0; t < out.cnt; t++) {
+    int64_t pos = 0;
+    while (ids[pos] != out.ids[t]) pos++;
+    memcpy(out.vals + t * w, V + pos * w, sizeof(double) * (size_t)w);
+  }
+  free(ids); free(V); free(B);
+  return out;
+}
+
+static void ck_push(ck_tree* T, int64_t lev, ck_node nd) {
+  if (lev >= T->nlev) { /* grow */
+    int64_t nl = T->nlev * 2 + 4;
+    T->pend = (ck_node*)realloc(T->pend, sizeof(ck_node) * (size_t)(nl * T->arity));
+    T->npend = (int64_t*)realloc(T->npend, sizeof(int64_t) * (size_t)nl);
+    T->total = (int64_t*)realloc(T->total, sizeof(int64_t) * (size_t)nl);
+    for (int64_t l = T->nlev; l < nl; l++) { T->npend[l] = 0; T->total[l] = 0; }
+    T->nlev = nl;
+  }
+  T->pend[lev * T->arity + T->npend[lev]++] = nd;
+  T->total[lev]++;
+  if (T->npend[lev] == T->arity) {
+    ck_node parent = ck_combine(T->pend + lev * T->arity, T->arity, T->w);
+    for (int64_t i = 0; i < T->arity; i++) ck_node_free(T->pend + lev * T->arity + i);
+    T->npend[lev] = 0;
+    ck_push(T, lev + 1, parent);
+  }
+}
+
+/* end of the stream: close every level's trailing partial group, bottom up */
+static void ck_finish(ck_tree* T) {
+  for (int64_t lev = 0; lev < T->nlev; lev++) {
+    if (T->total[lev] == 1 && T->npend[lev] == 1) { /* the only node of its level: the root */
+      T->root = T->pend[lev * T->arity];
+      T->npend[lev] = 0;
+      T->have_root = 1;
+      return;
+    }
+    if (T->npend[lev] > 0) {
+      ck_node parent = ck_combine(T->pend + lev * T->arity, T->npend[lev], T->w);
+      for (int64_t i = 0; i < T->npend[lev]; i++) ck_node_free(T->pend + lev * T->arity + i);
+      T->npend[lev] = 0;
+      ck_push(T, lev + 1, parent);
+    }
+  }
+}
+
+/* a row's current values after pivots 0..K-1 (columns < jmax): the elimination chain */
+static void ck_eliminate(double* a, int64_t K, int64_t jmax, int64_t n, const double* U, const double* rd) {
+  for (int64_t k = 0; k < K; k++) {
+    double l = a[k] * rd[k];
+    a[k] = l;
+    for (int64_t j = k + 1; j < jmax; j++) a[j] = fma(-l, U[k * n + j], a[j]);
+  }
+}
+
+/* row of L (l_row's values): a pivot row takes its L11 row, any other row is its X row run
+ * through all n pivots by the elimination chain -- per element the same fma sequence as
+ * l_row's substitution (k increasing), evaluated column-oriented so it vectorises */
+static void ck_lrow(const double* x, int64_t n, const double* U, const double* rd, const double* L11, int64_t pp,
+                    double* l) {
+  if (pp >= 0) { memcpy(l, L11 + pp * n, sizeof(double) * (size_t)n); return; }
+  memcpy(l, x, sizeof(double) * (size_t)n);
+  ck_eliminate(l, n, n, n, U, rd);
+}
+
+static int cmp_i64(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* position k of row id in piv[0..cnt) (sorted copy with positions), -1 if not a pivot */
+typedef struct { int64_t id, k; } ck_pp;
+static int cmp_pp(const void* a, const void* b) {
+  int64_t x = ((const ck_pp*)a)->id, y = ((const ck_pp*)b)->id;
+  return x < y ? -1 : x > y;
+}
+static int64_t ck_pivpos(const ck_pp* srt, int64_t cnt, int64_t id) {
+  int64_t lo = 0, hi = cnt;
+  while (lo < hi) { int64_t mid = (lo + hi) / 2; if (srt[mid].id < id) lo = mid + 1; else hi = mid; }
+  return (lo < cnt && srt[lo].id == id) ? srt[lo].k : -1;
+}
+
+/* out = A T^{-1}: ora_trsm_right_upper's per-element sequence (acc = a_k; acc -= o_j T_jk as a
+ * rounded product then a rounded difference, j increasing; o_k = acc / T_kk) evaluated
+ * column-oriented (o_k final before it is used), so the loop over later columns is
+ * independent per element and vectorises; every element sees the identical operation
+ * sequence (tests/test_oracle_chunked.py checks the bits against ora_trsm_right_upper). */
+static int ck_trsm(const double* A, int64_t rows, int64_t n, const double* T, double* out, int stage,
+                   ora_info* info) {
+  for (int64_t k = 0; k < n; k++)
+    if (T[k * n + k] == 0.0 || !isfinite(T[k * n + k])) return set_err(info, ORA_ESINGULAR, stage, k);
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; i++) {
+    double* o = out + i * n;
+    if (o != A + i * n) memcpy(o, A + i * n, sizeof(double) * (size_t)n);
+    for (int64_t k = 0; k < n; k++) {
+      double ok = o[k] / T[k * n + k];
+      o[k] = ok;
+      const double* t = T + k * n;
+      for (int64_t j = k + 1; j < n; j++) o[j] -= ok * t[j];
+    }
+  }
+  return ORA_OK;
+}
+
+int ora_num_threads(void);
+
+/* Gram partial stack (ora_gram's pairwise tree, streamed).  Buffers are recycled through a
+ * free list (a fresh calloc per 64-row partial page-faults 512 KB at n = 256). */
+typedef struct { double* P; int64_t size; } ck_gp;
+typedef struct { ck_gp* s; int64_t top, cap, nn; double** pool; int64_t npool, cappool; } ck_gstack;
+static double* ck_gtake(ck_gstack* g) {
+  if (g->npool > 0) return g->pool[--g->npool];
+  return (double*)malloc(sizeof(double) * (size_t)g->nn);
+}
+static void ck_ggive(ck_gstack* g, double* P) {
+  if (g->npool == g->cappool) {
+    g->cappool = g->cappool * 2 + 8;
+    g->pool = (double**)realloc(g->pool, sizeof(double*) * (size_t)g->cappool);
+  }
+  g->pool[g->npool++] = P;
+}
+/* push the next 64-row partial (copied): merge equal-size neighbours, left += right */
+static void ck_gpush(ck_gstack* g, const double* src) {
+  double* cur = ck_gtake(g);
+  memcpy(cur, src, sizeof(double) * (size_t)g->nn);
+  int64_t size = 1;
+  while (g->top > 0 && g->s[g->top - 1].size == size) {
+    double* left = g->s[--g->top].P;
+    for (int64_t t = 0; t < g->nn; t++) left[t] += cur[t];
+    ck_ggive(g, cur);
+    cur = left; size *= 2;
+  }
+  if (g->top == g->cap) { g->cap = g->cap * 2 + 8; g->s = (ck_gp*)realloc(g->s, sizeof(ck_gp) * (size_t)g->cap); }
+  g->s[g->top].P = cur; g->s[g->top].size = size; g->top++;
+}
+static void ck_gfree(ck_gstack* g) {
+  while (g->top > 0) free(g->s[--g->top].P);
+  while (g->npool > 0) free(g->pool[--g->npool]);
+  free(g->s); free(g->pool);
+  g->s = NULL; g->pool = NULL; g->cap = g->cappool = 0;
+}
+static void ck_gfinish(ck_gstack* g, int64_t n, double* G) {
+  double* P;
+  if (g->top == 0) { P = ck_gtake(g); memset(P, 0, sizeof(double) * (size_t)g->nn); }
+  else {
+    P = g->s[--g->top].P;
+    while (g->top > 0) {
+      double* left = g->s[--g->top].P;
+      for (int64_t t = 0; t < g->nn; t++) left[t] += P[t];
+      ck_ggive(g, P);
+      P = left;
+    }
+  }
+  for (int64_t i = 0; i < n; i++)
+    for (int64_t j = i; j < n; j++) { G[i * n + j] = P[i * n + j]; G[j * n + i] = P[i * n + j]; }
+  ck_ggive(g, P);
+  ck_gfree(g);
+}
+/* 64-row partials of rows (chunks are multiples of 64 rows; only the last may be ragged),
+ * computed NT at a time in per-thread buffers, then pushed in row order */
+static void ck_gram_rows(ck_gstack* g, const double* A, int64_t rows, int64_t n) {
+  const int64_t CH = 64;
+  int64_t nch = (rows + CH - 1) / CH;
+  int nt = ora_num_threads();
+  double* buf = (double*)malloc(sizeof(double) * (size_t)nt * (size_t)(n * n));
+  for (int64_t c0 = 0; c0 < nch; c0 += nt) {
+    int64_t c1 = c0 + nt < nch ? c0 + nt : nch;
+    #pragma omp parallel for schedule(static, 1)
+    for (int64_t c = c0; c < c1; c++) {
+      double* P = buf + (size_t)(c - c0) * (size_t)(n * n);
+      memset(P, 0, sizeof(double) * (size_t)(n * n));
+      int64_t r1 = (c + 1) * CH < rows ? (c + 1) * CH : rows;
+      /* ora_gram's P[i,j] += a_r[i] a_r[j] over r ascending, tiled over (i, j) so a tile of
+       * P stays in L1 (per element the same sequence) */
+      for (int64_t ib = 0; ib < n; ib += 32)
+        for (int64_t jb = ib; jb < n; jb += 32) {
+          int64_t ie = ib + 32 < n ? ib + 32 : n, je = jb + 32 < n ? jb + 32 : n;
+          for (int64_t r = c * CH; r < r1; r++) {
+            const double* a = A + r * n;
+            for (int64_t i = ib; i < ie; i++) {
+              double ai = a[i];
+              for (int64_t j = (i > jb ? i : jb); j < je; j++) P[i * n + j] += ai * a[j];
+            }
+          }
+        }
+    }
+    for (int64_t c = c0; c < c1; c++) ck_gpush(g, buf + (size_t)(c - c0) * (size_t)(n * n));
+  }
+  free(buf);
+}
+
+int ora_lhc3_chunked(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2, uint64_t seed, int64_t b,
+                     int64_t arity, int64_t panel, int64_t chunk_rows, ora_rows_fn get, ora_qrows_fn put, void* user,
+                     double* R, int64_t* piv, ora_stages* st, ora_info* info) {
+  if (info) { info->code = 0; info->stage = 0; info->index = 0; }
+  const int sslhc = algo == 1;
+  const int64_t s = s_or_s1, s1 = s_or_s1;
+  if (m < n || n < 1 || b < 1 || arity < 2 || panel < 1 || panel > 64 || !get || chunk_rows < 1 ||
+      chunk_rows % b || chunk_rows % 64)
+    return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  if (sslhc ? (s2 < n || s1 < s2 || s1 > m) : (s < n || s > m)) return set_err(info, ORA_EINVAL, ST_INPUT, 0);
+  const size_t nn = (size_t)(n * n);
+  double* Xc = (double*)malloc(sizeof(double) * (size_t)(chunk_rows * n));
+  double* Wc = (double*)malloc(sizeof(double) * (size_t)(chunk_rows * n));
+  double* Sv = (double*)malloc(sizeof(double) * (size_t)(chunk_rows * (panel < n ? panel : n)));
+  double* U = (double*)calloc(nn, sizeof(double));
+  double* L11 = (double*)calloc(nn, sizeof(double));
+  double* rd = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t* chosen = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t nchosen = 0;
+  int rc = ORA_OK;
+  /* O0: finite input */
+  for (int64_t c0 = 0; c0 < m && rc == ORA_OK; c0 += chunk_rows) {
+    int64_t rows = (m - c0) < chunk_rows ? (m - c0) : chunk_rows;
+    get(user, c0, rows, Xc);
+    for (int64_t t = 0; t < rows * n; t++)
+      if (!isfinite(Xc[t])) { rc = set_err(info, ORA_ENONFINITE, ST_INPUT, c0 * n + t); break; }
+  }
+  /* TSLU over panels */
+  for (int64_t p0 = 0; p0 < n && rc == ORA_OK; p0 += panel) {
+    const int64_t w = (n - p0) < panel ? (n - p0) : panel;
+    ck_tree T = {w, arity, 0, NULL, NULL, NULL, {0, {0}, NULL}, 0};
+    for (int64_t c0 = 0; c0 < m; c0 += chunk_rows) {
+      int64_t rows = (m - c0) < chunk_rows ? (m - c0) : chunk_rows;
+      get(user, c0, rows, Xc);
+      #pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; i++) {
+        double* a = Xc + i * n;
+        ck_eliminate(a, p0, p0 + w, n, U, rd);
+        memcpy(Sv + i * w, a + p0, sizeof(double) * (size_t)w);
+      }
+      int64_t nl = (rows + b - 1) / b;
+      ck_node* leaves = (ck_node*)malloc(sizeof(ck_node) * (size_t)nl);
+      #pragma omp parallel for schedule(dynamic, 4)
+      for (int64_t l = 0; l < nl; l++) {
+        int64_t r0 = l * b, r1 = (r0 + b < rows) ? r0 + b : rows;
+        ck_node leaf; leaf.cnt = 0;
+        leaf.vals = (double*)malloc(sizeof(double) * (size_t)(w * w));
+        int64_t* ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(r1 - r0));
+        double* B = (double*)malloc(sizeof(double) * (size_t)((r1 - r0) * w));
+        int64_t c = 0;
+        for (int64_t i = r0; i < r1; i++) {
+          int64_t id = c0 + i;
+          if (bsearch(&id, chosen, (size_t)nchosen, sizeof(int64_t), cmp_i64)) continue;
+          ids[c] = id;
+          memcpy(B + c * w, Sv + i * w, sizeof(double) * (size_t)w);
+          c++;
+        }
+        leaf.cnt = gepp_select(B, ids, c, w, leaf.ids);
+        for (int64_t t = 0; t < leaf.cnt; t++) {
+          int64_t pos = 0;
+          while (ids[pos] != leaf.ids[t]) pos++;
+          memcpy(leaf.vals + t * w, Sv + (ids[pos] - c0) * w, sizeof(double) * (size_t)w);
+        }
+        free(ids); free(B);
+        leaves[l] = leaf;
+      }
+      for (int64_t l = 0; l < nl; l++) ck_push(&T, 0, leaves[l]);
+      free(leaves);
+    }
+    ck_finish(&T);
+    if (T.root.cnt < w) rc = set_err(info, ORA_ERANKDEF, ST_LU, p0 + T.root.cnt);
+    for (int64_t t = 0; t < w && rc == ORA_OK; t++) piv[p0 + t] = T.root.ids[t];
+    ck_node_free(&T.root);
+    free(T.pend); free(T.npend); free(T.total);
+    /* this panel's U / L11 rows: pivot row k through pivots 0..k-1 */
+    for (int64_t k = p0; k < p0 + w && rc == ORA_OK; k++) {
+      double* a = Wc;
+      get(user, piv[k], 1, a);
+      ck_eliminate(a, k, n, n, U, rd);
+      if (a[k] == 0.0) { rc = set_err(info, ORA_ERANKDEF, ST_LU, k); break; }
+      for (int64_t j = k; j < n; j++) U[k * n + j] = a[j];
+      for (int64_t j = 0; j < k; j++) L11[k * n + j] = a[j];
+      L11[k * n + k] = 1.0;
+      rd[k] = 1.0 / U[k * n + k];
+    }
+    for (int64_t t = 0; t < w && rc == ORA_OK; t++) chosen[nchosen++] = piv[p0 + t];
+    qsort(chosen, (size_t)nchosen, sizeof(int64_t), cmp_i64);
+  }
+  double *Lt = NULL, *Ls = NULL, *part = NULL;
+  double *S = NULL, *Y = NULL, *G = NULL, *D = NULL, *J = NULL, *N = NULL, *A = NULL;
+  ck_pp* srt = NULL;
+  const int64_t srows = sslhc ? s2 : s;
+  if (rc) goto out;
+  if (st && st->U) memcpy(st->U, U, sizeof(double) * nn);
+  if (st && st->L11) memcpy(st->L11, L11, sizeof(double) * nn);
+  for (int64_t k = 0; k < n; k++) rd[k] = 1.0 / U[k * n + k];
+  srt = (ck_pp*)malloc(sizeof(ck_pp) * (size_t)n);
+  for (int64_t k = 0; k < n; k++) { srt[k].id = piv[k]; srt[k].k = k; }
+  qsort(srt, (size_t)n, sizeof(ck_pp), cmp_pp);
+  /* L rows and their sketch (P:280 / P:294) */
+  Ls = (double*)malloc(sizeof(double) * (size_t)(srows * n));
+  if (sslhc) {
+    Lt = (double*)calloc((size_t)(s1 * n), sizeof(double));
+    int32_t* bucket = (int32_t*)malloc(sizeof(int32_t) * (size_t)chunk_rows);
+    int8_t* sign = (int8_t*)malloc((size_t)chunk_rows);
+    for (int64_t c0 = 0; c0 < m; c0 += chunk_rows) {
+      int64_t rows = (m - c0) < chunk_rows ? (m - c0) : chunk_rows;
+      get(user, c0, rows, Xc);
+      #pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; i++) ck_lrow(Xc + i * n, n, U, rd, L11, ck_pivpos(srt, n, c0 + i), Wc + i * n);
+      ora_cs_hash(seed, c0, rows, s1, bucket, sign);
+      for (int64_t j = 0; j < rows; j++) { /* ora_cs_apply's ascending-row accumulation */
+        double* o = Lt + (int64_t)bucket[j] * n;
+        const double* a = Wc + j * n;
+        if (sign[j] > 0) for (int64_t c = 0; c < n; c++) o[c] += a[c];
+        else             for (int64_t c = 0; c < n; c++) o[c] -= a[c];
+      }
+    }
+    free(bucket); free(sign);
+    if (st && st->Lt) memcpy(st->Lt, Lt, sizeof(double) * (size_t)(s1 * n));
+    ora_sketch_gauss(Lt, s1, n, n, 0, s2, seed, 1u, Ls);
+  } else {
+    /* ora_sketch_gauss's 64 partials over the fixed row partition [m ch/64, m (ch+1)/64) */
+    const int NCH = 64;
+    part = (double*)calloc((size_t)NCH * s * n, sizeof(double));
+    for (int64_t c0 = 0; c0 < m; c0 += chunk_rows) {
+      int64_t rows = (m - c0) < chunk_rows ? (m - c0) : chunk_rows;
+      get(user, c0, rows, Xc);
+      #pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; i++) ck_lrow(Xc + i * n, n, U, rd, L11, ck_pivpos(srt, n, c0 + i), Wc + i * n);
+      #pragma omp parallel for schedule(static)
+      for (int ch = 0; ch < NCH; ch++) {
+        int64_t a0 = m * ch / NCH, a1 = m * (ch + 1) / NCH;
+        if (a0 < c0) a0 = c0;
+        if (a1 > c0 + rows) a1 = c0 + rows;
+        double* P = part + (size_t)ch * s * n;
+        double* om = (double*)malloc(sizeof(double) * (size_t)s);
+        for (int64_t j = a0; j < a1; j++) {
+          for (int64_t i = 0; i < s; i += 2) {
+            double z0, z1;
+            ora_gauss_pair(seed, (uint64_t)j, (uint32_t)(i >> 1), 0u, &z0, &z1);
+            double sc = 1.0 / sqrt((double)s);
+            om[i] = z0 * sc;
+            if (i + 1 < s) om[i + 1] = z1 * sc;
+          }
+          const double* a = Wc + (j - c0) * n;
+          for (int64_t i = 0; i < s; i++) {
+            double wv = om[i];
+            double* p = P + i * n;
+            for (int64_t c = 0; c < n; c++) p[c] += wv * a[c];
+          }
+        }
+        free(om);
+      }
+    }
+    memset(Ls, 0, sizeof(double) * (size_t)(s * n));
+    for (int ch = 0; ch < NCH; ch++)
+      for (int64_t t = 0; t < s * n; t++) Ls[t] += part[(size_t)ch * s * n + t];
+  }
+  if (st && st->Ls) memcpy(st->Ls, Ls, sizeof(double) * (size_t)(srows * n));
+  /* the tail of lhc_tail, with W and V recomputed per chunk */
+  S = (double*)malloc(sizeof(double) * nn); Y = (double*)malloc(sizeof(double) * nn);
+  G = (double*)malloc(sizeof(double) * nn); D = (double*)malloc(sizeof(double) * nn);
+  J = (double*)malloc(sizeof(double) * nn); N = (double*)malloc(sizeof(double) * nn);
+  A = (double*)malloc(sizeof(double) * (size_t)(srows * n));
+  memcpy(A, Ls, sizeof(double) * (size_t)(srows * n));
+  rc = ora_hqr_r(A, srows, n, S, info);
+  if (rc) goto out;
+  for (int64_t k = 0; k < n; k++)
+    if ((S[k * n + k] < 0.0) != (U[k * n + k] < 0.0))
+      for (int64_t j = 0; j < n; j++) S[k * n + j] = -S[k * n + j];
+  ora_trmm_uu(S, U, n, Y);
+  if (st && st->S) memcpy(st->S, S, sizeof(double) * nn);
+  if (st && st->Y) memcpy(st->Y, Y, sizeof(double) * nn);
+  for (int pass = 0; pass < 3 && rc == ORA_OK; pass++) {
+    ck_gstack gs = {NULL, 0, 0, (int64_t)nn, NULL, 0, 0};
+    for (int64_t c0 = 0; c0 < m && rc == ORA_OK; c0 += chunk_rows) {
+      int64_t rows = (m - c0) < chunk_rows ? (m - c0) : chunk_rows;
+      get(user, c0, rows, Xc);
+      rc = ck_trsm(Xc, rows, n, Y, Wc, ST_SOLVE_Y, info);                 /* W */
+      if (!rc && pass >= 1) rc = ck_trsm(Wc, rows, n, D, Wc, ST_SOLVE_D, info); /* V */
+      if (!rc && pass >= 2) rc = ck_trsm(Wc, rows, n, J, Wc, ST_SOLVE_J, info); /* Q */
+      if (rc) break;
+      if (pass < 2) ck_gram_rows(&gs, Wc, rows, n);
+      else if (put) put(user, c0, rows, Wc);
+    }
+    if (rc) { ck_gfree(&gs); break; }
+    if (pass == 0) {
+      ck_gfinish(&gs, n, G);
+      if (st && st->G1) memcpy(st->G1, G, sizeof(double) * nn);
+      rc = ora_chol(G, n, D, ST_CHOL1, info);
+    } else if (pass == 1) {
+      ck_gfinish(&gs, n, G);
+      if (st && st->G2) memcpy(st->G2, G, sizeof(double) * nn);
+      rc = ora_chol(G, n, J, ST_CHOL2, info);
+    } else {
+      ck_gfree(&gs);
+    }
+  }
+  if (rc) goto out;
+  ora_trmm_uu(D, Y, n, N);
+  ora_trmm_uu(J, N, n, R);
+  if (st && st->D) memcpy(st->D, D, sizeof(double) * nn);
+  if (st && st->J) memcpy(st->J, J, sizeof(double) * nn);
+out:
+  free(Xc); free(Wc); free(Sv); free(U); free(L11); free(rd); free(chosen); free(srt);
+  free(Lt); free(Ls); free(part); free(S); free(Y); free(G); free(D); free(J); free(N); free(A);
+  return rc;
+}
+
 int ora_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

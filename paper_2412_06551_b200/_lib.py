@@ -97,6 +97,10 @@ def lib():
     L.rlhc_tslu_local_workspace_size.argtypes = [I64, I64, PC]
     L.rlhc_tslu_local_workspace_size.restype = SZ
     L.rlhc_tslu_reduce.argtypes = [P, I64, I64, I64, I64, I64, P, PC, P, P, P, P, SZ, P]
+    L.rlhc_tslu_reduce_to.argtypes = [P, I64, I64, I64, I64, I64, P, PC, I64, P, P, P, P, SZ, P]
+    L.rlhc_tslu_reduce_to.restype = I
+    L.rlhc_tslu_local_slots.argtypes = [I64, PC]
+    L.rlhc_tslu_local_slots.restype = I64
     L.rlhc_tslu_combine.argtypes = [P, P, P, I64, I64, PC, P, P, P, P, SZ, P]
     L.rlhc_owned_rows.argtypes = [P, I64, I64, I64, P, P, I64, I64, I64, P, P]
     L.rlhc_tslu_panel_workspace_size.argtypes = [I64]
@@ -157,7 +161,8 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_gram_workspace_size", "rlhc_gram", "rlhc_trsm_apply_workspace_size", "rlhc_trsm_apply",
             "rlhc_hqr_workspace_size", "rlhc_hqr_r", "rlhc_cholesky", "rlhc_version", "rlhc_last_error",
             "rlhc_launch_count", "rlhc_stage_timing", "rlhc_stage_times", "rlhc_stage_name",
-            "rlhc_tslu_local_workspace_size", "rlhc_tslu_reduce", "rlhc_tslu_combine", "rlhc_owned_rows",
+            "rlhc_tslu_local_workspace_size", "rlhc_tslu_reduce", "rlhc_tslu_reduce_to", "rlhc_tslu_local_slots",
+            "rlhc_tslu_combine", "rlhc_owned_rows",
             "rlhc_tslu_panel_workspace_size", "rlhc_tslu_panel_factor_rows", "rlhc_tslu_eliminate_workspace_size",
             "rlhc_tslu_eliminate", "rlhc_lfactor_workspace_size", "rlhc_l11", "rlhc_lfactor", "rlhc_trmm_upper",
             "rlhc_cholesky_workspace_size", "rlhc_cholesky_ws", "rlhc_comm_unique_id", "rlhc_comm_init",

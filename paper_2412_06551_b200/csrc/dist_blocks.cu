@@ -65,26 +65,40 @@ LevelBufs carve_levels(void* ws, int64_t slots, int W) {
   }
   return b;
 }
-// reduce `nslots` slots in buffer `cur` down to one (node levels), returns final buffer index.
-// rsrc (local rows): the levels read candidate rows from it and only the final slot carries
-// values; else every slot carries values (slots gathered from other ranks)
+// reduce `nslots` slots in buffer `cur` down to `target` (node levels; nslots / target a
+// power of the arity, or target = 1), returns the final buffer index.  rsrc (local rows): the
+// levels read candidate rows from it and only the final level carries values; else every
+// slot carries values (slots gathered from other ranks)
 int reduce_levels(LevelBufs& b, int cur, int nslots, int arity, int w, int W, cudaStream_t st, int* out_cur,
-                  const RowSrc* rsrc = nullptr) {
-  while (nslots > 1) {
+                  const RowSrc* rsrc = nullptr, int target = 1) {
+  while (nslots > target) {
     const int nout = (nslots + arity - 1) / arity;
     TRY(launch_tslu_node(W, b.ids[cur], b.cnt[cur], rsrc ? nullptr : b.vals[cur], nslots, arity, w, b.ids[cur ^ 1],
-                         b.cnt[cur ^ 1], (rsrc && nout > 1) ? nullptr : b.vals[cur ^ 1], st, nullptr, rsrc));
+                         b.cnt[cur ^ 1], (rsrc && nout > target) ? nullptr : b.vals[cur ^ 1], st, nullptr, rsrc));
     nslots = nout;
     cur ^= 1;
   }
   *out_cur = cur;
   return RLHC_OK;
 }
-int copy_slot(LevelBufs& b, int cur, int W, int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st) {
-  TRY(cudaMemcpyAsync(out_ids, b.ids[cur], W * 4, cudaMemcpyDeviceToDevice, st));
-  TRY(cudaMemcpyAsync(out_cnt, b.cnt[cur], 4, cudaMemcpyDeviceToDevice, st));
-  TRY(cudaMemcpyAsync(out_vals, b.vals[cur], (size_t)W * W * 8, cudaMemcpyDeviceToDevice, st));
+int copy_slot(LevelBufs& b, int cur, int W, int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st,
+              int64_t k = 1) {
+  TRY(cudaMemcpyAsync(out_ids, b.ids[cur], k * W * 4, cudaMemcpyDeviceToDevice, st));
+  TRY(cudaMemcpyAsync(out_cnt, b.cnt[cur], k * 4, cudaMemcpyDeviceToDevice, st));
+  TRY(cudaMemcpyAsync(out_vals, b.vals[cur], (size_t)k * W * W * 8, cudaMemcpyDeviceToDevice, st));
   return RLHC_OK;
+}
+// levels from `leaves` slots down to `k` (-1: leaves / k is not a power of the arity)
+int levels_to(int64_t leaves, int64_t k, int arity) {
+  if (k < 1 || leaves % k) return -1;
+  int64_t q = leaves / k;
+  int lev = 0;
+  while (q > 1) {
+    if (q % arity) return -1;
+    q /= arity;
+    lev++;
+  }
+  return lev;
 }
 bool cfg_valid(const rlhc_tslu_cfg* c, int64_t w) {
   return c && c->panel >= 1 && c->panel <= 64 && w >= 1 && w <= c->panel && c->arity >= 2 &&
@@ -102,29 +116,47 @@ size_t rlhc_tslu_local_workspace_size(int64_t rows, int64_t nslots_in, const rlh
   return level_bytes(slots, W);
 }
 
-int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
-                     const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals,
-                     void* ws, size_t ws_bytes, rlhc_stream_t stream) {
+int64_t rlhc_tslu_local_slots(int64_t rows_local, const rlhc_tslu_cfg* cfg) {
+  if (!cfg || cfg->leaf_rows < 1 || cfg->arity < 2 || rows_local < 1) return 0;
+  int64_t k = ceil_div<int64_t>(rows_local, cfg->leaf_rows);
+  while (k % cfg->arity == 0) k /= cfg->arity;
+  return k;
+}
+
+int rlhc_tslu_reduce_to(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
+                        const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids,
+                        int* out_cnt, double* out_vals, void* ws, size_t ws_bytes, rlhc_stream_t stream) {
   if (!src || !out_ids || !out_cnt || !out_vals || !ws || rows < 1) return fail(RLHC_EINVAL, "bad arguments");
   if (!cfg_valid(cfg, w)) return fail(RLHC_EINVAL, "bad tslu configuration");
   if (ws_bytes < rlhc_tslu_local_workspace_size(rows, 0, cfg)) return fail(RLHC_EWORKSPACE, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const int W = kw(cfg->panel);
   const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
+  const int lev = nslots_out == 1 ? -1 : levels_to(nleaves, nslots_out, cfg->arity);
+  if (nslots_out != 1 && lev < 0)
+    return fail(RLHC_EINVAL, "the rank's leaves do not split into nslots_out complete subtrees");
   LevelBufs b = carve_levels(ws, nleaves, W);
   if (cfg->leaf_rows == 128 && cfg->arity >= 2 && cfg->arity <= 8 && w <= 16) {
     // the warp tournament (the default contract): every local level in one launch
-    TRY(run_tslw_local_tree(src, lds, rows, row0, (int)p0, (int)w, chosen, cfg->arity, b.ids, b.cnt, b.vals, out_ids,
-                            out_cnt, out_vals, st));
+    TRY(run_tslw_local_tree(src, lds, rows, row0, (int)p0, (int)w, chosen, cfg->arity, lev, b.ids, b.cnt, b.vals,
+                            out_ids, out_cnt, out_vals, st));
     return RLHC_OK;
   }
+  const int target = (int)nslots_out;
   TRY(launch_tslu_leaf(W, cfg->leaf_rows, src, lds, rows, row0, (int)p0, (int)w, chosen, b.ids[0], b.cnt[0],
-                       nleaves == 1 ? b.vals[0] : nullptr, st));
+                       nleaves == target ? b.vals[0] : nullptr, st));
   const RowSrc rsrc{src, lds, row0, (int)p0};
   int cur = 0;
-  int rc = reduce_levels(b, 0, nleaves, cfg->arity, (int)w, W, st, &cur, &rsrc);
+  int rc = reduce_levels(b, 0, nleaves, cfg->arity, (int)w, W, st, &cur, &rsrc, target);
   if (rc) return rc;
-  return copy_slot(b, cur, W, out_ids, out_cnt, out_vals, st);
+  return copy_slot(b, cur, W, out_ids, out_cnt, out_vals, st, target);
+}
+
+int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
+                     const uint8_t* chosen, const rlhc_tslu_cfg* cfg, int* out_ids, int* out_cnt, double* out_vals,
+                     void* ws, size_t ws_bytes, rlhc_stream_t stream) {
+  return rlhc_tslu_reduce_to(src, lds, rows, row0, p0, w, chosen, cfg, 1, out_ids, out_cnt, out_vals, ws, ws_bytes,
+                             stream);
 }
 
 int rlhc_tslu_combine(const int* in_ids, const int* in_cnt, const double* in_vals, int64_t nslots, int64_t w,

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <mutex>
 
 #include "../../include/rlhc.h"
@@ -32,8 +33,8 @@ namespace {
 // ---- the few NCCL entry points used (the C API is ABI-stable across 2.x)
 typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
-typedef enum { ncclInt32 = 2, ncclFloat64 = 8 } ncclDataType_t;
-typedef enum { ncclSum = 0 } ncclRedOp_t;
+typedef enum { ncclInt32 = 2, ncclUint64 = 5, ncclFloat64 = 8 } ncclDataType_t;
+typedef enum { ncclSum = 0, ncclMax = 2, ncclMin = 3 } ncclRedOp_t;
 typedef int ncclResult_t;
 
 struct Nccl {
@@ -93,7 +94,8 @@ int kernel_width(int panel) { return panel <= 16 ? 16 : panel <= 32 ? 32 : 64; }
 
 // first non-OK info of the pipeline, in order (device side: no host synchronisation); the
 // input check reports this rank's local element index, made global with row0 * n
-__global__ void first_info_kernel(const rlhc_info_t* infos, int k, int64_t input_offset, rlhc_info_t* out) {
+__global__ void first_info_kernel(const rlhc_info_t* infos, int k, int64_t input_offset,
+                                  const unsigned long long* mismatch, rlhc_info_t* out) {
   if (threadIdx.x != 0) return;
   rlhc_info_t r{0, 0, 0};
   for (int i = 0; i < k; i++)
@@ -102,12 +104,53 @@ __global__ void first_info_kernel(const rlhc_info_t* infos, int k, int64_t input
       if (r.stage == RLHC_STAGE_INPUT) r.index += input_offset;
       break;
     }
+  if (r.code == 0 && mismatch && *mismatch) r = rlhc_info_t{RLHC_ENCCL, RLHC_STAGE_COMM, (int64_t)*mismatch};
   *out = r;
 }
 
-constexpr int kMaxInfos = 64;
+// RLHC_DIST_CHECK: an order-sensitive 64-bit hash of `count` words (one block; debug path)
+__global__ void hash_words_kernel(const unsigned long long* __restrict__ p, size_t count, unsigned long long* hmax,
+                                  unsigned long long* hmin) {
+  __shared__ unsigned long long red[1024];
+  unsigned long long h = 0;
+  for (size_t i = threadIdx.x; i < count; i += blockDim.x) {
+    unsigned long long x = p[i] ^ (0x9E3779B97F4A7C15ull * (i + 1));
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+    h += x;
+  }
+  red[threadIdx.x] = h;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *hmax = *hmin = red[0];
+}
+// after the max / min all-reduces: count the replicated inputs whose hashes differ
+__global__ void hash_compare_kernel(const unsigned long long* hmax, const unsigned long long* hmin,
+                                    unsigned long long* mismatches) {
+  if (threadIdx.x == 0 && *hmax != *hmin) *mismatches += 1;
+}
+cudaError_t launch_hash_words(const void* p, size_t count, unsigned long long* hmax, unsigned long long* hmin,
+                              cudaStream_t st) {
+  note_launch();
+  hash_words_kernel<<<1, 1024, 0, st>>>((const unsigned long long*)p, count, hmax, hmin);
+  return cudaGetLastError();
+}
+cudaError_t launch_hash_compare(const unsigned long long* hmax, const unsigned long long* hmin,
+                                unsigned long long* mismatches, cudaStream_t st) {
+  note_launch();
+  hash_compare_kernel<<<1, 32, 0, st>>>(hmax, hmin, mismatches);
+  return cudaGetLastError();
+}
+
+// one info per stage call: the input check, one per panel, HQR, three solves, two Choleskys
+inline int64_t max_infos(int64_t n, const rlhc_tslu_cfg& cfg) { return 1 + ceil_div<int64_t>(n, cfg.panel) + 8; }
 
 struct DistWs {
+  int64_t nslots;  // slots this rank reduces to (complete subtrees of the global tree)
+  int64_t ninfos;
+  unsigned long long* hash;  // RLHC_DIST_CHECK: [sum, max, min] of the replicated inputs' hashes
   int *slot_ids, *slot_cnt, *all_ids, *all_cnt, *root_ids, *root_cnt;
   double *slot_vals, *all_vals, *root_vals;
   uint8_t* chosen;
@@ -122,7 +165,7 @@ size_t scratch_need(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64
                     int nranks) {
   size_t s = 0;
   s = std::max(s, rlhc_tslu_local_workspace_size(m_local, 0, &cfg));
-  s = std::max(s, rlhc_tslu_local_workspace_size(0, nranks, &cfg));
+  s = std::max(s, rlhc_tslu_local_workspace_size(0, (int64_t)nranks * rlhc_tslu_local_slots(m_local, &cfg), &cfg));
   s = std::max(s, rlhc_tslu_panel_workspace_size(n));
   s = std::max(s, rlhc_tslu_eliminate_workspace_size(n));
   s = std::max(s, rlhc_lfactor_workspace_size(m_local, n));
@@ -143,12 +186,16 @@ size_t scratch_need(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64
 void carve_dist(Carve& c, int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2, const rlhc_tslu_cfg& cfg,
                 int nranks, DistWs& d) {
   const int W = kernel_width(cfg.panel);
-  d.slot_ids = c.take<int>(W);
-  d.slot_cnt = c.take<int>(1);
-  d.slot_vals = c.take<double>((size_t)W * W);
-  d.all_ids = c.take<int>((size_t)nranks * W);
-  d.all_cnt = c.take<int>(nranks);
-  d.all_vals = c.take<double>((size_t)nranks * W * W);
+  const int64_t k = std::max<int64_t>(1, rlhc_tslu_local_slots(m_local, &cfg));
+  d.nslots = k;
+  d.ninfos = max_infos(n, cfg);
+  d.hash = c.take<unsigned long long>(4);
+  d.slot_ids = c.take<int>((size_t)k * W);
+  d.slot_cnt = c.take<int>(k);
+  d.slot_vals = c.take<double>((size_t)k * W * W);
+  d.all_ids = c.take<int>((size_t)nranks * k * W);
+  d.all_cnt = c.take<int>((size_t)nranks * k);
+  d.all_vals = c.take<double>((size_t)nranks * k * W * W);
   d.root_ids = c.take<int>(W);
   d.root_cnt = c.take<int>(1);
   d.root_vals = c.take<double>((size_t)W * W);
@@ -159,7 +206,7 @@ void carve_dist(Carve& c, int algo, int64_t m_local, int64_t n, int64_t s_or_s1,
   const int64_t srows = algo == RLHC_SLHC3 ? s_or_s1 : s2;
   d.Ls = c.take<double>((size_t)srows * n);
   d.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
-  d.infos = c.take<rlhc_info_t>(kMaxInfos);
+  d.infos = c.take<rlhc_info_t>((size_t)d.ninfos);
   d.scratch_bytes = scratch_need(algo, m_local, n, s_or_s1, s2, cfg, nranks);
   d.scratch = c.take<char>(d.scratch_bytes);
 }
@@ -191,16 +238,17 @@ struct rlhc_comm_s {
 
 static int check_dist(const DistArgs& a, int nranks) {
   if (!a.X || !a.Q || !a.R || !a.piv || !a.ws || !a.info) return fail(RLHC_EINVAL, "null pointer argument");
+  // the contract first: nothing below may divide by leaf_rows or loop on the arity before
+  if (a.cfg.panel < 1 || a.cfg.panel > 64 || a.cfg.leaf_rows < 1 || a.cfg.arity < 2)
+    return fail(RLHC_EINVAL, "bad tslu configuration (panel 1..64, leaf_rows >= 1, arity >= 2)");
   if (a.n < 1 || a.m_local < 1 || a.m_global < a.n) return fail(RLHC_EINVAL, "need m_global >= n >= 1, m_local >= 1");
+  if (a.cfg.panel > a.n) return fail(RLHC_EINVAL, "bad tslu configuration (panel > n)");
   if (a.m_global > 0x7fffffffLL) return fail(RLHC_EINVAL, "m_global must be < 2^31 (int32 row ids)");
   if (a.ldx < a.n || a.ldq < a.n) return fail(RLHC_EINVAL, "leading dimension < n");
   if (a.m_local * nranks != a.m_global || a.row0 % a.m_local) return fail(RLHC_EINVAL, "shards must be equal");
-  if (a.m_local % a.cfg.leaf_rows) return fail(RLHC_EINVAL, "m_local must be a multiple of leaf_rows");
-  if (nranks > 1) {
-    int64_t leaves = a.m_local / a.cfg.leaf_rows, p = 1;
-    while (p < leaves) p *= a.cfg.arity;
-    if (p != leaves) return fail(RLHC_EINVAL, "local leaf count must be a power of the arity");
-  }
+  // equal shards of whole leaves: every rank's rows are rlhc_tslu_local_slots complete
+  // subtrees of the global tree, so the pivots are the single-process contract's
+  if (nranks > 1 && a.m_local % a.cfg.leaf_rows) return fail(RLHC_EINVAL, "m_local must be a multiple of leaf_rows");
   if (a.algo == RLHC_SLHC3 && (a.s_or_s1 < a.n || a.s_or_s1 > a.m_global)) return fail(RLHC_EINVAL, "need n <= s <= m");
   if (a.algo == RLHC_SSLHC3 && (a.s2 < a.n || a.s_or_s1 < a.s2 || a.s_or_s1 > a.m_global))
     return fail(RLHC_EINVAL, "need n <= s2 <= s1 <= m");
@@ -230,13 +278,40 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   if (a.ws_bytes < c.used) return fail(RLHC_EWORKSPACE, "workspace too small");
   void* sc = d.scratch;
   const size_t scb = d.scratch_bytes;
+  std::function<int(const void*, size_t)> check_fn;
   auto allreduce = [&](double* p, size_t count) -> int {
     if (nr > 1) NTRY(N.AllReduce(p, p, count, ncclFloat64, ncclSum, comm->comm, st));
-    return RLHC_OK;
+    return check_fn ? check_fn(p, count * sizeof(double)) : RLHC_OK;
   };
   int ninfo = 0;
-  auto next_info = [&]() { return d.infos + ninfo++; };
-  if (cudaMemsetAsync(d.infos, 0, kMaxInfos * sizeof(rlhc_info_t), st)) return fail(RLHC_ECUDA, "memset");
+  auto next_info = [&]() { return d.infos + std::min<int64_t>(ninfo++, d.ninfos - 1); };
+  if (cudaMemsetAsync(d.infos, 0, (size_t)d.ninfos * sizeof(rlhc_info_t), st)) return fail(RLHC_ECUDA, "memset");
+  // RLHC_DIST_CHECK=1: the replicated inputs (gathered tournament slots, all-reduced pivot
+  // rows, sketch, Grams) hashed on every rank and compared through a max/min all-reduce; a
+  // mismatch (e.g. a non-deterministic NVLS reduction) is reported as RLHC_ENCCL
+  static const bool dcheck = [] { const char* e = getenv("RLHC_DIST_CHECK"); return e && atoi(e) != 0; }();
+  if (dcheck && cudaMemsetAsync(d.hash, 0, 4 * sizeof(unsigned long long), st)) return fail(RLHC_ECUDA, "memset");
+  auto check_replicated = [&](const void* p, size_t bytes) -> int {
+    if (!dcheck || nr <= 1) return RLHC_OK;
+    if (launch_hash_words(p, bytes / 8, d.hash + 1, d.hash + 2, st)) return fail(RLHC_ECUDA, "launch failed");
+    NTRY(N.AllReduce(d.hash + 1, d.hash + 1, 1, ncclUint64, ncclMax, comm->comm, st));
+    NTRY(N.AllReduce(d.hash + 2, d.hash + 2, 1, ncclUint64, ncclMin, comm->comm, st));
+    if (launch_hash_compare(d.hash + 1, d.hash + 2, d.hash + 3, st)) return fail(RLHC_ECUDA, "launch failed");
+    return RLHC_OK;
+  };
+  check_fn = check_replicated;
+  const int64_t K = d.nslots;
+  auto gather_slots = [&](int64_t w) -> int {  // all-gather the K slots of every rank, then the top levels
+    NTRY(N.GroupStart());
+    NTRY(N.AllGather(d.slot_ids, d.all_ids, (size_t)K * W, ncclInt32, comm->comm, st));
+    NTRY(N.AllGather(d.slot_cnt, d.all_cnt, (size_t)K, ncclInt32, comm->comm, st));
+    NTRY(N.AllGather(d.slot_vals, d.all_vals, (size_t)K * W * W, ncclFloat64, comm->comm, st));
+    NTRY(N.GroupEnd());
+    DTRY(check_replicated(d.all_vals, (size_t)nr * K * W * W * sizeof(double)));
+    DTRY(rlhc_tslu_combine(d.all_ids, d.all_cnt, d.all_vals, nr * K, w, &a.cfg, d.root_ids, d.root_cnt, d.root_vals,
+                           sc, scb, st));
+    return RLHC_OK;
+  };
   if (cudaMemsetAsync(d.U, 0, (size_t)n * n * sizeof(double), st)) return fail(RLHC_ECUDA, "memset");
   if (cudaMemsetAsync(d.chosen, 0, (size_t)m, st)) return fail(RLHC_ECUDA, "memset");
   // finiteness of this rank's rows (stage INPUT), first in pipeline order
@@ -252,17 +327,11 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   for (int64_t p0 = 0; warp && p0 < n; p0 += a.cfg.panel) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
     DTRY(rlhc_tslw_schur(a.X, m, n, a.ldx, a.Q, a.ldq, p0, d.U, st));
-    DTRY(rlhc_tslu_reduce(a.Q, a.ldq, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, d.slot_ids, d.slot_cnt,
-                          d.slot_vals, sc, scb, st));
+    DTRY(rlhc_tslu_reduce_to(a.Q, a.ldq, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, nr > 1 ? K : 1,
+                             d.slot_ids, d.slot_cnt, d.slot_vals, sc, scb, st));
     const int* root = d.slot_ids;
     if (nr > 1) {
-      NTRY(N.GroupStart());
-      NTRY(N.AllGather(d.slot_ids, d.all_ids, W, ncclInt32, comm->comm, st));
-      NTRY(N.AllGather(d.slot_cnt, d.all_cnt, 1, ncclInt32, comm->comm, st));
-      NTRY(N.AllGather(d.slot_vals, d.all_vals, (size_t)W * W, ncclFloat64, comm->comm, st));
-      NTRY(N.GroupEnd());
-      DTRY(rlhc_tslu_combine(d.all_ids, d.all_cnt, d.all_vals, nr, w, &a.cfg, d.root_ids, d.root_cnt, d.root_vals, sc,
-                             scb, st));
+      DTRY(gather_slots(w));
       root = d.root_ids;
     }
     DTRY(rlhc_tslw_owned_rows(a.X, a.ldx, a.Q, a.ldq, m, a.row0, root, w, p0, n, d.U, d.prow, st));
@@ -275,17 +344,11 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
     const double* src = p0 == 0 ? a.X : a.Q;
     const int64_t lds = p0 == 0 ? a.ldx : a.ldq;
-    DTRY(rlhc_tslu_reduce(src, lds, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, d.slot_ids, d.slot_cnt,
-                          d.slot_vals, sc, scb, st));
+    DTRY(rlhc_tslu_reduce_to(src, lds, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, nr > 1 ? K : 1,
+                             d.slot_ids, d.slot_cnt, d.slot_vals, sc, scb, st));
     const int* root = d.slot_ids;
     if (nr > 1) {
-      NTRY(N.GroupStart());
-      NTRY(N.AllGather(d.slot_ids, d.all_ids, W, ncclInt32, comm->comm, st));
-      NTRY(N.AllGather(d.slot_cnt, d.all_cnt, 1, ncclInt32, comm->comm, st));
-      NTRY(N.AllGather(d.slot_vals, d.all_vals, (size_t)W * W, ncclFloat64, comm->comm, st));
-      NTRY(N.GroupEnd());
-      DTRY(rlhc_tslu_combine(d.all_ids, d.all_cnt, d.all_vals, nr, w, &a.cfg, d.root_ids, d.root_cnt, d.root_vals, sc,
-                             scb, st));
+      DTRY(gather_slots(w));
       root = d.root_ids;
     }
     DTRY(rlhc_owned_rows(src, lds, m, a.row0, root, nullptr, w, p0, n - p0, d.prow, st));
@@ -326,7 +389,8 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   DTRY(rlhc_trmm_upper(d.D, d.Y, n, d.N, st));
   DTRY(rlhc_trmm_upper(d.J, d.N, n, a.R, st));
   note_launch();
-  first_info_kernel<<<1, 32, 0, st>>>(d.infos, ninfo, a.row0 * n, a.info);
+  first_info_kernel<<<1, 32, 0, st>>>(d.infos, (int)std::min<int64_t>(ninfo, d.ninfos), a.row0 * n,
+                                      dcheck ? d.hash + 3 : nullptr, a.info);
   if (cudaGetLastError()) return fail(RLHC_ECUDA, "launch failed");
   return RLHC_OK;
 }
@@ -368,6 +432,7 @@ int rlhc_comm_destroy(rlhc_comm_t comm) {
 size_t rlhc_dist_workspace_size(int algo, int64_t m_local, int64_t n, int64_t s_or_s1, int64_t s2,
                                 const rlhc_tslu_cfg* cfg, int nranks) {
   if (!cfg || n < 1 || m_local < 1 || nranks < 1) return 0;
+  if (cfg->panel < 1 || cfg->panel > 64 || cfg->leaf_rows < 1 || cfg->arity < 2) return 0;
   if (algo != RLHC_SLHC3 && algo != RLHC_SSLHC3) return 0;
   Carve c(nullptr);
   DistWs d;

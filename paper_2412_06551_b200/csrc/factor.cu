@@ -530,11 +530,8 @@ cudaError_t launch_hqr(const double* A, int s, int n, int64_t lda, const double*
 #define HQR_REG(RR, QC)                                                                            \
   if (s <= 32 * RR && n <= HQ_WARPS * QC) {                                                        \
     constexpr int smem = (int)sizeof(HqpSmem<RR, QC>);                                             \
-    static bool attr = false;                                                                      \
-    if (!attr) {                                                                                   \
-      cudaFuncSetAttribute(hqr_pipe_kernel<RR, QC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-      attr = true;                                                                                 \
-    }                                                                                              \
+    static DevFlags attr;                                                                          \
+    if (cudaError_t e_ = smem_attr(attr, hqr_pipe_kernel<RR, QC>, smem)) return e_;                \
     note_launch();                                                                                 \
     hqr_pipe_kernel<RR, QC><<<1, 32 * HQ_WARPS, smem, st>>>(A, s, n, lda, sgn_ref, S, status);     \
     return cudaGetLastError();                                                                     \
@@ -703,11 +700,8 @@ template <int RR, int QC>
 static cudaError_t run_chol_pipe(const double* G, int64_t ldg, int n, double* R, int64_t ldr, double* rdiag, int stage,
                                  int koff, unsigned long long* status, cudaStream_t st) {
   constexpr int smem = (int)sizeof(CholSmem<RR, QC>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(chol_pipe_kernel<RR, QC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static DevFlags attr;
+  if (cudaError_t e = smem_attr(attr, chol_pipe_kernel<RR, QC>, smem)) return e;
   note_launch();
   chol_pipe_kernel<RR, QC><<<1, 512, smem, st>>>(G, ldg, n, R, ldr, rdiag, stage, koff, status);
   return cudaGetLastError();

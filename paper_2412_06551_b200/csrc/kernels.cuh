@@ -63,10 +63,11 @@ struct TslwRoot {          // root outputs of one panel (all null below the root
 bool tslw_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
 bool tslg_cfg(const rlhc_tslu_cfg& c, int64_t m, int64_t n);
 size_t tslw_slots(int64_t rows);
-// row-sharded local tree of the warp contract down to one slot (rlhc_tslu_reduce)
+// row-sharded local tree of the warp contract down to the slots of level stop_lev (-1: one
+// slot, the local root) -- rlhc_tslu_reduce_to
 cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                                const uint8_t* chosen, int arity, int* ids[2], int* cnt[2], double* vals[2],
-                                int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st);
+                                const uint8_t* chosen, int arity, int stop_lev, int* ids[2], int* cnt[2],
+                                double* vals[2], int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st);
 // row-sharded left-looking TSLU blocks (the warp contract): a panel's Schur complement of
 // this rank's rows (U's reciprocals from its diagonal), the winners' current rows this rank
 // owns (0 for the others), and the last panel's L plus the local pivot rows' L11 rows

@@ -597,13 +597,8 @@ gemm_sub_kernel(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, con
 cudaError_t launch_gemm_update(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
                                int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, cudaStream_t st) {
   if (rows <= 0 || N <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(GemmSmem));
-    if (e) return e;
-    attr = true;
-  }
+  static DevFlags attr;
+  if (cudaError_t e = smem_attr(attr, gemm_sub_kernel, (int)sizeof(GemmSmem))) return e;
   dim3 grid((unsigned)ceil_div<int64_t>(rows, GS_M), (unsigned)ceil_div(N, GS_N));
   note_launch();
   gemm_sub_kernel<<<grid, 256, sizeof(GemmSmem), st>>>(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N);
@@ -884,11 +879,8 @@ cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, doubl
   GramGeom gg = gram_geom(rows, n);
   dim3 grid(gg.ntiles, gg.nsplit);
   constexpr int smem = 4 * GK * (GT + 4) * (int)sizeof(double);
-  static bool attr = false;  // idempotent
-  if (!attr) {
-    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static DevFlags attr;
+  if (cudaError_t e0 = smem_attr(attr, gram_kernel, smem)) return e0;
   note_launch(); gram_kernel<<<grid, 128, smem, st>>>(A, lda, rows, n, gg.nt, gg.rows_per_split, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
@@ -1053,13 +1045,9 @@ cudaError_t launch_subst_ms(const double* A, int64_t lda, int64_t rows, int n, c
                             double* out, int64_t ldo, double* gpart, double* G, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   const int smem = sms_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(subst_ms_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (!e) e = cudaFuncSetAttribute(subst_ms_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e) return e;
-    attr = true;
-  }
+  static DevFlags attr_t, attr_f;
+  if (cudaError_t e = smem_attr(attr_t, subst_ms_kernel<true>, smem)) return e;
+  if (cudaError_t e = smem_attr(attr_f, subst_ms_kernel<false>, smem)) return e;
   const int grid = sms_grid(rows);
   note_launch();
   if (G) subst_ms_kernel<true><<<grid, SMS_R, smem, st>>>(A, lda, rows, n, T, ldt, out, ldo, gpart);

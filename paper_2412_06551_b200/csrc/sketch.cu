@@ -250,12 +250,8 @@ template <int NTW, bool OMEM>
 static void gauss_launch(dim3 grid, const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
                          uint64_t seed, uint32_t stream_id, int64_t rps, double* part, const double* Om,
                          int64_t ldom, cudaStream_t st) {
-  static bool attr = false;  // idempotent, once per process and instantiation
-  if (!attr) {
-    cudaFuncSetAttribute(gauss_sketch_kernel<NTW, OMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(GaussSmem<NTW, OMEM>));
-    attr = true;
-  }
+  static DevFlags attr;  // per device and instantiation
+  smem_attr(attr, gauss_sketch_kernel<NTW, OMEM>, (int)sizeof(GaussSmem<NTW, OMEM>));
   gauss_sketch_kernel<NTW, OMEM><<<grid, 64 * NTW, sizeof(GaussSmem<NTW, OMEM>), st>>>(
       A, lda, rows, n, row0, s, seed, stream_id, rps, part, Om, ldom);
 }

@@ -330,12 +330,9 @@ static cudaError_t run_leaf(int64_t leaf_rows, const double* src, int64_t lds, i
   if (leaf_rows < 1 || leaf_rows > 32 * RS) return cudaErrorInvalidValue;
   int nleaves = (int)ceil_div<int64_t>(rows, leaf_rows);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
-  static bool attr = false;  // once per instantiation (idempotent, so a race is harmless)
-  if (!attr) {
-    cudaFuncSetAttribute(tslu_leaf_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static DevFlags attr_l, attr_n;  // per device and instantiation
+  if (cudaError_t e = smem_attr(attr_l, tslu_leaf_kernel<W, NW, RS>, smem)) return e;
+  if (cudaError_t e = smem_attr(attr_n, tslu_node_kernel<W, NW, RS>, smem)) return e;
   note_launch(); tslu_leaf_kernel<W, NW, RS><<<nleaves, 32 * NW, smem, st>>>(src, lds, rows, leaf_rows, row0, p0, w, chosen, ids, cnt, vals,
                                                                             root, finite_status);
   return cudaGetLastError();
@@ -346,12 +343,9 @@ static cudaError_t run_node(const int* in_ids, const int* in_cnt, const double* 
                             const RowSrc& rsrc) {
   int nout = ceil_div(nin, arity);
   constexpr int smem = (int)sizeof(SelSmem<W, NW, RS>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tslu_leaf_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(tslu_node_kernel<W, NW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static DevFlags attr_l, attr_n;
+  if (cudaError_t e = smem_attr(attr_l, tslu_leaf_kernel<W, NW, RS>, smem)) return e;
+  if (cudaError_t e = smem_attr(attr_n, tslu_node_kernel<W, NW, RS>, smem)) return e;
   note_launch();
   return launch_pdl(tslu_node_kernel<W, NW, RS>, dim3(nout), dim3(32 * NW), smem, st, in_ids, in_cnt, in_vals, nin,
                     arity, w, ids, cnt, vals, root, rsrc);

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(32 * WPB)
 tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64_t row0, int p0, int w,
                  const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
                  int* __restrict__ idsN, int* __restrict__ cntN, double* __restrict__ vals0,
-                 double* __restrict__ valsN, int* __restrict__ arrive, int arity, TslwRoot ro) {
+                 double* __restrict__ valsN, int* __restrict__ arrive, int arity, int stop_lev, TslwRoot ro) {
   extern __shared__ __align__(16) unsigned char raw[];
   WSel& sm = reinterpret_cast<WSel*>(raw)[warp_id()];
   pdl_trigger();
@@ -654,7 +654,7 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
     TW_G(ga)
     select_and_emit(sm, act, w, slot, oids, ocnt, ovals, nsl == 1 ? ro : TslwRoot{}, p0);
     TW_G(gb)
-    if (nsl == 1) {
+    if (nsl == 1 || lev == stop_lev) {  // the root, or a rank's top level (row-sharded path)
       TW_LV(lev, ga, gb, gb, gb)
       break;
     }
@@ -1043,33 +1043,35 @@ size_t tslg_ws_bytes(int64_t rows) { return (size_t)rows * WW * sizeof(double) +
 // count, the winners' panel rows) is copied to out_*.  cnt[1] holds the packed counts of the
 // levels >= 1 followed by their arrival counters.
 cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
-                                const uint8_t* chosen, int arity, int* ids[2], int* cnt[2], double* vals[2],
-                                int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st) {
+                                const uint8_t* chosen, int arity, int stop_lev, int* ids[2], int* cnt[2],
+                                double* vals[2], int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st) {
   cudaError_t e;
   const int nleaves = (int)tslw_slots(rows);
-  size_t above = 0, top = 0;  // packed slots of the levels >= 1; offset of the top level
-  for (int ns = nleaves; ns > 1; ns = ceil_div(ns, arity)) {
+  // packed slots of the levels >= 1; offset and size of the output level (the root, or
+  // level stop_lev when this rank's rows hold several complete subtrees)
+  size_t above = 0, top = 0;
+  int lev = 0, nout = nleaves;
+  for (int ns = nleaves; ns > 1 && lev != stop_lev; ns = ceil_div(ns, arity)) {
     top = above;
     above += ceil_div(ns, arity);
+    lev++;
+    nout = ceil_div(ns, arity);
   }
   int* arrive = cnt[1] + above;
   if (above && (e = cudaMemsetAsync(arrive, 0, above * sizeof(int), st))) return e;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tslw_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static DevFlags attr;
+  if ((e = smem_attr(attr, tslw_tree_kernel, 227 * 1024))) return e;
   note_launch();
   e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st, src, lds,
                  rows, row0, p0, w, chosen, ids[0], cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity,
-                 TslwRoot{});
+                 stop_lev, TslwRoot{});
   if (e) return e;
-  const int* tid = nleaves == 1 ? ids[0] : ids[1] + top * WW;
-  const int* tcnt = nleaves == 1 ? cnt[0] : cnt[1] + top;
-  const double* tval = nleaves == 1 ? vals[0] : vals[1] + top * WW * WW;
-  if ((e = cudaMemcpyAsync(out_ids, tid, WW * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
-  if ((e = cudaMemcpyAsync(out_cnt, tcnt, sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
-  return cudaMemcpyAsync(out_vals, tval, (size_t)WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  const int* tid = lev == 0 ? ids[0] : ids[1] + top * WW;
+  const int* tcnt = lev == 0 ? cnt[0] : cnt[1] + top;
+  const double* tval = lev == 0 ? vals[0] : vals[1] + top * WW * WW;
+  if ((e = cudaMemcpyAsync(out_ids, tid, (size_t)nout * WW * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(out_cnt, tcnt, (size_t)nout * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  return cudaMemcpyAsync(out_vals, tval, (size_t)nout * WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
@@ -1091,13 +1093,9 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   if ((e = cudaMemsetAsync(chosen, 0, (size_t)rows, st))) return e;
   if ((e = cudaMemsetAsync(U, 0, (size_t)n * n * sizeof(double), st))) return e;
   if ((e = cudaMemsetAsync(arrive, 0, above * sizeof(int), st))) return e;
-  static bool attr = false;
-  if (!attr) {
-    const int mx = 227 * 1024;
-    cudaFuncSetAttribute(tslw_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
-    attr = true;
-  }
+  static DevFlags attr_t, attr_s;
+  if ((e = smem_attr(attr_t, tslw_tree_kernel, 227 * 1024))) return e;
+  if ((e = smem_attr(attr_s, tslw_schur_dmma_kernel, (int)sizeof(SchurDSmem)))) return e;
   const TslwRoot root{U, piv, rd, nullptr, chosen, status, row0, n};
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
@@ -1110,10 +1108,14 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
                         ldl, rows, w, n, check_input ? status : nullptr);
     if (e) return e;
     if (Sw) {  // exact GEPP: one cooperative launch per panel
-      static int per_sm = 0;
-      if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tslg_kernel, 256, 0);
+      // co-resident grid of the current device (SM count and occupancy queried per call: a
+      // MIG slice or another device may have fewer SMs than a full B200)
+      int dev = 0, sms = 0, per_sm = 0;
+      if ((e = cudaGetDevice(&dev))) return e;
+      if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tslg_kernel, 256, 0))) return e;
       const int gridg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, 256),
-                                                                    (int64_t)kSMs * std::max(per_sm, 1)));
+                                                                    (int64_t)sms * std::max(per_sm, 1)));
       const double* Lbc = Lb;
       int p0v = p0, wv = w;
       int64_t rowsv = rows, row0v = row0, ldlv = ldl;
@@ -1127,7 +1129,7 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
       note_launch();
       e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
                      (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0],
-                     cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity, root);
+                     cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity, -1, root);
       if (e) return e;
     }
     if (p0 + w < n) {
@@ -1150,11 +1152,8 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
 // ------------------------------------------------------------------ row-sharded TSLU blocks
 cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
                               const double* U, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tslw_schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurDSmem));
-    attr = true;
-  }
+  static DevFlags attr;
+  if (cudaError_t e = smem_attr(attr, tslw_schur_dmma_kernel, (int)sizeof(SchurDSmem))) return e;
   note_launch();
   if (p0 == 0)
     return launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx, Lb,

@@ -2,13 +2,14 @@
 
 Rank r holds the global rows [row0, row0 + m_local) of X.  Per call:
 
-* PX = LU: per panel, each rank reduces its leaves and its local tree levels to ONE
-  tournament slot (rlhc_tslu_reduce); the slots are all-gathered and every rank runs the
-  remaining tree levels (rlhc_tslu_combine) -> identical pivots everywhere.  The pivot
-  rows' current values are assembled by an all-reduce SUM of per-rank masked copies
-  (rlhc_owned_rows; exact: x + 0 + ... + 0 = x), U rows follow (replicated), each rank
-  eliminates its own rows.  With equal shards of arity^k * leaf_rows rows the tree is the
-  global tree of the single-GPU contract, so the pivots do not depend on the GPU count.
+* PX = LU: per panel, each rank reduces its leaves and its local tree levels to K
+  tournament slots (rlhc_tslu_reduce_to): its rows are K complete subtrees of the global
+  tree (K = leaves / the largest power of the arity dividing it, local_slots).  The K slots
+  of every rank are all-gathered (global order) and every rank runs the remaining tree levels
+  (rlhc_tslu_combine) -> identical pivots everywhere, and the pivots of the single-GPU
+  contract: the tree is the global one at every GPU count.  The pivot rows' current values
+  are assembled by an all-reduce SUM of per-rank masked copies (rlhc_owned_rows; exact:
+  x + 0 + ... + 0 = x), U rows follow (replicated), each rank eliminates its own rows.
 * L of the local rows, local sketch partials (Omega columns / CountSketch hashes indexed
   by global row ids) -> all-reduce SUM -> replicated HouseholderQR, Y = S U.
 * W = X Y^{-1} with the local Gram partial -> all-reduce -> replicated Cholesky; same for V;
@@ -21,7 +22,6 @@ backend with the same methods to check this orchestration on CPU.
 from __future__ import annotations
 
 import ctypes
-import math
 
 import torch
 import torch.distributed as dist
@@ -62,12 +62,13 @@ class CudaBackend:
                 torch.zeros(count, dtype=torch.int32, device=self.dev),
                 torch.zeros(count, self.W * self.W, dtype=torch.float64, device=self.dev))
 
-    def tslu_reduce(self, src, row0, p0, w, chosen):
+    def tslu_reduce(self, src, row0, p0, w, chosen, nslots: int = 1):
         rows = src.shape[0]
-        ids, cnt, vals = self.new_slot()
+        ids, cnt, vals = self.new_slot(nslots)
         ws = self._ws(self.L.rlhc_tslu_local_workspace_size(rows, 0, ctypes.byref(self.cfg)))
-        check(self.L.rlhc_tslu_reduce(_p(src), src.stride(0), rows, row0, p0, w, _p(chosen), ctypes.byref(self.cfg),
-                                      _p(ids), _p(cnt), _p(vals), _p(ws), ws.numel(), self._st()))
+        check(self.L.rlhc_tslu_reduce_to(_p(src), src.stride(0), rows, row0, p0, w, _p(chosen),
+                                         ctypes.byref(self.cfg), nslots, _p(ids), _p(cnt), _p(vals), _p(ws),
+                                         ws.numel(), self._st()))
         return ids, cnt, vals
 
     def tslu_combine(self, ids, cnt, vals, w):
@@ -192,18 +193,26 @@ class CudaBackend:
         return int(v[0].item() & 0xffffffff), int((v[0].item() >> 32) & 0xffffffff), int(v[1].item())
 
 
+def local_slots(m_local: int, cfg: TsluCfg) -> int:
+    """Slots a rank of m_local rows reduces to: its leaf count divided by the largest power of
+    the arity dividing it -- the rank's rows are that many complete subtrees of the global
+    tree (rlhc_tslu_local_slots)."""
+    k = -(-m_local // cfg.leaf_rows)
+    while k % cfg.arity == 0:
+        k //= cfg.arity
+    return k
+
+
 def check_shard_contract(m_global: int, m_local: int, world: int, cfg: TsluCfg):
-    """Equal shards whose leaf count is a power of the arity: each rank's local tree is a
-    complete subtree of the global tournament tree."""
+    """Equal shards of whole leaves: each rank's rows are local_slots(m_local) complete
+    subtrees of the global tournament tree, so every GPU count runs
+    the single-GPU contract's tree and picks its pivots."""
+    if cfg.leaf_rows < 1 or cfg.arity < 2 or not 1 <= cfg.panel <= 64:
+        raise ValueError("bad tournament contract")
     if m_local * world != m_global:
         raise ValueError("row shards must be equal")
-    if m_local % cfg.leaf_rows:
+    if world > 1 and m_local % cfg.leaf_rows:
         raise ValueError("m_local must be a multiple of leaf_rows")
-    leaves = m_local // cfg.leaf_rows
-    if world > 1:
-        k = round(math.log(leaves, cfg.arity)) if leaves > 1 else 0
-        if cfg.arity ** k != leaves:
-            raise ValueError(f"local leaf count {leaves} is not a power of arity {cfg.arity}")
 
 
 class DistPlan:
@@ -221,6 +230,7 @@ class DistPlan:
         self.row0 = self.rank * self.m_local
         self.cfg = cfg if cfg is not None else dist_default_cfg(m_global, n, self.world)
         check_shard_contract(m_global, self.m_local, self.world, self.cfg)
+        self.K = local_slots(self.m_local, self.cfg) if self.world > 1 else 1
         self.B = backend if backend is not None else CudaBackend(device, self.cfg)
 
     # ---- collectives (torch.distributed; no-ops on one rank)
@@ -254,7 +264,7 @@ class DistPlan:
             for p0 in range(0, n, cfg.panel):
                 w = min(cfg.panel, n - p0)
                 B.tslw_schur(X, Q, p0, U)
-                ids, cnt, vals = B.tslu_reduce(Q, self.row0, p0, w, chosen if p0 > 0 else None)
+                ids, cnt, vals = B.tslu_reduce(Q, self.row0, p0, w, chosen if p0 > 0 else None, self.K)
                 if self.world > 1:
                     ids, cnt, vals = B.tslu_combine(self._allgather(ids), self._allgather(cnt),
                                                     self._allgather(vals), w)
@@ -268,7 +278,7 @@ class DistPlan:
         for p0 in (range(0, n, cfg.panel) if L is None else ()):
             w = min(cfg.panel, n - p0)
             src = X if p0 == 0 else Q
-            ids, cnt, vals = B.tslu_reduce(src, self.row0, p0, w, chosen if p0 > 0 else None)
+            ids, cnt, vals = B.tslu_reduce(src, self.row0, p0, w, chosen if p0 > 0 else None, self.K)
             if self.world > 1:
                 ids, cnt, vals = B.tslu_combine(self._allgather(ids), self._allgather(cnt), self._allgather(vals), w)
             root = ids[0, :w].contiguous()
@@ -352,19 +362,12 @@ def setup_bench(cfg, rank: int, world: int, device, strong: bool = True, use_c: 
 
 
 def dist_default_cfg(m_global: int, n: int, world: int) -> TsluCfg:
-    """The single-GPU default contract (rlhc_default_tslu_cfg) when each rank's leaf count
-    is a power of its arity -- the rank subtrees are then complete subtrees of the global
-    tree and the pivots equal the single-GPU run; otherwise arity 2 (check_shard_contract
-    rejects shards that fit neither)."""
-    panel = min(max(n, 1), 64)
-    W = kernel_width(panel)
-    rows = 256 if W == 64 else 512
-    arity = max(2, rows // panel)
-    leaves = (m_global // max(world, 1)) // rows
-    k = round(math.log(leaves, arity)) if leaves > 1 else 0
-    if world > 1 and arity ** k != leaves:
-        arity = 2
-    return TsluCfg(rows, arity, panel)
+    """The single-GPU default contract (rlhc_default_tslu_cfg: 128-row leaves, 8-ary nodes,
+    16-column panels) at every GPU count: equal shards of whole leaves are unions of complete
+    subtrees of its global tree, so the pivots equal the single-GPU run's."""
+    c = TsluCfg()
+    lib().rlhc_default_tslu_cfg(m_global, n, ctypes.byref(c))
+    return c
 
 
 # ---------------------------------------------------------------- C orchestration over NCCL

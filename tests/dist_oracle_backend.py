@@ -50,8 +50,10 @@ class OracleBackend:
         pos = {int(i): r for r, i in enumerate(cand_ids)}
         return win, np.stack([cand_vals[pos[int(i)]] for i in win])
 
-    def _tree(self, slots, w):
-        while len(slots) > 1:
+    def _tree(self, slots, w, target=None):
+        """Tree levels over `slots` down to one slot (returned), or down to `target` slots
+        (returned as a list) when given."""
+        while len(slots) > (target or 1):
             nxt = []
             for c0 in range(0, len(slots), self.cfg.arity):
                 grp = slots[c0:c0 + self.cfg.arity]
@@ -59,10 +61,10 @@ class OracleBackend:
                 vals = np.concatenate([g[1] for g in grp]) if len(ids) else np.zeros((0, w))
                 nxt.append(self._select(ids, vals, w))
             slots = nxt
-        return slots[0]
+        return slots if target else slots[0]
 
     # ---------------------------------------------------------------- tournament
-    def tslu_reduce(self, src, row0, p0, w, chosen):
+    def tslu_reduce(self, src, row0, p0, w, chosen, nslots=1):
         A = src.numpy()
         rows = A.shape[0]
         ch = chosen.numpy() if chosen is not None else np.zeros(rows, np.uint8)
@@ -73,8 +75,9 @@ class OracleBackend:
             ids = np.array([row0 + i for i in loc], np.int64)
             vals = A[loc, p0:p0 + w].copy() if loc else np.zeros((0, w))
             slots.append(self._select(ids, vals, w))
-        ids, vals = self._tree(slots, w)
-        return self._slot(ids, vals, w)
+        slots = self._tree(slots, w, nslots)
+        out = [self._slot(i, v, w) for i, v in slots]
+        return tuple(torch.cat([o[j] for o in out]) for j in range(3))
 
     def tslu_combine(self, ids, cnt, vals, w):
         W = self.W

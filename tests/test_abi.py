@@ -96,10 +96,13 @@ def test_dist_entry_host_errors():
     rc = L.rlhc_slhc3_dist(None, 4096, 64, 64, 0, 4096, 128, ctypes.c_uint64(1), ctypes.byref(cfg), dummy, 64, dummy,
                            dummy, dummy, 1 << 30, info, None, None)
     assert rc == _lib.RLHC_EINVAL
-    # m_local not a multiple of leaf_rows
-    rc = L.rlhc_sslhc3_dist(dummy, 4000, 64, 64, 0, 4000, 512, 128, ctypes.c_uint64(1), ctypes.byref(cfg), dummy, 64,
-                            dummy, dummy, dummy, 1 << 30, info, None, None)
-    assert rc == _lib.RLHC_EINVAL and b"leaf_rows" in L.rlhc_last_error()
+    # the contract is validated before any arithmetic on it (leaf_rows = 0 used to divide by
+    # zero, arity 1 to loop forever)
+    for bad in (_lib.TsluCfg(0, 4, 64), _lib.TsluCfg(256, 1, 64), _lib.TsluCfg(256, 4, 0)):
+        rc = L.rlhc_sslhc3_dist(dummy, 4096, 64, 64, 0, 4096, 512, 128, ctypes.c_uint64(1), ctypes.byref(bad), dummy,
+                                64, dummy, dummy, dummy, 1 << 30, info, None, None)
+        assert rc == _lib.RLHC_EINVAL and b"configuration" in L.rlhc_last_error()
+        assert L.rlhc_dist_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(bad), 8) == 0
     assert L.rlhc_dist_workspace_size(0, 65536, 64, 128, 0, ctypes.byref(cfg), 8) > 0
 
 

@@ -21,6 +21,11 @@ CASES = [
     ("sslhc3", 4096, 24, dict(s1=192, s2=48), (512, 2, 24)),
     ("slhc3", 4096, 40, dict(s=80), (256, 2, 40)),
     ("sslhc3", 8192, 72, dict(s1=576, s2=144), (256, 2, 64)),   # two panels
+    # the default contract (128, 8, 16) with shards that are SEVERAL complete subtrees:
+    # 16 leaves per rank = 2 subtrees of 8 (K = 2), 3 panels
+    ("sslhc3", 4096, 48, dict(s1=384, s2=96), (128, 8, 16)),
+    # 3 leaves per rank: no local level at all, every leaf slot is gathered (K = 3)
+    ("slhc3", 768, 20, dict(s=40), (128, 8, 16)),
 ]
 
 
@@ -87,12 +92,21 @@ def test_single_rank_plan_matches_oracle(ora):
     assert np.linalg.norm(R.numpy() - ref.R) <= 1e-13 * np.linalg.norm(ref.R)
 
 
-def test_shard_contract_rejects_bad_shards():
-    from paper_2412_06551_b200._lib import TsluCfg
-    from paper_2412_06551_b200.dist import check_shard_contract
-    cfg = TsluCfg(256, 2, 64)
-    check_shard_contract(8 * 65536, 65536, 8, cfg)
-    with pytest.raises(ValueError):
-        check_shard_contract(3 * 256 * 3, 256 * 3, 3, cfg)   # 3 leaves: not a power of 2
+def test_shard_contract_and_local_slots():
+    """Equal shards of whole leaves are accepted at every GPU count; each rank reduces to
+    local_slots complete subtrees (cfg5 = 2^24 rows, 128-row leaves, arity 8: 2^17 leaves)."""
+    from paper_2412_06551_b200._lib import TsluCfg, lib
+    from paper_2412_06551_b200.dist import check_shard_contract, local_slots
+    cfg = TsluCfg(128, 8, 16)
+    m = 1 << 24
+    for world, k in ((1, 4), (2, 2), (4, 1), (8, 4)):
+        check_shard_contract(m, m // world, world, cfg)
+        assert local_slots(m // world, cfg) == k
+        assert lib().rlhc_tslu_local_slots(m // world, cfg) == k   # the C entry point agrees
+    assert local_slots(3 * 128, cfg) == 3
     with pytest.raises(ValueError):
         check_shard_contract(1000, 500, 2, cfg)               # not a multiple of leaf_rows
+    with pytest.raises(ValueError):
+        check_shard_contract(4096, 1024, 3, cfg)              # unequal shards
+    with pytest.raises(ValueError):
+        check_shard_contract(4096, 2048, 2, TsluCfg(0, 8, 16))  # invalid contract

@@ -41,7 +41,7 @@ def test_world1_matches_single_call(ora):
         assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) <= 1e-13 * np.sqrt(n)
 
 
-def _worker(rank, world, port, out_path, cfgt):
+def _worker(rank, world, port, out_path, cfgt, m):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -49,7 +49,7 @@ def _worker(rank, world, port, out_path, cfgt):
         import synth
         from paper_2412_06551_b200._lib import TsluCfg
         from paper_2412_06551_b200.dist import DistPlan
-        m, n = (32768 if cfgt[0] == 256 else 131072), 48  # rank subtrees complete (512 = 8^3 leaves)
+        n = 48
         cfg = TsluCfg(*cfgt)
         mloc = m // world
         X = synth.baseline_matrix(m, n, 9, 4, device="cuda", row0=rank * mloc, rows=mloc)
@@ -62,14 +62,20 @@ def _worker(rank, world, port, out_path, cfgt):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfgt", [(256, 2, 48), (128, 8, 16)])
-def test_two_gloo_ranks_on_one_gpu(ora, cfgt):
+@pytest.mark.parametrize("cfgt,m", [((256, 2, 48), 32768),
+                                    ((128, 8, 16), 131072),    # 512 = 8^3 leaves per rank: one subtree
+                                    ((128, 8, 16), 262144),    # 1024 leaves per rank: two subtrees (K = 2)
+                                    ((128, 8, 16), 98304)])    # 384 leaves per rank: 6 level-2 subtrees
+def test_two_gloo_ranks_on_one_gpu(ora, cfgt, m):
+    """Two gloo ranks driving the CUDA stage calls on one GPU (the N > 1 orchestration of
+    dist.py); each rank's rows are K >= 1 complete subtrees of the global tree, so the pivots
+    are the single-process contract's."""
     import synth
     d = tempfile.mkdtemp()
     out = os.path.join(d, "r")
-    mp.spawn(_worker, args=(2, 29700 + os.getpid() % 200 + cfgt[0] % 7, out, cfgt), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, 29700 + os.getpid() % 200 + (m >> 12) % 97, out, cfgt, m), nprocs=2, join=True)
     res = [np.load(out + f".{r}.npz") for r in range(2)]
-    X = synth.baseline_matrix(32768 if cfgt[0] == 256 else 131072, 48, 9, 4, device="cuda").cpu().numpy()
+    X = synth.baseline_matrix(m, 48, 9, 4, device="cuda").cpu().numpy()
     ref = ora.sslhc3(X, 384, 96, 6, *cfgt)
     for r in res:
         assert tuple(r["info"]) == (0, 0, 0)

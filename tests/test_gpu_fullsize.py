@@ -7,11 +7,9 @@ What is compared, per config (DESIGN.md §7 lists the same table):
                     R against the oracle's R, orthogonality and residual gates.
   cfg4a, cfg4b      the oracle's TSLU at full size (pivots, U, L11 bit-exact) and the oracle's
                     L rows on sampled row blocks (first, last/ragged, interior); full Q, R gates.
-  cfg5              too large for the CPU oracle's TSLU in a test (2^24 x 256): every
-                    CountSketch bucket/sign against the oracle's hash, and properties that hold
-                    at any size -- pivots a valid injection, P X = L U on the pivot rows,
-                    R upper with diag > 0, orthogonality and residual gates, and the pipeline's
-                    pivots equal to rlhc_getrf_ts's (one contract, two entry points).
+  cfg5              the row-chunked oracle (ora_lhc3_chunked, bit-identical to ora_sslhc3, X
+                    streamed in 65536-row chunks): pivots, U, L11 and L_t bit-exact, R, sampled
+                    Q row blocks, every CountSketch bucket/sign, full Q, R gates.
 Gates are north_star's: orthogonality <= 1e-13 sqrt(n), residual <= 1e-14 n, and
 ||R - R_oracle||_F / ||R_oracle||_F <= 1e-9 for kappa <= 1e8.  Beyond kappa = 1e8 north_star
 states no R tolerance; DESIGN.md §3 ("Tolerances") fixes 1e-12."""
@@ -150,25 +148,53 @@ def test_fullsize_cfg4(rl, ora, cfg4_data, name):
     check_gates(cfg, res, X)
 
 
-def test_fullsize_cfg5_properties(rl, ora):
+@pytest.mark.slow
+def test_fullsize_cfg5_vs_chunked_oracle(rl, ora):
+    """cfg5 (SSLHC3, 2^24 x 256, the north-star config) against the row-chunked oracle
+    (ora_lhc3_chunked, bit-identical to ora_sslhc3; X streamed from the device in 65536-row
+    chunks): pivots, U, L11 and the CountSketch L_t bit-exact, R within DESIGN.md's 1e-12,
+    sampled Q row blocks, every bucket/sign, the north-star gates on the full Q."""
     cfg = synth.CONFIGS["cfg5"]
+    m, n = cfg.m, cfg.n
     free, _ = torch.cuda.mem_get_info()
-    need = 2 * cfg.m * cfg.n * 8 + (8 << 30)
+    need = 3 * m * n * 8 + (8 << 30)
     if free < need:
         pytest.skip(f"cfg5 needs ~{need >> 30} GiB of device memory, {free >> 30} GiB free")
     X = synth.config_matrix(cfg, device=DEV)
     check_buckets(rl, ora, cfg)
-    _, res = run_plan(rl, cfg, X)
-    n = cfg.n
-    piv = res.piv
-    assert int(piv.min()) >= 0 and int(piv.max()) < cfg.m
-    assert torch.unique(piv).numel() == n
-    orth, resid = check_gates(cfg, res, X)
-    # one contract, two entry points: rlhc_getrf_ts picks the same pivots; P X = L U on them
-    piv2, U, L11, _, info = rl.getrf_ts(X)
+    plan, res = run_plan(rl, cfg, X)  # bench.py's launch configuration
+    contract = plan.cfg.as_tuple()
+    assert contract == (128, 8, 16)
+    check_gates(cfg, res, X)
+    piv_g, R_g = res.piv.cpu().numpy(), res.R.cpu().numpy()
+    # stage entry points on the same X: the LU (with L) and the CountSketch of L
+    piv2, U, L11, L, info = rl.getrf_ts(X, cfg=contract, want_L=True)
     assert info == (0, 0, 0)
-    assert torch.equal(piv2, piv)
-    assert torch.equal(torch.triu(L11, 1), torch.zeros_like(L11))
-    assert torch.equal(torch.diagonal(L11), torch.ones(n, dtype=torch.float64, device=DEV))
-    Xp = X[piv]
-    assert (torch.linalg.norm(L11 @ U - Xp) / torch.linalg.norm(Xp)).item() <= 1e-14 * n
+    Lt = rl.sketch_count(L, cfg.s1, cfg.seed).cpu().numpy()
+    del L
+    torch.cuda.empty_cache()
+    chunk = 65536
+    pin = torch.empty(chunk, n, dtype=torch.float64).pin_memory()
+
+    def get(r0, rows):
+        pin[:rows].copy_(X[r0:r0 + rows])
+        return pin[:rows].numpy()
+    rng = np.random.default_rng(5)
+    sample = {0, m // chunk - 1} | {int(v) for v in rng.integers(1, m // chunk - 1, 4)}
+    qerr = []
+
+    def put(r0, q):
+        if r0 // chunk in sample:
+            g = res.Q[r0:r0 + len(q)].cpu().numpy()
+            qerr.append(float(np.linalg.norm(g - q) / np.linalg.norm(q)))
+    ref = ora.lhc3_chunked("sslhc3", m, n, get, cfg.s1, cfg.s2, cfg.seed, *contract, chunk_rows=chunk, put_q=put,
+                           stages=True)
+    assert np.array_equal(piv_g, ref.piv)
+    assert np.array_equal(piv2.cpu().numpy(), ref.piv)
+    assert np.array_equal(U.cpu().numpy(), ref.stages["U"])
+    assert np.array_equal(L11.cpu().numpy(), ref.stages["L11"])
+    assert np.array_equal(Lt, ref.stages["Lt"])
+    assert rel_fro(R_g, ref.R) <= r_tol(cfg)
+    assert len(qerr) == len(sample)
+    print(f"cfg5 R rel diff {rel_fro(R_g, ref.R):.3e}; sampled Q blocks rel diff max {max(qerr):.3e}")
+    assert max(qerr) <= 1e-8
