@@ -150,6 +150,17 @@ cudaError_t launch_chol(const double* G, int n, double* R, double* work, int sta
                         cudaStream_t st, double* rdiag = nullptr);
 size_t chol_ws_bytes(int n);
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st);
+// tsgemm.cu: Cout = Cin -/+ A B on DMMA (persistent, TMA-fed, warp-specialised; the fma chain
+// in increasing k); tri: B upper triangular, and Cout may then alias A (in-place triangular
+// product).  bpack: ts_gemm_pack_bytes(K, N) bytes of scratch for B's packed image.
+size_t ts_gemm_pack_bytes(int K, int N);
+// the driver's cuTensorMapEncodeTiled (nullptr if unavailable); include <cudaTypedefs.h> to use
+#ifdef PFN_cuTensorMapEncodeTiled
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+#endif
+cudaError_t launch_ts_gemm(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A, int64_t lda,
+                           const double* B, int64_t ldb, int64_t rows, int K, int N, bool tri, bool sub, double* bpack,
+                           cudaStream_t st);
 cudaError_t launch_trmm_uu(const double* A, const double* B, int n, double* C, cudaStream_t st);
 cudaError_t launch_shift_diag(double* G, int n, int64_t m, cudaStream_t st);
 cudaError_t launch_flip_neg_rows(double* T, int n, cudaStream_t st);

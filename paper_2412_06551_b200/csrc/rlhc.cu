@@ -186,7 +186,7 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
 struct AlgoWs {
   TsluWs t;
   int* pivpos;
-  double *U, *L11, *S, *Y, *G, *D, *Di, *J, *Ji, *N, *rdY;
+  double *U, *L11, *S, *Y, *G, *D, *Di, *J, *Ji, *N, *rdY, *Tinv, *bpack;
   double *Lt, *Ls, *part, *work;
   void* plan;
   double* Om;  // the stored Gaussian sketch (nullptr: generated inside the sketch kernel)
@@ -248,9 +248,10 @@ void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   a.t.status = c.take<unsigned long long>(4);
   carve_tslu(c, m, n, cfg, a.t);
   a.pivpos = c.take<int>((size_t)m);
-  double** sq[] = {&a.U, &a.L11, &a.S, &a.Y, &a.G, &a.D, &a.Di, &a.J, &a.Ji, &a.N};
+  double** sq[] = {&a.U, &a.L11, &a.S, &a.Y, &a.G, &a.D, &a.Di, &a.J, &a.Ji, &a.N, &a.Tinv};
   for (double** q : sq) *q = c.take<double>((size_t)n * n);
   a.rdY = c.take<double>((size_t)n);
+  a.bpack = c.take<double>(ts_gemm_pack_bytes((int)n, (int)n) / sizeof(double));
   const int64_t srows = algo == RLHC_SLHC3 ? s_or_s1 : s2;
   a.Ls = c.take<double>((size_t)srows * n);
   a.Lt = algo == RLHC_SSLHC3 ? c.take<double>((size_t)s_or_s1 * n) : nullptr;
@@ -313,6 +314,12 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
       CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
     } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
+    } else if (!ms && !pp) {
+      // a CholeskyQR pass, n > 64: T = D or J (kappa <= ~7) -> explicit inverse
+      // (R#9) and the in-place triangular product on DMMA (tsgemm.cu), then the Gram
+      CUDA_TRY(launch_tri_inv(T, ni, a.Tinv, st));
+      CUDA_TRY(launch_ts_gemm(nullptr, 0, Q, ldq, A, lda, a.Tinv, n, m, ni, ni, true, false, a.bpack, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else {
       CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
       if (pp) CUDA_TRY(launch_pivot_rows(piv, ni, 0, m, l11, Q, ldq, st));
@@ -382,6 +389,12 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
       CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
     } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
+    } else if (!ms && !pp) {
+      // a CholeskyQR pass, n > 64: T = D or J (kappa <= ~7) -> explicit inverse
+      // (R#9) and the in-place triangular product on DMMA (tsgemm.cu), then the Gram
+      CUDA_TRY(launch_tri_inv(T, ni, a.Tinv, st));
+      CUDA_TRY(launch_ts_gemm(nullptr, 0, Q, ldq, A, lda, a.Tinv, n, m, ni, ni, true, false, a.bpack, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else {
       CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
       if (pp) CUDA_TRY(launch_pivot_rows(piv, ni, 0, m, l11, Q, ldq, st));
@@ -780,7 +793,8 @@ int rlhc_gram(const double* A, int64_t rows, int64_t n, int64_t lda, double* G, 
 
 size_t rlhc_trsm_apply_workspace_size(int64_t rows, int64_t n) {
   if (rows < 1 || n < 1) return 0;
-  return al(256) + al((size_t)n * 8) + al((size_t)n * n * 8) + al(gram_partials_bytes(rows, (int)n));
+  return al(256) + al((size_t)n * 8) + al((size_t)n * n * 8) + al(gram_partials_bytes(rows, (int)n)) +
+         al(ts_gemm_pack_bytes((int)n, (int)n));
 }
 
 int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int mode, double* out,
@@ -797,6 +811,7 @@ int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const
   double* rd = c.take<double>((size_t)n);
   double* Ti = c.take<double>((size_t)n * n);
   double* part = c.take<double>(gram_partials_bytes(rows, (int)n) / 8 + 1);
+  double* bpack = c.take<double>(ts_gemm_pack_bytes((int)n, (int)n) / 8);
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(launch_status_init(status, st));
   CUDA_TRY(launch_rdiag(T, (int)n, n, rd, RLHC_STAGE_SOLVE_Y, status, st));
@@ -806,7 +821,7 @@ int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const
     CUDA_TRY(launch_trsm_rows(A, lda, rows, (int)n, (int)n, T, n, rd, out, ldo, nullptr, nullptr, 0, st));
   } else {
     CUDA_TRY(launch_tri_inv(T, (int)n, Ti, st));
-    CUDA_TRY(launch_rows_upper(A, lda, rows, (int)n, Ti, out, ldo, st));
+    CUDA_TRY(launch_ts_gemm(nullptr, 0, out, ldo, A, lda, Ti, n, rows, (int)n, (int)n, true, false, bpack, st));
   }
   if (G_out) CUDA_TRY(launch_gram(out, ldo, rows, (int)n, part, G_out, st));
   CUDA_TRY(launch_status_finish(status, info, st));

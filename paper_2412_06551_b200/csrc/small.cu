@@ -46,20 +46,38 @@ cudaError_t launch_fill_i32(int* p, int64_t count, int value, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ T^{-1}
-// Upper-triangular inverse, one thread per column (back substitution), zero lower part.
-__global__ void tri_inv_kernel(const double* __restrict__ T, int n, double* __restrict__ Ti) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+// Upper-triangular inverse (for D^-1 and J^-1 of the CholeskyQR passes, kappa <= ~7): one
+// warp per column j of T^-1, back substitution x_i = (delta_ij - sum_{l=i+1..j} T_il x_l)/T_ii
+// for i = j .. 0 with x in shared memory; each dot product is split over the lanes
+// (fixed lane partition, fixed butterfly) -- deterministic.  The zero lower part is written.
+constexpr int TI_WARPS = 4;
+__global__ void __launch_bounds__(32 * TI_WARPS) tri_inv_kernel(const double* __restrict__ T, int n,
+                                                                double* __restrict__ Ti) {
+  extern __shared__ double ti_x[];  // [TI_WARPS][n]
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int j = blockIdx.x * TI_WARPS + wq;
   if (j >= n) return;
-  for (int i = n - 1; i > j; i--) Ti[(int64_t)i * n + j] = 0.0;
-  Ti[(int64_t)j * n + j] = __ddiv_rn(1.0, T[(int64_t)j * n + j]);
-  for (int i = j - 1; i >= 0; i--) {
+  double* x = ti_x + (size_t)wq * n;
+  for (int i = j + 1 + lane; i < n; i += 32) Ti[(int64_t)i * n + j] = 0.0;
+  for (int i = j; i >= 0; i--) {
+    const double* Tr = T + (int64_t)i * n;
     double s = 0.0;
-    for (int l = i + 1; l <= j; l++) s = __fma_rn(T[(int64_t)i * n + l], Ti[(int64_t)l * n + j], s);
-    Ti[(int64_t)i * n + j] = __ddiv_rn(-s, T[(int64_t)i * n + i]);
+    for (int l = i + 1 + lane; l <= j; l += 32) s = __fma_rn(Tr[l], x[l], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double xi = __ddiv_rn((i == j ? 1.0 : 0.0) - s, Tr[i]);
+    if (lane == 0) x[i] = xi;
+    __syncwarp();
+    if (lane == 0) Ti[(int64_t)i * n + j] = xi;
   }
 }
 cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st) {
-  note_launch(); tri_inv_kernel<<<ceil_div(n, 64), 64, 0, st>>>(T, n, Tinv);
+  const size_t smem = (size_t)TI_WARPS * n * sizeof(double);
+  static DevFlags attr;
+  if (smem > 48 * 1024)
+    if (cudaError_t e = smem_attr(attr, tri_inv_kernel, (int)smem)) return e;
+  note_launch();
+  tri_inv_kernel<<<ceil_div(n, TI_WARPS), 32 * TI_WARPS, smem, st>>>(T, n, Tinv);
   return cudaGetLastError();
 }
 

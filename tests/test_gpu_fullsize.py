@@ -197,4 +197,7 @@ def test_fullsize_cfg5_vs_chunked_oracle(rl, ora):
     assert rel_fro(R_g, ref.R) <= r_tol(cfg)
     assert len(qerr) == len(sample)
     print(f"cfg5 R rel diff {rel_fro(R_g, ref.R):.3e}; sampled Q blocks rel diff max {max(qerr):.3e}")
-    assert max(qerr) <= 1e-8
+    # Q itself is determined by X only to ~kappa_2(X) u = 1e14 * 1.1e-16 ~ 1e-2 (first-order
+    # QR perturbation, backward errors ~u ||X||); measured 3.0e-4.  The gates above check Q
+    # at full size; this catches a wrong row order or a stale block.
+    assert max(qerr) <= 1e14 * 2.0 ** -53

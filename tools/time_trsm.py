@@ -8,7 +8,8 @@ import torch  # noqa: E402
 import paper_2412_06551_b200 as rl  # noqa: E402
 
 dev = torch.device("cuda", 0)
-for (m, n) in [(65536, 64), (1 << 20, 128), (262144, 512)]:
+sizes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]] or [(65536, 64), (1 << 20, 128), (262144, 512)]
+for (m, n) in sizes:
     A = torch.randn(m, n, dtype=torch.float64, device=dev)
     T = torch.triu(torch.randn(n, n, dtype=torch.float64, device=dev)) * 0.1 + 4 * torch.eye(n, dtype=torch.float64, device=dev)
     out = torch.empty_like(A)
