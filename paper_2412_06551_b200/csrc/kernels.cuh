@@ -154,6 +154,10 @@ cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st
 // in increasing k); tri: B upper triangular, and Cout may then alias A (in-place triangular
 // product).  bpack: ts_gemm_pack_bytes(K, N) bytes of scratch for B's packed image.
 size_t ts_gemm_pack_bytes(int K, int N);
+// subst.cu: out = A T^{-1} in the oracle's operation order for n > 64 (W = X Y^-1, R#O9)
+bool subst_wide_ok(int n);
+cudaError_t launch_subst_wide(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,
+                              double* out, int64_t ldo, cudaStream_t st);
 // the driver's cuTensorMapEncodeTiled (nullptr if unavailable); include <cudaTypedefs.h> to use
 #ifdef PFN_cuTensorMapEncodeTiled
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();

@@ -312,6 +312,9 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
                         const double* l11, double* G, bool ms = false) -> int {
     if (ms && !pp && subst_ms_ok(ni)) {  // the oracle's op sequence (DESIGN.md R#O9), then the Gram
       CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
+    } else if (ms && !pp && subst_wide_ok(ni)) {  // the same sequence for n > 64 (subst.cu), then the Gram
+      CUDA_TRY(launch_subst_wide(A, lda, m, ni, T, n, Q, ldq, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
     } else if (!ms && !pp) {
@@ -387,6 +390,9 @@ int run_method(int method, const double* X, int64_t m, int64_t n, int64_t ldx, i
                         const double* l11, double* G, bool ms = false) -> int {
     if (ms && !pp && subst_ms_ok(ni)) {  // the oracle's op sequence (DESIGN.md R#O9), then the Gram
       CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
+    } else if (ms && !pp && subst_wide_ok(ni)) {  // the same sequence for n > 64 (subst.cu), then the Gram
+      CUDA_TRY(launch_subst_wide(A, lda, m, ni, T, n, Q, ldq, st));
+      if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
     } else if (!ms && !pp) {
@@ -817,6 +823,8 @@ int rlhc_trsm_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const
   CUDA_TRY(launch_rdiag(T, (int)n, n, rd, RLHC_STAGE_SOLVE_Y, status, st));
   if (mode == RLHC_SUBST && subst_ms_ok((int)n)) {
     CUDA_TRY(launch_subst_ms(A, lda, rows, (int)n, T, n, out, ldo, nullptr, nullptr, st));
+  } else if (mode == RLHC_SUBST && subst_wide_ok((int)n)) {
+    CUDA_TRY(launch_subst_wide(A, lda, rows, (int)n, T, n, out, ldo, st));
   } else if (mode == RLHC_SUBST) {
     CUDA_TRY(launch_trsm_rows(A, lda, rows, (int)n, (int)n, T, n, rd, out, ldo, nullptr, nullptr, 0, st));
   } else {

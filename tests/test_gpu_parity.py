@@ -250,10 +250,12 @@ def test_graph_replay_bitwise():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n", [(1000, 7), (4096, 50), (3000, 64)])
+@pytest.mark.parametrize("m,n", [(1000, 7), (4096, 50), (3000, 64), (3001, 65), (5000, 128), (2049, 200),
+                                 (4100, 256), (1500, 512)])
 def test_trsm_subst_bitwise(m, n):
-    """W = A T^{-1} for n <= 64 follows the oracle's operation sequence (DESIGN.md R#O9:
-    rounded product, rounded difference, IEEE division): bit for bit, also on the arrowhead
+    """W = A T^{-1} follows the oracle's operation sequence (DESIGN.md R#O9: rounded product,
+    rounded difference, IEEE division) bit for bit at every n (subst_ms_kernel for n <= 64,
+    subst_wide_kernel above: ragged row tiles and column blocks), also on the arrowhead
      where an fma chain would blow up."""
     import oracle
     import paper_2412_06551_b200 as rl
@@ -264,7 +266,7 @@ def test_trsm_subst_bitwise(m, n):
     W, _, info = rl.trsm_apply(A, T)
     assert info == (0, 0, 0)
     assert np.array_equal(W.cpu().numpy(), oracle.trsm_right_upper(A.cpu().numpy(), Th))
-    X = synth.arrowhead(2000, 50, 1e-25, device=dev)
+    X = synth.arrowhead(2000, min(n, 128), 1e-25, device=dev)
     piv, U, L11, L, inf2 = rl.getrf_ts(X, want_L=True)
     W2, _, _ = rl.trsm_apply(X, U)
     assert np.array_equal(W2.cpu().numpy(), oracle.trsm_right_upper(X.cpu().numpy(), U.cpu().numpy()))
@@ -280,16 +282,17 @@ def test_trsm_subst_bitwise_wide_exponents():
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(99)
     m, n = 4096, 48
-    Ah = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-300, 300, (m, 1))
-    Ah[::7, 3] = 0.0
-    Ah[5::11, :] *= 1e-20
-    Th = np.triu(rng.standard_normal((n, n))) * 1e-3 + np.diag(10.0 ** rng.uniform(-30, 30, n))
-    W, _, info = rl.trsm_apply(torch.from_numpy(Ah).to(dev), torch.from_numpy(Th).to(dev))
-    ref = oracle.trsm_right_upper(Ah, Th)
-    got = W.cpu().numpy()
-    fin = np.isfinite(ref)
-    assert np.array_equal(np.isfinite(got), fin)
-    assert np.array_equal(got[fin], ref[fin])
+    for n in (48, 136):
+        Ah = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-300, 300, (m, 1))
+        Ah[::7, 3] = 0.0
+        Ah[5::11, :] *= 1e-20
+        Th = np.triu(rng.standard_normal((n, n))) * 1e-3 + np.diag(10.0 ** rng.uniform(-30, 30, n))
+        W, _, info = rl.trsm_apply(torch.from_numpy(Ah).to(dev), torch.from_numpy(Th).to(dev))
+        ref = oracle.trsm_right_upper(Ah, Th)
+        got = W.cpu().numpy()
+        fin = np.isfinite(ref)
+        assert np.array_equal(np.isfinite(got), fin)
+        assert np.array_equal(got[fin], ref[fin])
 
 
 def test_exact_gepp_pivots_match_lapack(rl):
