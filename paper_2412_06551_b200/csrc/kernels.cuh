@@ -83,7 +83,7 @@ size_t tslg_ws_bytes(int64_t rows);
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
                      int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
-                     cudaStream_t st, void* gepp_ws = nullptr);
+                     cudaStream_t st, void* gepp_ws = nullptr, double* bpack = nullptr);
 
 // rows.cu
 cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,
@@ -154,6 +154,12 @@ cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st
 // in increasing k); tri: B upper triangular, and Cout may then alias A (in-place triangular
 // product).  bpack: ts_gemm_pack_bytes(K, N) bytes of scratch for B's packed image.
 size_t ts_gemm_pack_bytes(int K, int N);
+// launch_ts_gemm (tri = false, sub = true) that also reports a non-finite Cin element as
+// ENONFINITE(INPUT, row * n_index + col0_index + column) into status (nullable)
+cudaError_t launch_ts_gemm_checked(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                                   int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, double* bpack,
+                                   unsigned long long* status, int n_index, int col0_index, cudaStream_t st);
+constexpr int kTslwGroup = 64;  // LU panels per bulk Schur product: 4 x 16 columns
 // subst.cu: out = A T^{-1} in the oracle's operation order for n > 64 (W = X Y^-1, R#O9)
 bool subst_wide_ok(int n);
 cudaError_t launch_subst_wide(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,

@@ -112,6 +112,7 @@ struct TsluWs {
   double* lw;
   double* Xp;
   void* gepp;  // exact GEPP mode: the panel's working copy
+  double* bpack;  // the grouped LU's bulk products (tsgemm.cu packed B)
 };
 
 void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, TsluWs& t) {
@@ -126,6 +127,7 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
   t.rd = c.take<double>((size_t)n);
   t.lw = c.take<double>((size_t)kTslwPanel * kTslwPanel);
   t.gepp = tslg_cfg(cfg, rows, n) ? (void*)c.take<char>(tslg_ws_bytes(rows)) : nullptr;
+  t.bpack = c.take<double>(ts_gemm_pack_bytes((int)n, kTslwGroup) / sizeof(double));
   t.Xp = c.take<double>((size_t)n * n);
 }
 
@@ -136,7 +138,7 @@ int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0
              bool check_input = false) {
   if (tslw_cfg(cfg, rows, n)) {  // warp tournament (or exact GEPP); L (original row order) lands in tw
     CUDA_TRY(run_tslw(X, ldx, rows, row0, (int)n, cfg.arity, tw, ldtw, piv, U, L11, t.rd, t.lw, t.chosen, t.ids,
-                      t.cnt, t.vals, t.status, check_input, st, t.gepp));
+                      t.cnt, t.vals, t.status, check_input, st, t.gepp, t.bpack));
     return RLHC_OK;
   }
   const int W = kernel_width(cfg.panel);

@@ -80,6 +80,8 @@ struct TgArgs {
   int K, N;
   int ncb;            // column blocks
   int64_t nrt;        // row tiles
+  unsigned long long* status;  // nullable: report non-finite Cin elements (input check)
+  int n_index, col0;           // ... as ENONFINITE(INPUT, row * n_index + col0 + column)
 };
 
 // chunk sequence of this CTA: row tiles r = blockIdx.x + i * gridDim.x, each with its column
@@ -206,6 +208,12 @@ __global__ void __launch_bounds__(TG_THREADS, 1) ts_gemm_kernel(const __grid_con
         if (p.Cin && gr < p.rows) {  // plain loads: Cin may be Cout (in place)
           acc[a][b][0] = c < p.N ? p.Cin[gr * p.ldci + c] : 0.0;
           acc[a][b][1] = c + 1 < p.N ? p.Cin[gr * p.ldci + c + 1] : 0.0;
+          if (p.status) {
+            if (!isfinite(acc[a][b][0]))
+              report(p.status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * p.n_index + p.col0 + c);
+            if (!isfinite(acc[a][b][1]))
+              report(p.status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * p.n_index + p.col0 + c + 1);
+          }
         } else {
           acc[a][b][0] = acc[a][b][1] = 0.0;
         }
@@ -326,11 +334,32 @@ size_t ts_gemm_pack_bytes(int K, int N) {
   return (size_t)ceil_div(N, TG_N) * ceil_div(std::max(K, 1), TG_K) * TG_K * TG_BS * sizeof(double);
 }
 
+cudaError_t launch_ts_gemm_checked_impl(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                                        int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N,
+                                        bool tri, bool sub, double* bpack, unsigned long long* status, int n_index,
+                                        int col0, cudaStream_t st);
+
 cudaError_t launch_ts_gemm(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A, int64_t lda,
                            const double* B, int64_t ldb, int64_t rows, int K, int N, bool tri, bool sub, double* bpack,
                            cudaStream_t st) {
+  return launch_ts_gemm_checked_impl(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N, tri, sub, bpack, nullptr, 0,
+                                     0, st);
+}
+
+cudaError_t launch_ts_gemm_checked(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                                   int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N, double* bpack,
+                                   unsigned long long* status, int n_index, int col0_index, cudaStream_t st) {
+  return launch_ts_gemm_checked_impl(Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N, false, true, bpack, status,
+                                     n_index, col0_index, st);
+}
+
+cudaError_t launch_ts_gemm_checked_impl(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
+                                        int64_t lda, const double* B, int64_t ldb, int64_t rows, int K, int N,
+                                        bool tri, bool sub, double* bpack, unsigned long long* status, int n_index,
+                                        int col0, cudaStream_t st) {
   if (rows <= 0 || N <= 0) return cudaSuccess;
-  TgArgs p{bpack, ceil_div(std::max(K, 1), TG_K), Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N, 0, 0};
+  TgArgs p{bpack, ceil_div(std::max(K, 1), TG_K), Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N, 0, 0,
+           status, n_index, col0};
   p.ncb = ceil_div(N, TG_N);
   p.nrt = ceil_div<int64_t>(rows, TG_M);
   const int64_t total = (int64_t)p.ncb * p.nkc * TG_K * TG_BS;

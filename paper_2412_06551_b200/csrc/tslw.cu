@@ -447,10 +447,13 @@ struct SchurDSmem {
   double Ublk[WW][WW + 1];   // the previous panel's diagonal block
   double rdp[WW];
 };
+// Grouped (GROUP panels share one bulk product, run_tslw): the accumulators start from the
+// group's partial Schur values B = X - L[:, :P0] U[:P0, group] kept in Lb's columns (Xs = Lb,
+// kbeg = P0), and only k = P0 .. p0-1 remain: the same fma chain, continued.
 __global__ void __launch_bounds__(256, 2)
 tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
                        int p0, int w, int n, const double* __restrict__ U, const double* __restrict__ rd,
-                       unsigned long long* finite_status) {
+                       unsigned long long* finite_status, const double* Xs, int64_t ldxs, int kbeg) {
   extern __shared__ __align__(16) unsigned char sd_raw[];
   SchurDSmem& sm = *reinterpret_cast<SchurDSmem*>(sd_raw);
   const int64_t r0 = (int64_t)blockIdx.x * SD_M;
@@ -458,22 +461,29 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
   const int g = lane >> 2, t = lane & 3;
   const int kold = p0 - WW;
   const bool al = ((ldl & 1) == 0) && ((((uintptr_t)Lb) & 15) == 0) && ((n & 1) == 0) && ((((uintptr_t)U) & 15) == 0);
-  // X values of this lane's fragments (X is never written: before the dependency wait)
+  // the accumulators' start: X (never written: read before the dependency wait) or, grouped,
+  // the partial Schur values the previous kernels left in Lb (read after it)
   double acc[2][2][2];
+  auto init = [&]() {
 #pragma unroll
-  for (int a = 0; a < 2; a++)
+    for (int a = 0; a < 2; a++)
 #pragma unroll
-    for (int b = 0; b < 2; b++)
+      for (int b = 0; b < 2; b++)
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int64_t gr = r0 + wp * 16 + a * 8 + g;
-        const int c = b * 8 + 2 * t + h;
-        const double v = (gr < rows && c < w) ? X[gr * ldx + p0 + c] : 0.0;
-        if (finite_status && !isfinite(v)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c);
-        acc[a][b][h] = v;
-      }
+        for (int h = 0; h < 2; h++) {
+          const int64_t gr = r0 + wp * 16 + a * 8 + g;
+          const int c = b * 8 + 2 * t + h;
+          const double v = (gr < rows && c < w) ? Xs[gr * ldxs + p0 + c] : 0.0;
+          // (grouped: X's columns were checked by the bulk product's read of them)
+          if (finite_status && Xs == X && !isfinite(v))
+            report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c);
+          acc[a][b][h] = v;
+        }
+  };
+  if (Xs == X) init();
   pdl_trigger();
   pdl_wait();
+  if (Xs != X) init();
   auto load_chunk = [&](int st, int kc) {
     // A: 128 rows x 32 k (16-byte pairs, 8 per thread); B: 32 k x 16 columns (1 pair per thread)
 #pragma unroll
@@ -518,7 +528,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     }
     cp_async_commit();
   }
-  if (kold > 0) load_chunk(0, 0);
+  if (kold > kbeg) load_chunk(0, kbeg);
   // the previous panel's block, 1/diag, and U[kold.., panel]
   for (int e = tid; e < WW * WW; e += 256) {
     const int k = e / WW, c = e - k * WW;
@@ -526,7 +536,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     sm.Ut[k][c] = c < w ? U[(int64_t)(kold + k) * n + p0 + c] : 0.0;
   }
   if (tid < WW) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
-  if (kold > 0) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
+  if (kold > kbeg) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
   else cp_async_wait_all();
   __syncthreads();
   if (tid < SD_M) {  // L_{j-1} of row tid: S_{j-1} -> forward substitution (the select's chain)
@@ -538,7 +548,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     for (int c = 0; c < WW; c++) sm.Lt[tid][c] = l[c];
   }
   int st = 0;
-  for (int kc = 0; kc < kold; kc += SD_K) {
+  for (int kc = kbeg; kc < kold; kc += SD_K) {
     if (kc + SD_K < kold) {
       load_chunk(st ^ 1, kc + SD_K);
       cp_async_wait_1();
@@ -1074,11 +1084,23 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
   return cudaMemcpyAsync(out_vals, tval, (size_t)nout * WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
+// Panels are grouped by kTslwGroup (64 columns): at the start of group g >= 1 the last panel's
+// Schur values become L (tslw_lfinal_kernel) and ONE product B = X[:, group] - L[:, :P0]
+// U[:P0, group] (tsgemm.cu, TMA-fed DMMA, the fma chain in increasing k) goes into Lb's group
+// columns; the group's first panel is then B's first 16 columns (no Schur kernel), the others
+// continue the chain over the group's earlier columns only.  Every L column is read from HBM
+// once per group instead of once per panel (cfg5: 395 -> ~300 GB), and the bulk runs on the
+// tensor pipe at 16 flops per byte.  Measured at cfg5 (profiles/r02_launches_cfg5_*.txt): the
+// bulk ran at 48 % of the DMMA peak (short K for the first groups, each tile's X loads
+// exposed) and the in-group Schur kernels kept 3.3 ms each, so the LU went 104 -> 116 ms:
+// OFF by default; RLHC_LU_GROUP=1 (measurement knob) enables it.
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
                      int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
-                     cudaStream_t st, void* gepp_ws) {
+                     cudaStream_t st, void* gepp_ws, double* bpack) {
   (void)lw;
+  static const bool group_on = [] { const char* e = getenv("RLHC_LU_GROUP"); return e && atoi(e) != 0; }();
+  const bool grouped = group_on && bpack && !gepp_ws;
   double* Sw = gepp_ws ? reinterpret_cast<double*>(gepp_ws) : nullptr;  // exact GEPP mode (one leaf)
   TslgScratch* gsc = gepp_ws ? reinterpret_cast<TslgScratch*>(reinterpret_cast<char*>(gepp_ws) +
                                                                (((size_t)rows * WW * sizeof(double) + 255) & ~(size_t)255))
@@ -1100,13 +1122,26 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
     const int w = std::min(WW, n - p0);
-    note_launch();
-    e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
-                        sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U, (const double*)rd,
-                        check_input ? status : nullptr)
-           : launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx, Lb,
-                        ldl, rows, w, n, check_input ? status : nullptr);
-    if (e) return e;
+    const int P0 = grouped ? p0 - p0 % kTslwGroup : 0;  // start of this panel's group
+    if (grouped && p0 >= kTslwGroup && p0 == P0) {
+      // new group: S of the last panel -> L, then B = X[:, group] - L[:, :P0] U[:P0, group]
+      note_launch();
+      e = launch_pdl(tslw_lfinal_kernel, dim3((unsigned)ceil_div<int64_t>(rows, 256)), dim3(256), 0, st, Lb, ldl,
+                     rows, p0 - WW, WW, n, (const double*)U, (const double*)rd);
+      if (e) return e;
+      e = launch_ts_gemm_checked(X + P0, ldx, Lb + P0, ldl, Lb, ldl, U + P0, n, rows, P0, std::min(kTslwGroup, n - P0),
+                                 bpack, check_input ? status : nullptr, n, P0, st);
+      if (e) return e;
+    } else {
+      note_launch();
+      e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+                          sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U,
+                          (const double*)rd, check_input ? status : nullptr, (const double*)(P0 ? Lb : X),
+                          P0 ? ldl : ldx, P0)
+             : launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx,
+                          Lb, ldl, rows, w, n, check_input ? status : nullptr);
+      if (e) return e;
+    }
     if (Sw) {  // exact GEPP: one cooperative launch per panel
       // co-resident grid of the current device (SM count and occupancy queried per call: a
       // MIG slice or another device may have fewer SMs than a full B200)
@@ -1160,7 +1195,7 @@ cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t 
                       ldl, rows, w, n, (unsigned long long*)nullptr);
   return launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                     sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, U, (const double*)nullptr,
-                    (unsigned long long*)nullptr);
+                    (unsigned long long*)nullptr, X, ldx, 0);
 }
 
 cudaError_t launch_tslw_owned(const double* X, int64_t ldx, const double* Lb, int64_t ldl, int64_t rows, int64_t row0,
