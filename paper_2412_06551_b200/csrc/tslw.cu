@@ -453,7 +453,7 @@ struct SchurDSmem {
 __global__ void __launch_bounds__(256, 2)
 tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __restrict__ Lb, int64_t ldl, int64_t rows,
                        int p0, int w, int n, const double* __restrict__ U, const double* __restrict__ rd,
-                       unsigned long long* finite_status, const double* Xs, int64_t ldxs, int kbeg) {
+                       unsigned long long* finite_status, const double* Xs, int64_t ldxs, int kbeg, int pre_only) {
   extern __shared__ __align__(16) unsigned char sd_raw[];
   SchurDSmem& sm = *reinterpret_cast<SchurDSmem*>(sd_raw);
   const int64_t r0 = (int64_t)blockIdx.x * SD_M;
@@ -518,7 +518,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     cp_async_commit();
   };
   // S_{j-1} of the CTA's rows -> Lt (coalesced, 16 threads per row), then the first L chunk
-  {
+  if (!pre_only) {
     const int c = tid & 15;
 #pragma unroll
     for (int j = 0; j < SD_M / 16; j++) {
@@ -529,17 +529,18 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     cp_async_commit();
   }
   if (kold > kbeg) load_chunk(0, kbeg);
-  // the previous panel's block, 1/diag, and U[kold.., panel]
-  for (int e = tid; e < WW * WW; e += 256) {
+  // the previous panel's block, 1/diag, and U[kold.., panel] (pre_only: not needed -- and still
+  // being produced by the previous panel's tournament)
+  for (int e = tid; e < (pre_only ? 0 : WW * WW); e += 256) {
     const int k = e / WW, c = e - k * WW;
     sm.Ublk[k][c] = U[(int64_t)(kold + k) * n + kold + c];
     sm.Ut[k][c] = c < w ? U[(int64_t)(kold + k) * n + p0 + c] : 0.0;
   }
-  if (tid < WW) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
-  if (kold > kbeg) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
+  if (tid < WW && !pre_only) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
+  if (kold > kbeg && !pre_only) cp_async_wait_1();  // S_{j-1} landed (the L chunk may be in flight)
   else cp_async_wait_all();
   __syncthreads();
-  if (tid < SD_M) {  // L_{j-1} of row tid: S_{j-1} -> forward substitution (the select's chain)
+  if (tid < SD_M && !pre_only) {  // L_{j-1} of row tid: S_{j-1} -> forward substitution (the select's chain)
     double l[WW];
 #pragma unroll
     for (int c = 0; c < WW; c++) l[c] = sm.Lt[tid][c];
@@ -572,7 +573,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     st ^= 1;
   }
   __syncthreads();  // Lt complete
-  {  // L_{j-1} to L (coalesced)
+  if (!pre_only) {  // L_{j-1} to L (coalesced)
     const int c = tid & 15;
 #pragma unroll
     for (int j = 0; j < SD_M / 16; j++) {
@@ -581,7 +582,7 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
     }
   }
 #pragma unroll
-  for (int k0 = 0; k0 < WW; k0 += 4) {
+  for (int k0 = 0; k0 < (pre_only ? 0 : WW); k0 += 4) {
     double af[2], bf[2];
 #pragma unroll
     for (int a = 0; a < 2; a++) af[a] = -sm.Lt[wp * 16 + a * 8 + g][k0 + t];
@@ -1084,6 +1085,27 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
   return cudaMemcpyAsync(out_vals, tval, (size_t)nout * WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
+// per host thread and device: the look-ahead's side stream and its fork / join events
+struct LookAhead {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static cudaError_t look_ahead_streams(LookAhead** out) {
+  static thread_local LookAhead per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  LookAhead& la = per_dev[dev];
+  if (!la.side) {
+    if ((e = cudaStreamCreateWithFlags(&la.side, cudaStreamNonBlocking))) return e;
+    if ((e = cudaEventCreateWithFlags(&la.fork, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&la.join, cudaEventDisableTiming))) return e;
+  }
+  *out = &la;
+  return cudaSuccess;
+}
+
 // Panels are grouped by kTslwGroup (64 columns): at the start of group g >= 1 the last panel's
 // Schur values become L (tslw_lfinal_kernel) and ONE product B = X[:, group] - L[:, :P0]
 // U[:P0, group] (tsgemm.cu, TMA-fed DMMA, the fma chain in increasing k) goes into Lb's group
@@ -1101,6 +1123,17 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   (void)lw;
   static const bool group_on = [] { const char* e = getenv("RLHC_LU_GROUP"); return e && atoi(e) != 0; }();
   const bool grouped = group_on && bpack && !gepp_ws;
+  // look-ahead (RLHC_LU_LOOKAHEAD=1, measurement knob): panel p+1's Schur complement minus its
+  // last 16 terms runs on a side stream while panel p's tournament -- a latency chain that
+  // leaves HBM idle -- climbs its tree.  Measured slower (cfg5 TSLU 106 -> 128 ms, cfg3 3.2 ->
+  // 3.5 ms): the tree's leaf wave fills every SM, so the two kernels only slow each other,
+  // and the split adds a write and a read of the partial panel.  Off by default.
+  static const bool look_on = [] { const char* e = getenv("RLHC_LU_LOOKAHEAD"); return e && atoi(e) != 0; }();
+  LookAhead* la = nullptr;
+  if (look_on && !grouped && !gepp_ws) {
+    if (cudaError_t e0 = look_ahead_streams(&la)) return e0;
+  }
+  const bool look = la != nullptr;
   double* Sw = gepp_ws ? reinterpret_cast<double*>(gepp_ws) : nullptr;  // exact GEPP mode (one leaf)
   TslgScratch* gsc = gepp_ws ? reinterpret_cast<TslgScratch*>(reinterpret_cast<char*>(gepp_ws) +
                                                                (((size_t)rows * WW * sizeof(double) + 255) & ~(size_t)255))
@@ -1132,15 +1165,38 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
       e = launch_ts_gemm_checked(X + P0, ldx, Lb + P0, ldl, Lb, ldl, U + P0, n, rows, P0, std::min(kTslwGroup, n - P0),
                                  bpack, check_input ? status : nullptr, n, P0, st);
       if (e) return e;
+    } else if (look && p0 >= 2 * WW) {
+      // the look-ahead's second half: wait for this panel's bulk (pre-only, side stream), then
+      // S_{p-1} -> L_{p-1} and the last 16 terms (k = p0-16 .. p0-1), from the partial in Lb
+      if ((e = cudaStreamWaitEvent(st, la->join, 0))) return e;
+      note_launch();
+      e = launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+                     sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U, (const double*)rd,
+                     (unsigned long long*)nullptr, (const double*)Lb, ldl, p0 - WW, 0);
+      if (e) return e;
     } else {
       note_launch();
       e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                           sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U,
                           (const double*)rd, check_input ? status : nullptr, (const double*)(P0 ? Lb : X),
-                          P0 ? ldl : ldx, P0)
+                          P0 ? ldl : ldx, P0, 0)
              : launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx,
                           Lb, ldl, rows, w, n, check_input ? status : nullptr);
       if (e) return e;
+    }
+    if (look && p0 + WW < n && p0 + WW >= 2 * WW) {
+      // look-ahead: the next panel's bulk X[:, q] - L[:, :p0] U[:p0, q] (every term but the
+      // last 16; L[:, :p0] is final now) on the side stream, overlapping this panel's
+      // tournament, into the next panel's columns of Lb
+      const int q0 = p0 + WW, wq = std::min(WW, n - q0);
+      if ((e = cudaEventRecord(la->fork, st))) return e;
+      if ((e = cudaStreamWaitEvent(la->side, la->fork, 0))) return e;
+      note_launch();
+      e = launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+                     sizeof(SchurDSmem), la->side, X, ldx, Lb, ldl, rows, q0, wq, n, (const double*)U,
+                     (const double*)rd, check_input ? status : nullptr, X, ldx, 0, 1);
+      if (e) return e;
+      if ((e = cudaEventRecord(la->join, la->side))) return e;
     }
     if (Sw) {  // exact GEPP: one cooperative launch per panel
       // co-resident grid of the current device (SM count and occupancy queried per call: a
@@ -1195,7 +1251,7 @@ cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t 
                       ldl, rows, w, n, (unsigned long long*)nullptr);
   return launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                     sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, U, (const double*)nullptr,
-                    (unsigned long long*)nullptr, X, ldx, 0);
+                    (unsigned long long*)nullptr, X, ldx, 0, 0);
 }
 
 cudaError_t launch_tslw_owned(const double* X, int64_t ldx, const double* Lb, int64_t ldl, int64_t rows, int64_t row0,
