@@ -37,9 +37,14 @@ import synth  # noqa: E402
 
 PEAK_FP64_DMMA_TFLOPS = 37.08  # measured by tools/probe/probe.cu (profiles/r01_probe_fp64_hbm.txt)
 # scalar FP64 FMA (DFMA) peak: measured 36.86 TF/s (same probe); from unit counts
-# 148 SMs x 64 FP64 lanes x 2 flop x 1.965 GHz = 37.2 TF/s
+# 148 SMs x 64 FP64 lanes x 2 flop x 1.965 GHz = 37.2 TF/s.  The FP64 pipe
+# issues 148 x 64 x 1.965e9 = 18.6e12 lane-operations per second; a DMUL or DADD is one of them
+# (a DFMA too, for two flops), so the oracle-order substitution (a rounded product, then a
+# rounded difference per term) is bound by PEAK_FP64_OPS, not by the FMA flop rate.
 PEAK_FP64_ALU_TFLOPS = 36.86
+PEAK_FP64_OPS_T = PEAK_FP64_ALU_TFLOPS / 2  # 1e12 FP64 pipe operations per second
 ALU_STAGES = {"tslu"}  # scalar-FMA stages (GEPP select / elimination), not tensor-core work
+OPS_STAGES = {"solve_w"}  # scalar DMUL + DADD (n > 64; subst_wide_kernel), counted in pipe ops
 
 
 def _peaks():
@@ -51,20 +56,25 @@ def _peaks():
 
 
 def stage_model(cfg: synth.Config) -> dict:
-    """Algorithmic bytes and flops per stage."""
+    """Algorithmic bytes and work per stage: (bytes, flops) -- for
+    solve_w at n > 64 the work is FP64 pipe operations (n(n-1) products and differences + n
+    divisions per row), for the others flops."""
     m, n = cfg.m, cfg.n
     M = 8.0 * m * n
     tri = m * n * (n + 1.0)  # triangular row product / Gram upper half: flops
     srows = cfg.s if cfg.algo == "slhc3" else cfg.s1
     sk_flops = 2.0 * cfg.s * m * n if cfg.algo == "slhc3" else m * n + 2.0 * cfg.s2 * cfg.s1 * n
+    fused = n <= 64  # the solve kernels fuse their Gram (the gram stages are empty)
     return {
         # tslu: the warp tournament reads X and writes L (the L factor is its by-product,
         # the lfactor stage is empty); m n^2 flop of elimination + the panels' Schur updates
         "check_finite": (M, 0.0), "tslu": (2 * M, m * n * n * 1.0), "lfactor": (2 * M, m * n * n * 1.0),
         "sketch": (M + 8.0 * srows * n, sk_flops), "hqr_y": (0.0, 2.0 * srows * n * n),
-        "solve_w_gram1": (2 * M, m * n * n + tri), "chol1": (0.0, n ** 3 / 3.0),
-        "solve_v_gram2": (2 * M, m * n * n + tri), "chol2": (0.0, n ** 3 / 3.0),
-        "solve_q": (2 * M, m * n * n * 1.0), "r_finish": (0.0, 2.0 * n ** 3 / 3),
+        "solve_w": (2 * M, (m * n * n + tri) if fused else m * n * n * 1.0), "gram1": (M, tri),
+        "chol1": (0.0, n ** 3 / 3.0),
+        "solve_v": (2 * M, (m * n * n + tri) if fused else tri), "gram2": (M, tri),
+        "chol2": (0.0, n ** 3 / 3.0),
+        "solve_q": (2 * M, m * n * n * 1.0 if fused else tri), "r_finish": (0.0, 2.0 * n ** 3 / 3),
     }
 
 
@@ -267,6 +277,10 @@ def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, 
         t = stages.get(name, 0.0) / calls * 1e-3
         if t <= 0:
             continue
+        # the dominant KERNEL: at n > 64 every stage but tslu (16 tournaments, 15 Schur kernels,
+        # U rows, ...) is one kernel launch (solve_w = subst_wide, gram = gram_kernel, ...)
+        if name == "tslu" and cfg.n > 64:
+            continue
         if best is None or t > best[1]:
             best = (name, t, byts, flops)
     name, t, byts, flops = best
@@ -277,6 +291,14 @@ def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, 
         traffic = prof.get(f"{cfg.name}:{name}")
     except Exception:
         pass
+    if name in OPS_STAGES and cfg.n > 64:
+        ach = flops / t / 1e12
+        return {"kernel": "subst_wide_kernel (" + name + ")", "bound": "alu", "achieved": ach, "peak": PEAK_FP64_OPS_T,
+                "unit": "T FP64-pipe ops/s", "frac": ach / PEAK_FP64_OPS_T, "traffic": traffic,
+                "peak_source": "half the scalar DFMA rate measured on this pool (36.86 TF/s, "
+                               "profiles/r01_probe_fp64_hbm.txt): one DMUL or DADD per lane per cycle",
+                "ms": t * 1e3, "note": "oracle-order substitution: a rounded product and a rounded difference "
+                                       "per term (DESIGN.md R#O9), no FMA"}
     if name in ALU_STAGES:
         ach = flops / t / 1e12
         return {"kernel": name, "bound": "alu", "achieved": ach, "peak": PEAK_FP64_ALU_TFLOPS, "unit": "TFLOP/s",

@@ -358,7 +358,7 @@ void rlhc_stage_timing(int enable);
  * (k < max_stages), returns the number of calls consumed (or -1 on a CUDA error). */
 int rlhc_stage_times(double* ms, int max_stages);
 const char* rlhc_stage_name(int k);
-#define RLHC_NUM_TIMED_STAGES 11
+#define RLHC_NUM_TIMED_STAGES 13
 
 #ifdef __cplusplus
 }

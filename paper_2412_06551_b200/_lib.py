@@ -171,7 +171,7 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_graph_begin", "rlhc_graph_end", "rlhc_graph_launch", "rlhc_graph_destroy",
             "rlhc_tslw_schur", "rlhc_tslw_owned_rows", "rlhc_tslw_finish",
             "rlhc_host_pipeline_workspace_size", "rlhc_host_pipeline"]
-NUM_TIMED_STAGES = 11
+NUM_TIMED_STAGES = 13
 
 
 def stage_times(reset: bool = True) -> dict:

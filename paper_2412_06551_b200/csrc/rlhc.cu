@@ -36,8 +36,8 @@ namespace {
 
 // ---------------------------------------------------------------- stage timing
 constexpr int kStages = RLHC_NUM_TIMED_STAGES;
-const char* kStageNames[kStages] = {"check_finite", "tslu", "lfactor", "sketch", "hqr_y", "solve_w_gram1",
-                                    "chol1", "solve_v_gram2", "chol2", "solve_q", "r_finish"};
+const char* kStageNames[kStages] = {"check_finite", "tslu",  "lfactor", "sketch", "hqr_y", "solve_w", "gram1",
+                                    "chol1",        "solve_v", "gram2",  "chol2",  "solve_q", "r_finish"};
 using MarkSet = std::array<cudaEvent_t, kStages + 1>;
 struct StageProf {
   std::mutex mu;
@@ -310,24 +310,31 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   // one streaming pass: out = A T^{-1} (substitution) [+ G = out^T out fused]
   // ms: the oracle's op sequence (DESIGN.md R#O9) for solves with an ill-conditioned T (W = X Y^{-1});
   // the CholeskyQR passes (kappa(D), kappa(J) <= ~7) keep the faster fma chain
+  // gmark: stage marker between the solve and a separate Gram (-1: none; with a fused Gram the
+  // Gram stage is empty)
   auto solve_pass = [&](const double* A, int64_t lda, const double* T, const double* rd, const int* pp,
-                        const double* l11, double* G, bool ms = false) -> int {
+                        const double* l11, double* G, bool ms = false, int gmark = -1) -> int {
     if (ms && !pp && subst_ms_ok(ni)) {  // the oracle's op sequence (DESIGN.md R#O9), then the Gram
       CUDA_TRY(launch_subst_ms(A, lda, m, ni, T, n, Q, ldq, a.part, G, st));
+      if (gmark >= 0) mk.mark(gmark);
     } else if (ms && !pp && subst_wide_ok(ni)) {  // the same sequence for n > 64 (subst.cu), then the Gram
       CUDA_TRY(launch_subst_wide(A, lda, m, ni, T, n, Q, ldq, st));
+      if (gmark >= 0) mk.mark(gmark);
       if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else if (rowsolve_ok(ni)) {
       CUDA_TRY(launch_rowsolve(A, lda, m, ni, T, rd, Q, ldq, pp ? piv : nullptr, l11, a.part, G, st));
+      if (gmark >= 0) mk.mark(gmark);
     } else if (!ms && !pp) {
       // a CholeskyQR pass, n > 64: T = D or J (kappa <= ~7) -> explicit inverse
       // (R#9) and the in-place triangular product on DMMA (tsgemm.cu), then the Gram
       CUDA_TRY(launch_tri_inv(T, ni, a.Tinv, st));
       CUDA_TRY(launch_ts_gemm(nullptr, 0, Q, ldq, A, lda, a.Tinv, n, m, ni, ni, true, false, a.bpack, st));
+      if (gmark >= 0) mk.mark(gmark);
       if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     } else {
       CUDA_TRY(launch_trsm_blocked(A, lda, m, ni, ni, T, n, rd, Q, ldq, st));
       if (pp) CUDA_TRY(launch_pivot_rows(piv, ni, 0, m, l11, Q, ldq, st));
+      if (gmark >= 0) mk.mark(gmark);
       if (G) CUDA_TRY(launch_gram(Q, ldq, m, ni, a.part, G, st));
     }
     return RLHC_OK;
@@ -353,24 +360,24 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   CUDA_TRY(launch_rdiag(a.Y, ni, n, a.rdY, RLHC_STAGE_SOLVE_Y, status, st));
   mk.mark(5);
   // W = X Y^{-1} by substitution, fused G1 = W^T W (first Gram of CholeskyQR2)
-  if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true))) return rc;
-  mk.mark(6);
+  if ((rc = solve_pass(X, ldx, a.Y, a.rdY, nullptr, nullptr, a.G, true, 6))) return rc;
+  mk.mark(7);
   // CholeskyQR2(W): D = chol(G1), V = W D^{-1} (+ G2), J = chol(G2), Q = V J^{-1}
   CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st, ni <= 128 ? a.Di : nullptr));
   if (ni > 128) CUDA_TRY(launch_rdiag(a.D, ni, n, a.Di, RLHC_STAGE_SOLVE_D, status, st));
-  mk.mark(7);
-  if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G))) return rc;
   mk.mark(8);
+  if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G, false, 9))) return rc;
+  mk.mark(10);
   CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st, ni <= 128 ? a.Ji : nullptr));
   if (ni > 128) CUDA_TRY(launch_rdiag(a.J, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
-  mk.mark(9);
+  mk.mark(11);
   if ((rc = solve_pass(Q, ldq, a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
-  mk.mark(10);
+  mk.mark(12);
   // R = Z Y = J (D Y)
   CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, a.N, st));
   CUDA_TRY(launch_trmm_uu(a.J, a.N, ni, R, st));
   CUDA_TRY(launch_status_finish(status, info, st));
-  mk.mark(11);
+  mk.mark(13);
   prof_end(mk);
   return RLHC_OK;
 }

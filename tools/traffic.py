@@ -27,52 +27,54 @@ def launches(path):
         if not hdr or len(r) != len(hdr):
             continue
         d = dict(zip(hdr, r))
-        key = (d["ID"], d["Kernel Name"].split("(")[0].replace("void ", "").replace("rlhc::", ""))
+        key = (d["ID"], d["Kernel Name"].split("(")[0].replace("void ", "").replace("rlhc::", "")
+               .replace("<unnamed>::", ""))
         v = float(d["Metric Value"].replace(",", "")) * UNITS.get(d["Metric Unit"], 1)
         per.setdefault(key, {})[d["Metric Name"]] = v
     return [(k[1], m) for k, m in per.items()]
 
 
-def split_stages(call):
-    """Kernel launches of one call -> stage names (run_algo order)."""
+def _base(name):
+    """Kernel base name: namespaces and template arguments stripped."""
+    b = name.replace("<unnamed>::", "").replace("rlhc::", "").replace("void ", "")
+    return b.split("<")[0].split("::")[-1]
+
+
+def split_stages(call, n):
+    """Kernel launches of one call -> stage names (run_algo order, rlhc.cu kStageNames).
+    After HouseholderQR each CholeskyQR pass starts with a recognisable kernel: the W solve
+    (subst_ms / subst_wide), tri_inv for V and Q when n > 64 (rowsolve when n <= 64; the
+    blocked Cholesky of n > 128 also runs rowsolve / gemm_sub inside its stage), the Gram
+    (gram_kernel), the Cholesky (chol_*), the final trmm_uu."""
     out = []
     stage = "check_finite"
-    seen_tslu = False
-    rowsolve_n = 0
-    rdiag_n = 0
+    post = False
     for name, m in call:
-        base = name.split("<")[0]
-        if base in ("status_init_kernel", "check_finite_kernel"):
-            stage = "check_finite"
-        elif base.startswith(("tslu_", "tslw_", "<unnamed>::tslw_")) or base in ("gather_rows_kernel", "l11_fixup_kernel", "trsm_rows_kernel") \
-                and stage in ("check_finite", "tslu"):
-            stage = "tslu"
-            seen_tslu = True
-        elif base in ("fill_i32_kernel", "pivpos_kernel") and seen_tslu:
-            stage = "lfactor"
-        elif base.startswith(("gauss_", "cs_")):
-            stage = "sketch"
-        elif base.startswith("hqr"):
-            stage = "hqr_y"
-        elif base.startswith("chol") or base in ("transpose_kernel", "zero_lower_kernel"):
-            stage = {"solve_w_gram1": "chol1", "solve_v_gram2": "chol2"}.get(stage, stage)
-        elif base in ("rowsolve_kernel", "subst_ms_kernel", "gemm_update_kernel", "gram_kernel", "gram_reduce_kernel",
-                      "gram_part_reduce_kernel", "pivot_rows_kernel"):
-            if base in ("rowsolve_kernel", "subst_ms_kernel") or \
-                    (base == "gemm_update_kernel" and stage in ("hqr_y", "chol1", "chol2")):
-                if stage in ("hqr_y",):
-                    stage = "solve_w_gram1"
-                elif stage == "chol1":
-                    stage = "solve_v_gram2"
-                elif stage == "chol2":
-                    stage = "solve_q"
-                rowsolve_n += 1
-        elif base == "rdiag_kernel":
-            rdiag_n += 1
-        elif base == "trmm_uu_kernel":
-            stage = "hqr_y" if stage == "hqr_y" else ("r_finish" if stage == "solve_q" else stage)
-        elif base == "status_finish_kernel":
-            stage = "r_finish"
+        b = _base(name)
+        pass_start = b == "tri_inv_kernel" if n > 64 else b == "rowsolve_kernel"
+        if not post:
+            if b in ("status_init_kernel", "check_finite_kernel"):
+                stage = "check_finite"
+            elif b.startswith(("tslu_", "tslw_", "tslg_", "gather_rows", "l11_fixup", "trsm_rows", "pivpos",
+                               "fill_i32")) or (b in ("ts_gemm_kernel", "pack_b_kernel") and stage == "tslu"):
+                stage = "tslu"
+            elif b.startswith(("gauss_", "cs_", "omega_gen")):
+                stage = "sketch"
+            elif b.startswith("hqr") or (stage == "hqr_y" and b in ("trmm_uu_kernel", "rdiag_kernel")):
+                stage = "hqr_y"
+            elif stage == "hqr_y" and b in ("subst_ms_kernel", "subst_wide_kernel", "rowsolve_kernel",
+                                            "gemm_sub_kernel"):
+                post = True
+                stage = "solve_w"
+        else:
+            if b == "gram_kernel":
+                stage = {"solve_w": "gram1", "solve_v": "gram2"}.get(stage, stage)
+            elif b.startswith("chol_"):
+                stage = {"solve_w": "chol1", "gram1": "chol1", "solve_v": "chol2", "gram2": "chol2"}.get(stage, stage)
+            elif pass_start:
+                stage = {"chol1": "solve_v", "chol2": "solve_q"}.get(stage, stage)
+            elif b == "trmm_uu_kernel" and stage == "solve_q":
+                stage = "r_finish"
         out.append((stage, name, m))
     return out
 
@@ -90,7 +92,10 @@ def main():
     calls.append(cur)
     call = calls[-1]
     agg = OrderedDict()
-    for stage, name, m in split_stages(call):
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import synth
+    for stage, name, m in split_stages(call, synth.CONFIGS[cfg].n):
         a = agg.setdefault(stage, {"us": 0.0, "dram_bytes": 0.0, "kernels": 0})
         a["us"] += m.get("gpu__time_duration.sum", 0.0)
         a["dram_bytes"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
