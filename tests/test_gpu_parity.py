@@ -333,3 +333,24 @@ def test_host_pipeline_matches_device_calls(rl, algo, m, n, kw):
         res = fn(Xs[i].to(dev), seed=seeds[i], **kw)
         assert torch.equal(res.Q.cpu(), Qs[i]) and torch.equal(res.R.cpu(), Rs[i])
         assert torch.equal(res.piv.cpu(), ps[i])
+
+
+@pytest.mark.gpu
+def test_arrowhead_breakdown_is_a_value(rl):
+    """On the arrowhead at beta = 1e-25 (kappa ~ 1e25 >> 1/u) SSLHC3 may break
+    down; a breakdown must come back as EBREAKDOWN from a Cholesky stage, never as
+    a 'success' carrying NaN or Inf."""
+    dev = torch.device("cuda", 0)
+    X = synth.arrowhead(20000, 50, 1e-25, device=dev)
+    plan = rl.Plan("sslhc3", 20000, 50, s1=17000, s2=50, device=dev)
+    seen = set()
+    for k in range(24):
+        plan.seed = 1000 + k
+        res = plan.run(X)
+        code = res.info()
+        if code[0] == 0:
+            assert torch.isfinite(res.Q).all().item() and torch.isfinite(res.R).all().item()
+        else:
+            assert code[0] == 5 and code[1] in (5, 7), code  # EBREAKDOWN, CHOL1 / CHOL2
+        seen.add(code[0])
+    assert 0 in seen  # most trials succeed
