@@ -905,9 +905,10 @@ namespace rlhc {
 // out = A T^{-1} (T upper, n <= 64) with the oracle's operation sequence (ora_trsm_right_upper,
 // DESIGN.md R#O9): acc = a_k; acc = acc - (o_j * T[j][k]) for j < k (a rounded product, then a
 // rounded difference: no fma); o_k = acc / T[k][k] (IEEE division).  Used for W = X Y^{-1}
-// and the CholeskyQR passes: the fma chain amplifies cancellation in W on the
-// arrowhead of P:1071-1082 (|W| 1.5e10 instead of 19 at beta = 1e-25, tools/arrow_fma.py),
-// this sequence does not; W is then bit-identical to the oracle's.  Thread per row, the
+// (n > 64: subst.cu) -- the CholeskyQR passes V = W D^-1, Q = V J^-1 keep the fma
+// chain (rowsolve_kernel) or, for n > 64, the explicit inverse (R#9): the fma chain amplifies
+// cancellation in W on the arrowhead of P:1071-1082 (|W| 1.5e10 instead of 19 at beta =
+// 1e-25, tools/arrow_fma.py), this sequence does not; W is bit-identical to the oracle's.  Thread per row, the
 // row in registers (static indices), T in shared memory (broadcast reads), row tiles staged
 // through shared memory with coalesced cp.async; out may alias A.
 constexpr int SMS_R = 128, SMS_LD = 65;

@@ -102,10 +102,13 @@ def svd_stack(m: int, n: int, sigma: float, seed: int, blocks: int = 10, device=
     return X1.repeat(blocks, 1)
 
 
-def lower_tri_stack(m: int, n: int, a: float, device="cpu") -> torch.Tensor:
-    """stacked lower-triangular F (100 on the diagonal, a below)."""
+def lower_tri_stack(m: int, n: int, a: float, device="cpu", diag: float = 1.0) -> torch.Tensor:
+    """stacked lower-triangular F (a below the diagonal).  The paper prints 100 on
+    the diagonal, but its tables (tab:Ok1/Rk1) give kappa_2(X) = 2.65e12, 5.10e13,
+    8.29e14, 1.13e16 for a = -0.7 .. -1, which a unit diagonal reproduces (2.65e12, 5.10e13,
+    8.27e14, 1.06e16; with 100 on the diagonal kappa_2 is 1.21 .. 1.33): DESIGN.md R#25."""
     F = torch.full((n, n), float(a), dtype=torch.float64, device=device).tril(-1) + \
-        100.0 * torch.eye(n, dtype=torch.float64, device=device)
+        float(diag) * torch.eye(n, dtype=torch.float64, device=device)
     reps = -(-m // n)
     return F.repeat(reps, 1)[:m].contiguous()
 
