@@ -273,6 +273,31 @@ def test_trsm_subst_bitwise(m, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [96, 136, 200])
+def test_trsm_subst_strides_and_in_place(n):
+    """Both n > 64 substitution kernels -- the TMA-fed one (even leading dimensions, 16-byte
+    aligned) and the cp.async one it falls back to (an odd leading dimension) -- and the
+    in-place call (out = A) give the oracle's W bit for bit."""
+    import oracle
+    import paper_2412_06551_b200 as rl
+    dev = torch.device("cuda", 0)
+    m = 3001
+    big = synth.baseline_matrix(m, n + 1, 10, 12, device=dev)
+    Th = np.triu(np.random.default_rng(n + 5).standard_normal((n, n))) + 4 * np.eye(n)
+    T = torch.from_numpy(Th).to(dev)
+    A = big[:, :n]                                   # lda = n + 1 (odd): fallback kernel
+    ref = oracle.trsm_right_upper(A.cpu().numpy(), Th)
+    W, _, info = rl.trsm_apply(A, T)
+    assert info == (0, 0, 0) and np.array_equal(W.cpu().numpy(), ref)
+    outw = torch.empty(m, n + 2, dtype=torch.float64, device=dev)[:, :n]
+    W2, _, _ = rl.trsm_apply(A.contiguous(), T, out=outw)   # ldo = n + 2 (even): TMA kernel
+    assert np.array_equal(W2.cpu().numpy(), ref)
+    Ai = A.contiguous()
+    rl.trsm_apply(Ai, T, out=Ai)                     # in place
+    assert np.array_equal(Ai.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
 def test_trsm_subst_bitwise_wide_exponents():
     """The substitution's division (reciprocal + two residual steps, the library division
     outside 2^-900..2^900 and for zero quotients) is IEEE division bit for bit: diagonal and
