@@ -44,7 +44,7 @@ PEAK_FP64_DMMA_TFLOPS = 37.08  # measured by tools/probe/probe.cu (profiles/r01_
 PEAK_FP64_ALU_TFLOPS = 36.86
 PEAK_FP64_OPS_T = PEAK_FP64_ALU_TFLOPS / 2  # 1e12 FP64 pipe operations per second
 ALU_STAGES = {"tslu"}  # scalar-FMA stages (GEPP select / elimination), not tensor-core work
-OPS_STAGES = {"solve_w"}  # scalar DMUL + DADD (n > 64; subst_wide_kernel), counted in pipe ops
+OPS_STAGES = {"solve_w"}  # scalar DMUL + DADD (n > 64; subst_wide_tma_kernel), counted in pipe ops
 
 
 def _peaks():
@@ -293,10 +293,11 @@ def roofline(cfg: synth.Config, stages: dict, world: int, step_ms: float = 0.0, 
         pass
     if name in OPS_STAGES and cfg.n > 64:
         ach = flops / t / 1e12
-        return {"kernel": "subst_wide_kernel (" + name + ")", "bound": "alu", "achieved": ach, "peak": PEAK_FP64_OPS_T,
+        return {"kernel": "subst_wide_tma_kernel (" + name + ")", "bound": "alu", "achieved": ach, "peak": PEAK_FP64_OPS_T,
                 "unit": "T FP64-pipe ops/s", "frac": ach / PEAK_FP64_OPS_T, "traffic": traffic,
-                "peak_source": "half the scalar DFMA rate measured on this pool (36.86 TF/s, "
-                               "profiles/r01_probe_fp64_hbm.txt): one DMUL or DADD per lane per cycle",
+                "peak_source": "the scalar DFMA instruction rate measured on this pool (36.86 TF/s = 18.43 T "
+                               "DFMA/s, profiles/r01_probe_fp64_hbm.txt); a DMUL or a DADD costs the FP64 "
+                               "pipe what a DFMA does (tools/probe/pdmuladd.cu, profiles/r02_probe_dmul_dadd.txt)",
                 "ms": t * 1e3, "note": "oracle-order substitution: a rounded product and a rounded difference "
                                        "per term (DESIGN.md R#O9), no FMA"}
     if name in ALU_STAGES:

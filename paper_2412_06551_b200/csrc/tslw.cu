@@ -20,8 +20,12 @@
 // the last S into L and tslw_fixup_kernel gives the pivot rows their L11 rows.
 // Every element of S, L and U is the oracle's fma chain (oracle ora_tslu / l_row: the
 // elimination and the substitution are the same chain), so piv, U, L11 and L are bit-exact.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -614,6 +618,216 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
   }
 }
 
+// The same Schur complement as a warp-specialised TMA pipeline (the default when L is
+// TMA-describable): persistent CTAs, one per SM, 128-row tiles; one elected producer thread
+// streams, per tile, first S_{j-1} (L's columns [kold, p0)) and then L's columns
+// [16 c, 16 c + 16) for c < kold/16 as 128 x 16 boxes (128-byte swizzle) into ST_S stages
+// completing on mbarriers; the 8 consumer warps never load A themselves.  Warps 0-3 turn
+// S_{j-1} into L_{j-1} (row substitution, thread = row) into a double-buffered swizzled Lt
+// and L, while the producer keeps streaming the tile's chunks; the last k-chunk multiplies
+// Lt after one named barrier.  U[:p0, panel] (B) is staged once per CTA.  Same chain per
+// element as tslw_schur_dmma_kernel: acc = X, then k = 0 .. p0-1 in increasing order.
+// (That kernel's two-stage cp.async loop kept the L stream at 49 % of HBM: one 32 KB chunk
+// in flight while the last was computed.)
+constexpr int ST_M = 128, ST_S = 6, ST_CW = 8, ST_BS = WW + 4;
+constexpr int ST_THREADS = 32 * (ST_CW + 1);
+struct __align__(1024) SchurTSmem {
+  double A[ST_S][ST_M][WW];  // k chunks (and S_{j-1}), swizzled
+  double Lt[2][ST_M][WW];    // L_{j-1} of the tile, swizzled, by tile parity
+  double Ublk[WW][WW + 1];
+  double rdp[WW];
+  unsigned long long full[ST_S], empty[ST_S];
+  // followed by Bs[p0][ST_BS]: U[k][p0 + c]
+};
+__device__ __forceinline__ int st_off(int row, int k) { return row * WW + ((((k >> 1) ^ row) & 7) << 1) + (k & 1); }
+size_t schur_tma_smem(int p0) { return sizeof(SchurTSmem) + (size_t)p0 * ST_BS * sizeof(double) + 1024; }
+
+__global__ void __launch_bounds__(ST_THREADS, 1)
+tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
+                      double* __restrict__ Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
+                      const double* __restrict__ U, const double* __restrict__ rd, unsigned long long* finite_status) {
+  extern __shared__ __align__(1024) unsigned char stm_raw[];
+  SchurTSmem& sm = *reinterpret_cast<SchurTSmem*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
+  double* Bs = reinterpret_cast<double*>(&sm + 1);
+  const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
+  const int kold = p0 - WW, nk = kold / WW;
+  const int64_t ntiles = ceil_div<int64_t>(rows, ST_M);
+  if (tid < ST_S) {
+    mbar_init(&sm.full[tid], 1);
+    mbar_init(&sm.empty[tid], ST_CW);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
+  if (wp == ST_CW) {
+    // ---------------- producer
+    if (lane != 0) return;
+    uint32_t q = 0;
+    for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      for (int c = -2; c < nk; c++, q++) {  // -2: X's panel columns, -1: S_{j-1}, then L's k chunks
+        const int s = (int)(q % ST_S);
+        if (q >= ST_S) mbar_wait(&sm.empty[s], ((q / ST_S) - 1) & 1);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
+                     "r"((uint32_t)(ST_M * WW * 8))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
+            "l"(reinterpret_cast<uint64_t>(c == -2 ? &tmX : &tmL)), "r"(c == -2 ? p0 : c < 0 ? kold : c * WW),
+            "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  // ---------------- consumers (256 threads): B, the previous panel's block, 1/diag
+  for (int e = tid; e < p0 * WW; e += 32 * ST_CW) {
+    const int k = e / WW, c = e - k * WW;
+    Bs[k * ST_BS + c] = c < w ? U[(int64_t)k * n + p0 + c] : 0.0;
+  }
+  for (int e = tid; e < WW * WW; e += 32 * ST_CW) {
+    const int k = e / WW, c = e - k * WW;
+    sm.Ublk[k][c] = U[(int64_t)(kold + k) * n + kold + c];
+  }
+  if (tid < WW) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
+  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");
+  const int g = lane >> 2, tq = lane & 3;
+  auto frow = [&](int a) { return wp * 16 + 2 * g + a; };  // conflict-free against the swizzle
+  const bool st16 = (ldl & 1) == 0;                          // (TMA-describable L: base 16-byte aligned)
+  uint32_t q = 0;
+  int par = 0;
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, par ^= 1) {
+    const int64_t r0 = tl * ST_M;
+    double acc[2][2][2];
+    {  // X's panel columns (zero outside the matrix), with the input check
+      const int s = (int)(q % ST_S);
+      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+      const double* xs = &sm.A[s][0][0];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          const int c = b * 8 + 2 * tq;
+          const double2 v = *reinterpret_cast<const double2*>(xs + st_off(frow(a), c));
+          acc[a][b][0] = v.x, acc[a][b][1] = v.y;
+          if (finite_status) {
+            const int64_t gr = r0 + frow(a);
+            if (!isfinite(v.x)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c);
+            if (!isfinite(v.y)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c + 1);
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      q++;
+    }
+    {  // S_{j-1} -> L_{j-1}: thread = tile row, warps 0-3 on even tiles, 4-7 on odd ones
+      const int s = (int)(q % ST_S);
+      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+      if ((wp >> 2) == par) {
+        const int row = tid & (ST_M - 1);
+        const double* src = &sm.A[s][0][0];
+        double l[WW];
+#pragma unroll
+        for (int c = 0; c < WW; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(src + st_off(row, c));
+          l[c] = v.x, l[c + 1] = v.y;
+        }
+        subst_row_rl(l, WW, [&](int k, int c) { return sm.Ublk[k][c]; }, [&](int k) { return sm.rdp[k]; });
+        double* lt = &sm.Lt[par][0][0];
+#pragma unroll
+        for (int c = 0; c < WW; c += 2) *reinterpret_cast<double2*>(lt + st_off(row, c)) = make_double2(l[c], l[c + 1]);
+        if (r0 + row < rows) {
+          double* dst = Lb + (r0 + row) * ldl + kold;
+          if (st16) {
+#pragma unroll
+            for (int c = 0; c < WW; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(l[c], l[c + 1]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < WW; c++) dst[c] = l[c];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      q++;
+    }
+    auto mma16 = [&](const double* As, int kb) {  // 16 k's: A stage (swizzled), B rows kb ..
+#pragma unroll
+      for (int k0 = 0; k0 < WW; k0 += 4) {
+        double af[2], bf[2];
+#pragma unroll
+        for (int a = 0; a < 2; a++) af[a] = -As[st_off(frow(a), k0 + tq)];
+#pragma unroll
+        for (int b = 0; b < 2; b++) bf[b] = Bs[(kb + k0 + tq) * ST_BS + b * 8 + g];
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+          for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      }
+    };
+    for (int c = 0; c < nk; c++, q++) {
+      const int s = (int)(q % ST_S);
+      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+      mma16(&sm.A[s][0][0], c * WW);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
+    mma16(&sm.Lt[par][0][0], kold);
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++) {
+        const int64_t gr = r0 + frow(a);
+        const int c = b * 8 + 2 * tq;
+        if (gr < rows) {
+          double* dst = Lb + gr * ldl + p0 + c;
+          if (st16 && c + 1 < w) {
+            *reinterpret_cast<double2*>(dst) = make_double2(acc[a][b][0], acc[a][b][1]);
+          } else {
+            if (c < w) dst[0] = acc[a][b][0];
+            if (c + 1 < w) dst[1] = acc[a][b][1];
+          }
+        }
+      }
+  }
+}
+
+// launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
+// tells the caller whether it ran
+static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0,
+                                    int w, int n, const double* U, const double* rd, unsigned long long* status,
+                                    cudaStream_t st, bool* done) {
+  *done = false;
+  static const bool on = [] { const char* e = getenv("RLHC_SCHUR_TMA"); return !e || atoi(e) != 0; }();
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  const size_t smem = schur_tma_smem(p0);
+  if (!on || !enc || p0 < WW || (ldl & 1) || (ldx & 1) || (reinterpret_cast<uintptr_t>(Lb) & 15) ||
+      (reinterpret_cast<uintptr_t>(X) & 15) || smem > 227 * 1024 || rows >= (int64_t(1) << 31))
+    return cudaSuccess;
+  auto make = [&](CUtensorMap* m, const double* base, int64_t ld, int cols) {
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {WW, ST_M};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  CUtensorMap mL, mX;
+  if (!make(&mL, Lb, ldl, p0) || !make(&mX, X, ldx, p0 + w)) return cudaSuccess;
+  static DevFlags attr;
+  if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel, 227 * 1024)) return e;
+  int dev = 0, sms = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) return e;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, ST_M), sms));
+  note_launch();
+  *done = true;
+  return launch_pdl(tslw_schur_tma_kernel, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb, ldl, rows, p0,
+                    w, n, U, rd, status);
+}
+
 // The tournament of one panel, all levels in one launch.  Warp = leaf (rows
 // [leaf*128, leaf*128 + 128) of the local rows, their S_j rows from L's panel columns);
 // the LAST child to finish a node runs the node (arrival counters, reset by the node's
@@ -1175,8 +1389,14 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
                      (unsigned long long*)nullptr, (const double*)Lb, ldl, p0 - WW, 0);
       if (e) return e;
     } else {
-      note_launch();
-      e = p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
+      bool done = false;
+      if (p0 && !grouped && !look) {
+        e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, rd, check_input ? status : nullptr, st, &done);
+        if (e) return e;
+      }
+      if (!done) note_launch();
+      e = done ? cudaSuccess
+        : p0 ? launch_pdl(tslw_schur_dmma_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SD_M)), dim3(256),
                           sizeof(SchurDSmem), st, X, ldx, Lb, ldl, rows, p0, w, n, (const double*)U,
                           (const double*)rd, check_input ? status : nullptr, (const double*)(P0 ? Lb : X),
                           P0 ? ldl : ldx, P0, 0)
