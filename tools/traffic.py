@@ -62,7 +62,7 @@ def split_stages(call, n):
                 stage = "sketch"
             elif b.startswith("hqr") or (stage == "hqr_y" and b in ("trmm_uu_kernel", "rdiag_kernel")):
                 stage = "hqr_y"
-            elif stage == "hqr_y" and b in ("subst_ms_kernel", "subst_wide_kernel", "rowsolve_kernel",
+            elif stage == "hqr_y" and b in ("subst_ms_kernel", "subst_wide_kernel", "subst_wide_tma_kernel", "rowsolve_kernel",
                                             "gemm_sub_kernel"):
                 post = True
                 stage = "solve_w"
