@@ -620,35 +620,54 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
 
 // The same Schur complement as a warp-specialised TMA pipeline (the default when L is
 // TMA-describable): persistent CTAs, one per SM, 128-row tiles; one elected producer thread
-// streams, per tile, first S_{j-1} (L's columns [kold, p0)) and then L's columns
+// streams, per tile, X's panel columns, S_{j-1} (L's columns [kold, p0)) and then L's columns
 // [16 c, 16 c + 16) for c < kold/16 as 128 x 16 boxes (128-byte swizzle) into ST_S stages
-// completing on mbarriers; the 8 consumer warps never load A themselves.  Warps 0-3 turn
-// S_{j-1} into L_{j-1} (row substitution, thread = row) into a double-buffered swizzled Lt
-// and L, while the producer keeps streaming the tile's chunks; the last k-chunk multiplies
-// Lt after one named barrier.  U[:p0, panel] (B) is staged once per CTA.  Same chain per
-// element as tslw_schur_dmma_kernel: acc = X, then k = 0 .. p0-1 in increasing order.
-// (That kernel's two-stage cp.async loop kept the L stream at 49 % of HBM: one 32 KB chunk
-// in flight while the last was computed.)
-constexpr int ST_M = 128, ST_S = 6, ST_CW = 8, ST_BS = WW + 4;
-constexpr int ST_THREADS = 32 * (ST_CW + 1);
+// completing on mbarriers; the 8 consumer warps never load A themselves.  Half of them (by
+// tile parity) turn S_{j-1} into L_{j-1} (row substitution, thread = row) into a
+// double-buffered swizzled Lt and L while the producer keeps streaming the tile's chunks; the
+// last k-chunk multiplies Lt after one named barrier.  U[:p0, panel] (B) is staged once per
+// CTA.  Same chain per element as tslw_schur_dmma_kernel: acc = X, then k = 0 .. p0-1 in
+// increasing order.  (That kernel's two-stage cp.async loop kept the L stream at 49 % of
+// HBM: one 32 KB chunk in flight while the last was computed.)
+//
+// Leaves (ids0 non-null): a tile's 128 rows are one tournament leaf, so the tile's S_j goes
+// from the accumulators straight into the staging tile of one of three SELECT warps (tiles
+// rotate), which run the tree kernel's own leaf code (select_and_emit: same winners, same
+// slot contents) while the consumers stream the next tiles; tslw_tree_kernel then starts at
+// level 1.  Saves the tree's re-read of S_j and its leaf wave (a latency chain at 8 warps per
+// SM: 25 of the 106 ms LU at cfg5).  Register split by setmaxnreg: the consumer warpgroups
+// drop to 128 registers, the producer / select warpgroup rises to 248 (the select holds a
+// 128 x 16 tile in registers).  (A first version selected inside the consumer warps, thread
+// = row, with named barriers per step: the select lag stalled the stage ring, LU 90 -> 137 ms.)
+constexpr int ST_M = 128, ST_S = 5, ST_CW = 8, ST_BS = WW + 4;
+constexpr int ST_THREADS = 32 * (ST_CW + 4);  // + producer warp, 3 select warps
+constexpr int ST_SEL = 3;                     // select warps
 struct __align__(1024) SchurTSmem {
   double A[ST_S][ST_M][WW];  // k chunks (and S_{j-1}), swizzled
   double Lt[2][ST_M][WW];    // L_{j-1} of the tile, swizzled, by tile parity
   double Ublk[WW][WW + 1];
   double rdp[WW];
   unsigned long long full[ST_S], empty[ST_S];
-  // followed by Bs[p0][ST_BS]: U[k][p0 + c]
+  unsigned long long ready[ST_SEL], freeb[ST_SEL];  // select warp k's staging tile: filled / free
+  // followed by Bs[p0][ST_BS]: U[k][p0 + c], then (leaves) WSel[ST_SEL]
 };
 __device__ __forceinline__ int st_off(int row, int k) { return row * WW + ((((k >> 1) ^ row) & 7) << 1) + (k & 1); }
-size_t schur_tma_smem(int p0) { return sizeof(SchurTSmem) + (size_t)p0 * ST_BS * sizeof(double) + 1024; }
+__host__ __device__ inline size_t schur_bs_bytes(int p0) { return (((size_t)p0 * ST_BS * sizeof(double)) + 15) & ~(size_t)15; }
+size_t schur_tma_smem(int p0, bool leaves) {
+  return sizeof(SchurTSmem) + schur_bs_bytes(p0) + (leaves ? ST_SEL * sizeof(WSel) : 0) + 1024;
+}
 
 __global__ void __launch_bounds__(ST_THREADS, 1)
 tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
                       double* __restrict__ Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
-                      const double* __restrict__ U, const double* __restrict__ rd, unsigned long long* finite_status) {
+                      const double* __restrict__ U, const double* __restrict__ rd, unsigned long long* finite_status,
+                      const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
+                      double* __restrict__ vals0, int64_t row0) {
   extern __shared__ __align__(1024) unsigned char stm_raw[];
   SchurTSmem& sm = *reinterpret_cast<SchurTSmem*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
   double* Bs = reinterpret_cast<double*>(&sm + 1);
+  WSel* wsel = reinterpret_cast<WSel*>(reinterpret_cast<unsigned char*>(Bs) + schur_bs_bytes(p0));
+  const bool leaves = ids0 != nullptr;
   const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
   const int kold = p0 - WW, nk = kold / WW;
   const int64_t ntiles = ceil_div<int64_t>(rows, ST_M);
@@ -656,47 +675,78 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
     mbar_init(&sm.full[tid], 1);
     mbar_init(&sm.empty[tid], ST_CW);
   }
+  if (tid < ST_SEL) {
+    mbar_init(&sm.ready[tid], ST_CW);
+    mbar_init(&sm.freeb[tid], 1);
+  }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
   pdl_trigger();
   pdl_wait();
-  if (wp == ST_CW) {
-    // ---------------- producer
-    if (lane != 0) return;
-    uint32_t q = 0;
-    for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-      for (int c = -2; c < nk; c++, q++) {  // -2: X's panel columns, -1: S_{j-1}, then L's k chunks
-        const int s = (int)(q % ST_S);
-        if (q >= ST_S) mbar_wait(&sm.empty[s], ((q / ST_S) - 1) & 1);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
-                     "r"((uint32_t)(ST_M * WW * 8))
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
-            "l"(reinterpret_cast<uint64_t>(c == -2 ? &tmX : &tmL)), "r"(c == -2 ? p0 : c < 0 ? kold : c * WW),
-            "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
-            : "memory");
+  if (wp >= ST_CW) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 248;\n" ::: "memory");
+    if (wp == ST_CW) {
+      // ---------------- producer
+      if (lane != 0) return;
+      uint32_t q = 0;
+      for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        for (int c = -2; c < (p0 ? nk : -1); c++, q++) {  // -2: X's panel columns, -1: S_{j-1}, then L's k chunks
+          const int s = (int)(q % ST_S);
+          if (q >= ST_S) mbar_wait(&sm.empty[s], ((q / ST_S) - 1) & 1);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
+                       "r"((uint32_t)(ST_M * WW * 8))
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+              "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
+              "l"(reinterpret_cast<uint64_t>(c == -2 ? &tmX : &tmL)), "r"(c == -2 ? p0 : c < 0 ? kold : c * WW),
+              "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
+              : "memory");
+        }
       }
+      return;
+    }
+    const int k = wp - ST_CW - 1;
+    if (!leaves || k >= ST_SEL) return;
+    // ---------------- select warp k: the leaves of this CTA's tiles i = k, k + ST_SEL, ...
+    WSel& ws = wsel[k];
+    uint32_t i = 0;
+    for (int64_t tl = blockIdx.x + (int64_t)k * gridDim.x; tl < ntiles; tl += (int64_t)ST_SEL * gridDim.x, i++) {
+      const int64_t rb = tl * ST_M;
+      unsigned act = 0;
+#pragma unroll
+      for (int s = 0; s < RS; s++) {
+        const int64_t r = rb + s * 32 + lane;
+        ws.sid[s * 32 + lane] = r < rows ? (int)(row0 + r) : INT_MAX;
+        ws.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
+        act |= ((r < rows && !(chosen && chosen[r])) ? 1u : 0u) << s;
+      }
+      mbar_wait(&sm.ready[k], i & 1);  // the consumers staged S_j of tile tl
+      __syncwarp();
+      select_and_emit(ws, act, w, (int)tl, ids0, cnt0, vals0, TslwRoot{}, p0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.freeb[k]);
     }
     return;
   }
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 128;\n" ::: "memory");
   // ---------------- consumers (256 threads): B, the previous panel's block, 1/diag
   for (int e = tid; e < p0 * WW; e += 32 * ST_CW) {
-    const int k = e / WW, c = e - k * WW;
-    Bs[k * ST_BS + c] = c < w ? U[(int64_t)k * n + p0 + c] : 0.0;
+    const int kk = e / WW, c = e - kk * WW;
+    Bs[kk * ST_BS + c] = c < w ? U[(int64_t)kk * n + p0 + c] : 0.0;
   }
-  for (int e = tid; e < WW * WW; e += 32 * ST_CW) {
-    const int k = e / WW, c = e - k * WW;
-    sm.Ublk[k][c] = U[(int64_t)(kold + k) * n + kold + c];
+  for (int e = tid; e < (p0 ? WW * WW : 0); e += 32 * ST_CW) {
+    const int kk = e / WW, c = e - kk * WW;
+    sm.Ublk[kk][c] = U[(int64_t)(kold + kk) * n + kold + c];
   }
-  if (tid < WW) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
+  if (tid < WW && p0) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
   asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");
   const int g = lane >> 2, tq = lane & 3;
   auto frow = [&](int a) { return wp * 16 + 2 * g + a; };  // conflict-free against the swizzle
   const bool st16 = (ldl & 1) == 0;                          // (TMA-describable L: base 16-byte aligned)
-  uint32_t q = 0;
+  uint32_t q = 0, ti = 0;
   int par = 0;
-  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, par ^= 1) {
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, par ^= 1, ti++) {
     const int64_t r0 = tl * ST_M;
     double acc[2][2][2];
     {  // X's panel columns (zero outside the matrix), with the input check
@@ -720,7 +770,7 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       q++;
     }
-    {  // S_{j-1} -> L_{j-1}: thread = tile row, warps 0-3 on even tiles, 4-7 on odd ones
+    if (p0) {  // S_{j-1} -> L_{j-1}: thread = tile row, warps 0-3 on even tiles, 4-7 on odd ones
       const int s = (int)(q % ST_S);
       mbar_wait(&sm.full[s], (q / ST_S) & 1);
       if ((wp >> 2) == par) {
@@ -732,7 +782,7 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
           const double2 v = *reinterpret_cast<const double2*>(src + st_off(row, c));
           l[c] = v.x, l[c + 1] = v.y;
         }
-        subst_row_rl(l, WW, [&](int k, int c) { return sm.Ublk[k][c]; }, [&](int k) { return sm.rdp[k]; });
+        subst_row_rl(l, WW, [&](int kk, int c) { return sm.Ublk[kk][c]; }, [&](int kk) { return sm.rdp[kk]; });
         double* lt = &sm.Lt[par][0][0];
 #pragma unroll
         for (int c = 0; c < WW; c += 2) *reinterpret_cast<double2*>(lt + st_off(row, c)) = make_double2(l[c], l[c + 1]);
@@ -772,8 +822,10 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
-    mma16(&sm.Lt[par][0][0], kold);
+    if (p0) {
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
+      mma16(&sm.Lt[par][0][0], kold);
+    }
 #pragma unroll
     for (int a = 0; a < 2; a++)
 #pragma unroll
@@ -790,19 +842,41 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
           }
         }
       }
+    if (leaves) {  // S_j -> the staging tile of select warp ti % ST_SEL (zero outside the panel)
+      const int k = (int)(ti % ST_SEL);
+      if (ti >= ST_SEL) mbar_wait(&sm.freeb[k], ((ti / ST_SEL) - 1) & 1);
+      double* tile = wsel[k].tile;
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          const int c = b * 8 + 2 * tq;
+          *reinterpret_cast<double2*>(tile + frow(a) * TS + c) =
+              make_double2(c < w ? acc[a][b][0] : 0.0, c + 1 < w ? acc[a][b][1] : 0.0);
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.ready[k]);
+    }
   }
 }
 
 // launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
 // tells the caller whether it ran
+// launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
+// tells the caller whether it ran, *leaves_done whether it also selected the leaves (ids0
+// non-null asks for it: more than one leaf, and room for the leaf buffers)
 static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0,
                                     int w, int n, const double* U, const double* rd, unsigned long long* status,
-                                    cudaStream_t st, bool* done) {
+                                    const uint8_t* chosen, int* ids0, int* cnt0, double* vals0, int64_t row0,
+                                    cudaStream_t st, bool* done, bool* leaves_done) {
   *done = false;
+  *leaves_done = false;
   static const bool on = [] { const char* e = getenv("RLHC_SCHUR_TMA"); return !e || atoi(e) != 0; }();
+  static const bool leaves_on = [] { const char* e = getenv("RLHC_SCHUR_LEAVES"); return !e || atoi(e) != 0; }();
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-  const size_t smem = schur_tma_smem(p0);
-  if (!on || !enc || p0 < WW || (ldl & 1) || (ldx & 1) || (reinterpret_cast<uintptr_t>(Lb) & 15) ||
+  bool leaves = leaves_on && ids0 && rows > ST_M && schur_tma_smem(p0, true) <= 227 * 1024;
+  const size_t smem = schur_tma_smem(p0, leaves);
+  if (!on || !enc || (ldl & 1) || (ldx & 1) || (reinterpret_cast<uintptr_t>(Lb) & 15) ||
       (reinterpret_cast<uintptr_t>(X) & 15) || smem > 227 * 1024 || rows >= (int64_t(1) << 31))
     return cudaSuccess;
   auto make = [&](CUtensorMap* m, const double* base, int64_t ld, int cols) {
@@ -815,7 +889,7 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   CUtensorMap mL, mX;
-  if (!make(&mL, Lb, ldl, p0) || !make(&mX, X, ldx, p0 + w)) return cudaSuccess;
+  if (!make(&mX, X, ldx, p0 + w) || !make(&mL, p0 ? Lb : X, p0 ? ldl : ldx, p0 ? p0 : w)) return cudaSuccess;
   static DevFlags attr;
   if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel, 227 * 1024)) return e;
   int dev = 0, sms = 0;
@@ -824,79 +898,52 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, ST_M), sms));
   note_launch();
   *done = true;
+  *leaves_done = leaves;
   return launch_pdl(tslw_schur_tma_kernel, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb, ldl, rows, p0,
-                    w, n, U, rd, status);
+                    w, n, U, rd, status, chosen, leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0);
 }
 
-// The tournament of one panel, all levels in one launch.  Warp = leaf (rows
-// [leaf*128, leaf*128 + 128) of the local rows, their S_j rows from L's panel columns);
-// the LAST child to finish a node runs the node (arrival counters, reset by the node's
-// runner for the next panel), up to the root, which emits piv, U's diagonal block and
-// 1/diag(U).  No launch per level, and the select code stays hot in the instruction cache.
-// Slots: level 0 in ids0/cnt0, levels >= 1 packed in idsN/cntN (arrival counters alike).
-__global__ void __launch_bounds__(32 * WPB)
-tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64_t row0, int p0, int w,
-                 const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
-                 int* __restrict__ idsN, int* __restrict__ cntN, double* __restrict__ vals0,
-                 double* __restrict__ valsN, int* __restrict__ arrive, int arity, int stop_lev, TslwRoot ro) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  WSel& sm = reinterpret_cast<WSel*>(raw)[warp_id()];
-  pdl_trigger();
-  pdl_wait();
-  TW_T(t0)
+// The tournament's climb for one warp: select the node held in sm (active mask act) and emit
+// it into `slot` of level lev, then, if this warp's child is the last of its parent to arrive,
+// run the parent -- up to the root (or level stop_lev).  skip_first: the level-0 slots are
+// already emitted (the Schur kernel selected the leaves): start as `slot`'s parent's runner.
+RLHC_DEV void tree_climb(WSel& sm, int nleaves, int slot, unsigned act, const int* cids, const double* cvals,
+                         int* ids0, int* cnt0, double* vals0, int* idsN, int* cntN, double* valsN, int* arrive,
+                         int arity, int stop_lev, const TslwRoot& ro, int p0, int w, bool skip_first) {
   const int lane = lane_id();
-  const int nleaves = (int)ceil_div<int64_t>(rows, WR);
-  const int leaf = blockIdx.x * WPB + warp_id();
-  if (leaf >= nleaves) return;
-  const bool v16 = (ldl & 1) == 0 && (reinterpret_cast<uintptr_t>(Lb) & 15) == 0;
-  const int64_t rb = (int64_t)leaf * WR;
-  unsigned act = 0;
-#pragma unroll
-  for (int s = 0; s < RS; s++) {
-    const int64_t r = rb + s * 32 + lane;
-    sm.sid[s * 32 + lane] = r < rows ? (int)(row0 + r) : INT_MAX;
-    sm.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
-  }
-  __syncwarp();
-  stage_rows(sm, w, Lb, ldl, row0, p0, v16, false);  // in flight while the flags load
-#pragma unroll
-  for (int s = 0; s < RS; s++) {
-    const int64_t r = rb + s * 32 + lane;
-    act |= ((r < rows && !(chosen && chosen[r])) ? 1u : 0u) << s;
-  }
-  if (v16) {
-    cp_async_wait_all();
-    __syncwarp();
-  }
-  TW_T(t1)
-  int nsl = nleaves, slot = leaf;
+  int nsl = nleaves;
   int *oids = ids0, *ocnt = cnt0;
   double* ovals = vals0;
-  const int* cids = nullptr;
-  const double* cvals = nullptr;
   int lev = 0;
   for (;;) {
     TW_G(ga)
-    select_and_emit(sm, act, w, slot, oids, ocnt, ovals, nsl == 1 ? ro : TslwRoot{}, p0);
-    TW_G(gb)
-    if (nsl == 1 || lev == stop_lev) {  // the root, or a rank's top level (row-sharded path)
-      TW_LV(lev, ga, gb, gb, gb)
-      break;
+    int parent, nout, nchild;
+    if (!skip_first) {
+      select_and_emit(sm, act, w, slot, oids, ocnt, ovals, nsl == 1 ? ro : TslwRoot{}, p0);
+      TW_G(gb)
+      if (nsl == 1 || lev == stop_lev) {  // the root, or a rank's top level (row-sharded path)
+        TW_LV(lev, ga, gb, gb, gb)
+        break;
+      }
+      // climb: the last child of the parent runs it
+      if (cids) arrive += nsl;  // counters of this level's parents follow the previous level's
+      parent = slot / arity, nout = (nsl + arity - 1) / arity;
+      nchild = min(arity, nsl - parent * arity);
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atom_add_acq_rel_gpu(&arrive[parent], 1);  // releases this slot, acquires the others
+      old = __shfl_sync(0xffffffffu, old, 0);
+      TW_G(gc)
+      if (old != nchild - 1) {
+        TW_LV(lev + 100, ga, gb, gc, gc)
+        break;
+      }
+      if (lane == 0) arrive[parent] = 0;  // every child has arrived: ready for the next panel
+    } else {
+      skip_first = false;
+      parent = slot / arity, nout = (nsl + arity - 1) / arity;
+      nchild = min(arity, nsl - parent * arity);
     }
-    // climb: the last child of the parent runs it
-    if (cids) arrive += nsl;  // counters of this level's parents follow the previous level's
-    const int parent = slot / arity, nout = (nsl + arity - 1) / arity;
-    const int nchild = min(arity, nsl - parent * arity);
-    __syncwarp();
-    int old = 0;
-    if (lane == 0) old = atom_add_acq_rel_gpu(&arrive[parent], 1);  // releases this slot, acquires the others
-    old = __shfl_sync(0xffffffffu, old, 0);
-    TW_G(gc)
-    if (old != nchild - 1) {
-      TW_LV(lev + 100, ga, gb, gc, gc)
-      break;
-    }
-    if (lane == 0) arrive[parent] = 0;  // every child has arrived: ready for the next panel
     const bool first = cids == nullptr;
     cids = oids;
     cvals = ovals;
@@ -938,11 +985,66 @@ tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64
     cp_async_wait_all();
     __syncwarp();
     TW_G(gd)
-    TW_LV(lev, ga, gb, gc, gd)
+    TW_LV(lev, ga, ga, ga, gd)
     lev++;
     slot = parent;
     nsl = nout;
   }
+}
+
+// The tournament of one panel, all levels in one launch.  Warp = leaf (rows
+// [leaf*128, leaf*128 + 128) of the local rows, their S_j rows from L's panel columns);
+// the LAST child to finish a node runs the node (arrival counters, reset by the node's
+// runner for the next panel), up to the root, which emits piv, U's diagonal block and
+// 1/diag(U).  No launch per level, and the select code stays hot in the instruction cache.
+// Slots: level 0 in ids0/cnt0, levels >= 1 packed in idsN/cntN (arrival counters alike).
+__global__ void __launch_bounds__(32 * WPB)
+tslw_tree_kernel(const double* __restrict__ Lb, int64_t ldl, int64_t rows, int64_t row0, int p0, int w,
+                 const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
+                 int* __restrict__ idsN, int* __restrict__ cntN, double* __restrict__ vals0,
+                 double* __restrict__ valsN, int* __restrict__ arrive, int arity, int stop_lev, TslwRoot ro,
+                 int start1) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  WSel& sm = reinterpret_cast<WSel*>(raw)[warp_id()];
+  pdl_trigger();
+  pdl_wait();
+  TW_T(t0)
+  const int lane = lane_id();
+  const int nleaves = (int)ceil_div<int64_t>(rows, WR);
+  if (start1) {
+    // the leaves were selected by the Schur kernel (tslw_schur_tma_kernel, slots ids0 / cnt0 /
+    // vals0): warp = node of level 1, run as its last-arriving child would
+    const int node = blockIdx.x * WPB + warp_id();
+    if (node >= ceil_div(nleaves, arity)) return;
+    tree_climb(sm, nleaves, node * arity, 0, nullptr, nullptr, ids0, cnt0, vals0, idsN, cntN, valsN, arrive, arity,
+               stop_lev, ro, p0, w, true);
+    return;
+  }
+  const int leaf = blockIdx.x * WPB + warp_id();
+  if (leaf >= nleaves) return;
+  const bool v16 = (ldl & 1) == 0 && (reinterpret_cast<uintptr_t>(Lb) & 15) == 0;
+  const int64_t rb = (int64_t)leaf * WR;
+  unsigned act = 0;
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    const int64_t r = rb + s * 32 + lane;
+    sm.sid[s * 32 + lane] = r < rows ? (int)(row0 + r) : INT_MAX;
+    sm.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
+  }
+  __syncwarp();
+  stage_rows(sm, w, Lb, ldl, row0, p0, v16, false);  // in flight while the flags load
+#pragma unroll
+  for (int s = 0; s < RS; s++) {
+    const int64_t r = rb + s * 32 + lane;
+    act |= ((r < rows && !(chosen && chosen[r])) ? 1u : 0u) << s;
+  }
+  if (v16) {
+    cp_async_wait_all();
+    __syncwarp();
+  }
+  TW_T(t1)
+  tree_climb(sm, nleaves, leaf, act, nullptr, nullptr, ids0, cnt0, vals0, idsN, cntN, valsN, arrive, arity, stop_lev,
+             ro, p0, w, false);
   TW_T(t2)
   TW_T(t3)
   TW_REC(0, t0, t1, t2, t3)
@@ -1289,7 +1391,7 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
   note_launch();
   e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st, src, lds,
                  rows, row0, p0, w, chosen, ids[0], cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity,
-                 stop_lev, TslwRoot{});
+                 stop_lev, TslwRoot{}, 0);
   if (e) return e;
   const int* tid = lev == 0 ? ids[0] : ids[1] + top * WW;
   const int* tcnt = lev == 0 ? cnt[0] : cnt[1] + top;
@@ -1369,6 +1471,7 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
     const int w = std::min(WW, n - p0);
+    bool leaves_done = false;  // the Schur kernel selected this panel's leaves
     const int P0 = grouped ? p0 - p0 % kTslwGroup : 0;  // start of this panel's group
     if (grouped && p0 >= kTslwGroup && p0 == P0) {
       // new group: S of the last panel -> L, then B = X[:, group] - L[:, :P0] U[:P0, group]
@@ -1390,8 +1493,9 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
       if (e) return e;
     } else {
       bool done = false;
-      if (p0 && !grouped && !look) {
-        e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, rd, check_input ? status : nullptr, st, &done);
+      if (!grouped && !look) {
+        e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, rd, check_input ? status : nullptr, chosen,
+                             Sw ? nullptr : ids[0], cnt[0], vals[0], row0, st, &done, &leaves_done);
         if (e) return e;
       }
       if (!done) note_launch();
@@ -1438,9 +1542,10 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
       if (e) return e;
     } else {
       note_launch();
-      e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nleaves, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
+      const int nwarps = leaves_done ? ceil_div(nleaves, arity) : nleaves;  // leaves_done: from level 1
+      e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(nwarps, WPB)), dim3(32 * WPB), WPB * sizeof(WSel), st,
                      (const double*)Lb, ldl, rows, row0, p0, w, (const uint8_t*)(p0 ? chosen : nullptr), ids[0],
-                     cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity, -1, root);
+                     cnt[0], ids[1], cnt[1], vals[0], vals[1], arrive, arity, -1, root, leaves_done ? 1 : 0);
       if (e) return e;
     }
     if (p0 + w < n) {

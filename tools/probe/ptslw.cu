@@ -10,6 +10,11 @@
 #include "../../paper_2412_06551_b200/csrc/tslw.cu"
 namespace rlhc {
 void note_launch() {}
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return nullptr; }
+cudaError_t launch_ts_gemm_checked(const double*, int64_t, double*, int64_t, const double*, int64_t, const double*,
+                                   int64_t, int64_t, int, int, double*, unsigned long long*, int, int, cudaStream_t) {
+  return cudaErrorNotSupported;
+}
 }
 using namespace rlhc;
 
