@@ -205,7 +205,10 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     Rh = torch.empty(cfg.n, cfg.n, dtype=torch.float64).pin_memory()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     big = 8 * m_rows * cfg.n > (4 << 30)
-    e2e_steps = min(args.steps, 5) if big else args.steps  # each cfg5 step moves 64 GiB over PCIe
+    # K problems streamed like the device-side K steps (each cfg5 step moves 64 GiB over PCIe:
+    # ~0.8 s at the measured 91 GB/s duplex rate, tools/pcie_bw.py; the pipeline's fill and
+    # drain -- one H2D before the first solve, one D2H after the last -- amortise over K)
+    e2e_steps = args.steps
     e2e_warm = 1 if big else args.warmup
     e2e = {"unit": "GB/s", "h2d_bytes_per_step": 8 * m_rows * cfg.n,
            "d2h_bytes_per_step": 8 * (m_rows * cfg.n + cfg.n * cfg.n), "per": "rank", "steps": e2e_steps}

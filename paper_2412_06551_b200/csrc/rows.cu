@@ -785,6 +785,8 @@ gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int 
   // a diagonal tile's lower 32 x 32 quarter is never used (G is mirrored from its upper
   // triangle, gram_reduce_kernel): that warp skips its contraction
   const bool lower_warp = ti == tj && wi > wj;
+  // ... and in a diagonal 32 x 32 quarter the fragments strictly below the diagonal (a > b)
+  const bool diag_warp = ti == tj && wi == wj;
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; a++)
@@ -843,7 +845,16 @@ gram_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n, int 
       for (int a = 0; a < 4; a++) af[a] = Ai[buf][kk + t][wi + a * 8 + g];
 #pragma unroll
       for (int b = 0; b < 4; b++) bf[b] = Aj[buf][kk + t][wj + b * 8 + g];
-      if (!lower_warp) {
+      if (diag_warp) {
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++)
+            if (a <= b)
+              asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                  : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                  : "d"(af[a]), "d"(bf[b]));
+      } else if (!lower_warp) {
 #pragma unroll
         for (int a = 0; a < 4; a++)
 #pragma unroll

@@ -221,8 +221,37 @@ __global__ void __launch_bounds__(TG_THREADS, 1) ts_gemm_kernel(const __grid_con
     for (; it.c < it.nk; it.c++, q++) {
       const int s = (int)(q % TG_S);
       mbar_wait(&sm.full[s], (q / TG_S) & 1);
-      // triangular B: this warp's columns [c0 + wj, c0 + wj + 32) need k < c0 + wj + 32 only
-      if (!TRI || it.c * TG_K < c0 + wj + 32) {
+      // triangular B: this warp's columns [c0 + wj, c0 + wj + 32) need k < c0 + wj + 32 only,
+      // and in the two chunks on the warp's diagonal (d = k - (c0 + wj) = 0 or 16) fragment b
+      // (columns c0 + wj + 8 b ..) only k <= c0 + wj + 8 b + 7: B is exactly zero below that, so
+      // those steps would only add signed zeros
+      const int dk = it.c * TG_K - (c0 + wj);
+      if (TRI && (dk == 0 || dk == 16)) {
+#pragma unroll
+        for (int k0 = 0; k0 < TG_K; k0 += 4) {
+          double af[4], bf[4];
+#pragma unroll
+          for (int a = 0; a < 4; a++) {
+            const double v = (&sm.A[s][0][0])[a_off(frow(a), k0 + tq)];
+            af[a] = SUB ? -v : v;
+          }
+#pragma unroll
+          for (int b = 0; b < 4; b++) bf[b] = sm.B[s][k0 + tq][wj + b * 8 + g];
+          if (dk == 0) {
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++)
+                if (k0 <= 8 * b + 7) dmma_s(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++)
+                if (16 + k0 <= 8 * b + 7) dmma_s(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+          }
+        }
+      } else if (!TRI || dk < 32) {
 #pragma unroll
         for (int k0 = 0; k0 < TG_K; k0 += 4) {
           double af[4], bf[4];
