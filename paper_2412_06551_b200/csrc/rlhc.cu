@@ -366,12 +366,25 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   CUDA_TRY(launch_chol(a.G, ni, a.D, a.work, RLHC_STAGE_CHOL1, status, st, ni <= 128 ? a.Di : nullptr));
   if (ni > 128) CUDA_TRY(launch_rdiag(a.D, ni, n, a.Di, RLHC_STAGE_SOLVE_D, status, st));
   mk.mark(8);
-  if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G, false, 9))) return rc;
+  // NEXT-4 (n <= 64, RLHC_Q_JD=1): V = W D^{-1} is formed tile by tile only for G2 and never
+  // stored (Q keeps W), and Q = W (J D)^{-1} -- 7 passes of m x n instead of 8
+  static const bool q_jd = [] { const char* e = getenv("RLHC_Q_JD"); return e && atoi(e) != 0; }();
+  const bool jd = q_jd && rowsolve_ok(ni);
+  if (jd) {
+    CUDA_TRY(launch_rowsolve(Q, ldq, m, ni, a.D, a.Di, nullptr, ldq, nullptr, nullptr, a.part, a.G, st));
+    mk.mark(9);
+  } else if ((rc = solve_pass(Q, ldq, a.D, a.Di, nullptr, nullptr, a.G, false, 9))) {
+    return rc;
+  }
   mk.mark(10);
   CUDA_TRY(launch_chol(a.G, ni, a.J, a.work, RLHC_STAGE_CHOL2, status, st, ni <= 128 ? a.Ji : nullptr));
   if (ni > 128) CUDA_TRY(launch_rdiag(a.J, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
+  if (jd) {  // T = J D (S is free since Y = S U), 1/diag(T) over J's reciprocals
+    CUDA_TRY(launch_trmm_uu(a.J, a.D, ni, a.S, st));
+    CUDA_TRY(launch_rdiag(a.S, ni, n, a.Ji, RLHC_STAGE_SOLVE_J, status, st));
+  }
   mk.mark(11);
-  if ((rc = solve_pass(Q, ldq, a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
+  if ((rc = solve_pass(Q, ldq, jd ? a.S : a.J, a.Ji, nullptr, nullptr, nullptr))) return rc;
   mk.mark(12);
   // R = Z Y = J (D Y)
   CUDA_TRY(launch_trmm_uu(a.D, a.Y, ni, a.N, st));

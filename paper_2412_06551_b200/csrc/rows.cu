@@ -337,8 +337,8 @@ rowsolve_kernel(const double* A, int64_t lda, int64_t rows, int n, const double*
     }
     RS_TRACE(trc++)
     __syncthreads();
-    // ---- store the tile (16-byte stores)
-    {
+    // ---- store the tile (16-byte stores; out == nullptr: the Gram only)
+    if (out) {
       const int c2 = threadIdx.x % nc2, r0 = threadIdx.x / nc2, rstep = blockDim.x / nc2;
       const int c = 2 * c2;
       const bool ofull = c + 1 < n && ((ldo & 1) == 0) && ((((uintptr_t)out) & 15) == 0);
