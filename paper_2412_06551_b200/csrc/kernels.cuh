@@ -99,6 +99,9 @@ cudaError_t launch_trsm_rows(const double* A, int64_t lda, int64_t rows, int nco
 cudaError_t launch_rows_upper(const double* A, int64_t lda, int64_t rows, int n, const double* Tinv, double* out,
                               int64_t ldo, cudaStream_t st);
 size_t gram_partials_bytes(int64_t rows, int n);
+size_t syrk_partials_bytes(int n);
+cudaError_t launch_syrk(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st,
+                        bool* done);
 // fused persistent substitution (+ optional Gram of the output when G != nullptr), n <= 128
 bool rowsolve_ok(int n);
 size_t rowsolve_partials_bytes(int64_t rows, int n);

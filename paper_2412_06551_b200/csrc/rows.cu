@@ -757,7 +757,7 @@ static GramGeom gram_geom(int64_t rows, int n) {
 }
 size_t gram_partials_bytes(int64_t rows, int n) {
   GramGeom g = gram_geom(rows, n);
-  return (size_t)g.nsplit * g.ntiles * GT * GT * sizeof(double);
+  return std::max((size_t)g.nsplit * g.ntiles * GT * GT * sizeof(double), syrk_partials_bytes(n));
 }
 
 __global__ void __launch_bounds__(128, 3)
@@ -895,6 +895,9 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nsplit, 
 }
 
 cudaError_t launch_gram(const double* A, int64_t lda, int64_t rows, int n, double* part, double* G, cudaStream_t st) {
+  bool done = false;  // n <= 256, TMA-describable A: the fragment-balanced TMA kernel (syrk.cu)
+  if (cudaError_t e = launch_syrk(A, lda, rows, n, part, G, st, &done)) return e;
+  if (done) return cudaSuccess;
   GramGeom gg = gram_geom(rows, n);
   dim3 grid(gg.ntiles, gg.nsplit);
   constexpr int smem = 4 * GK * (GT + 4) * (int)sizeof(double);
