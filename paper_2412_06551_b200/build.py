@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librlhc.so")
-SOURCES = ["tslu.cu", "tslw.cu", "rows.cu", "sketch.cu", "small.cu", "factor.cu", "tsgemm.cu", "subst.cu", "syrk.cu", "dist_blocks.cu",
+SOURCES = ["tslu.cu", "tslw.cu", "rows.cu", "sketch.cu", "small.cu", "factor.cu", "tsgemm.cu", "subst.cu", "syrk.cu", "trmm.cu", "dist_blocks.cu",
            "dist_c.cu", "rlhc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

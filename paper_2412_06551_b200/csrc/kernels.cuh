@@ -157,6 +157,9 @@ cudaError_t launch_tri_inv(const double* T, int n, double* Tinv, cudaStream_t st
 // in increasing k); tri: B upper triangular, and Cout may then alias A (in-place triangular
 // product).  bpack: ts_gemm_pack_bytes(K, N) bytes of scratch for B's packed image.
 size_t ts_gemm_pack_bytes(int K, int N);
+size_t tri_pack_bytes(int n);
+cudaError_t launch_tri_tma(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int n, double* C,
+                           int64_t ldc, double* bpack, cudaStream_t st, bool* done);
 // launch_ts_gemm (tri = false, sub = true) that also reports a non-finite Cin element as
 // ENONFINITE(INPUT, row * n_index + col0_index + column) into status (nullable)
 cudaError_t launch_ts_gemm_checked(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,

@@ -360,7 +360,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // writing it, tiles are disjoint).  Cout may alias A only when tri and K == N (in-place
 // triangular product: the descending column blocks never read what they overwrote).
 size_t ts_gemm_pack_bytes(int K, int N) {
-  return (size_t)ceil_div(N, TG_N) * ceil_div(std::max(K, 1), TG_K) * TG_K * TG_BS * sizeof(double);
+  return std::max((size_t)ceil_div(N, TG_N) * ceil_div(std::max(K, 1), TG_K) * TG_K * TG_BS * sizeof(double),
+                  K == N ? tri_pack_bytes(N) : (size_t)0);
 }
 
 cudaError_t launch_ts_gemm_checked_impl(const double* Cin, int64_t ldci, double* Cout, int64_t ldco, const double* A,
@@ -387,6 +388,11 @@ cudaError_t launch_ts_gemm_checked_impl(const double* Cin, int64_t ldci, double*
                                         bool tri, bool sub, double* bpack, unsigned long long* status, int n_index,
                                         int col0, cudaStream_t st) {
   if (rows <= 0 || N <= 0) return cudaSuccess;
+  if (tri && !sub && !Cin && K == N) {  // the in-place CholeskyQR products: trmm.cu
+    bool done = false;
+    if (cudaError_t e = launch_tri_tma(A, lda, B, ldb, rows, N, Cout, ldco, bpack, st, &done)) return e;
+    if (done) return cudaSuccess;
+  }
   TgArgs p{bpack, ceil_div(std::max(K, 1), TG_K), Cin, ldci, Cout, ldco, A, lda, B, ldb, rows, K, N, 0, 0,
            status, n_index, col0};
   p.ncb = ceil_div(N, TG_N);
