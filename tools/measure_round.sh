@@ -1,6 +1,6 @@
 #!/bin/bash
 # One measurement session on a GPU box (round 2): bench lines, ncu launch lists with DRAM bytes
-# per stage, and one full ncu capture of the dominant kernel.  Everything lands in gpurun_out/.
+# per stage, and full ncu captures of the pass kernels.  Everything lands in gpurun_out/.
 O=gpurun_out
 set -x
 python bench.py > $O/m_bench_cfg5.json 2> $O/m_bench_cfg5.err
@@ -15,8 +15,12 @@ for c in cfg2 cfg3 cfg5; do
   python tools/launches.py $O/m_l_$c.csv > $O/m_l_$c.txt
   python tools/traffic.py $O/m_l_$c.csv $c $O/m_traffic.json > $O/m_traffic_$c.txt 2>&1
 done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:subst_wide -c 1 -s 1 \
-  -o $O/m_ncu_subst_wide python tools/prof_trmm.py subst 1048576 256 > $O/m_ncu_subst_wide.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:ts_gemm -c 1 -s 1 \
-  -o $O/m_ncu_ts_gemm python tools/prof_trmm.py inv 4194304 256 > $O/m_ncu_ts_gemm.log 2>&1
+for spec in "subst:subst_wide" "gram:syrk_tma" "inv:tri_tma"; do
+  what=${spec%%:*}; k=${spec##*:}
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -s 1 \
+    -o $O/m_ncu_$what python tools/time_pass.py $what 16777216 256 1 > $O/m_ncu_$what.log 2>&1
+  ncu -i $O/m_ncu_$what.ncu-rep --page details --csv > $O/m_ncu_${what}_details.csv 2>/dev/null
+  ncu -i $O/m_ncu_$what.ncu-rep --page raw --csv > $O/m_ncu_${what}_raw.csv 2>/dev/null
+done
+python tools/pcie_bw.py 16 > $O/m_pcie.txt 2>&1
 echo done

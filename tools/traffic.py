@@ -45,7 +45,7 @@ def split_stages(call, n):
     After HouseholderQR each CholeskyQR pass starts with a recognisable kernel: the W solve
     (subst_ms / subst_wide), tri_inv for V and Q when n > 64 (rowsolve when n <= 64; the
     blocked Cholesky of n > 128 also runs rowsolve / gemm_sub inside its stage), the Gram
-    (gram_kernel), the Cholesky (chol_*), the final trmm_uu."""
+    (gram_kernel or syrk_tma_kernel), the Cholesky (chol_*), the final trmm_uu."""
     out = []
     stage = "check_finite"
     post = False
@@ -67,7 +67,7 @@ def split_stages(call, n):
                 post = True
                 stage = "solve_w"
         else:
-            if b == "gram_kernel":
+            if b in ("gram_kernel", "syrk_tma_kernel"):
                 stage = {"solve_w": "gram1", "solve_v": "gram2"}.get(stage, stage)
             elif b.startswith("chol_"):
                 stage = {"solve_w": "chol1", "gram1": "chol1", "solve_v": "chol2", "gram2": "chol2"}.get(stage, stage)
