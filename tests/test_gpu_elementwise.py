@@ -58,7 +58,10 @@ def test_sketch_gauss_elementwise(rl, ora, rows, n, s, row0):
     assert _within(out, ref, bound)
 
 
-@pytest.mark.parametrize("rows,n", [(100000, 64), (3333, 130), (20000, 256), (20000, 512)])
+@pytest.mark.parametrize("rows,n", [(100000, 64), (3333, 130), (20000, 256), (20000, 512),
+                                    # syrk_tma_kernel (n <= 256): ragged row chunks, n not a
+                                    # multiple of 8 or 16, fewer rows than one chunk
+                                    (100003, 40), (70001, 200), (29, 8), (65537, 128), (1000, 250)])
 def test_gram_elementwise(rl, rows, n):
     """G = A^T A: |G_gpu - A^T A| <= 2 gamma_rows (|A|^T |A|) per entry; G exactly
     symmetric."""
@@ -71,7 +74,10 @@ def test_gram_elementwise(rl, rows, n):
     assert _within(G.cpu().numpy(), ref, bound)
 
 
-@pytest.mark.parametrize("rows,n", [(4000, 16), (7000, 64), (1500, 200), (2000, 512)])
+@pytest.mark.parametrize("rows,n", [(4000, 16), (7000, 64), (1500, 200), (2000, 512),
+                                    # tri_tma_kernel (64 < n <= 256, >= 8 row tiles per SM):
+                                    # ragged last tile, n off the fragment grid
+                                    (160001, 72), (300007, 128), (90001, 200)])
 def test_trsm_elementwise(rl, ora, rows, n):
     """out = A T^{-1} by substitution and by the explicit inverse (R#9).
     Substitution: each row of out is a forward substitution, so out (T + dT) = A with

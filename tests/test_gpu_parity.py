@@ -273,6 +273,34 @@ def test_trsm_subst_bitwise(m, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("rows,n", [(160001, 72), (90001, 200), (80000, 256)])
+def test_tri_product_in_place_and_strided(rows, n):
+    """The CholeskyQR products' in-place triangular product (tri_tma_kernel, R#9):
+    out = A T^-1 with out = A gives the same bits as out of place, and an odd leading dimension
+    (the ts_gemm_kernel fallback, same k order per element) gives the same bits too; both
+    within the product's error bound of the oracle's substitution."""
+    import oracle
+    import paper_2412_06551_b200 as rl
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(dev).manual_seed(rows)
+    A = torch.randn(rows, n, dtype=torch.float64, device=dev, generator=g)
+    Th = np.triu(np.random.default_rng(n).standard_normal((n, n))) + 4 * np.eye(n)
+    T = torch.from_numpy(Th).to(dev)
+    out, _, info = rl.trsm_apply(A, T, mode=rl.RLHC_INV_GEMM)
+    assert info == (0, 0, 0)
+    Ai = A.clone()
+    rl.trsm_apply(Ai, T, mode=rl.RLHC_INV_GEMM, out=Ai)
+    assert torch.equal(Ai, out)
+    big = torch.empty(rows, n + 1, dtype=torch.float64, device=dev)
+    big[:, :n] = A
+    As = big[:, :n]                                  # lda = n + 1: not TMA-describable
+    out2, _, _ = rl.trsm_apply(As, T, mode=rl.RLHC_INV_GEMM)
+    assert torch.equal(out2, out)
+    ref = oracle.trsm_right_upper(A[:2000].cpu().numpy(), Th)
+    assert rel_fro(out[:2000].cpu().numpy(), ref) < 1e-14
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [96, 136, 200])
 def test_trsm_subst_strides_and_in_place(n):
     """Both n > 64 substitution kernels -- the TMA-fed one (even leading dimensions, 16-byte
