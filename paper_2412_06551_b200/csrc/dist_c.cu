@@ -382,10 +382,13 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   DTRY(rlhc_trsm_apply(a.X, m, n, a.ldx, d.Y, RLHC_SUBST, a.Q, a.ldq, d.G, sc, scb, next_info(), st));
   DTRY(allreduce(d.G, (size_t)n * n));
   DTRY(rlhc_cholesky_ws(d.G, n, d.D, RLHC_STAGE_CHOL1, sc, scb, next_info(), st));
-  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.D, RLHC_SUBST, a.Q, a.ldq, d.G, sc, scb, next_info(), st));
+  // the CholeskyQR passes as on one GPU (run_algo): n > 64 the explicit inverse and the in-place
+  // triangular product (R#9: kappa(D), kappa(J) <= ~7)
+  const int cq_mode = n > 64 ? RLHC_INV_GEMM : RLHC_SUBST;
+  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.D, cq_mode, a.Q, a.ldq, d.G, sc, scb, next_info(), st));
   DTRY(allreduce(d.G, (size_t)n * n));
   DTRY(rlhc_cholesky_ws(d.G, n, d.J, RLHC_STAGE_CHOL2, sc, scb, next_info(), st));
-  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.J, RLHC_SUBST, a.Q, a.ldq, nullptr, sc, scb, next_info(), st));
+  DTRY(rlhc_trsm_apply(a.Q, m, n, a.ldq, d.J, cq_mode, a.Q, a.ldq, nullptr, sc, scb, next_info(), st));
   DTRY(rlhc_trmm_upper(d.D, d.Y, n, d.N, st));
   DTRY(rlhc_trmm_upper(d.J, d.N, n, a.R, st));
   note_launch();

@@ -27,7 +27,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from ._lib import RLHC_SUBST, STAGE_CHOL1, STAGE_CHOL2, Info, TsluCfg, check, lib
+from ._lib import RLHC_INV_GEMM, RLHC_SUBST, STAGE_CHOL1, STAGE_CHOL2, Info, TsluCfg, check, lib
 
 
 def kernel_width(panel: int) -> int:
@@ -165,14 +165,17 @@ class CudaBackend:
         check(self.L.rlhc_trmm_upper(_p(A), _p(B), n, _p(C), self._st()))
         return C
 
-    def solve(self, A, T, out, gram: bool):
+    def solve(self, A, T, out, gram: bool, cholqr: bool = False):
+        """out = A T^-1 (+ G = out^T out): W by the oracle-order substitution; the CholeskyQR
+        passes (cholqr) as on one GPU -- n > 64 the explicit inverse and the triangular product."""
         rows, n = A.shape
         G = torch.zeros(n, n, dtype=torch.float64, device=self.dev) if gram else None
         info = self._info()
         if rows == 0:
             return G, info
         ws = self._ws(self.L.rlhc_trsm_apply_workspace_size(rows, n))
-        check(self.L.rlhc_trsm_apply(_p(A), rows, n, A.stride(0), _p(T), RLHC_SUBST, _p(out), out.stride(0), _p(G),
+        mode = RLHC_INV_GEMM if cholqr and n > 64 else RLHC_SUBST
+        check(self.L.rlhc_trsm_apply(_p(A), rows, n, A.stride(0), _p(T), mode, _p(out), out.stride(0), _p(G),
                                      _p(ws), ws.numel(), _p(info), self._st()))
         return G, info
 
@@ -304,11 +307,11 @@ class DistPlan:
         infos.append(info)
         D, info = B.cholesky(self._allreduce(G1), STAGE_CHOL1)
         infos.append(info)
-        G2, info = B.solve(Q, D, Q, gram=True)
+        G2, info = B.solve(Q, D, Q, gram=True, cholqr=True)
         infos.append(info)
         J, info = B.cholesky(self._allreduce(G2), STAGE_CHOL2)
         infos.append(info)
-        _, info = B.solve(Q, J, Q, gram=False)
+        _, info = B.solve(Q, J, Q, gram=False, cholqr=True)
         infos.append(info)
         R = B.trmm(J, B.trmm(D, Y))
         return Q, R, piv, infos

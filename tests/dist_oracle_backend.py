@@ -145,7 +145,7 @@ class OracleBackend:
     def trmm(self, A, B):
         return torch.from_numpy(oracle.trmm_uu(A.numpy(), B.numpy()))
 
-    def solve(self, A, T, out, gram):
+    def solve(self, A, T, out, gram, cholqr=False):
         res = oracle.trsm_right_upper(A.numpy(), T.numpy())
         out.copy_(torch.from_numpy(res))
         G = torch.from_numpy(oracle.gram(res)) if gram else None
