@@ -80,10 +80,17 @@ cudaError_t launch_tslw_finish(double* Lb, int64_t ldl, int64_t rows, int64_t ro
 // exact GEPP mode (one leaf of all rows): workspace of the panel's working copy
 size_t tslg_ws_bytes(int64_t rows);
 // gepp_ws != null: exact GEPP (one leaf holding every row) instead of the tournament
+// called by run_tslw right after each panel's Schur-complement launch (before its tournament):
+// lets the caller put independent work on a side stream into the tournament's idle SMs
+struct TslwPanelHook {
+  cudaError_t (*after_schur)(void* ctx, int panel, int npanels, cudaStream_t st);
+  void* ctx;
+};
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
                      int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
-                     cudaStream_t st, void* gepp_ws = nullptr, double* bpack = nullptr);
+                     cudaStream_t st, void* gepp_ws = nullptr, double* bpack = nullptr,
+                     const TslwPanelHook* hook = nullptr);
 
 // rows.cu
 cudaError_t launch_check_finite(const double* X, int64_t rows, int n, int64_t ldx, unsigned long long* status,
@@ -132,6 +139,9 @@ cudaError_t launch_sketch_gauss(const double* A, int64_t lda, int64_t rows, int 
 // Omega stored (s x cols, ld omega_ld(cols)) for the OMEM sketch; generated off the critical path
 int64_t omega_ld(int64_t cols);
 size_t omega_bytes(int64_t s, int64_t cols);
+// columns [c0, c0 + ncols) of the s x m Omega (stream 0, global row ids) into Om (ld omega_ld(m))
+cudaError_t launch_omega_gen_cols(uint64_t seed, int s, int64_t m, int64_t c0, int64_t ncols, double* Om,
+                                  cudaStream_t st);
 cudaError_t launch_omega_gen(uint64_t seed, uint32_t stream_id, int s, int64_t cols, int64_t row0, double* Om,
                              cudaStream_t st);
 size_t cs_plan_bytes(int64_t rows, int s1);

@@ -135,10 +135,10 @@ void carve_tslu(Carver& c, int64_t rows, int64_t n, const rlhc_tslu_cfg& cfg, Ts
 // panels lives in `tw` (rows x n, ldt).  Returns RLHC_OK or RLHC_ECUDA.
 int run_tslu(const double* X, int64_t rows, int64_t n, int64_t ldx, int64_t row0, const rlhc_tslu_cfg& cfg,
              TsluWs& t, double* tw, int64_t ldtw, int64_t* piv, double* U, double* L11, cudaStream_t st,
-             bool check_input = false) {
+             bool check_input = false, const TslwPanelHook* hook = nullptr) {
   if (tslw_cfg(cfg, rows, n)) {  // warp tournament (or exact GEPP); L (original row order) lands in tw
     CUDA_TRY(run_tslw(X, ldx, rows, row0, (int)n, cfg.arity, tw, ldtw, piv, U, L11, t.rd, t.lw, t.chosen, t.ids,
-                      t.cnt, t.vals, t.status, check_input, st, t.gepp, t.bpack));
+                      t.cnt, t.vals, t.status, check_input, st, t.gepp, t.bpack, hook));
     return RLHC_OK;
   }
   const int W = kernel_width(cfg.panel);
@@ -202,12 +202,24 @@ constexpr size_t kOmegaStoreMax = size_t(4) << 30;
 // every 256-column tile; below that the side-stream generator costs the TSLU more than it
 // saves the sketch (cfg2: TSLU +45 us, sketch -35 us).  RLHC_OMEGA_STORE=0/1 overrides
 // (measurement knob).
-static size_t omega_store_bytes(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2) {
+// SLHC3 with 16 < n <= 256 under the warp-tournament contract generates Omega in one chunk per
+// panel on a low-priority side stream, each chunk released when its panel's Schur kernel is
+// done, so that it runs in the SMs the panel's tournament leaves idle (RLHC_OMEGA_CHUNKS=0:
+// the in-kernel generator instead).
+static bool omega_chunked(int algo, int64_t m, int64_t n, const rlhc_tslu_cfg& cfg) {
+  static const int on = [] {
+    const char* e = getenv("RLHC_OMEGA_CHUNKS");
+    return e ? atoi(e) : 1;
+  }();
+  return on && algo == RLHC_SLHC3 && n > 16 && n <= 256 && tslw_cfg(cfg, m, n);  // >= 2 panels
+}
+static size_t omega_store_bytes(int algo, int64_t m, int64_t n, int64_t s_or_s1, int64_t s2,
+                                const rlhc_tslu_cfg& cfg) {
   static const int force = [] {
     const char* e = getenv("RLHC_OMEGA_STORE");
     return e ? atoi(e) : -1;
   }();
-  const bool want = force >= 0 ? force != 0 : (algo == RLHC_SSLHC3 || n > 256);
+  const bool want = force >= 0 ? force != 0 : (algo == RLHC_SSLHC3 || n > 256 || omega_chunked(algo, m, n, cfg));
   const size_t b = algo == RLHC_SLHC3 ? omega_bytes(s_or_s1, m) : omega_bytes(s2, s_or_s1);
   return want && b <= kOmegaStoreMax ? b : 0;
 }
@@ -225,7 +237,11 @@ static cudaError_t side_stream(SideStream** out) {
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   SideStream& ss = per_dev[dev];
   if (!ss.s) {
-    if ((e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking))) return e;
+    // lowest priority: its work is off the critical path, pending CTAs of the main stream
+    // are scheduled first
+    int least = 0, greatest = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&least, &greatest))) return e;
+    if ((e = cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, least))) return e;
     if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming))) return e;
   }
@@ -265,7 +281,7 @@ void carve_algo(Carver& c, int algo, int64_t m, int64_t n, int64_t s_or_s1, int6
   size_t work = std::max(hqr_ws_bytes((int)srows, (int)n), chol_ws_bytes((int)n));
   a.work = c.take<double>(work / sizeof(double) + 1);
   a.plan = algo == RLHC_SSLHC3 ? (void*)c.take<char>(cs_plan_bytes(m, (int)s_or_s1)) : nullptr;
-  const size_t ob = omega_store_bytes(algo, m, n, s_or_s1, s2);
+  const size_t ob = omega_store_bytes(algo, m, n, s_or_s1, s2, cfg);
   a.Om = ob ? c.take<double>(ob / sizeof(double)) : nullptr;
 }
 
@@ -279,7 +295,29 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   CUDA_TRY(launch_status_init(status, st));
   // side stream: Omega (SLHC3: s x m; SSLHC3: s2 x s1) and the CountSketch plan
   SideJoin side;
-  if (a.Om) {
+  const bool chunked = a.Om && omega_chunked(algo, m, n, cfg);
+  struct OmegaChunks {
+    SideStream* ss;
+    uint64_t seed;
+    int s;
+    int64_t m;
+    double* Om;
+  } oc{nullptr, seed, (int)s_or_s1, m, a.Om};
+  TslwPanelHook hook{[](void* ctx, int panel, int npanels, cudaStream_t st0) -> cudaError_t {
+                       OmegaChunks& o = *static_cast<OmegaChunks*>(ctx);
+                       const int64_t c0 = o.m * panel / npanels, c1 = o.m * (panel + 1) / npanels;
+                       cudaError_t e = cudaEventRecord(o.ss->fork, st0);
+                       if (!e) e = cudaStreamWaitEvent(o.ss->s, o.ss->fork, 0);
+                       if (!e) e = launch_omega_gen_cols(o.seed, o.s, o.m, c0, c1 - c0, o.Om, o.ss->s);
+                       if (!e) e = cudaEventRecord(o.ss->join, o.ss->s);
+                       return e;
+                     },
+                     &oc};
+  if (chunked) {
+    CUDA_TRY(side_stream(&oc.ss));
+    side.st = st;
+    side.ss = oc.ss;
+  } else if (a.Om) {
     SideStream* ss = nullptr;
     CUDA_TRY(side_stream(&ss));
     CUDA_TRY(cudaEventRecord(ss->fork, st));
@@ -299,7 +337,7 @@ int run_algo(int algo, const double* X, int64_t m, int64_t n, int64_t ldx, int64
   if (!fold_check) CUDA_TRY(launch_check_finite(X, m, ni, ldx, status, st));
   mk.mark(1);
   // PX = LU (P:279 / P:293); the Q buffer holds the trailing matrix of later panels
-  int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st, fold_check);
+  int rc = run_tslu(X, m, n, ldx, 0, cfg, a.t, Q, ldq, piv, a.U, a.L11, st, fold_check, chunked ? &hook : nullptr);
   if (rc) return rc;
   const bool l_done = tslw_cfg(cfg, m, n);  // the warp tournament leaves L in the Q buffer
   if (!l_done) {

@@ -246,6 +246,21 @@ cudaError_t launch_omega_gen(uint64_t seed, uint32_t stream_id, int s, int64_t c
   return cudaGetLastError();
 }
 
+cudaError_t launch_omega_gen_cols(uint64_t seed, int s, int64_t m, int64_t c0, int64_t ncols, double* Om,
+                                  cudaStream_t st) {
+  const int64_t total = (int64_t)((s + 1) / 2) * ncols;
+  if (total <= 0) return cudaSuccess;
+  // few CTAs per SM: the chunk shares the SMs with a latency-bound tournament, whose select
+  // warps need the issue slots (RLHC_OMEGA_CHUNK_CTAS, measurement knob)
+  static const int per_sm = [] {
+    const char* e = getenv("RLHC_OMEGA_CHUNK_CTAS");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), (int64_t)per_sm * kSMs);
+  note_launch(); omega_gen_kernel<<<grid, 256, 0, st>>>(seed, 0u, s, ncols, c0, Om + c0, omega_ld(m));
+  return cudaGetLastError();
+}
+
 template <int NTW, bool OMEM>
 static void gauss_launch(dim3 grid, const double* A, int64_t lda, int64_t rows, int n, int64_t row0, int s,
                          uint64_t seed, uint32_t stream_id, int64_t rps, double* part, const double* Om,

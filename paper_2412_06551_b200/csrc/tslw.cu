@@ -1435,7 +1435,7 @@ static cudaError_t look_ahead_streams(LookAhead** out) {
 cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, int n, int arity, double* Lb,
                      int64_t ldl, int64_t* piv, double* U, double* L11, double* rd, double* lw, uint8_t* chosen,
                      int* ids[2], int* cnt[2], double* vals[2], unsigned long long* status, bool check_input,
-                     cudaStream_t st, void* gepp_ws, double* bpack) {
+                     cudaStream_t st, void* gepp_ws, double* bpack, const TslwPanelHook* hook) {
   (void)lw;
   static const bool group_on = [] { const char* e = getenv("RLHC_LU_GROUP"); return e && atoi(e) != 0; }();
   const bool grouped = group_on && bpack && !gepp_ws;
@@ -1507,6 +1507,9 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
              : launch_pdl(tslw_schur0_kernel, dim3((unsigned)ceil_div<int64_t>(rows, SR)), dim3(SR), 0, st, X, ldx,
                           Lb, ldl, rows, w, n, check_input ? status : nullptr);
       if (e) return e;
+    }
+    if (hook) {
+      if ((e = hook->after_schur(hook->ctx, p0 / WW, ceil_div(n, WW), st))) return e;
     }
     if (look && p0 + WW < n && p0 + WW >= 2 * WW) {
       // look-ahead: the next panel's bulk X[:, q] - L[:, :p0] U[:p0, q] (every term but the
