@@ -345,11 +345,12 @@ class BenchRunner:
 
 
 def setup_bench(cfg, rank: int, world: int, device, strong: bool = True, use_c: bool = True, contract=None):
-    """bench.py's N-GPU workload.  Weak scaling (default): every rank holds cfg.m rows and the
-    job factors a (world * cfg.m) x n X under the single-GPU default contract (rank subtrees
-    of 4^k leaves are complete subtrees of the global arity-4 tree, so the pivots equal a
-    single-GPU run on the whole X).  Strong scaling: the job factors cfg's m x n X, each rank
-    holds m / world rows; arity 2 so that 1/2/4/8 ranks share one tournament."""
+    """bench.py's N-GPU workload.  Strong scaling (bench.py's default at N > 1): the job factors
+    cfg's m x n X, each rank holds m / world rows.  Weak scaling (--weak): every rank holds cfg.m
+    rows of a (world * cfg.m) x n X.  Either way the contract is the single-GPU default
+    (dist_default_cfg: 128-row leaves, 8-ary nodes, 16-column panels): a rank's equal shard of
+    whole leaves is a union of complete subtrees of the global tournament tree,
+    so the pivots equal a single-GPU run on the whole X."""
     import synth
     m_global = cfg.m if strong else cfg.m * world
     m_local = m_global // world
