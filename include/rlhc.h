@@ -233,6 +233,19 @@ int rlhc_tslu_eliminate(const double* src, int64_t lds, int64_t rows, int64_t p0
  * All asynchronous on `stream`; EINVAL for bad sizes. */
 int rlhc_tslw_schur(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl, int64_t p0,
                     const double* U, rlhc_stream_t stream);
+/* rlhc_tslw_schur_reduce_to: rlhc_tslw_schur followed by rlhc_tslu_reduce_to(L, ...) on the
+ *   panel just formed, fused as in the single-process pipeline: the leaves (128 of this rank's
+ *   rows each, tournament of R#3) are selected inside the Schur kernel while it
+ *   streams, then one launch runs this rank's levels >= 1 up to nslots_out complete subtrees
+ *   (1: the rank's root).  Same outputs, bits and workspace (rlhc_tslu_local_workspace_size)
+ *   as the two calls; falls back to them when X or L cannot be described to the TMA unit.
+ *   chosen: this rank's rows already pivots (NULL at p0 = 0).  EINVAL unless the contract is
+ *   the warp one (leaf_rows 128, panel 16, arity 2..8) and the leaves split into nslots_out
+ *   complete subtrees; EWORKSPACE for a short workspace. */
+int rlhc_tslw_schur_reduce_to(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl,
+                              int64_t row0, int64_t p0, const double* U, const uint8_t* chosen,
+                              const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids, int* out_cnt,
+                              double* out_vals, void* ws, size_t ws_bytes, rlhc_stream_t stream);
 int rlhc_tslw_owned_rows(const double* X, int64_t ldx, const double* L, int64_t ldl, int64_t rows, int64_t row0,
                          const int* ids, int64_t cnt, int64_t p0, int64_t n, const double* U, double* T,
                          rlhc_stream_t stream);

@@ -56,6 +56,7 @@ def lib():
                                ctypes.c_int)
     PC = ctypes.POINTER(TsluCfg)
     L.rlhc_tslw_schur.argtypes = [P, I64, I64, I64, P, I64, I64, P, P]
+    L.rlhc_tslw_schur_reduce_to.argtypes = [P, I64, I64, I64, P, I64, I64, I64, P, P, PC, I64, P, P, P, P, SZ, P]
     L.rlhc_tslw_owned_rows.argtypes = [P, I64, P, I64, I64, I64, P, I64, I64, I64, P, P, P]
     L.rlhc_tslw_finish.argtypes = [P, I64, I64, I64, I64, P, P, P]
     L.rlhc_host_pipeline_workspace_size.argtypes = [I, I64, I64, I64, I64, PC]
@@ -169,7 +170,7 @@ EXPORTED = ["rlhc_default_tslu_cfg", "rlhc_workspace_size", "rlhc_slhc3", "rlhc_
             "rlhc_comm_destroy", "rlhc_dist_workspace_size", "rlhc_slhc3_dist", "rlhc_sslhc3_dist",
             "rlhc_method_workspace_size", "rlhc_cholqr2", "rlhc_scholqr3", "rlhc_luc2", "rlhc_rhc",
             "rlhc_graph_begin", "rlhc_graph_end", "rlhc_graph_launch", "rlhc_graph_destroy",
-            "rlhc_tslw_schur", "rlhc_tslw_owned_rows", "rlhc_tslw_finish",
+            "rlhc_tslw_schur", "rlhc_tslw_schur_reduce_to", "rlhc_tslw_owned_rows", "rlhc_tslw_finish",
             "rlhc_host_pipeline_workspace_size", "rlhc_host_pipeline"]
 NUM_TIMED_STAGES = 13
 

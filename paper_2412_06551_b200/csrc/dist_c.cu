@@ -326,9 +326,8 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   const bool warp = a.cfg.leaf_rows == 128 && a.cfg.arity >= 2 && a.cfg.arity <= 8 && a.cfg.panel == 16 && n > 16;
   for (int64_t p0 = 0; warp && p0 < n; p0 += a.cfg.panel) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
-    DTRY(rlhc_tslw_schur(a.X, m, n, a.ldx, a.Q, a.ldq, p0, d.U, st));
-    DTRY(rlhc_tslu_reduce_to(a.Q, a.ldq, m, a.row0, p0, w, p0 > 0 ? d.chosen : nullptr, &a.cfg, nr > 1 ? K : 1,
-                             d.slot_ids, d.slot_cnt, d.slot_vals, sc, scb, st));
+    DTRY(rlhc_tslw_schur_reduce_to(a.X, m, n, a.ldx, a.Q, a.ldq, a.row0, p0, d.U, p0 > 0 ? d.chosen : nullptr,
+                                   &a.cfg, nr > 1 ? K : 1, d.slot_ids, d.slot_cnt, d.slot_vals, sc, scb, st));
     const int* root = d.slot_ids;
     if (nr > 1) {
       DTRY(gather_slots(w));

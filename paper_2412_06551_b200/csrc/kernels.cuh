@@ -68,6 +68,10 @@ size_t tslw_slots(int64_t rows);
 cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, int64_t row0, int p0, int w,
                                 const uint8_t* chosen, int arity, int stop_lev, int* ids[2], int* cnt[2],
                                 double* vals[2], int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st);
+cudaError_t run_tslw_schur_local_tree(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows,
+                                      int64_t row0, int p0, int w, int n, const double* U, const uint8_t* chosen,
+                                      int arity, int stop_lev, int* ids[2], int* cnt[2], double* vals[2],
+                                      int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st, bool* fused);
 // row-sharded left-looking TSLU blocks (the warp contract): a panel's Schur complement of
 // this rank's rows (U's reciprocals from its diagonal), the winners' current rows this rank
 // owns (0 for the others), and the last panel's L plus the local pivot rows' L11 rows

@@ -1401,6 +1401,51 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
   return cudaMemcpyAsync(out_vals, tval, (size_t)nout * WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
+// The row-sharded path's fused panel: this rank's Schur complement of panel p0 with its leaves
+// selected inside the TMA Schur kernel (as run_tslw does), then the rank's tournament levels
+// >= 1 up to stop_lev (-1: its root) in one launch, the top level's slots copied to out_*.
+// *fused = false: the TMA kernel is not available for these buffers and nothing was launched.
+cudaError_t run_tslw_schur_local_tree(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows,
+                                      int64_t row0, int p0, int w, int n, const double* U, const uint8_t* chosen,
+                                      int arity, int stop_lev, int* ids[2], int* cnt[2], double* vals[2],
+                                      int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st, bool* fused) {
+  *fused = false;
+  bool done = false, leaves_done = false;
+  cudaError_t e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, nullptr, nullptr, chosen, ids[0], cnt[0],
+                                   vals[0], row0, st, &done, &leaves_done);
+  if (e || !done) return e;
+  *fused = true;
+  if (!leaves_done)  // (one leaf, or no room for the select warps' buffers): the plain local tree
+    return run_tslw_local_tree(Lb, ldl, rows, row0, p0, w, chosen, arity, stop_lev, ids, cnt, vals, out_ids,
+                               out_cnt, out_vals, st);
+  const int nleaves = (int)tslw_slots(rows);
+  size_t above = 0, top = 0;
+  int lev = 0, nout = nleaves;
+  for (int ns = nleaves; ns > 1 && lev != stop_lev; ns = ceil_div(ns, arity)) {
+    top = above;
+    above += ceil_div(ns, arity);
+    lev++;
+    nout = ceil_div(ns, arity);
+  }
+  if (lev > 0) {
+    int* arrive = cnt[1] + above;
+    if ((e = cudaMemsetAsync(arrive, 0, above * sizeof(int), st))) return e;
+    static DevFlags attr;
+    if ((e = smem_attr(attr, tslw_tree_kernel, 227 * 1024))) return e;
+    note_launch();
+    e = launch_pdl(tslw_tree_kernel, dim3(ceil_div(ceil_div(nleaves, arity), WPB)), dim3(32 * WPB),
+                   WPB * sizeof(WSel), st, (const double*)Lb, ldl, rows, row0, p0, w, chosen, ids[0], cnt[0], ids[1],
+                   cnt[1], vals[0], vals[1], arrive, arity, stop_lev, TslwRoot{}, 1);
+    if (e) return e;
+  }
+  const int* tid = lev == 0 ? ids[0] : ids[1] + top * WW;
+  const int* tcnt = lev == 0 ? cnt[0] : cnt[1] + top;
+  const double* tval = lev == 0 ? vals[0] : vals[1] + top * WW * WW;
+  if ((e = cudaMemcpyAsync(out_ids, tid, (size_t)nout * WW * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(out_cnt, tcnt, (size_t)nout * sizeof(int), cudaMemcpyDeviceToDevice, st))) return e;
+  return cudaMemcpyAsync(out_vals, tval, (size_t)nout * WW * WW * sizeof(double), cudaMemcpyDeviceToDevice, st);
+}
+
 // per host thread and device: the look-ahead's side stream and its fork / join events
 struct LookAhead {
   cudaStream_t side = nullptr;
@@ -1571,6 +1616,12 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
 // ------------------------------------------------------------------ row-sharded TSLU blocks
 cudaError_t launch_tslw_schur(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
                               const double* U, cudaStream_t st) {
+  if (p0 > 0) {  // the TMA pipeline (same chain per element, so the same bits), leaves not fused
+    bool done = false, leaves_done = false;
+    cudaError_t e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                     nullptr, 0, st, &done, &leaves_done);
+    if (e || done) return e;
+  }
   static DevFlags attr;
   if (cudaError_t e = smem_attr(attr, tslw_schur_dmma_kernel, (int)sizeof(SchurDSmem))) return e;
   note_launch();
