@@ -156,27 +156,9 @@ int rlhc_tslw_schur_reduce_to(const double* X, int64_t rows, int64_t n, int64_t 
                               int64_t row0, int64_t p0, const double* U, const uint8_t* chosen,
                               const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids, int* out_cnt,
                               double* out_vals, void* ws, size_t ws_bytes, rlhc_stream_t stream) {
-  if (!X || !L || !U || !out_ids || !out_cnt || !out_vals || !ws || rows < 1 || n < 1 || ldx < n || ldl < n ||
-      p0 < 0 || p0 >= n || p0 % 16)
-    return fail(RLHC_EINVAL, "bad arguments");
-  const int64_t w = std::min<int64_t>(16, n - p0);
-  if (!cfg_valid(cfg, w) || cfg->leaf_rows != 128 || cfg->panel != 16 || cfg->arity < 2 || cfg->arity > 8)
-    return fail(RLHC_EINVAL, "bad tslu configuration (the warp contract: 128-row leaves, 16-column panels)");
-  if (ws_bytes < rlhc_tslu_local_workspace_size(rows, 0, cfg)) return fail(RLHC_EWORKSPACE, "workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
-  const int lev = nslots_out == 1 ? -1 : levels_to(nleaves, nslots_out, cfg->arity);
-  if (nslots_out != 1 && lev < 0)
-    return fail(RLHC_EINVAL, "the rank's leaves do not split into nslots_out complete subtrees");
-  LevelBufs b = carve_levels(ws, nleaves, kw(cfg->panel));
-  bool fused = false;
-  TRY(run_tslw_schur_local_tree(X, ldx, L, ldl, rows, row0, (int)p0, (int)w, (int)n, U, chosen, cfg->arity, lev,
-                                b.ids, b.cnt, b.vals, out_ids, out_cnt, out_vals, st, &fused));
-  if (fused) return RLHC_OK;
-  int rc = rlhc_tslw_schur(X, rows, n, ldx, L, ldl, p0, U, stream);
-  if (rc) return rc;
-  return rlhc_tslu_reduce_to(L, ldl, rows, row0, p0, w, chosen, cfg, nslots_out, out_ids, out_cnt, out_vals, ws,
-                             ws_bytes, stream);
+  bool checked = false;
+  return tslw_schur_reduce_to_impl(X, rows, n, ldx, L, ldl, row0, p0, U, chosen, cfg, nslots_out, out_ids, out_cnt,
+                                   out_vals, nullptr, &checked, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int rlhc_tslu_reduce(const double* src, int64_t lds, int64_t rows, int64_t row0, int64_t p0, int64_t w,
@@ -347,3 +329,36 @@ int rlhc_cholesky_ws(const double* G, int64_t n, double* Rout, int stage, void* 
 
 
 }  // extern "C"
+
+namespace rlhc {
+int tslw_schur_reduce_to_impl(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl,
+                              int64_t row0, int64_t p0, const double* U, const uint8_t* chosen,
+                              const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids, int* out_cnt,
+                              double* out_vals, unsigned long long* status, bool* checked, void* ws, size_t ws_bytes,
+                              cudaStream_t st) {
+  *checked = false;
+  if (!X || !L || !U || !out_ids || !out_cnt || !out_vals || !ws || rows < 1 || n < 1 || ldx < n || ldl < n ||
+      p0 < 0 || p0 >= n || p0 % 16)
+    return fail(RLHC_EINVAL, "bad arguments");
+  const int64_t w = std::min<int64_t>(16, n - p0);
+  if (!cfg_valid(cfg, w) || cfg->leaf_rows != 128 || cfg->panel != 16 || cfg->arity < 2 || cfg->arity > 8)
+    return fail(RLHC_EINVAL, "bad tslu configuration (the warp contract: 128-row leaves, 16-column panels)");
+  if (ws_bytes < rlhc_tslu_local_workspace_size(rows, 0, cfg)) return fail(RLHC_EWORKSPACE, "workspace too small");
+  const int nleaves = (int)ceil_div<int64_t>(rows, cfg->leaf_rows);
+  const int lev = nslots_out == 1 ? -1 : levels_to(nleaves, nslots_out, cfg->arity);
+  if (nslots_out != 1 && lev < 0)
+    return fail(RLHC_EINVAL, "the rank's leaves do not split into nslots_out complete subtrees");
+  LevelBufs b = carve_levels(ws, nleaves, kw(cfg->panel));
+  bool fused = false;
+  TRY(run_tslw_schur_local_tree(X, ldx, L, ldl, rows, row0, (int)p0, (int)w, (int)n, U, chosen, cfg->arity, lev,
+                                b.ids, b.cnt, b.vals, out_ids, out_cnt, out_vals, status, st, &fused));
+  if (fused) {
+    *checked = status != nullptr;
+    return RLHC_OK;
+  }
+  int rc = rlhc_tslw_schur(X, rows, n, ldx, L, ldl, p0, U, st);
+  if (rc) return rc;
+  return rlhc_tslu_reduce_to(L, ldl, rows, row0, p0, w, chosen, cfg, nslots_out, out_ids, out_cnt, out_vals, ws,
+                             ws_bytes, st);
+}
+}  // namespace rlhc

@@ -314,10 +314,11 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   };
   if (cudaMemsetAsync(d.U, 0, (size_t)n * n * sizeof(double), st)) return fail(RLHC_ECUDA, "memset");
   if (cudaMemsetAsync(d.chosen, 0, (size_t)m, st)) return fail(RLHC_ECUDA, "memset");
-  // finiteness of this rank's rows (stage INPUT), first in pipeline order
-  if (launch_status_init(d.status, st) || launch_check_finite(a.X, m, (int)n, a.ldx, d.status, st) ||
-      launch_status_finish(d.status, next_info(), st))
-    return fail(RLHC_ECUDA, "launch failed");
+  // finiteness of this rank's rows (stage INPUT), first in pipeline order: folded into the
+  // warp contract's Schur kernels (each reads its panel's X columns), else a pass of its own
+  rlhc_info_t* input_info = next_info();
+  if (launch_status_init(d.status, st)) return fail(RLHC_ECUDA, "launch failed");
+  bool all_checked = true;
   // ---------------- PX = LU (P:279 / P:293), tournament over panels
   // the warp contract (leaf 128, 16-column panels): left-looking panels with the single-process
   // pipeline's arithmetic -- this rank's Schur complement of the panel into Q, the local
@@ -326,8 +327,11 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
   const bool warp = a.cfg.leaf_rows == 128 && a.cfg.arity >= 2 && a.cfg.arity <= 8 && a.cfg.panel == 16 && n > 16;
   for (int64_t p0 = 0; warp && p0 < n; p0 += a.cfg.panel) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
-    DTRY(rlhc_tslw_schur_reduce_to(a.X, m, n, a.ldx, a.Q, a.ldq, a.row0, p0, d.U, p0 > 0 ? d.chosen : nullptr,
-                                   &a.cfg, nr > 1 ? K : 1, d.slot_ids, d.slot_cnt, d.slot_vals, sc, scb, st));
+    bool checked = false;
+    DTRY(tslw_schur_reduce_to_impl(a.X, m, n, a.ldx, a.Q, a.ldq, a.row0, p0, d.U, p0 > 0 ? d.chosen : nullptr,
+                                   &a.cfg, nr > 1 ? K : 1, d.slot_ids, d.slot_cnt, d.slot_vals, d.status, &checked,
+                                   sc, scb, st));
+    all_checked = all_checked && checked;
     const int* root = d.slot_ids;
     if (nr > 1) {
       DTRY(gather_slots(w));
@@ -339,6 +343,10 @@ static int run_dist(const DistArgs& a, rlhc_comm_t comm, cudaStream_t st) {
                                      st));
   }
   if (warp) DTRY(rlhc_tslw_finish(a.Q, a.ldq, m, a.row0, n, d.U, a.piv, st));
+  if (!warp || !all_checked) {
+    if (launch_check_finite(a.X, m, (int)n, a.ldx, d.status, st)) return fail(RLHC_ECUDA, "launch failed");
+  }
+  if (launch_status_finish(d.status, input_info, st)) return fail(RLHC_ECUDA, "launch failed");
   for (int64_t p0 = 0; !warp && p0 < n; p0 += a.cfg.panel) {
     const int64_t w = std::min<int64_t>(a.cfg.panel, n - p0);
     const double* src = p0 == 0 ? a.X : a.Q;

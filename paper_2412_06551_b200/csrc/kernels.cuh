@@ -71,7 +71,15 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
 cudaError_t run_tslw_schur_local_tree(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows,
                                       int64_t row0, int p0, int w, int n, const double* U, const uint8_t* chosen,
                                       int arity, int stop_lev, int* ids[2], int* cnt[2], double* vals[2],
-                                      int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st, bool* fused);
+                                      int* out_ids, int* out_cnt, double* out_vals, unsigned long long* status,
+                                      cudaStream_t st, bool* fused);
+// rlhc_tslw_schur_reduce_to with the input check folded in (status, nullable); *checked: the
+// panel's X columns were checked (false on the fallback path)
+int tslw_schur_reduce_to_impl(const double* X, int64_t rows, int64_t n, int64_t ldx, double* L, int64_t ldl,
+                              int64_t row0, int64_t p0, const double* U, const uint8_t* chosen,
+                              const rlhc_tslu_cfg* cfg, int64_t nslots_out, int* out_ids, int* out_cnt,
+                              double* out_vals, unsigned long long* status, bool* checked, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
 // row-sharded left-looking TSLU blocks (the warp contract): a panel's Schur complement of
 // this rank's rows (U's reciprocals from its diagonal), the winners' current rows this rank
 // owns (0 for the others), and the last panel's L plus the local pivot rows' L11 rows

@@ -1405,13 +1405,16 @@ cudaError_t run_tslw_local_tree(const double* src, int64_t lds, int64_t rows, in
 // selected inside the TMA Schur kernel (as run_tslw does), then the rank's tournament levels
 // >= 1 up to stop_lev (-1: its root) in one launch, the top level's slots copied to out_*.
 // *fused = false: the TMA kernel is not available for these buffers and nothing was launched.
+// status (nullable): non-finite elements of X's panel columns reported as ENONFINITE(INPUT,
+// row * n + column), as the single-process pipeline's folded input check.
 cudaError_t run_tslw_schur_local_tree(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows,
                                       int64_t row0, int p0, int w, int n, const double* U, const uint8_t* chosen,
                                       int arity, int stop_lev, int* ids[2], int* cnt[2], double* vals[2],
-                                      int* out_ids, int* out_cnt, double* out_vals, cudaStream_t st, bool* fused) {
+                                      int* out_ids, int* out_cnt, double* out_vals, unsigned long long* status,
+                                      cudaStream_t st, bool* fused) {
   *fused = false;
   bool done = false, leaves_done = false;
-  cudaError_t e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, nullptr, nullptr, chosen, ids[0], cnt[0],
+  cudaError_t e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, nullptr, status, chosen, ids[0], cnt[0],
                                    vals[0], row0, st, &done, &leaves_done);
   if (e || !done) return e;
   *fused = true;
