@@ -407,3 +407,33 @@ def test_arrowhead_breakdown_is_a_value(rl):
             assert code[0] == 5 and code[1] in (5, 7), code  # EBREAKDOWN, CHOL1 / CHOL2
         seen.add(code[0])
     assert 0 in seen  # most trials succeed
+
+
+_OMEGA_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2412_06551_b200 as rl, synth
+X = synth.baseline_matrix(65536, 64, 12, 1, device="cuda")
+res = rl.slhc3(X, s=128, seed=5)
+assert res.info() == (0, 0, 0), res.info()
+np.save(sys.argv[2], np.concatenate([res.Q.cpu().numpy().ravel(), res.R.cpu().numpy().ravel()]))
+"""
+
+
+@pytest.mark.gpu
+def test_omega_chunks_match_in_kernel(tmp_path):
+    """SLHC3's Omega generated in per-panel chunks on the side stream (the default for
+    16 < n <= 256) and streamed by the sketch, against Omega generated inside the sketch kernel
+    (RLHC_OMEGA_CHUNKS=0): the same Omega bits (R#19) and the same contraction order, so Q and
+    R are bit-identical (R alone could not tell: it is the unique QR of X whatever Omega is)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for chunks in ("1", "0"):
+        f = str(tmp_path / f"qr_{chunks}.npy")
+        env = dict(os.environ, RLHC_OMEGA_CHUNKS=chunks)
+        subprocess.run([sys.executable, "-c", _OMEGA_CHILD, root, f], env=env, check=True, timeout=600)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
