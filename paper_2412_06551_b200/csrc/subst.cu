@@ -188,6 +188,21 @@ __device__ __forceinline__ void sv_tma_store(const CUtensorMap* map, int x, int 
                "r"(x), "r"(y), "r"(smem_u32(src))
                : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void sv_tma_load_h(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void sv_tma_store_h(const CUtensorMap* map, int x, int y, const void* src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src)), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void sv_expect_tx(unsigned long long* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -197,7 +212,7 @@ __device__ __forceinline__ int sv_off(int r, int c) { return r * SV_B + ((((c >>
 __global__ void __launch_bounds__(SV_THREADS, 2)
 subst_wide_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO,
                       const __grid_constant__ CUtensorMap tmT, int64_t rows, int n, const double* __restrict__ T,
-                      int64_t ldt) {
+                      int64_t ldt, int hint) {
   extern __shared__ __align__(1024) unsigned char sv_raw[];
   SvSmem& sm = *reinterpret_cast<SvSmem*>(sv_raw + ((1024u - (smem_u32(sv_raw) & 1023u)) & 1023u));
   double* dg = reinterpret_cast<double*>(&sm + 1);  // [n] Y_kk, [n] RN(1/Y_kk)
@@ -221,6 +236,13 @@ subst_wide_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
   if (wp == SV_CW) {
     // ---------------- producer (one thread)
     if (lane != 0) return;
+    // hint (measurement knob RLHC_SV_HINT): X is read once (evict first), the outputs are
+    // re-read by the tile's later blocks (evict last)
+    uint64_t pol_first = 0, pol_last = 0;
+    if (hint) {
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
+    }
     int pend_b[SV_NS], pend_r0[SV_NS];  // a D item's output box still to be stored from the slot
     uint32_t pend_q[SV_NS];
     for (int s = 0; s < SV_NS; s++) pend_b[s] = -1, pend_r0[s] = 0, pend_q[s] = 0;
@@ -229,7 +251,8 @@ subst_wide_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
     auto flush = [&](int s) {
       if (pend_b[s] < 0) return;
       mbar_wait(&sm.empty[s], (pend_q[s] / SV_NS) & 1);  // D's consumers are done with the slot
-      sv_tma_store(&tmO, pend_b[s] * SV_B, pend_r0[s], &sm.slot[s].O[0][0]);
+      if (hint) sv_tma_store_h(&tmO, pend_b[s] * SV_B, pend_r0[s], &sm.slot[s].O[0][0], pol_last);
+      else sv_tma_store(&tmO, pend_b[s] * SV_B, pend_r0[s], &sm.slot[s].O[0][0]);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -247,12 +270,14 @@ subst_wide_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
           SvSlot& sl = sm.slot[s];
           if (e < 0) {
             sv_expect_tx(&sm.full[s], SV_R * SV_B * 8u);
-            sv_tma_load(&sl.O[0][0], &tmA, b * SV_B, r0, &sm.full[s]);
+            if (hint) sv_tma_load_h(&sl.O[0][0], &tmA, b * SV_B, r0, &sm.full[s], pol_first);
+            else sv_tma_load(&sl.O[0][0], &tmA, b * SV_B, r0, &sm.full[s]);
           } else if (e < b) {
             for (int k = 0; k < SV_NS; k++)   // block e's outputs must be in `out` first
               if (pend_b[k] == e && pend_r0[k] == r0) flush(k);
             sv_expect_tx(&sm.full[s], SV_R * SV_B * 8u + SV_B * SV_B * 8u);
-            sv_tma_load(&sl.O[0][0], &tmO, e * SV_B, r0, &sm.full[s]);
+            if (hint) sv_tma_load_h(&sl.O[0][0], &tmO, e * SV_B, r0, &sm.full[s], pol_last);
+            else sv_tma_load(&sl.O[0][0], &tmO, e * SV_B, r0, &sm.full[s]);
             sv_tma_load(&sl.Y[0][0], &tmT, b * SV_B, e * SV_B, &sm.full[s]);
           } else {
             sv_expect_tx(&sm.full[s], SV_B * SV_B * 8u);
@@ -391,8 +416,9 @@ static cudaError_t launch_subst_wide_tma(const double* A, int64_t lda, int64_t r
                                                               (int64_t)sms * std::max(per_sm, 1)));
   note_launch();
   *done = true;
+  static const int hint = [] { const char* e = getenv("RLHC_SV_HINT"); return e ? atoi(e) : 1; }();
   return launch_pdl(subst_wide_tma_kernel, dim3((unsigned)grid), dim3(SV_THREADS), (size_t)smem, st, mA, mO, mT, rows,
-                    n, T, ldt);
+                    n, T, ldt, hint);
 }
 
 cudaError_t launch_subst_wide(const double* A, int64_t lda, int64_t rows, int n, const double* T, int64_t ldt,
