@@ -639,39 +639,50 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
 // drop to 128 registers, the producer / select warpgroup rises to 248 (the select holds a
 // 128 x 16 tile in registers).  (A first version selected inside the consumer warps, thread
 // = row, with named barriers per step: the select lag stalled the stage ring, LU 90 -> 137 ms.)
-constexpr int ST_M = 128, ST_S = 5, ST_CW = 8, ST_BS = WW + 4;
+constexpr int ST_M = 128, ST_CW = 8;
 constexpr int ST_THREADS = 32 * (ST_CW + 4);  // + producer warp, 3 select warps
 constexpr int ST_SEL = 3;                     // select warps
+template <int S>
 struct __align__(1024) SchurTSmem {
-  double A[ST_S][ST_M][WW];  // k chunks (and S_{j-1}), swizzled
+  double A[S][ST_M][WW];     // k chunks (and S_{j-1}), swizzled
   double Lt[2][ST_M][WW];    // L_{j-1} of the tile, swizzled, by tile parity
   double Ublk[WW][WW + 1];
   double rdp[WW];
-  unsigned long long full[ST_S], empty[ST_S];
+  unsigned long long full[S], empty[S];
   unsigned long long ready[ST_SEL], freeb[ST_SEL];  // select warp k's staging tile: filled / free
-  // followed by Bs[p0][ST_BS]: U[k][p0 + c], then (leaves) WSel[ST_SEL]
+  // followed by Bs (U[:p0, panel] in DMMA fragment order: [p0/4][2][32]), in PAIR mode Bs2
+  // (U[:p0, next panel]), then (leaves) WSel[ST_SEL]
 };
 __device__ __forceinline__ int st_off(int row, int k) { return row * WW + ((((k >> 1) ^ row) & 7) << 1) + (k & 1); }
-__host__ __device__ inline size_t schur_bs_bytes(int p0) { return (((size_t)p0 * ST_BS * sizeof(double)) + 15) & ~(size_t)15; }
-size_t schur_tma_smem(int p0, bool leaves) {
-  return sizeof(SchurTSmem) + schur_bs_bytes(p0) + (leaves ? ST_SEL * sizeof(WSel) : 0) + 1024;
+__host__ __device__ inline size_t schur_bs_bytes(int p0) { return (size_t)p0 * WW * sizeof(double); }
+template <int S>
+size_t schur_tma_smem_t(int p0, bool pair, bool leaves) {
+  return sizeof(SchurTSmem<S>) + (pair ? 2 : 1) * schur_bs_bytes(p0) + (leaves ? ST_SEL * sizeof(WSel) : 0) + 1024;
 }
+size_t schur_tma_smem(int p0, bool leaves) { return schur_tma_smem_t<5>(p0, false, leaves); }
 
+// PAIR: the kernel of an even panel j also accumulates, from the same L chunks, the partial
+// Schur complement P_{j+1} = X[:, next panel] - L[:, :p0] U[:p0, next panel] of the next panel
+// (w2 columns, into L's columns [p0 + 16, p0 + 32)); the odd panel j+1 then starts from P_{j+1}
+// (its "X" map over L) and streams no L chunk from HBM (kbeg = nk): every L column is re-read
+// once per PAIR of panels.  Same fma chain per element (k increasing), so the same bits.
+template <int S, bool PAIR>
 __global__ void __launch_bounds__(ST_THREADS, 1)
 tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
                       double* __restrict__ Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
                       const double* __restrict__ U, const double* __restrict__ rd, unsigned long long* finite_status,
                       const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
-                      double* __restrict__ vals0, int64_t row0) {
+                      double* __restrict__ vals0, int64_t row0, int kbeg, int w2) {
   extern __shared__ __align__(1024) unsigned char stm_raw[];
-  SchurTSmem& sm = *reinterpret_cast<SchurTSmem*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
+  SchurTSmem<S>& sm = *reinterpret_cast<SchurTSmem<S>*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
   double* Bs = reinterpret_cast<double*>(&sm + 1);
-  WSel* wsel = reinterpret_cast<WSel*>(reinterpret_cast<unsigned char*>(Bs) + schur_bs_bytes(p0));
+  double* Bs2 = Bs + (size_t)p0 * WW;  // (PAIR)
+  WSel* wsel = reinterpret_cast<WSel*>(reinterpret_cast<unsigned char*>(Bs) + (PAIR ? 2 : 1) * schur_bs_bytes(p0));
   const bool leaves = ids0 != nullptr;
   const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
   const int kold = p0 - WW, nk = kold / WW;
   const int64_t ntiles = ceil_div<int64_t>(rows, ST_M);
-  if (tid < ST_S) {
+  if (tid < S) {
     mbar_init(&sm.full[tid], 1);
     mbar_init(&sm.empty[tid], ST_CW);
   }
@@ -686,22 +697,29 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
   if (wp >= ST_CW) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 248;\n" ::: "memory");
     if (wp == ST_CW) {
-      // ---------------- producer
+      // ---------------- producer: per tile X's panel columns, (PAIR) the next panel's X
+      // columns, S_{j-1}, then L's k chunks kbeg .. nk-1
       if (lane != 0) return;
       uint32_t q = 0;
+      const int first = PAIR ? -3 : -2;
       for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        for (int c = -2; c < (p0 ? nk : -1); c++, q++) {  // -2: X's panel columns, -1: S_{j-1}, then L's k chunks
-          const int s = (int)(q % ST_S);
-          if (q >= ST_S) mbar_wait(&sm.empty[s], ((q / ST_S) - 1) & 1);
+        for (int c = first; c < (p0 ? nk : -1); c++) {
+          if (c >= 0 && c < kbeg) c = kbeg;
+          if (c >= nk) break;
+          const int s = (int)(q % S);
+          if (q >= S) mbar_wait(&sm.empty[s], ((q / S) - 1) & 1);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
                        "r"((uint32_t)(ST_M * WW * 8))
                        : "memory");
+          const bool xs = PAIR ? c <= -2 : c == -2;
+          const int xc = PAIR ? (c == -3 ? p0 : c == -2 ? p0 + WW : c < 0 ? kold : c * WW)
+                              : (c == -2 ? p0 : c < 0 ? kold : c * WW);
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
               "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
-              "l"(reinterpret_cast<uint64_t>(c == -2 ? &tmX : &tmL)), "r"(c == -2 ? p0 : c < 0 ? kold : c * WW),
-              "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
+              "l"(reinterpret_cast<uint64_t>(xs ? &tmX : &tmL)), "r"(xc), "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
               : "memory");
+          q++;
         }
       }
       return;
@@ -730,10 +748,12 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
     return;
   }
   asm volatile("setmaxnreg.dec.sync.aligned.u32 128;\n" ::: "memory");
-  // ---------------- consumers (256 threads): B, the previous panel's block, 1/diag
+  // ---------------- consumers (256 threads): B in fragment order, the previous panel's block, 1/diag
   for (int e = tid; e < p0 * WW; e += 32 * ST_CW) {
-    const int kk = e / WW, c = e - kk * WW;
-    Bs[kk * ST_BS + c] = c < w ? U[(int64_t)kk * n + p0 + c] : 0.0;
+    const int kq = e >> 6, b = (e >> 5) & 1, ln = e & 31;
+    const int kk = 4 * kq + (ln & 3), c = 8 * b + (ln >> 2);
+    Bs[e] = c < w ? U[(int64_t)kk * n + p0 + c] : 0.0;
+    if (PAIR) Bs2[e] = c < w2 ? U[(int64_t)kk * n + p0 + WW + c] : 0.0;
   }
   for (int e = tid; e < (p0 ? WW * WW : 0); e += 32 * ST_CW) {
     const int kk = e / WW, c = e - kk * WW;
@@ -748,10 +768,11 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
   int par = 0;
   for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, par ^= 1, ti++) {
     const int64_t r0 = tl * ST_M;
-    double acc[2][2][2];
-    {  // X's panel columns (zero outside the matrix), with the input check
-      const int s = (int)(q % ST_S);
-      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+    double acc[2][2][2], acc2[1][2][2][2];  // acc2: PAIR only
+    // X's panel columns (zero outside the matrix), with the input check; PAIR: the next panel's
+    auto take_x = [&](double (&ac)[2][2][2], int col0) {
+      const int s = (int)(q % S);
+      mbar_wait(&sm.full[s], (q / S) & 1);
       const double* xs = &sm.A[s][0][0];
 #pragma unroll
       for (int a = 0; a < 2; a++)
@@ -759,20 +780,22 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         for (int b = 0; b < 2; b++) {
           const int c = b * 8 + 2 * tq;
           const double2 v = *reinterpret_cast<const double2*>(xs + st_off(frow(a), c));
-          acc[a][b][0] = v.x, acc[a][b][1] = v.y;
+          ac[a][b][0] = v.x, ac[a][b][1] = v.y;
           if (finite_status) {
             const int64_t gr = r0 + frow(a);
-            if (!isfinite(v.x)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c);
-            if (!isfinite(v.y)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + p0 + c + 1);
+            if (!isfinite(v.x)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + col0 + c);
+            if (!isfinite(v.y)) report(finite_status, RLHC_ENONFINITE, RLHC_STAGE_INPUT, gr * n + col0 + c + 1);
           }
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       q++;
-    }
+    };
+    take_x(acc, p0);
+    if (PAIR) take_x(acc2[0], p0 + WW);
     if (p0) {  // S_{j-1} -> L_{j-1}: thread = tile row, warps 0-3 on even tiles, 4-7 on odd ones
-      const int s = (int)(q % ST_S);
-      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+      const int s = (int)(q % S);
+      mbar_wait(&sm.full[s], (q / S) & 1);
       if ((wp >> 2) == par) {
         const int row = tid & (ST_M - 1);
         const double* src = &sm.A[s][0][0];
@@ -807,17 +830,27 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         double af[2], bf[2];
 #pragma unroll
         for (int a = 0; a < 2; a++) af[a] = -As[st_off(frow(a), k0 + tq)];
+        const double* bp = Bs + (size_t)((kb + k0) >> 2) * 64 + lane;
 #pragma unroll
-        for (int b = 0; b < 2; b++) bf[b] = Bs[(kb + k0 + tq) * ST_BS + b * 8 + g];
+        for (int b = 0; b < 2; b++) bf[b] = bp[b * 32];
 #pragma unroll
         for (int a = 0; a < 2; a++)
 #pragma unroll
           for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        if (PAIR) {
+          const double* bp2 = Bs2 + (size_t)((kb + k0) >> 2) * 64 + lane;
+#pragma unroll
+          for (int b = 0; b < 2; b++) bf[b] = bp2[b * 32];
+#pragma unroll
+          for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) dmma(acc2[0][a][b][0], acc2[0][a][b][1], af[a], bf[b]);
+        }
       }
     };
-    for (int c = 0; c < nk; c++, q++) {
-      const int s = (int)(q % ST_S);
-      mbar_wait(&sm.full[s], (q / ST_S) & 1);
+    for (int c = kbeg; c < nk; c++, q++) {
+      const int s = (int)(q % S);
+      mbar_wait(&sm.full[s], (q / S) & 1);
       mma16(&sm.A[s][0][0], c * WW);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -826,22 +859,26 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
       mma16(&sm.Lt[par][0][0], kold);
     }
+    auto store = [&](const double (&ac)[2][2][2], int col0, int wc) {
 #pragma unroll
-    for (int a = 0; a < 2; a++)
+      for (int a = 0; a < 2; a++)
 #pragma unroll
-      for (int b = 0; b < 2; b++) {
-        const int64_t gr = r0 + frow(a);
-        const int c = b * 8 + 2 * tq;
-        if (gr < rows) {
-          double* dst = Lb + gr * ldl + p0 + c;
-          if (st16 && c + 1 < w) {
-            *reinterpret_cast<double2*>(dst) = make_double2(acc[a][b][0], acc[a][b][1]);
-          } else {
-            if (c < w) dst[0] = acc[a][b][0];
-            if (c + 1 < w) dst[1] = acc[a][b][1];
+        for (int b = 0; b < 2; b++) {
+          const int64_t gr = r0 + frow(a);
+          const int c = b * 8 + 2 * tq;
+          if (gr < rows) {
+            double* dst = Lb + gr * ldl + col0 + c;
+            if (st16 && c + 1 < wc) {
+              *reinterpret_cast<double2*>(dst) = make_double2(ac[a][b][0], ac[a][b][1]);
+            } else {
+              if (c < wc) dst[0] = ac[a][b][0];
+              if (c + 1 < wc) dst[1] = ac[a][b][1];
+            }
           }
         }
-      }
+    };
+    store(acc, p0, w);
+    if (PAIR) store(acc2[0], p0 + WW, w2);
     if (leaves) {  // S_j -> the staging tile of select warp ti % ST_SEL (zero outside the panel)
       const int k = (int)(ti % ST_SEL);
       if (ti >= ST_SEL) mbar_wait(&sm.freeb[k], ((ti / ST_SEL) - 1) & 1);
@@ -861,21 +898,24 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
 }
 
 // launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
-// tells the caller whether it ran
-// launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
 // tells the caller whether it ran, *leaves_done whether it also selected the leaves (ids0
-// non-null asks for it: more than one leaf, and room for the leaf buffers)
+// non-null asks for it: more than one leaf, and room for the leaf buffers).
+// mode 0: the panel from X, every L chunk; mode 1 (PAIR): also the next panel's partial Schur
+// complement (w2 columns) into L; mode 2: the panel from the partial in L (the odd panel after
+// a PAIR), no L chunk from HBM.
 static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0,
                                     int w, int n, const double* U, const double* rd, unsigned long long* status,
                                     const uint8_t* chosen, int* ids0, int* cnt0, double* vals0, int64_t row0,
-                                    cudaStream_t st, bool* done, bool* leaves_done) {
+                                    cudaStream_t st, bool* done, bool* leaves_done, int mode = 0, int w2 = 0) {
   *done = false;
   *leaves_done = false;
   static const bool on = [] { const char* e = getenv("RLHC_SCHUR_TMA"); return !e || atoi(e) != 0; }();
   static const bool leaves_on = [] { const char* e = getenv("RLHC_SCHUR_LEAVES"); return !e || atoi(e) != 0; }();
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-  bool leaves = leaves_on && ids0 && rows > ST_M && schur_tma_smem(p0, true) <= 227 * 1024;
-  const size_t smem = schur_tma_smem(p0, leaves);
+  const bool pair = mode == 1;
+  auto smem_of = [&](bool lv) { return pair ? schur_tma_smem_t<4>(p0, true, lv) : schur_tma_smem_t<5>(p0, false, lv); };
+  bool leaves = leaves_on && ids0 && rows > ST_M && smem_of(true) <= 227 * 1024;
+  const size_t smem = smem_of(leaves);
   if (!on || !enc || (ldl & 1) || (ldx & 1) || (reinterpret_cast<uintptr_t>(Lb) & 15) ||
       (reinterpret_cast<uintptr_t>(X) & 15) || smem > 227 * 1024 || rows >= (int64_t(1) << 31))
     return cudaSuccess;
@@ -889,18 +929,28 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   CUtensorMap mL, mX;
-  if (!make(&mX, X, ldx, p0 + w) || !make(&mL, p0 ? Lb : X, p0 ? ldl : ldx, p0 ? p0 : w)) return cudaSuccess;
-  static DevFlags attr;
-  if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel, 227 * 1024)) return e;
+  const bool xok = mode == 2 ? make(&mX, Lb, ldl, p0 + w) : make(&mX, X, ldx, pair ? p0 + WW + w2 : p0 + w);
+  if (!xok || !make(&mL, p0 ? Lb : X, p0 ? ldl : ldx, p0 ? p0 : w)) return cudaSuccess;
   int dev = 0, sms = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
   if (cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) return e;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, ST_M), sms));
+  const int kbeg = mode == 2 ? std::max(0, (p0 - WW) / WW) : 0;
   note_launch();
   *done = true;
   *leaves_done = leaves;
-  return launch_pdl(tslw_schur_tma_kernel, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb, ldl, rows, p0,
-                    w, n, U, rd, status, chosen, leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0);
+  if (pair) {
+    static DevFlags attr;
+    if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel<4, true>, 227 * 1024)) return e;
+    return launch_pdl(tslw_schur_tma_kernel<4, true>, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb,
+                      ldl, rows, p0, w, n, U, rd, status, chosen, leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0,
+                      kbeg, w2);
+  }
+  static DevFlags attr;
+  if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel<5, false>, 227 * 1024)) return e;
+  return launch_pdl(tslw_schur_tma_kernel<5, false>, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb,
+                    ldl, rows, p0, w, n, U, rd, mode == 2 ? (unsigned long long*)nullptr : status, chosen,
+                    leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0, kbeg, 0);
 }
 
 // The tournament's climb for one warp: select the node held in sm (active mask act) and emit
@@ -1516,6 +1566,9 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   if ((e = smem_attr(attr_t, tslw_tree_kernel, 227 * 1024))) return e;
   if ((e = smem_attr(attr_s, tslw_schur_dmma_kernel, (int)sizeof(SchurDSmem)))) return e;
   const TslwRoot root{U, piv, rd, nullptr, chosen, status, row0, n};
+  static const bool pair_on = [] { const char* e = getenv("RLHC_LU_PAIR"); return !e || atoi(e) != 0; }();
+  static const int pair_min = [] { const char* e = getenv("RLHC_LU_PAIR_MIN"); return e ? std::max(2, atoi(e)) : 6; }();
+  bool prev_pair = false;  // the previous panel's kernel left this panel's partial in Lb
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
     const int w = std::min(WW, n - p0);
@@ -1542,9 +1595,21 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
     } else {
       bool done = false;
       if (!grouped && !look) {
+        // panel pairs (RLHC_LU_PAIR, default on): an even panel p >= 2 also forms the next
+        // panel's partial Schur complement from the same L chunks; the odd panel after it
+        // starts from that partial (mode 2) and re-reads no L chunk
+        const int pidx = p0 / WW, np = ceil_div(n, WW);
+        int mode = 0, w2 = 0;
+        if (pair_on && pidx >= pair_min && pidx % 2 == 0 && pidx + 1 < np) {
+          mode = 1;
+          w2 = std::min(WW, n - p0 - WW);
+        } else if (prev_pair) {
+          mode = 2;
+        }
         e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, rd, check_input ? status : nullptr, chosen,
-                             Sw ? nullptr : ids[0], cnt[0], vals[0], row0, st, &done, &leaves_done);
+                             Sw ? nullptr : ids[0], cnt[0], vals[0], row0, st, &done, &leaves_done, mode, w2);
         if (e) return e;
+        prev_pair = done && mode == 1;
       }
       if (!done) note_launch();
       e = done ? cudaSuccess
