@@ -60,6 +60,9 @@ LU_CASES = [
     (2048, 16, None), (5000, 16, None), (65536, 64, None), (10000, 40, None), (3000, 33, None),
     (4100, 100, None), (20000, 128, None), (9000, 200, None), (6000, 64, (256, 2, 64)), (8192, 32, (512, 8, 32)),
     (300, 64, None), (64, 64, None),
+    # panel pairs (RLHC_LU_PAIR, from panel 6): a short second panel of the pair (n = 216), the
+    # last panel paired (n = 256), an unpaired last panel and a ragged last leaf (30011 x 232)
+    (12000, 216, None), (20000, 256, None), (30011, 232, None),
     # exact GEPP (one leaf holding every row)
     (4096, 50, (4096, 2, 16)), (3000, 64, (3000, 2, 16)), (2000, 5, (2000, 2, 5)), (400000, 24, (400000, 2, 16)),
     # an 8-wide panel at 128-row leaves runs on the CTA kernels (not the warp kernels' 16-wide panels)
