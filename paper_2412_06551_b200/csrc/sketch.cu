@@ -435,6 +435,49 @@ cs_apply_kernel(const double* __restrict__ A, int64_t lda, int n, int s1, const 
   if (cok) out[(int64_t)b * n + c] = acc;
 }
 
+// The same sums with two columns per lane (16-byte loads, 64-column slices): half the warps, each
+// row's slice one 512-byte request.  Per output element the same additions in the same (bucket
+// row) order, so the same bits.  A, lda: 16-byte aligned rows.
+__global__ void __launch_bounds__(256)
+cs_apply2_kernel(const double* __restrict__ A, int64_t lda, int n, int s1, const int32_t* __restrict__ perm,
+                 const int32_t* __restrict__ start, const int8_t* __restrict__ sign, double* __restrict__ out) {
+  const int nslice = (n + 63) / 64;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int b = wg / nslice, slice = wg - b * nslice;
+  if (b >= s1) return;
+  const int c = slice * 64 + 2 * lane_id();
+  const bool c0ok = c < n, c1ok = c + 1 < n;
+  const int p0 = start[b], p1 = start[b + 1];
+  double acc0 = 0.0, acc1 = 0.0;
+  int p = p0;
+  for (; p + 8 <= p1; p += 8) {
+    int r[8];
+    double2 v[8];
+    bool ng[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) r[u] = perm[p + u];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      ng[u] = sign[r[u]] < 0;
+      v[u] = c1ok ? *reinterpret_cast<const double2*>(A + (int64_t)r[u] * lda + c)
+                  : make_double2(c0ok ? A[(int64_t)r[u] * lda + c] : 0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      acc0 = __dadd_rn(acc0, ng[u] ? -v[u].x : v[u].x);
+      acc1 = __dadd_rn(acc1, ng[u] ? -v[u].y : v[u].y);
+    }
+  }
+  for (; p < p1; p++) {
+    const int r = perm[p];
+    const double x = c0ok ? A[(int64_t)r * lda + c] : 0.0, y = c1ok ? A[(int64_t)r * lda + c + 1] : 0.0;
+    acc0 = __dadd_rn(acc0, sign[r] < 0 ? -x : x);
+    acc1 = __dadd_rn(acc1, sign[r] < 0 ? -y : y);
+  }
+  if (c0ok) out[(int64_t)b * n + c] = acc0;
+  if (c1ok) out[(int64_t)b * n + c + 1] = acc1;
+}
+
 __global__ void copy_i32_kernel(const int32_t* a, int32_t* b, int64_t cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -463,6 +506,14 @@ cudaError_t launch_cs_plan(int64_t rows, int64_t row0, int s1, uint64_t seed, vo
 cudaError_t launch_cs_apply(const double* A, int64_t lda, int64_t rows, int n, int s1, void* plan_ws, double* out,
                             cudaStream_t st) {
   CsPlan pl = carve_plan(plan_ws, rows, s1);
+  static const int wide = [] { const char* e = getenv("RLHC_CS_WIDE"); return e ? atoi(e) : 1; }();
+  if (wide && (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    const int64_t warps = (int64_t)s1 * ((n + 63) / 64);
+    note_launch();
+    cs_apply2_kernel<<<(int)ceil_div<int64_t>(warps, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start, pl.sign,
+                                                                       out);
+    return cudaGetLastError();
+  }
   const int64_t warps = (int64_t)s1 * ((n + 31) / 32);
   note_launch(); cs_apply_kernel<<<(int)ceil_div<int64_t>(warps, 8), 256, 0, st>>>(A, lda, n, s1, pl.perm, pl.start,
                                                                                     pl.sign, out);
