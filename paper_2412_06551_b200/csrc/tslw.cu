@@ -20,6 +20,7 @@
 // the last S into L and tslw_fixup_kernel gives the pivot rows their L11 rows.
 // Every element of S, L and U is the oracle's fma chain (oracle ora_tslu / l_row: the
 // elimination and the substitution are the same chain), so piv, U, L11 and L are bit-exact.
+#include <type_traits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -672,7 +673,7 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
                       double* __restrict__ Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
                       const double* __restrict__ U, const double* __restrict__ rd, unsigned long long* finite_status,
                       const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
-                      double* __restrict__ vals0, int64_t row0, int kbeg, int w2) {
+                      double* __restrict__ vals0, int64_t row0, int kbeg, int w2, int b2) {
   extern __shared__ __align__(1024) unsigned char stm_raw[];
   SchurTSmem<S>& sm = *reinterpret_cast<SchurTSmem<S>*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
   double* Bs = reinterpret_cast<double*>(&sm + 1);
@@ -824,7 +825,8 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       q++;
     }
-    auto mma16 = [&](const double* As, int kb) {  // 16 k's: A stage (swizzled), B rows kb ..
+    // two: (PAIR) the chunk also feeds the next panel's partial (chunks c < b2 only)
+    auto mma16 = [&](const double* As, int kb, auto two) {  // 16 k's: A stage (swizzled), B rows kb ..
 #pragma unroll
       for (int k0 = 0; k0 < WW; k0 += 4) {
         double af[2], bf[2];
@@ -837,7 +839,7 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         for (int a = 0; a < 2; a++)
 #pragma unroll
           for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-        if (PAIR) {
+        if (PAIR && decltype(two)::value) {
           const double* bp2 = Bs2 + (size_t)((kb + k0) >> 2) * 64 + lane;
 #pragma unroll
           for (int b = 0; b < 2; b++) bf[b] = bp2[b * 32];
@@ -851,13 +853,19 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
     for (int c = kbeg; c < nk; c++, q++) {
       const int s = (int)(q % S);
       mbar_wait(&sm.full[s], (q / S) & 1);
-      mma16(&sm.A[s][0][0], c * WW);
+      if (PAIR && c < b2)
+        mma16(&sm.A[s][0][0], c * WW, std::true_type{});
+      else
+        mma16(&sm.A[s][0][0], c * WW, std::false_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
     if (p0) {
       asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
-      mma16(&sm.Lt[par][0][0], kold);
+      if (PAIR && nk < b2)
+        mma16(&sm.Lt[par][0][0], kold, std::true_type{});
+      else
+        mma16(&sm.Lt[par][0][0], kold, std::false_type{});
     }
     auto store = [&](const double (&ac)[2][2][2], int col0, int wc) {
 #pragma unroll
@@ -906,7 +914,8 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
 static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, int64_t ldl, int64_t rows, int p0,
                                     int w, int n, const double* U, const double* rd, unsigned long long* status,
                                     const uint8_t* chosen, int* ids0, int* cnt0, double* vals0, int64_t row0,
-                                    cudaStream_t st, bool* done, bool* leaves_done, int mode = 0, int w2 = 0) {
+                                    cudaStream_t st, bool* done, bool* leaves_done, int mode = 0, int w2 = 0,
+                                    int split = -1) {
   *done = false;
   *leaves_done = false;
   static const bool on = [] { const char* e = getenv("RLHC_SCHUR_TMA"); return !e || atoi(e) != 0; }();
@@ -935,7 +944,10 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
   if (cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) return e;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, ST_M), sms));
-  const int kbeg = mode == 2 ? std::max(0, (p0 - WW) / WW) : 0;
+  // split (modes 1 and 2): the partial covers L chunks [0, split) only (-1: all of [0, p0/16)
+  // in mode 1, i.e. the odd panel streams no chunk); the odd panel streams [split, p0/16 - 1)
+  const int kbeg = mode == 2 ? (split >= 0 ? split : std::max(0, (p0 - WW) / WW)) : 0;
+  const int b2 = mode == 1 && split >= 0 ? split : p0 / WW;
   note_launch();
   *done = true;
   *leaves_done = leaves;
@@ -944,13 +956,13 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
     if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel<4, true>, 227 * 1024)) return e;
     return launch_pdl(tslw_schur_tma_kernel<4, true>, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb,
                       ldl, rows, p0, w, n, U, rd, status, chosen, leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0,
-                      kbeg, w2);
+                      kbeg, w2, b2);
   }
   static DevFlags attr;
   if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel<5, false>, 227 * 1024)) return e;
   return launch_pdl(tslw_schur_tma_kernel<5, false>, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb,
                     ldl, rows, p0, w, n, U, rd, mode == 2 ? (unsigned long long*)nullptr : status, chosen,
-                    leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0, kbeg, 0);
+                    leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0, kbeg, 0, 0);
 }
 
 // The tournament's climb for one warp: select the node held in sm (active mask act) and emit
@@ -1568,7 +1580,11 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
   const TslwRoot root{U, piv, rd, nullptr, chosen, status, row0, n};
   static const bool pair_on = [] { const char* e = getenv("RLHC_LU_PAIR"); return !e || atoi(e) != 0; }();
   static const int pair_min = [] { const char* e = getenv("RLHC_LU_PAIR_MIN"); return e ? std::max(2, atoi(e)) : 6; }();
+  // RLHC_LU_PAIR_SPLIT=f (percent, measurement knob): the even panel j's partial for panel j+1
+  // covers only L chunks [0, round(f j / 100)); the odd panel streams the rest (same chain order)
+  static const int pair_split = [] { const char* e = getenv("RLHC_LU_PAIR_SPLIT"); return e ? atoi(e) : 100; }();
   bool prev_pair = false;  // the previous panel's kernel left this panel's partial in Lb
+  int split = -1;          // chunks the partial covers (-1: all)
   int pl = 0, wl = 0;
   for (int p0 = 0; p0 < n; p0 += WW) {
     const int w = std::min(WW, n - p0);
@@ -1603,11 +1619,13 @@ cudaError_t run_tslw(const double* X, int64_t ldx, int64_t rows, int64_t row0, i
         if (pair_on && pidx >= pair_min && pidx % 2 == 0 && pidx + 1 < np) {
           mode = 1;
           w2 = std::min(WW, n - p0 - WW);
+          split = pair_split >= 100 ? -1 : std::max(0, std::min(pidx, (pair_split * pidx + 50) / 100));
         } else if (prev_pair) {
           mode = 2;
         }
         e = launch_schur_tma(X, ldx, Lb, ldl, rows, p0, w, n, U, rd, check_input ? status : nullptr, chosen,
-                             Sw ? nullptr : ids[0], cnt[0], vals[0], row0, st, &done, &leaves_done, mode, w2);
+                             Sw ? nullptr : ids[0], cnt[0], vals[0], row0, st, &done, &leaves_done, mode, w2,
+                             mode ? split : -1);
         if (e) return e;
         prev_pair = done && mode == 1;
       }
