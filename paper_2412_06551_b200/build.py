@@ -12,7 +12,7 @@ SOURCES = ["tslu.cu", "tslw.cu", "rows.cu", "sketch.cu", "small.cu", "factor.cu"
            "dist_c.cu", "rlhc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("RLHC_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:

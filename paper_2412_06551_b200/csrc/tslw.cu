@@ -640,34 +640,46 @@ tslw_schur_dmma_kernel(const double* __restrict__ X, int64_t ldx, double* __rest
 // drop to 128 registers, the producer / select warpgroup rises to 248 (the select holds a
 // 128 x 16 tile in registers).  (A first version selected inside the consumer warps, thread
 // = row, with named barriers per step: the select lag stalled the stage ring, LU 90 -> 137 ms.)
+#ifdef RLHC_ST_PROF  // in-kernel phase clocks of CTA 0 (consumer warp 0, select warp 0), printed per launch
+#define STP_DECL long long stp_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, stp_t = clock64(), stp_n = 0;
+#define STP(i) { const long long c_ = clock64(); stp_[i] += c_ - stp_t; stp_t = c_; }
+#else
+#define STP_DECL
+#define STP(i)
+#endif
 constexpr int ST_M = 128, ST_CW = 8;
 constexpr int ST_THREADS = 32 * (ST_CW + 4);  // + producer warp, 3 select warps
 constexpr int ST_SEL = 3;                     // select warps
-template <int S>
+// CW consumer warps (8, or 4 in the LIGHT layout: panels whose Schur work is a few chunks are
+// bound by the leaf selects, so half the consumers' registers go to NSEL = 6 select warps).
+template <int S, int NSEL>
 struct __align__(1024) SchurTSmem {
   double A[S][ST_M][WW];     // k chunks (and S_{j-1}), swizzled
   double Lt[2][ST_M][WW];    // L_{j-1} of the tile, swizzled, by tile parity
   double Ublk[WW][WW + 1];
   double rdp[WW];
   unsigned long long full[S], empty[S];
-  unsigned long long ready[ST_SEL], freeb[ST_SEL];  // select warp k's staging tile: filled / free
+  unsigned long long ready[NSEL], freeb[NSEL];  // select warp k's staging tile: filled / free
   // followed by Bs (U[:p0, panel] in DMMA fragment order: [p0/4][2][32]), in PAIR mode Bs2
-  // (U[:p0, next panel]), then (leaves) WSel[ST_SEL]
+  // (U[:p0, next panel]), then (leaves) WSel[NSEL]; only U's rows [16 kbeg, p0) are staged
 };
 __device__ __forceinline__ int st_off(int row, int k) { return row * WW + ((((k >> 1) ^ row) & 7) << 1) + (k & 1); }
 __host__ __device__ inline size_t schur_bs_bytes(int p0) { return (size_t)p0 * WW * sizeof(double); }
-template <int S>
-size_t schur_tma_smem_t(int p0, bool pair, bool leaves) {
-  return sizeof(SchurTSmem<S>) + (pair ? 2 : 1) * schur_bs_bytes(p0) + (leaves ? ST_SEL * sizeof(WSel) : 0) + 1024;
+template <int S, int NSEL = ST_SEL>
+size_t schur_tma_smem_t(int brows, bool pair, bool leaves) {  // brows: rows of U staged (p0 - 16 kbeg)
+  return sizeof(SchurTSmem<S, NSEL>) + (pair ? 2 : 1) * schur_bs_bytes(brows) + (leaves ? NSEL * sizeof(WSel) : 0) + 1024;
 }
-size_t schur_tma_smem(int p0, bool leaves) { return schur_tma_smem_t<5>(p0, false, leaves); }
+constexpr int ST_LCW = 4, ST_LSEL = 6, ST_LS = 3;  // the LIGHT layout: consumer warps, select warps, stages
 
 // PAIR: the kernel of an even panel j also accumulates, from the same L chunks, the partial
 // Schur complement P_{j+1} = X[:, next panel] - L[:, :p0] U[:p0, next panel] of the next panel
 // (w2 columns, into L's columns [p0 + 16, p0 + 32)); the odd panel j+1 then starts from P_{j+1}
 // (its "X" map over L) and streams no L chunk from HBM (kbeg = nk): every L column is re-read
 // once per PAIR of panels.  Same fma chain per element (k increasing), so the same bits.
-template <int S, bool PAIR>
+// PIC (producer in a consumer): lane 0 of consumer warp 0 issues the TMA loads itself -- after it
+// releases item q it loads item q + S - 1 (whose stage every consumer released one item ago) --
+// and the warp freed carries a FOURTH select warp (the select-bound panels: early and odd ones).
+template <int S, bool PAIR, int CW = ST_CW, int NSEL = ST_SEL, bool PIC = false>
 __global__ void __launch_bounds__(ST_THREADS, 1)
 tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmX,
                       double* __restrict__ Lb, int64_t ldl, int64_t rows, int p0, int w, int n,
@@ -675,108 +687,183 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
                       const uint8_t* __restrict__ chosen, int* __restrict__ ids0, int* __restrict__ cnt0,
                       double* __restrict__ vals0, int64_t row0, int kbeg, int w2, int b2) {
   extern __shared__ __align__(1024) unsigned char stm_raw[];
-  SchurTSmem<S>& sm = *reinterpret_cast<SchurTSmem<S>*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
+  static_assert(CW == 8 || (CW == 4 && !PAIR), "consumer layouts");
+  static_assert(CW + (PIC ? 0 : 1) + NSEL <= ST_THREADS / 32, "warp roles");
+  constexpr int H = 8 / CW;  // 64-row halves of the tile per consumer warp
+  using Smem = SchurTSmem<S, NSEL>;
+  Smem& sm = *reinterpret_cast<Smem*>(stm_raw + ((1024u - (smem_u32(stm_raw) & 1023u)) & 1023u));
+  const int bs0 = kbeg * WW;  // U's rows [bs0, p0) are staged (chunks before kbeg are not streamed)
   double* Bs = reinterpret_cast<double*>(&sm + 1);
-  double* Bs2 = Bs + (size_t)p0 * WW;  // (PAIR)
-  WSel* wsel = reinterpret_cast<WSel*>(reinterpret_cast<unsigned char*>(Bs) + (PAIR ? 2 : 1) * schur_bs_bytes(p0));
+  double* Bs2 = Bs + (size_t)(p0 - bs0) * WW;  // (PAIR)
+  WSel* wsel = reinterpret_cast<WSel*>(reinterpret_cast<unsigned char*>(Bs) + (PAIR ? 2 : 1) * schur_bs_bytes(p0 - bs0));
   const bool leaves = ids0 != nullptr;
   const int tid = threadIdx.x, lane = lane_id(), wp = warp_id();
   const int kold = p0 - WW, nk = kold / WW;
   const int64_t ntiles = ceil_div<int64_t>(rows, ST_M);
   if (tid < S) {
     mbar_init(&sm.full[tid], 1);
-    mbar_init(&sm.empty[tid], ST_CW);
+    mbar_init(&sm.empty[tid], CW);
   }
-  if (tid < ST_SEL) {
-    mbar_init(&sm.ready[tid], ST_CW);
+  if (tid < NSEL) {
+    mbar_init(&sm.ready[tid], CW);
     mbar_init(&sm.freeb[tid], 1);
   }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   pdl_trigger();
   pdl_wait();
-  if (wp >= ST_CW) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 248;\n" ::: "memory");
-    if (wp == ST_CW) {
-      // ---------------- producer: per tile X's panel columns, (PAIR) the next panel's X
-      // columns, S_{j-1}, then L's k chunks kbeg .. nk-1
+  // the item stream (both sides walk it in the same order): per tile X's panel columns, (PAIR)
+  // the next panel's X columns, S_{j-1}, then L's k chunks kbeg .. nk-1
+  struct Prod {
+    uint32_t q;
+    int64_t tl;
+    int c;
+    bool done;
+  };
+  const int pfirst = PAIR ? -3 : -2, pend = p0 ? nk : -1;
+  auto prod_issue = [&](Prod& ps) {  // loads the next item (after its stage is free); false: none left
+    if (ps.done) return false;
+    const int s = (int)(ps.q % S), c = ps.c;
+    if (ps.q >= S) mbar_wait(&sm.empty[s], ((ps.q / S) - 1) & 1);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
+                 "r"((uint32_t)(ST_M * WW * 8))
+                 : "memory");
+    const bool xs = PAIR ? c <= -2 : c == -2;
+    const int xc = PAIR ? (c == -3 ? p0 : c == -2 ? p0 + WW : c < 0 ? kold : c * WW)
+                        : (c == -2 ? p0 : c < 0 ? kold : c * WW);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
+        "l"(reinterpret_cast<uint64_t>(xs ? &tmX : &tmL)), "r"(xc), "r"((int)(ps.tl * ST_M)), "r"(smem_u32(&sm.full[s]))
+        : "memory");
+    ps.q++;
+    ps.c++;
+    if (ps.c >= 0 && ps.c < kbeg) ps.c = kbeg;
+    if (ps.c >= pend) {
+      ps.c = pfirst;
+      ps.tl += gridDim.x;
+      ps.done = ps.tl >= ntiles;
+    }
+    return true;
+  };
+  if (wp >= CW) {
+    if (CW == 8)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 248;\n" ::: "memory");
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    if (!PIC && wp == CW) {
+      // ---------------- producer warp (one lane)
       if (lane != 0) return;
-      uint32_t q = 0;
-      const int first = PAIR ? -3 : -2;
-      for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        for (int c = first; c < (p0 ? nk : -1); c++) {
-          if (c >= 0 && c < kbeg) c = kbeg;
-          if (c >= nk) break;
-          const int s = (int)(q % S);
-          if (q >= S) mbar_wait(&sm.empty[s], ((q / S) - 1) & 1);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&sm.full[s])),
-                       "r"((uint32_t)(ST_M * WW * 8))
-                       : "memory");
-          const bool xs = PAIR ? c <= -2 : c == -2;
-          const int xc = PAIR ? (c == -3 ? p0 : c == -2 ? p0 + WW : c < 0 ? kold : c * WW)
-                              : (c == -2 ? p0 : c < 0 ? kold : c * WW);
-          asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-              "[%4];\n" ::"r"(smem_u32(&sm.A[s][0][0])),
-              "l"(reinterpret_cast<uint64_t>(xs ? &tmX : &tmL)), "r"(xc), "r"((int)(tl * ST_M)), "r"(smem_u32(&sm.full[s]))
-              : "memory");
-          q++;
-        }
+      Prod ps{0u, (int64_t)blockIdx.x, pfirst, (int64_t)blockIdx.x >= ntiles};
+      while (prod_issue(ps)) {
       }
       return;
     }
-    const int k = wp - ST_CW - 1;
-    if (!leaves || k >= ST_SEL) return;
-    // ---------------- select warp k: the leaves of this CTA's tiles i = k, k + ST_SEL, ...
+    const int k = wp - CW - (PIC ? 0 : 1);
+    if (!leaves || k >= NSEL) return;
+    // ---------------- select warp k: the leaves of this CTA's tiles i = k, k + NSEL, ...
     WSel& ws = wsel[k];
     uint32_t i = 0;
-    for (int64_t tl = blockIdx.x + (int64_t)k * gridDim.x; tl < ntiles; tl += (int64_t)ST_SEL * gridDim.x, i++) {
-      const int64_t rb = tl * ST_M;
+    // active rows of tile tl (bit s: row s * 32 + lane); the next tile's flags are loaded before
+    // this tile's select so that their latency is off the select chain
+    // (volatile loads: issued here, before the select; their values are combined after it)
+    auto flags = [&](int64_t tl, unsigned (&f)[RS]) {
+#pragma unroll
+      for (int s = 0; s < RS; s++) {
+        const int64_t r = tl * ST_M + s * 32 + lane;
+        f[s] = r < rows ? 0u : 1u;
+        if (chosen && r < rows) asm volatile("ld.global.nc.u8 %0, [%1];\n" : "=r"(f[s]) : "l"(chosen + r));
+      }
+    };
+    auto active = [&](const unsigned (&f)[RS]) {
       unsigned act = 0;
+#pragma unroll
+      for (int s = 0; s < RS; s++) act |= (f[s] ? 0u : 1u) << s;
+      return act;
+    };
+    const int64_t tstep = (int64_t)NSEL * gridDim.x;
+    int64_t tl = blockIdx.x + (int64_t)k * gridDim.x;
+    unsigned fl[RS] = {1u, 1u, 1u, 1u};
+    if (tl < ntiles) flags(tl, fl);
+    unsigned act = active(fl);
+    STP_DECL
+    for (; tl < ntiles; tl += tstep, i++) {
+      const int64_t rb = tl * ST_M;
+      if (tl + tstep < ntiles) flags(tl + tstep, fl);
 #pragma unroll
       for (int s = 0; s < RS; s++) {
         const int64_t r = rb + s * 32 + lane;
         ws.sid[s * 32 + lane] = r < rows ? (int)(row0 + r) : INT_MAX;
         ws.rank[s * 32 + lane] = s * 32 + lane;  // the leaf's rows are in increasing-id order
-        act |= ((r < rows && !(chosen && chosen[r])) ? 1u : 0u) << s;
       }
+      STP(0)
       mbar_wait(&sm.ready[k], i & 1);  // the consumers staged S_j of tile tl
       __syncwarp();
+      STP(1)
       select_and_emit(ws, act, w, (int)tl, ids0, cnt0, vals0, TslwRoot{}, p0);
       __syncwarp();
+      STP(2)
       if (lane == 0) mbar_arrive(&sm.freeb[k]);
+      act = active(fl);
+#ifdef RLHC_ST_PROF
+      stp_n++;
+#endif
     }
+#ifdef RLHC_ST_PROF
+    if (blockIdx.x == 0 && k == 0 && lane == 0)
+      printf("STP sel p0=%d CW=%d NSEL=%d tiles=%lld prep=%lld wait_ready=%lld select=%lld\n", p0, CW, NSEL, stp_n,
+             stp_[0] / stp_n, stp_[1] / stp_n, stp_[2] / stp_n);
+#endif
     return;
   }
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 128;\n" ::: "memory");
-  // ---------------- consumers (256 threads): B in fragment order, the previous panel's block, 1/diag
-  for (int e = tid; e < p0 * WW; e += 32 * ST_CW) {
+  if (CW == 8)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 128;\n" ::: "memory");
+  else
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+  // ---------------- consumers (32 CW threads): B in fragment order, the previous panel's block, 1/diag
+  for (int e = tid; e < (p0 - bs0) * WW; e += 32 * CW) {
     const int kq = e >> 6, b = (e >> 5) & 1, ln = e & 31;
-    const int kk = 4 * kq + (ln & 3), c = 8 * b + (ln >> 2);
+    const int kk = bs0 + 4 * kq + (ln & 3), c = 8 * b + (ln >> 2);
     Bs[e] = c < w ? U[(int64_t)kk * n + p0 + c] : 0.0;
     if (PAIR) Bs2[e] = c < w2 ? U[(int64_t)kk * n + p0 + WW + c] : 0.0;
   }
-  for (int e = tid; e < (p0 ? WW * WW : 0); e += 32 * ST_CW) {
+  for (int e = tid; e < (p0 ? WW * WW : 0); e += 32 * CW) {
     const int kk = e / WW, c = e - kk * WW;
     sm.Ublk[kk][c] = U[(int64_t)(kold + kk) * n + kold + c];
   }
   if (tid < WW && p0) sm.rdp[tid] = rd ? rd[kold + tid] : __ddiv_rn(1.0, U[(int64_t)(kold + tid) * (n + 1)]);
-  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * CW) : "memory");
   const int g = lane >> 2, tq = lane & 3;
-  auto frow = [&](int a) { return wp * 16 + 2 * g + a; };  // conflict-free against the swizzle
+  // fragment row a (0, 1) of 64-row half h: conflict-free against the swizzle
+  auto frow = [&](int a) { return (a >> 1) * 64 + wp * 16 + 2 * g + (a & 1); };
+  constexpr int NA = 2 * H;  // fragment rows per lane
   const bool st16 = (ldl & 1) == 0;                          // (TMA-describable L: base 16-byte aligned)
   uint32_t q = 0, ti = 0;
   int par = 0;
+  Prod ps{0u, (int64_t)blockIdx.x, pfirst, (int64_t)blockIdx.x >= ntiles};  // (PIC, warp 0 lane 0)
+  // PIC: item qc released by this warp -> load the items up to qc + S - 1
+  auto released = [&](uint32_t qc) {
+    if (PIC && wp == 0 && lane == 0) {
+      while (ps.q < qc + S && prod_issue(ps)) {
+      }
+    }
+  };
+  if (PIC && wp == 0 && lane == 0) {
+    while (ps.q < (uint32_t)S && prod_issue(ps)) {
+    }
+  }
+  STP_DECL
   for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, par ^= 1, ti++) {
     const int64_t r0 = tl * ST_M;
-    double acc[2][2][2], acc2[1][2][2][2];  // acc2: PAIR only
+    STP(0)
+    double acc[NA][2][2], acc2[1][NA][2][2];  // acc2: PAIR only
     // X's panel columns (zero outside the matrix), with the input check; PAIR: the next panel's
-    auto take_x = [&](double (&ac)[2][2][2], int col0) {
+    auto take_x = [&](double (&ac)[NA][2][2], int col0) {
       const int s = (int)(q % S);
       mbar_wait(&sm.full[s], (q / S) & 1);
       const double* xs = &sm.A[s][0][0];
 #pragma unroll
-      for (int a = 0; a < 2; a++)
+      for (int a = 0; a < NA; a++)
 #pragma unroll
         for (int b = 0; b < 2; b++) {
           const int c = b * 8 + 2 * tq;
@@ -790,14 +877,17 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
+      released(q);
       q++;
     };
     take_x(acc, p0);
     if (PAIR) take_x(acc2[0], p0 + WW);
+    STP(1)
     if (p0) {  // S_{j-1} -> L_{j-1}: thread = tile row, warps 0-3 on even tiles, 4-7 on odd ones
       const int s = (int)(q % S);
       mbar_wait(&sm.full[s], (q / S) & 1);
-      if ((wp >> 2) == par) {
+      STP(2)
+      if (CW == 4 || (wp >> 2) == par) {
         const int row = tid & (ST_M - 1);
         const double* src = &sm.A[s][0][0];
         double l[WW];
@@ -823,28 +913,30 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
+      released(q);
       q++;
+      STP(3)
     }
     // two: (PAIR) the chunk also feeds the next panel's partial (chunks c < b2 only)
     auto mma16 = [&](const double* As, int kb, auto two) {  // 16 k's: A stage (swizzled), B rows kb ..
 #pragma unroll
       for (int k0 = 0; k0 < WW; k0 += 4) {
-        double af[2], bf[2];
+        double af[NA], bf[2];
 #pragma unroll
-        for (int a = 0; a < 2; a++) af[a] = -As[st_off(frow(a), k0 + tq)];
-        const double* bp = Bs + (size_t)((kb + k0) >> 2) * 64 + lane;
+        for (int a = 0; a < NA; a++) af[a] = -As[st_off(frow(a), k0 + tq)];
+        const double* bp = Bs + (size_t)((kb - bs0 + k0) >> 2) * 64 + lane;
 #pragma unroll
         for (int b = 0; b < 2; b++) bf[b] = bp[b * 32];
 #pragma unroll
-        for (int a = 0; a < 2; a++)
+        for (int a = 0; a < NA; a++)
 #pragma unroll
           for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
         if (PAIR && decltype(two)::value) {
-          const double* bp2 = Bs2 + (size_t)((kb + k0) >> 2) * 64 + lane;
+          const double* bp2 = Bs2 + (size_t)((kb - bs0 + k0) >> 2) * 64 + lane;
 #pragma unroll
           for (int b = 0; b < 2; b++) bf[b] = bp2[b * 32];
 #pragma unroll
-          for (int a = 0; a < 2; a++)
+          for (int a = 0; a < NA; a++)
 #pragma unroll
             for (int b = 0; b < 2; b++) dmma(acc2[0][a][b][0], acc2[0][a][b][1], af[a], bf[b]);
         }
@@ -859,17 +951,20 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         mma16(&sm.A[s][0][0], c * WW, std::false_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
+      released(q);
     }
+    STP(4)
     if (p0) {
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * ST_CW) : "memory");  // Lt[par] complete
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * CW) : "memory");  // Lt[par] complete
+      STP(5)
       if (PAIR && nk < b2)
         mma16(&sm.Lt[par][0][0], kold, std::true_type{});
       else
         mma16(&sm.Lt[par][0][0], kold, std::false_type{});
     }
-    auto store = [&](const double (&ac)[2][2][2], int col0, int wc) {
+    auto store = [&](const double (&ac)[NA][2][2], int col0, int wc) {
 #pragma unroll
-      for (int a = 0; a < 2; a++)
+      for (int a = 0; a < NA; a++)
 #pragma unroll
         for (int b = 0; b < 2; b++) {
           const int64_t gr = r0 + frow(a);
@@ -885,14 +980,17 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
           }
         }
     };
+    STP(6)
     store(acc, p0, w);
     if (PAIR) store(acc2[0], p0 + WW, w2);
+    STP(7)
     if (leaves) {  // S_j -> the staging tile of select warp ti % ST_SEL (zero outside the panel)
-      const int k = (int)(ti % ST_SEL);
-      if (ti >= ST_SEL) mbar_wait(&sm.freeb[k], ((ti / ST_SEL) - 1) & 1);
+      const int k = (int)(ti % NSEL);
+      if (ti >= NSEL) mbar_wait(&sm.freeb[k], ((ti / NSEL) - 1) & 1);
+      STP(8)
       double* tile = wsel[k].tile;
 #pragma unroll
-      for (int a = 0; a < 2; a++)
+      for (int a = 0; a < NA; a++)
 #pragma unroll
         for (int b = 0; b < 2; b++) {
           const int c = b * 8 + 2 * tq;
@@ -901,8 +999,19 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.ready[k]);
+      STP(9)
     }
+#ifdef RLHC_ST_PROF
+    stp_n++;
+#endif
   }
+#ifdef RLHC_ST_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    printf("STP con p0=%d CW=%d NSEL=%d tiles=%lld loop=%lld wait_x=%lld wait_s=%lld subst=%lld chunks=%lld bar=%lld lt_mma=%lld "
+           "store=%lld wait_free=%lld stage=%lld\n", p0, CW, NSEL, stp_n, stp_[0] / stp_n, stp_[1] / stp_n, stp_[2] / stp_n,
+           stp_[3] / stp_n, stp_[4] / stp_n, stp_[5] / stp_n, stp_[6] / stp_n, stp_[7] / stp_n, stp_[8] / stp_n,
+           stp_[9] / stp_n);
+#endif
 }
 
 // launch the TMA Schur kernel if L is TMA-describable and its shared memory fits; *done
@@ -922,9 +1031,30 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
   static const bool leaves_on = [] { const char* e = getenv("RLHC_SCHUR_LEAVES"); return !e || atoi(e) != 0; }();
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   const bool pair = mode == 1;
-  auto smem_of = [&](bool lv) { return pair ? schur_tma_smem_t<4>(p0, true, lv) : schur_tma_smem_t<5>(p0, false, lv); };
-  bool leaves = leaves_on && ids0 && rows > ST_M && smem_of(true) <= 227 * 1024;
-  const size_t smem = smem_of(leaves);
+  // split (modes 1 and 2): the partial covers L chunks [0, split) only (-1: all of [0, p0/16)
+  // in mode 1, i.e. the odd panel streams no chunk); the odd panel streams [split, p0/16 - 1)
+  const int kbeg = mode == 2 ? (split >= 0 ? split : std::max(0, (p0 - WW) / WW)) : 0;
+  const int b2 = mode == 1 && split >= 0 ? split : p0 / WW;
+  const int brows = p0 - kbeg * WW;
+  // LIGHT layout (4 consumer warps, 6 select warps), RLHC_SCHUR_LIGHT=<max p0>: the early panels
+  // (p0 <= light_p0) and the odd panels of pairs (no L chunk streamed)
+  static const int light_p0 = [] { const char* e = getenv("RLHC_SCHUR_LIGHT"); return e ? atoi(e) : -1; }();
+  // P4 layout (the producer inside consumer warp 0, 4 select warps), RLHC_SCHUR_P4=<max p0>: the plain
+  // panels up to that p0 and the odd panels of pairs.  Both layouts are measurement knobs, off by
+  // default: neither beat the default layout.
+  static const int p4_p0 = [] { const char* e = getenv("RLHC_SCHUR_P4"); return e ? atoi(e) : -1; }();
+  const bool light_want = leaves_on && ids0 && rows > ST_M && light_p0 >= 0 &&
+                          ((mode == 0 && p0 <= light_p0) || (mode == 2 && split < 0)) &&
+                          schur_tma_smem_t<ST_LS, ST_LSEL>(brows, false, true) <= 227 * 1024;
+  auto smem_of = [&](bool lv) {
+    return pair ? schur_tma_smem_t<4>(brows, true, lv) : schur_tma_smem_t<5>(brows, false, lv);
+  };
+  const bool p4_want = !light_want && leaves_on && ids0 && rows > ST_M && !pair && p4_p0 >= 0 && (p0 <= p4_p0 || mode == 2) &&
+                       schur_tma_smem_t<5, 4>(brows, false, true) <= 227 * 1024;
+  bool leaves = light_want || p4_want || (leaves_on && ids0 && rows > ST_M && smem_of(true) <= 227 * 1024);
+  const size_t smem = light_want ? schur_tma_smem_t<ST_LS, ST_LSEL>(brows, false, true)
+                      : p4_want  ? schur_tma_smem_t<5, 4>(brows, false, true)
+                                 : smem_of(leaves);
   if (!on || !enc || (ldl & 1) || (ldx & 1) || (reinterpret_cast<uintptr_t>(Lb) & 15) ||
       (reinterpret_cast<uintptr_t>(X) & 15) || smem > 227 * 1024 || rows >= (int64_t(1) << 31))
     return cudaSuccess;
@@ -944,10 +1074,6 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
   if (cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) return e;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(rows, ST_M), sms));
-  // split (modes 1 and 2): the partial covers L chunks [0, split) only (-1: all of [0, p0/16)
-  // in mode 1, i.e. the odd panel streams no chunk); the odd panel streams [split, p0/16 - 1)
-  const int kbeg = mode == 2 ? (split >= 0 ? split : std::max(0, (p0 - WW) / WW)) : 0;
-  const int b2 = mode == 1 && split >= 0 ? split : p0 / WW;
   note_launch();
   *done = true;
   *leaves_done = leaves;
@@ -957,6 +1083,20 @@ static cudaError_t launch_schur_tma(const double* X, int64_t ldx, double* Lb, in
     return launch_pdl(tslw_schur_tma_kernel<4, true>, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb,
                       ldl, rows, p0, w, n, U, rd, status, chosen, leaves ? ids0 : (int*)nullptr, cnt0, vals0, row0,
                       kbeg, w2, b2);
+  }
+  if (light_want) {
+    static DevFlags attr;
+    auto kern = tslw_schur_tma_kernel<ST_LS, false, ST_LCW, ST_LSEL>;
+    if (cudaError_t e = smem_attr(attr, kern, 227 * 1024)) return e;
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb, ldl, rows, p0, w, n, U, rd,
+                      mode == 2 ? (unsigned long long*)nullptr : status, chosen, ids0, cnt0, vals0, row0, kbeg, 0, 0);
+  }
+  if (p4_want) {
+    static DevFlags attr;
+    auto kern = tslw_schur_tma_kernel<5, false, ST_CW, 4, true>;
+    if (cudaError_t e = smem_attr(attr, kern, 227 * 1024)) return e;
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(ST_THREADS), smem, st, mL, mX, Lb, ldl, rows, p0, w, n, U, rd,
+                      mode == 2 ? (unsigned long long*)nullptr : status, chosen, ids0, cnt0, vals0, row0, kbeg, 0, 0);
   }
   static DevFlags attr;
   if (cudaError_t e = smem_attr(attr, tslw_schur_tma_kernel<5, false>, 227 * 1024)) return e;
