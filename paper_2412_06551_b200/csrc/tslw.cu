@@ -660,7 +660,6 @@ struct __align__(1024) SchurTSmem {
   double rdp[WW];
   unsigned long long full[S], empty[S];
   unsigned long long ready[NSEL], freeb[NSEL];  // select warp k's staging tile: filled / free
-  unsigned long long lt_ready[2], lt_free[2];   // Lt[par]: written by the substituting warps / read by every consumer
   // followed by Bs (U[:p0, panel] in DMMA fragment order: [p0/4][2][32]), in PAIR mode Bs2
   // (U[:p0, next panel]), then (leaves) WSel[NSEL]; only U's rows [16 kbeg, p0) are staged
 };
@@ -708,10 +707,6 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
   if (tid < NSEL) {
     mbar_init(&sm.ready[tid], CW);
     mbar_init(&sm.freeb[tid], 1);
-  }
-  if (tid < 2) {
-    mbar_init(&sm.lt_ready[tid], 4);
-    mbar_init(&sm.lt_free[tid], CW);
   }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
@@ -893,9 +888,6 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
       mbar_wait(&sm.full[s], (q / S) & 1);
       STP(2)
       if (CW == 4 || (wp >> 2) == par) {
-        // (the tile's two warp halves are not barrier-aligned: Lt[par] is handed over by
-        // mbarriers, so one half's substitution overlaps the other half's DMMA stream)
-        if (ti >= 2) mbar_wait(&sm.lt_free[par], ((ti >> 1) - 1) & 1);
         const int row = tid & (ST_M - 1);
         const double* src = &sm.A[s][0][0];
         double l[WW];
@@ -918,8 +910,6 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
             for (int c = 0; c < WW; c++) dst[c] = l[c];
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.lt_ready[par]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -965,14 +955,12 @@ tslw_schur_tma_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_cons
     }
     STP(4)
     if (p0) {
-      mbar_wait(&sm.lt_ready[par], (ti >> 1) & 1);  // Lt[par] complete
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * CW) : "memory");  // Lt[par] complete
       STP(5)
       if (PAIR && nk < b2)
         mma16(&sm.Lt[par][0][0], kold, std::true_type{});
       else
         mma16(&sm.Lt[par][0][0], kold, std::false_type{});
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.lt_free[par]);
     }
     auto store = [&](const double (&ac)[NA][2][2], int col0, int wc) {
 #pragma unroll

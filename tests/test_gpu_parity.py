@@ -440,3 +440,41 @@ def test_omega_chunks_match_in_kernel(tmp_path):
         subprocess.run([sys.executable, "-c", _OMEGA_CHILD, root, f], env=env, check=True, timeout=600)
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+_SCHUR_LAYOUT_CHILD = """
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import paper_2412_06551_b200 as rl
+import synth
+out = []
+for (m, n) in ((30011, 232), (4096, 48), (65536, 64)):
+    X = synth.baseline_matrix(m, n, 6.0, 7).cuda()
+    piv, U, L11, L, info = rl.getrf_ts(X, cfg=(128, 8, 16), want_L=True)
+    assert info == (0, 0, 0), info
+    out += [piv.cpu().numpy().astype(np.float64).ravel(), U.cpu().numpy().ravel(), L.cpu().numpy().ravel()]
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+@pytest.mark.gpu
+def test_schur_layouts_bitwise(tmp_path):
+    """The TMA Schur kernel's warp layouts (measurement knobs) -- the default (8
+    consumer warps, a producer warp, 3 select warps), LIGHT (4 consumer + 6 select warps) and P4
+    (the producer inside consumer warp 0, 4 select warps) on every panel they take -- run the same
+    chain per element and the same leaf select: pivots, U and L are bit-identical (panel pairs,
+    a short pair partner and ragged rows included)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for knobs in ({}, {"RLHC_SCHUR_LIGHT": "240"}, {"RLHC_SCHUR_P4": "240"}):
+        f = str(tmp_path / f"lu_{len(outs)}.npy")
+        env = {k: v for k, v in os.environ.items() if k not in ("RLHC_SCHUR_LIGHT", "RLHC_SCHUR_P4")}
+        env.update(knobs)
+        subprocess.run([sys.executable, "-c", _SCHUR_LAYOUT_CHILD, root, f], env=env, check=True, timeout=600)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])

@@ -1,6 +1,7 @@
 #!/bin/bash
 # End-of-session verification on one B200: GPU tests, smoke, bench lines of every config, the
-# reference arm, ncu launch list + DRAM bytes per stage for cfg5.  Outputs under gpurun_out/.
+# reference arm, ncu launch list + DRAM bytes per stage for cfg5/cfg3, and a full ncu capture of a
+# panel pair's two Schur kernels.  Outputs under gpurun_out/.
 O=gpurun_out
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $O/f_smi.txt 2>&1
@@ -18,4 +19,10 @@ for c in cfg5 cfg3; do
   python tools/launches.py $O/f_l_$c.csv > $O/f_l_$c.txt
   python tools/traffic.py $O/f_l_$c.csv $c $O/f_traffic.json > $O/f_traffic_$c.txt 2>&1
 done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tslw_schur_tma_kernel -s 12 -c 2 -o $O/f_schur \
+   python tools/prof_lu.py 4194304 256 0 > $O/f_schur.log 2>&1
+ncu -i $O/f_schur.ncu-rep --page details --csv > $O/f_schur_details.csv 2>&1
+ncu -i $O/f_schur.ncu-rep --page raw --csv > $O/f_schur_raw.csv 2>&1
+ncu -i $O/f_schur.ncu-rep --page source --csv --print-source sass > $O/f_schur_source.csv 2>&1
+rm -f $O/f_schur.ncu-rep
 echo done
