@@ -122,6 +122,36 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+_CHECK: dict = {}
+
+
+def check_result(X, res, n: int) -> dict:
+    """Gates on the LAST timed step's output, outside every timed region (verification only:
+    plain torch fp64, chunked): ||Q^T Q - I||_F <= 1e-13 sqrt(n) and, on the first and last 65536
+    rows, ||Q R - X||_F / ||X||_F <= 1e-14 n (the tests' gates); diag(R) > 0.  A step that timed
+    garbage fails the bench instead of printing a number."""
+    Q, R = res.Q, res.R
+    m = Q.shape[0]
+    G = torch.zeros(n, n, dtype=torch.float64, device=Q.device)
+    step = 1 << 20
+    for i in range(0, m, step):
+        G.addmm_(Q[i:i + step].T, Q[i:i + step])
+    orth = float(torch.linalg.norm(G - torch.eye(n, dtype=torch.float64, device=Q.device)))
+    num = den = 0.0
+    rows = sorted({0, max(0, m - 65536)})
+    for i in rows:
+        d = Q[i:i + 65536] @ R - X[i:i + 65536]
+        num += float((d * d).sum())
+        den += float((X[i:i + 65536] ** 2).sum())
+    resid = (num / max(den, 1e-300)) ** 0.5
+    diag_pos = bool((torch.diagonal(R) > 0).all())
+    out = {"orth_fro": orth, "resid_sample": resid, "diag_R_positive": diag_pos,
+           "gates": {"orth_fro": 1e-13 * n ** 0.5, "resid_sample": 1e-14 * n}}
+    if not (orth <= out["gates"]["orth_fro"] and resid <= out["gates"]["resid_sample"] and diag_pos):
+        raise RuntimeError(f"timed step's result fails its gates: {out}")
+    return out
+
+
 def run_ours(args, cfg: synth.Config, rank: int, world: int):
     import paper_2412_06551_b200 as rl
     from paper_2412_06551_b200 import _lib
@@ -193,6 +223,8 @@ def run_ours(args, cfg: synth.Config, rank: int, world: int):
     code = res.info()
     if code[0] != 0:
         raise RuntimeError(f"timed run failed: info={code}")
+    if world == 1:
+        _CHECK.update(check_result(X, res, cfg.n))
 
     # ---- end to end through the public API with host buffers: every step copies this
     # rank's rows of X from pinned host memory and reads Q (its rows) and R back; device
@@ -474,6 +506,8 @@ def main():
     line = dict(base, value=value, ms_per_step=per_step, gpu_launches=launches, clocks=clocks,
                 roofline=roofline(cfg, stages, world, per_step, m_global // world, passes), e2e=e2e,
                 stages_ms={k: v / max(stages.get("calls", 1), 1) for k, v in stages.items() if k != "calls" and v})
+    if _CHECK:
+        line["check"] = dict(_CHECK)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, Xh, method=args.method)
     print(json.dumps(line), flush=True)
