@@ -34,3 +34,19 @@ for (m, n, seed) in ((65536, 64, 21), (40000, 64, 3), (262144, 128, 5), (100000,
                     print(f"{m}x{n} it {it}: {name} differs from the first call")
     print(f"{m}x{n}: {iters} iterations done, mismatches so far {bad}", flush=True)
 print("SOAK", "FAILED" if bad else "OK", bad)
+
+# the whole pipelines: Q and R of repeated calls bit-equal to the first call's
+for (algo, m, n, kw) in (("slhc3", 65536, 64, dict(s=128)), ("sslhc3", 1048576, 128, dict(s1=1024, s2=256)),
+                         ("sslhc3", 262144, 256, dict(s1=2048, s2=512))):
+    X = synth.baseline_matrix(m, n, 12, 4, device="cuda")
+    ref = None
+    for it in range(max(10, iters // 4)):
+        r = getattr(rl, algo)(X, seed=4, **kw)
+        cur = (r.Q.clone(), r.R.clone(), r.piv.clone())
+        if ref is None:
+            ref = cur
+        elif not all(torch.equal(a, b) for a, b in zip(ref, cur)):
+            bad += 1
+            print(f"{algo} {m}x{n} it {it}: Q, R or piv differs from the first call")
+    print(f"{algo} {m}x{n}: done, mismatches so far {bad}", flush=True)
+print("SOAK(all)", "FAILED" if bad else "OK", bad)
